@@ -1,0 +1,216 @@
+/*
+ * specwalk-b200 — C ABI of the B200 (sm_100a) online hot path of the
+ * adaptable-precomputation random walker (arXiv 1607.04174).
+ *
+ * Every entry point is `extern "C"`, returns an int status (SWB_OK == 0),
+ * takes plain device pointers, int64 extents and a cudaStream_t passed as
+ * `void*`.  Nothing allocates: scratch comes from a caller-provided
+ * workspace whose size is given by the matching *_workspace_bytes query.
+ * Calls are stream-ordered and stateless; concurrent calls on different
+ * streams with disjoint buffers are safe.  No C++ exception crosses the ABI.
+ *
+ * Layouts
+ *   - Voxels are flat x-fastest indices x + nx*(y + ny*z)
+ *     (reference pkg/src/specwalk/indexing.py:1-6).
+ *   - The eigenbasis V is ROW-MAJOR N x M float64 with leading dimension
+ *     ldv >= M (even), one row per voxel.  (The reference keeps V
+ *     column-major, fastrw.py:243; row-major gives coalesced stencil and
+ *     row-tile access on the GPU.)  `row_base` is the global voxel index of
+ *     row 0 of the V pointer, so a z-slab shard with a one-plane halo passes
+ *     V at its first halo row.
+ *   - Stencil coefficients: what[x*ndir + d] = magnitude of the normalized
+ *     Laplacian off-diagonal between voxel x and its forward neighbour in
+ *     direction d (L^_{x,y} = -what), 0 for edges off the grid or cut;
+ *     diag[x] = L^_{x,x}.
+ *
+ * Status codes map 1:1 onto the reference exception taxonomy
+ * (pkg/src/specwalk/errors.py:1-76).
+ */
+#ifndef SPECWALK_B200_H
+#define SPECWALK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SWB_OK 0
+#define SWB_INVALID_PARAM 1          /* errors.InvalidParam          */
+#define SWB_INSUFFICIENT_BASIS 2     /* errors.InsufficientBasis     */
+#define SWB_SINGULAR_SMALL_SYSTEM 3  /* errors.SingularSmallSystem   */
+#define SWB_DEGENERATE_GRAPH 4       /* errors.DegenerateGraph       */
+#define SWB_CUDA_ERROR 5             /* device / launch failure      */
+#define SWB_WORKSPACE_TOO_SMALL 6    /* caller workspace too small   */
+
+/* Lattice description.  connectivity: 4 (2-D, reference), 8 (2-D,
+ * BASELINE config-2 extension) or 6 (3-D, reference); nz == 1 in 2-D.
+ * weight_mode: 0 = max(exp(-beta*|dI|), 1e-8) (reference graphs.py:134-136),
+ * 1 = max(exp(-beta*dI^2), 1e-8) (BASELINE configs).
+ * Forward directions d: 4-conn {+x,+y}; 6-conn {+x,+y,+z};
+ * 8-conn {+x, +y, (+1,+1), (-1,+1)}. */
+typedef struct swb_lattice {
+  int64_t nx, ny, nz;
+  int32_t connectivity;
+  int32_t weight_mode;
+} swb_lattice;
+
+int swb_abi_version(void);
+const char* swb_status_string(int status);
+const char* swb_last_cuda_error(void);
+int swb_num_directions(const swb_lattice* lat);
+
+/* ---- graph (replaces graphs.py:127-140 build_graph + :143-159
+ *      laplacian_from_weights, NORMALIZED mode) ------------------------ */
+/* cut_mask (nullable): N*ndir bytes, nonzero = forward edge removed
+ * (topology-change extension).  degenerate_flag: device int32, set to 1
+ * when some degree <= 0 (DegenerateGraph); the caller reads it. */
+int swb_graph_build(const swb_lattice* lat, const double* intensities, double beta,
+                    const uint8_t* cut_mask, double* what, double* diag, double* d_sqrt,
+                    int32_t* degenerate_flag, void* stream);
+
+/* ---- stencil passes over V (refresh.py:75-77) ----------------------- */
+/* rows [r_begin, r_end) (global voxel indices) are processed; neighbour rows
+ * are read from V (which must hold them: halo planes for shards).
+ * Outputs are per-column sums over the processed rows, written (not
+ * accumulated) to quad/norm2/vtd (M each):
+ *   quad_j = sum_x v_xj (L^ v_j)_x,  norm2_j = sum_x v_xj^2,
+ *   vtd_j  = sum_x v_xj d_sqrt_x.
+ * Deterministic (fixed reduction order). */
+size_t swb_stencil_workspace_bytes(int64_t M);
+int swb_stencil_rayleigh(const swb_lattice* lat, const double* V, int64_t ldv, int64_t row_base,
+                         int64_t r_begin, int64_t r_end, int64_t M,
+                         const double* what, const double* diag, const double* d_sqrt,
+                         double* quad, double* norm2, double* vtd,
+                         void* workspace, size_t workspace_bytes, void* stream);
+/* Same pass, also materialising W = (L^new - L^old) V for rows
+ * [r_begin, r_end) into W (row r at W + (r - r_begin)*ldw);
+ * quad uses L^new. */
+int swb_stencil_delta(const swb_lattice* lat, const double* V, int64_t ldv, int64_t row_base,
+                      int64_t r_begin, int64_t r_end, int64_t M,
+                      const double* what_old, const double* diag_old,
+                      const double* what_new, const double* diag_new, const double* d_sqrt_new,
+                      double* W, int64_t ldw, double* quad, double* norm2, double* vtd,
+                      void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- FP64 tensor-core (DMMA) GEMMs ---------------------------------- */
+/* out[M1 x M2] = X^T Y, X rows x M1 (ldx), Y rows x M2 (ldy), reduction
+ * over rows; symmetric != 0 computes the upper triangle blocks only and
+ * mirrors (X == Y columns assumed to give a symmetric result).
+ * Deterministic split-row reduction through the workspace. */
+size_t swb_gemm_tn_workspace_bytes(int64_t rows, int64_t M1, int64_t M2);
+int swb_gemm_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t rows,
+                int64_t M1, int64_t M2, int symmetric, double* out, int64_t ldo,
+                void* workspace, size_t workspace_bytes, void* stream);
+/* out[rows x M2] = A[rows x K] B[K x M2] (+ beta_acc * out when
+ * accumulate != 0).  A row-major (lda), B row-major (ldb), out (ldo);
+ * out must not alias A. */
+int swb_gemm_nn(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows,
+                int64_t K, int64_t M2, double* out, int64_t ldo, int accumulate, void* stream);
+
+/* ---- eigen update coefficients (refresh.py:78-79 + first-order) ------ */
+/* method 0 (rayleigh, reference refresh): lam_new = sort(max(quad/norm2,0)),
+ *   order = stable argsort; C untouched.
+ * method 1 (first_order): additionally C[M x M] (row-major, ldc) =
+ *   Cfo[:, order] * s[order] with Cfo_ii = 1,
+ *   Cfo_ji = P_ji/(lam_i - lam_j) if |P_ji| <= gap_guard*|lam_i-lam_j| else 0,
+ *   s_i = 1/||Cfo[:, i]||.  P row-major (ldp), lam_old the stored values. */
+int swb_update_coeffs(int method, const double* P, int64_t ldp, const double* lam_old,
+                      const double* quad, const double* norm2, int64_t M, double gap_guard,
+                      double* C, int64_t ldc, double* lam_new, int64_t* order, void* stream);
+
+/* ---- reduced-basis RW solve (fastrw.py:352-467) ---------------------- */
+/* Seed rows of L^ in ELL form (S x R, R = 2*ndir+1), from the stencil. */
+int swb_seed_rows(const swb_lattice* lat, const double* what, const double* diag,
+                  const int64_t* seed_idx, int64_t S, int64_t* ell_idx, double* ell_val,
+                  void* stream);
+/* Pass 1 seed projections (fastrw.py:405-422, 428, 445, 449);
+ * q_s / b_qn rows have leading dimension ldq, lsu is S x L:
+ *   q_s[i,j]   = V[s_i, col(j)]
+ *   b_qn[i,j]  = sum_{y in row s_i, y not a seed} L^_{s_i,y} V[y, col(j)]
+ *   bg[i]      = sum_{y in row s_i, y not a seed} L^_{s_i,y} g_y
+ *   lsu[i,k]   = sum_{t seed in row s_i} L^_{s_i,s_t} [lab_t == k] d_sqrt_{s_t}
+ *   dsq_s[i]   = d_sqrt[s_i]
+ * col(j) = col_map ? col_map[j] : j; g = d_sqrt / dnorm (dnorm = ||d_sqrt||).
+ * Rows not in [own_begin, own_end) contribute zero (z-slab shards). */
+int swb_seed_project(const double* V, int64_t ldv, int64_t row_base, int64_t own_begin,
+                     int64_t own_end, int64_t m, const int32_t* col_map,
+                     const int64_t* seed_idx, const int32_t* seed_lab, int64_t S,
+                     const int64_t* ell_idx, const double* ell_val, int64_t R,
+                     const double* d_sqrt, double dnorm, int64_t L, double* q_s,
+                     int64_t ldq, double* b_qn, double* bg, double* lsu, double* dsq_s,
+                     void* stream);
+/* Dense seed system of fastrw.py:399-454 + LU/rcond/solve of :332-344.
+ * Computes the spectral weights w from values (m; 1/(lam+gamma), or the
+ * deflated 1/lam for lam > 1e-10 at gamma == 0), g_s = dsq_s/dnorm,
+ * gq = vtg - q_s^T g_s (gamma == 0; vtg[j] = sum_x V[x,col(j)] g_x), builds
+ * the (S+1)^2 bordered (gamma == 0) or S^2 system, factors and solves it and
+ * returns coeff (m x L, ld L) and extra (L; gamma == 0).
+ * q_s, b_qn: S x m (ld ldq, even); lsu: S x L; t_p: m x L (ld ldt, gamma > 0).
+ * rcond_out: device double; swb_check_rcond maps it to
+ * SWB_SINGULAR_SMALL_SYSTEM after the stream is synchronised. */
+size_t swb_small_solve_workspace_bytes(int64_t S, int64_t m, int64_t L);
+int swb_small_solve(double gamma, int64_t S, int64_t m, int64_t L, const double* q_s,
+                    const double* b_qn, int64_t ldq, const double* bg, const double* lsu,
+                    const double* dsq_s, double dnorm, const int32_t* seed_lab,
+                    const double* values, const double* vtg, const double* t_p, int64_t ldt,
+                    double* coeff, double* extra, double* rcond_out,
+                    void* workspace, size_t workspace_bytes, void* stream);
+int swb_check_rcond(double rcond);
+
+/* Dense LU with partial pivoting, 1-norm rcond (Hager/Higham) and solve.
+ * A is n x n row-major (lda); replaced by its LU factors. */
+size_t swb_lu_workspace_bytes(int64_t n);
+int swb_lu_factor(double* A, int64_t n, int64_t lda, int32_t* piv, double* anorm_out,
+                  void* workspace, size_t workspace_bytes, void* stream);
+int swb_lu_rcond(const double* LU, int64_t n, int64_t lda, const int32_t* piv,
+                 const double* anorm, double* rcond_out, void* workspace,
+                 size_t workspace_bytes, void* stream);
+int swb_lu_solve(const double* LU, int64_t n, int64_t lda, const int32_t* piv, double* B,
+                 int64_t nrhs, int64_t ldb, void* stream);
+
+/* Pass 2 + finalize + hard labels (fastrw.py:456-466, solver.py:55-66,
+ * images.py:128-130) for rows [r_begin, r_end):
+ *   u = (V[x, :mr] coeff + g_x*extra) / d_sqrt_x, clip >= 0, dead row ->
+ *   1/L, normalise; label = argmax (ties -> lowest), top2 = p1 - p2.
+ * coeff is mr x L (ld L) in V-column space: a permuted / truncated basis
+ * passes its coefficients through swb_scatter_rows first.  g = d_sqrt/dnorm.
+ * Seed rows are then overwritten by swb_apply_seeds.  U (nullable for
+ * L <= 8; required, ldu even, for more labels), labels (int32), top2
+ * (nullable) are indexed by (r - r_begin). */
+int swb_reconstruct_label(const double* V, int64_t ldv, int64_t row_base, int64_t r_begin,
+                          int64_t r_end, int64_t mr, const double* coeff, const double* extra,
+                          double dnorm, const double* d_sqrt, int64_t L, double* U, int64_t ldu,
+                          int32_t* labels, double* top2, void* stream);
+/* dst[j, :ncols] = src[row_map[j], :ncols], j < m. */
+int swb_gather_rows(const double* src, int64_t lds, const int32_t* row_map, int64_t m,
+                    int64_t ncols, double* dst, int64_t ldd, void* stream);
+/* dst (mr x L, zeroed) row col_map[j] = src row j, j < m. */
+int swb_scatter_rows(const double* src, int64_t m, int64_t L, const int32_t* col_map,
+                     double* dst, int64_t mr, void* stream);
+int swb_apply_seeds(const int64_t* seed_idx, const int32_t* seed_lab, int64_t S,
+                    int64_t r_begin, int64_t r_end, int64_t L, double* U, int64_t ldu,
+                    int32_t* labels, double* top2, void* stream);
+
+/* P^_masked (fastrw.py:395-397): out[r] = priors[r] * d_sqrt[r] for rows
+ * [row_begin, row_end) (out row 0 = row_begin), seed rows zeroed. */
+int swb_prior_hat(const double* priors, int64_t ldp, int64_t row_begin, int64_t row_end,
+                  int64_t L, const double* d_sqrt, const int64_t* seed_idx, int64_t S,
+                  double* out, int64_t ldo, void* stream);
+/* hard_labels of an existing field (images.py:128-130). */
+int swb_argmax_rows(const double* U, int64_t ldu, int64_t N, int64_t L, int32_t* labels,
+                    double* top2, void* stream);
+
+/* ---- small helpers used by the host layer --------------------------- */
+/* out = sum_x v[x]^2 over n entries (deterministic). */
+int swb_sumsq(const double* v, int64_t n, double* out, void* workspace,
+              size_t workspace_bytes, void* stream);
+/* dst[r, j] = src[r, col_map[j]] for j < m (column gather / permutation). */
+int swb_gather_columns(const double* src, int64_t lds, int64_t rows, const int32_t* col_map,
+                       int64_t m, double* dst, int64_t ldd, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECWALK_B200_H */

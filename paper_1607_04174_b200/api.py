@@ -1,0 +1,459 @@
+"""Public hot-path API — the drop-in for the reference's online path.
+
+Same names, argument meaning and error behaviour as the reference:
+
+  refresh(pack, image, new_beta)            refresh.py:63-82
+  refresh_from_set(packs, image, new_beta)  refresh.py:85-88
+  nearest_pack(packs, new_beta)             refresh.py:91-96
+  solve_fast(pack, lap, prob, m_use=None)   fastrw.py:352-467
+  hard_labels(field)                        images.py:128-130
+  update_basis(pack, image, new_beta, cut_edges, method, gap_guard)
+                                            north-star "update-basis" (new)
+
+Every numeric step runs in libspecwalk_b200.so on the current CUDA stream;
+results stay on the device and are materialised on the host only when a
+caller reads a host attribute (``.values``, ``.labels``, ``.eigen`` ...).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import weakref
+
+import numpy as np
+
+from . import _lib
+from .device import (WORKSPACE, DeviceGraph, DevicePack, LatticeSpec, gather_vector, ptr,
+                     require_cuda, round_up, stream_handle, to_device, torch_mod)
+from .errors import (ImageMismatch, InsufficientBasis, InvalidParam, SingularSmallSystem)
+from .types import MAX_SEEDS, LabelMap, LaplacianMode, ProbabilityField, content_hash
+
+# ---------------------------------------------------------------------------
+# image plumbing (hash check of refresh.py:71-72, device copy cache)
+# ---------------------------------------------------------------------------
+
+_image_cache: dict = {}
+
+
+def _image_entry(image):
+    key = id(image)
+    ent = _image_cache.get(key)
+    if ent is not None and ent[0]() is image:
+        return ent
+    try:
+        ref = weakref.ref(image, lambda _r, k=key: _image_cache.pop(k, None))
+    except TypeError:
+        ref = lambda: image  # noqa: E731 - non-weakrefable image object
+    ent = [ref, None, None]
+    _image_cache[key] = ent
+    return ent
+
+
+def image_hash(image) -> bytes:
+    ent = _image_entry(image)
+    if ent[1] is None:
+        ent[1] = content_hash(image)
+    return ent[1]
+
+
+def image_device(image):
+    ent = _image_entry(image)
+    if ent[2] is None:
+        torch = require_cuda()
+        ent[2] = torch.from_numpy(np.array(image.intensities, dtype=np.float64)).to("cuda")
+    return ent[2]
+
+
+def _check_image(pack, image):
+    want = getattr(getattr(pack, "provenance", None), "image_hash", None)
+    if want and image_hash(image) != want:
+        raise ImageMismatch("pack was precomputed from a different image")
+
+
+def _as_device(pack, image=None, connectivity=None, weight_mode=None) -> DevicePack:
+    if isinstance(pack, DevicePack):
+        if image is not None and pack.image_dev is None:
+            pack.image_dev = image_device(image)
+        return pack
+    dp = to_device(pack, image=None, connectivity=connectivity, weight_mode=weight_mode or "abs")
+    if image is not None:
+        dp.image_dev = image_device(image)
+    return dp
+
+
+def _cut_mask_device(lattice: LatticeSpec, cut_edges):
+    if cut_edges is None:
+        return None
+    torch = require_cuda()
+    if hasattr(cut_edges, "is_cuda"):
+        return cut_edges.to(torch.uint8).contiguous()
+    arr = np.asarray(cut_edges)
+    if arr.ndim == 2 and arr.shape == (lattice.n, lattice.ndir):
+        vm = arr.astype(np.uint8)
+    else:
+        vm = lattice.edge_mask_to_voxel_mask(arr)
+    return torch.from_numpy(np.ascontiguousarray(vm)).to("cuda")
+
+
+# ---------------------------------------------------------------------------
+# beta / topology update
+# ---------------------------------------------------------------------------
+
+class RefreshedPack(DevicePack):
+    """Base eigenvectors with Rayleigh-quotient values on the new graph
+    (refresh.py:25-51).  The column permutation is folded into the solve
+    kernels (col_map) instead of re-gathering V on every ``.eigen`` access."""
+
+    base = None
+    new_beta = None
+    order_dev = None
+
+    @property
+    def lambda_hat(self) -> np.ndarray:
+        return self.values
+
+    @property
+    def order(self) -> np.ndarray:
+        return self.order_dev.cpu().numpy().astype(np.int64)
+
+    @property
+    def laplacian(self) -> DeviceGraph:
+        return self.graph
+
+
+class UpdatedPack(RefreshedPack):
+    """First-order eigenpair update: V' = V C Pi diag(s), lam' = refresh lam^.
+    ``C`` (M x M, device) and ``P`` = V^T dL V are kept for inspection."""
+
+    C = None
+    P = None
+
+
+def _stencil_ws(m):
+    return WORKSPACE.get("stencil", _lib.size("swb_stencil_workspace_bytes", m))
+
+
+def refresh(pack, image, new_beta: float, *, connectivity=None, weight_mode=None) -> RefreshedPack:
+    """refresh.py:63-82 on the device: lam^ = max(diag(V^T L'V)/diag(V^T V), 0),
+    stable sort; one HBM pass over V (stencil) + an M-sized sort."""
+    if new_beta < 0:
+        raise InvalidParam("beta must be >= 0")
+    _check_image(pack, image)
+    torch = require_cuda()
+    dp = _as_device(pack, image, connectivity, weight_mode)
+    if dp.col_map is not None:
+        raise InvalidParam("refresh a base pack, not a refreshed one (reference semantics)")
+    graph = DeviceGraph.build(dp.image_dev, dp.lattice, new_beta)
+    m = dp.m
+    quad = torch.empty(m, dtype=torch.float64, device="cuda")
+    norm2 = torch.empty_like(quad)
+    vtd = torch.empty_like(quad)
+    ws = _stencil_ws(m)
+    lat = dp.lattice.c_struct()
+    st = stream_handle()
+    n = dp.n_vertices
+    _lib.call("swb_stencil_rayleigh", C.byref(lat), ptr(dp.V), dp.ldv, 0, 0, n, m, ptr(graph.what),
+              ptr(graph.diag), ptr(graph.d_sqrt_dev), ptr(quad), ptr(norm2), ptr(vtd), ptr(ws), ws.numel(), st)
+    lam = torch.empty(m, dtype=torch.float64, device="cuda")
+    order = torch.empty(m, dtype=torch.int64, device="cuda")
+    _lib.call("swb_update_coeffs", 0, None, 0, None, ptr(quad), ptr(norm2), m, 0.0, None, 0, ptr(lam),
+              ptr(order), st)
+    col_map = order.to(torch.int32)
+    vtg = gather_vector(vtd, col_map) / graph.dnorm
+    out = RefreshedPack(dp.V, m, lam, graph.d_sqrt_dev, graph.dnorm, dp.dims, dp.spacing, float(new_beta),
+                        dp.provenance, dp.lattice, image_dev=dp.image_dev, graph=graph, vtg=vtg,
+                        col_map=col_map, mr=dp.mr)
+    out.base = pack
+    out.new_beta = float(new_beta)
+    out.order_dev = order
+    return out
+
+
+def nearest_pack(packs, new_beta: float):
+    """refresh.py:91-96: nearest base pack on a log-beta scale."""
+    def distance(beta: float) -> float:
+        if beta <= 0 or new_beta <= 0:
+            return abs(beta - new_beta)
+        return abs(math.log(new_beta) - math.log(beta))
+    return min(packs.packs, key=lambda p: distance(p.beta))
+
+
+def refresh_from_set(packs, image, new_beta: float, **kw) -> RefreshedPack:
+    return refresh(nearest_pack(packs, new_beta), image, new_beta, **kw)
+
+
+def update_basis(pack, image, new_beta: float | None = None, cut_edges=None, method: str = "first_order",
+                 gap_guard: float = 0.5, *, connectivity=None, weight_mode=None, keep_P: bool = False):
+    """Update the eigenbasis for a new beta and/or cut edges (north-star (a)).
+
+    method="rayleigh": exactly the reference refresh (no rotation).
+    method="first_order": P = V^T (L^' - L^) V (difference stencil + DMMA
+    symmetric projection), gap-guarded divided differences C, rotation
+    V' = V C (DMMA GEMM), eigenvalues = refresh Rayleigh quotients, columns
+    stably sorted.  The old pack stays valid.
+    """
+    if method not in ("first_order", "rayleigh"):
+        raise InvalidParam(f"unknown method {method!r}")
+    dp0 = _as_device(pack, image, connectivity, weight_mode)
+    beta = dp0.beta if new_beta is None else float(new_beta)
+    if method == "rayleigh" and cut_edges is None:
+        return refresh(dp0 if isinstance(pack, DevicePack) else pack, image, beta)
+    if beta < 0:
+        raise InvalidParam("beta must be >= 0")
+    _check_image(pack, image)
+    torch = require_cuda()
+    dp = dp0
+    if dp.col_map is not None:  # materialise a refreshed pack's column order first
+        V2 = torch.zeros_like(dp.V)
+        _lib.call("swb_gather_columns", ptr(dp.V), dp.ldv, dp.n_vertices, ptr(dp.col_map), dp.m, ptr(V2),
+                  dp.ldv, stream_handle())
+        dp = DevicePack(V2, dp.m, dp.values_dev, dp.d_sqrt_dev, dp.dnorm, dp.dims, dp.spacing, dp.beta,
+                        dp.provenance, dp.lattice, image_dev=dp.image_dev, graph=dp.graph, vtg=dp.vtg)
+    g_old = dp.ensure_graph()
+    cut = _cut_mask_device(dp.lattice, cut_edges)
+    g_new = DeviceGraph.build(dp.image_dev, dp.lattice, beta, cut)
+    m, n, ldv = dp.m, dp.n_vertices, dp.ldv
+    st = stream_handle()
+    lat = dp.lattice.c_struct()
+    quad = torch.empty(m, dtype=torch.float64, device="cuda")
+    norm2 = torch.empty_like(quad)
+    vtd = torch.empty_like(quad)
+    lam = torch.empty(m, dtype=torch.float64, device="cuda")
+    order = torch.empty(m, dtype=torch.int64, device="cuda")
+    if method == "rayleigh":  # cut edges, no rotation
+        ws = _stencil_ws(m)
+        _lib.call("swb_stencil_rayleigh", C.byref(lat), ptr(dp.V), ldv, 0, 0, n, m, ptr(g_new.what),
+                  ptr(g_new.diag), ptr(g_new.d_sqrt_dev), ptr(quad), ptr(norm2), ptr(vtd), ptr(ws),
+                  ws.numel(), st)
+        _lib.call("swb_update_coeffs", 0, None, 0, None, ptr(quad), ptr(norm2), m, 0.0, None, 0, ptr(lam),
+                  ptr(order), st)
+        col_map = order.to(torch.int32)
+        out = RefreshedPack(dp.V, m, lam, g_new.d_sqrt_dev, g_new.dnorm, dp.dims, dp.spacing, beta,
+                            dp.provenance, dp.lattice, image_dev=dp.image_dev, graph=g_new,
+                            vtg=gather_vector(vtd, col_map) / g_new.dnorm, col_map=col_map, mr=dp.mr)
+    else:
+        W = torch.empty((n, ldv), dtype=torch.float64, device="cuda")   # becomes V' below
+        ws = _stencil_ws(m)
+        _lib.call("swb_stencil_delta", C.byref(lat), ptr(dp.V), ldv, 0, 0, n, m, ptr(g_old.what),
+                  ptr(g_old.diag), ptr(g_new.what), ptr(g_new.diag), ptr(g_new.d_sqrt_dev), ptr(W), ldv,
+                  ptr(quad), ptr(norm2), ptr(vtd), ptr(ws), ws.numel(), st)
+        ldp = round_up(m, 2)
+        P = torch.empty((m, ldp), dtype=torch.float64, device="cuda")
+        tws = WORKSPACE.get("gemm_tn", _lib.size("swb_gemm_tn_workspace_bytes", n, m, m))
+        _lib.call("swb_gemm_tn", ptr(dp.V), ldv, ptr(W), ldv, n, m, m, 1, ptr(P), ldp, ptr(tws), tws.numel(), st)
+        Cm = torch.empty((m, ldp), dtype=torch.float64, device="cuda")
+        _lib.call("swb_update_coeffs", 1, ptr(P), ldp, ptr(dp.values_dev), ptr(quad), ptr(norm2), m,
+                  float(gap_guard), ptr(Cm), ldp, ptr(lam), ptr(order), st)
+        Vn = W  # W is dead after the projection: the rotation writes V' into its buffer
+        if ldv > m:
+            Vn[:, m:].zero_()
+        _lib.call("swb_gemm_nn", ptr(dp.V), ldv, ptr(Cm), ldp, n, m, m, ptr(Vn), ldv, 0, st)
+        # V'^T d = C^T (V^T d): a 1-row NN product
+        vtd_row = torch.zeros((1, ldp), dtype=torch.float64, device="cuda")
+        vtd_row[0, :m].copy_(vtd)
+        vtg_row = torch.empty((1, ldp), dtype=torch.float64, device="cuda")
+        _lib.call("swb_gemm_nn", ptr(vtd_row), ldp, ptr(Cm), ldp, 1, m, m, ptr(vtg_row), ldp, 0, st)
+        out = UpdatedPack(Vn, m, lam, g_new.d_sqrt_dev, g_new.dnorm, dp.dims, dp.spacing, beta, dp.provenance,
+                          dp.lattice, image_dev=dp.image_dev, graph=g_new, vtg=vtg_row[0, :m] / g_new.dnorm)
+        out.C = Cm
+        if keep_P:
+            out.P = P
+    out.base = pack
+    out.new_beta = beta
+    out.order_dev = order
+    return out
+
+
+# ---------------------------------------------------------------------------
+# reduced-basis random walker solve
+# ---------------------------------------------------------------------------
+
+class DeviceField:
+    """Solve result on the device: labels, top-2 gap, and (lazily) U.
+
+    Host views mirror ProbabilityField (``values``, ``K``, ``dims``) and the
+    hard-label map; ``labels_dev`` / ``top2_dev`` stay on the GPU."""
+
+    def __init__(self, dims, k, labels_dev, top2_dev, U_dev=None, recompute=None):
+        self.dims = tuple(dims)
+        self._k = int(k)
+        self.labels_dev = labels_dev
+        self.top2_dev = top2_dev
+        self.U_dev = U_dev
+        self._recompute = recompute
+        self._field = None
+
+    @property
+    def K(self) -> int:
+        return self._k
+
+    def _u(self):
+        if self.U_dev is None:
+            self.U_dev = self._recompute()
+        return self.U_dev
+
+    @property
+    def values(self) -> np.ndarray:
+        return self.field().values
+
+    def field(self) -> ProbabilityField:
+        if self._field is None:
+            self._field = ProbabilityField(self.dims, self._u()[:, :self._k].cpu().numpy())
+        return self._field
+
+    def clamped(self) -> np.ndarray:
+        return np.clip(self.values, 0.0, 1.0)
+
+
+def _ell_from_lap(lap, seed_idx: np.ndarray):
+    """Seed rows of a host Laplacian (reference ``Laplacian`` / CSR) in ELL form."""
+    torch = torch_mod()
+    mat = lap.matrix if hasattr(lap, "matrix") else lap
+    rows = mat[seed_idx].tocsr()
+    rows.sort_indices()
+    s = seed_idx.size
+    r = int(np.diff(rows.indptr).max()) if s else 1
+    r = max(r, 1)
+    idx = np.full((s, r), -1, dtype=np.int64)
+    val = np.zeros((s, r), dtype=np.float64)
+    for i in range(s):
+        a, b = rows.indptr[i], rows.indptr[i + 1]
+        idx[i, : b - a] = rows.indices[a:b]
+        val[i, : b - a] = rows.data[a:b]
+    return torch.from_numpy(idx).to("cuda"), torch.from_numpy(val).to("cuda"), r
+
+
+def solve_fast(pack, lap, prob, m_use: int | None = None, streaming_block: int | None = None,
+               *, want_field: bool = False, check: bool = True) -> DeviceField:
+    """fastrw.py:352-467 on the device.
+
+    ``pack``: DevicePack / RefreshedPack / UpdatedPack, or a host pack
+    (uploaded).  ``lap``: a DeviceGraph (device stencil), None (the pack's
+    own graph), or a reference-style Laplacian (its seed rows are read on
+    the host, exactly like the reference reads ``lap.matrix[s_idx]``).
+    ``streaming_block`` is accepted for signature parity (V is resident).
+    """
+    torch = require_cuda()
+    dp = _as_device(pack)
+    n = dp.n_vertices
+    k = prob.K
+    M = dp.m
+    if m_use is None:
+        m_use = M
+    if not 1 <= m_use <= M:
+        raise InvalidParam(f"m_use must be in 1..{M}")
+    if m_use < k:
+        raise InsufficientBasis(f"m_use={m_use} cannot represent {k} labels")
+    if getattr(prob.laplacian_mode, "value", "normalized") != LaplacianMode.NORMALIZED.value:
+        raise InvalidParam("the fast path requires the normalized mode")
+    if lap is not None and lap.n_vertices != n:
+        raise InvalidParam("Laplacian size does not match the pack")
+    seeds = prob.seeds
+    s = int(seeds.n_seeds)
+    if s > MAX_SEEDS:
+        raise InvalidParam(f"at most {MAX_SEEDS} seeds supported, got {s}")
+    gamma = float(prob.gamma)
+    st = stream_handle()
+    sidx = torch.from_numpy(np.ascontiguousarray(seeds.seed_indices, dtype=np.int64)).to("cuda")
+    slab = torch.from_numpy(np.ascontiguousarray(seeds.seed_labels, dtype=np.int32)).to("cuda")
+    labels = torch.empty(n, dtype=torch.int32, device="cuda")
+    top2 = torch.empty(n, dtype=torch.float64, device="cuda")
+    ldu = round_up(k, 2)
+    if s == n:  # every voxel seeded: the one-hot field, no solve (fastrw.py:389-390)
+        U = torch.zeros((n, ldu), dtype=torch.float64, device="cuda")
+        _lib.call("swb_apply_seeds", ptr(sidx), ptr(slab), s, 0, n, k, ptr(U), ldu, ptr(labels), ptr(top2), st)
+        return DeviceField(dp.dims, k, labels, top2, U)
+
+    # seed rows of L^ (ELL)
+    if lap is None or isinstance(lap, DeviceGraph):
+        graph = lap if lap is not None else dp.ensure_graph()
+        R = 2 * graph.lattice.ndir + 1
+        ell_idx = torch.empty((max(s, 1), R), dtype=torch.int64, device="cuda")
+        ell_val = torch.empty((max(s, 1), R), dtype=torch.float64, device="cuda")
+        lat = graph.lattice.c_struct()
+        _lib.call("swb_seed_rows", C.byref(lat), ptr(graph.what), ptr(graph.diag), ptr(sidx), s, ptr(ell_idx),
+                  ptr(ell_val), st)
+    else:
+        ell_idx, ell_val, R = _ell_from_lap(lap, np.asarray(seeds.seed_indices, dtype=np.int64))
+
+    ldq = round_up(m_use, 2)
+    sa = max(s, 1)
+    q_s = torch.empty((sa, ldq), dtype=torch.float64, device="cuda")
+    b_qn = torch.empty((sa, ldq), dtype=torch.float64, device="cuda")
+    bg = torch.empty(sa, dtype=torch.float64, device="cuda")
+    lsu = torch.empty((sa, k), dtype=torch.float64, device="cuda")
+    dsq_s = torch.empty(sa, dtype=torch.float64, device="cuda")
+    col_map = dp.col_map
+    if s:
+        _lib.call("swb_seed_project", ptr(dp.V), dp.ldv, 0, 0, n, m_use, ptr(col_map), ptr(sidx), ptr(slab), s,
+                  ptr(ell_idx), ptr(ell_val), R, ptr(dp.d_sqrt_dev), dp.dnorm, k, ptr(q_s), ldq, ptr(b_qn),
+                  ptr(bg), ptr(lsu), ptr(dsq_s), st)
+    values = dp.values_dev[:m_use]
+    vtg = None
+    t_p = None
+    ldt = round_up(k, 2)
+    if gamma == 0:
+        vtg = dp.ensure_vtg()[:m_use].contiguous()
+    else:
+        priors = prob.priors
+        if not hasattr(priors, "is_cuda"):
+            priors = torch.from_numpy(np.ascontiguousarray(priors, dtype=np.float64)).to("cuda")
+        ph = torch.empty((n, ldt), dtype=torch.float64, device="cuda")
+        _lib.call("swb_prior_hat", ptr(priors), priors.stride(0), 0, n, k, ptr(dp.d_sqrt_dev), ptr(sidx), s,
+                  ptr(ph), ldt, st)
+        mr = dp.mr if col_map is not None else m_use
+        tp_full = torch.empty((mr, ldt), dtype=torch.float64, device="cuda")
+        tws = WORKSPACE.get("gemm_tn", _lib.size("swb_gemm_tn_workspace_bytes", n, mr, k))
+        _lib.call("swb_gemm_tn", ptr(dp.V), dp.ldv, ptr(ph), ldt, n, mr, k, 0, ptr(tp_full), ldt, ptr(tws),
+                  tws.numel(), st)
+        if col_map is not None:
+            t_p = torch.empty((m_use, ldt), dtype=torch.float64, device="cuda")
+            _lib.call("swb_gather_rows", ptr(tp_full), ldt, ptr(col_map), m_use, k, ptr(t_p), ldt, st)
+        else:
+            t_p = tp_full
+    coeff = torch.empty((m_use, k), dtype=torch.float64, device="cuda")
+    extra = torch.empty(k, dtype=torch.float64, device="cuda") if gamma == 0 else None
+    rcond = torch.empty(1, dtype=torch.float64, device="cuda")
+    sws = WORKSPACE.get("small_solve", _lib.size("swb_small_solve_workspace_bytes", s, m_use, k))
+    _lib.call("swb_small_solve", gamma, s, m_use, k, ptr(q_s), ptr(b_qn), ldq, ptr(bg), ptr(lsu), ptr(dsq_s),
+              dp.dnorm, ptr(slab), ptr(values), ptr(vtg), ptr(t_p), ldt, ptr(coeff), ptr(extra), ptr(rcond),
+              ptr(sws), sws.numel(), st)
+    if col_map is not None:
+        mr = dp.mr
+        cf = torch.empty((mr, k), dtype=torch.float64, device="cuda")
+        _lib.call("swb_scatter_rows", ptr(coeff), m_use, k, ptr(col_map), ptr(cf), mr, st)
+    else:
+        mr, cf = m_use, coeff
+
+    def reconstruct(with_u: bool):
+        U = torch.empty((n, ldu), dtype=torch.float64, device="cuda") if with_u else None
+        _lib.call("swb_reconstruct_label", ptr(dp.V), dp.ldv, 0, 0, n, mr, ptr(cf), ptr(extra), dp.dnorm,
+                  ptr(dp.d_sqrt_dev), k, ptr(U), ldu, ptr(labels), ptr(top2), stream_handle())
+        _lib.call("swb_apply_seeds", ptr(sidx), ptr(slab), s, 0, n, k, ptr(U), ldu, ptr(labels), ptr(top2),
+                  stream_handle())
+        return U
+
+    U = reconstruct(want_field or k > 8)
+    if check:
+        rc = float(rcond.item())
+        if _lib.load().swb_check_rcond(rc) != 0:
+            raise SingularSmallSystem(
+                f"seed system numerically singular (cond ~ {1.0 / max(rc, 1e-300):.3e})",
+                condition=1.0 / max(rc, 1e-300))
+    field = DeviceField(dp.dims, k, labels, top2, U, recompute=lambda: reconstruct(True))
+    field.rcond_dev = rcond
+    return field
+
+
+def hard_labels(field) -> LabelMap:
+    """images.py:128-130: argmax per voxel, ties to the lowest label."""
+    if isinstance(field, DeviceField):
+        return LabelMap(field.dims, field.labels_dev.cpu().numpy())
+    torch = require_cuda()
+    vals = np.ascontiguousarray(np.asarray(field.values, dtype=np.float64))
+    n, k = vals.shape
+    U = torch.from_numpy(vals).to("cuda")
+    labels = torch.empty(n, dtype=torch.int32, device="cuda")
+    _lib.call("swb_argmax_rows", ptr(U), k, n, k, ptr(labels), None, stream_handle())
+    return LabelMap(field.dims, labels.cpu().numpy())

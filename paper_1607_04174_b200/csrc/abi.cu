@@ -1,0 +1,37 @@
+// ABI plumbing: version, status strings, CUDA error capture, SM count.
+#include <atomic>
+#include "swb_common.cuh"
+
+namespace {
+thread_local cudaError_t g_last = cudaSuccess;
+std::atomic<int> g_sms{0};
+}  // namespace
+
+void swb_set_last_cuda(cudaError_t e) { g_last = e; }
+
+int swb_sm_count() {
+  int v = g_sms.load(std::memory_order_relaxed);
+  if (v > 0) return v;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sms <= 0) sms = 148;
+  g_sms.store(sms, std::memory_order_relaxed);
+  return sms;
+}
+
+extern "C" int swb_abi_version(void) { return 1; }
+
+extern "C" const char* swb_status_string(int status) {
+  switch (status) {
+    case SWB_OK: return "ok";
+    case SWB_INVALID_PARAM: return "InvalidParam";
+    case SWB_INSUFFICIENT_BASIS: return "InsufficientBasis";
+    case SWB_SINGULAR_SMALL_SYSTEM: return "SingularSmallSystem";
+    case SWB_DEGENERATE_GRAPH: return "DegenerateGraph";
+    case SWB_CUDA_ERROR: return "CudaError";
+    case SWB_WORKSPACE_TOO_SMALL: return "WorkspaceTooSmall";
+    default: return "unknown";
+  }
+}
+
+extern "C" const char* swb_last_cuda_error(void) { return cudaGetErrorString(g_last); }

@@ -1,0 +1,433 @@
+// FP64 tensor-core GEMMs for the N x K x K contractions of the hot path.
+//
+//   NN:  out[rows x M2] = A[rows x K] * B[K x M2]      (rotation V*C,
+//        reconstruction for many labels)
+//   TN:  out[M1 x M2]   = X^T Y, reduction over rows    (projection
+//        P = V^T (dL V), t_p = V^T P^, Gram matrices)
+//
+// sm_100a has no FP64 kind for tcgen05.mma, so the tensor-core path is the
+// warp-level DMMA (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4), fed from shared
+// memory that a multi-stage cp.async pipeline fills.  Shared tiles are padded
+// so every fragment load is bank-conflict free (stride = 4 mod 16 doubles).
+// Split-row TN reductions go through a workspace and are summed in a fixed
+// order, so results are bitwise deterministic run to run.
+#include "swb_common.cuh"
+
+namespace {
+
+constexpr int BK = 16;  // reduction depth per pipeline stage
+
+__host__ __device__ constexpr int pad4mod16(int n) { return n + ((4 - n % 16) + 16) % 16; }
+
+template <int WARPS_M, int WARPS_N, int WTM, int WTN, int STAGES, bool TN>
+struct Cfg {
+  static constexpr int BM = WARPS_M * WTM * 8;
+  static constexpr int BN = WARPS_N * WTN * 8;
+  static constexpr int THREADS = WARPS_M * WARPS_N * 32;
+  // A in smem: TN -> [BK][A_LD] (k-major), NN -> [BM][A_LD] (m-major)
+  static constexpr int A_LD = TN ? pad4mod16(BM) : pad4mod16(BK);
+  static constexpr int A_ELEMS = TN ? BK * A_LD : BM * A_LD;
+  static constexpr int B_LD = pad4mod16(BN);
+  static constexpr int B_ELEMS = BK * B_LD;
+  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+  static constexpr size_t SMEM = size_t(STAGES) * STAGE_ELEMS * sizeof(double);
+};
+
+// ---------------------------------------------------------------------------
+// shared mainloop: acc += A_tile * B_tile over k in [k_begin, k_end)
+// TN:  A(m, k) = X[k][m0+m],  B(k, n) = Y[k][n0+n]   (k = row index)
+// NN:  A(m, k) = A[m0+m][k],  B(k, n) = B[k][n0+n]
+// ---------------------------------------------------------------------------
+// Tile t -> (tile row, tile col).  Symmetric plans (BM == BN) enumerate the
+// upper-triangle tiles row by row: row i holds tiles j = i .. tn-1.
+__host__ __device__ __forceinline__ int2 decode_tile(int t, int tn, int symmetric) {
+  if (!symmetric) return make_int2(t / tn, t % tn);
+  int i = 0;
+  while (t >= tn - i) { t -= tn - i; ++i; }
+  return make_int2(i, i + t);
+}
+
+template <int WARPS_M, int WARPS_N, int WTM, int WTN, int STAGES, bool TN>
+__device__ __forceinline__ void load_stage(double* sA, double* sB, const double* A, int64_t lda,
+                                           const double* B, int64_t ldb, int64_t k0,
+                                           int64_t k_end, int64_t m0, int64_t m_lim,
+                                           int64_t n0, int64_t n_lim) {
+  using Cf = Cfg<WARPS_M, WARPS_N, WTM, WTN, STAGES, TN>;
+  const int tid = threadIdx.x;
+  if (TN) {
+    // X tile: BK rows (k) x BM cols, rows k0.., cols m0..
+    constexpr int CH = Cf::BM / 2;              // 16B chunks per row
+    for (int c = tid; c < BK * CH; c += Cf::THREADS) {
+      int kr = c / CH, cc = (c % CH) * 2;
+      int64_t gk = k0 + kr, gm = m0 + cc;
+      bool p = (gk < k_end) && (gm < m_lim);
+      const double* src = p ? (A + gk * lda + gm) : A;
+      cp_async16(sA + kr * Cf::A_LD + cc, src, p);
+    }
+  } else {
+    // A tile: BM rows x BK cols (k), rows m0.., cols k0..
+    constexpr int CH = BK / 2;
+    for (int c = tid; c < Cf::BM * CH; c += Cf::THREADS) {
+      int mr = c / CH, cc = (c % CH) * 2;
+      int64_t gm = m0 + mr, gk = k0 + cc;
+      bool p = (gm < m_lim) && (gk < k_end);
+      const double* src = p ? (A + gm * lda + gk) : A;
+      cp_async16(sA + mr * Cf::A_LD + cc, src, p);
+    }
+  }
+  if (((ldb & 1) == 0) && ((reinterpret_cast<uintptr_t>(B) & 15) == 0)) {
+    constexpr int CH = Cf::BN / 2;
+    for (int c = tid; c < BK * CH; c += Cf::THREADS) {
+      int kr = c / CH, cc = (c % CH) * 2;
+      int64_t gk = k0 + kr, gn = n0 + cc;
+      bool p = (gk < k_end) && (gn < n_lim);
+      const double* src = p ? (B + gk * ldb + gn) : B;
+      cp_async16(sB + kr * Cf::B_LD + cc, src, p);
+    }
+  } else {  // odd leading dimension (small label counts): 8-byte copies
+    for (int c = tid; c < BK * Cf::BN; c += Cf::THREADS) {
+      int kr = c / Cf::BN, cc = c % Cf::BN;
+      int64_t gk = k0 + kr, gn = n0 + cc;
+      bool p = (gk < k_end) && (gn < n_lim);
+      const double* src = p ? (B + gk * ldb + gn) : B;
+      cp_async8(sB + kr * Cf::B_LD + cc, src, p);
+    }
+  }
+}
+
+template <int WARPS_M, int WARPS_N, int WTM, int WTN, int STAGES, bool TN>
+__device__ __forceinline__ void mainloop(double (&acc)[WTM][WTN][2], double* smem,
+                                         const double* A, int64_t lda, const double* B,
+                                         int64_t ldb, int64_t k_begin, int64_t k_end,
+                                         int64_t m0, int64_t m_lim, int64_t n0, int64_t n_lim) {
+  using Cf = Cfg<WARPS_M, WARPS_N, WTM, WTN, STAGES, TN>;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int wm = warp / WARPS_N, wn = warp % WARPS_N;
+  const int64_t nk = (k_end - k_begin + BK - 1) / BK;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) {
+      double* st = smem + s * Cf::STAGE_ELEMS;
+      load_stage<WARPS_M, WARPS_N, WTM, WTN, STAGES, TN>(st, st + Cf::A_ELEMS, A, lda, B, ldb,
+                                                         k_begin + s * BK, k_end, m0, m_lim, n0, n_lim);
+    }
+    cp_async_commit();
+  }
+
+  const int lr = lane >> 2, lc = lane & 3;
+  for (int64_t kt = 0; kt < nk; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      int64_t nt = kt + STAGES - 1;
+      if (nt < nk) {
+        double* st = smem + (nt % STAGES) * Cf::STAGE_ELEMS;
+        load_stage<WARPS_M, WARPS_N, WTM, WTN, STAGES, TN>(st, st + Cf::A_ELEMS, A, lda, B, ldb,
+                                                           k_begin + nt * BK, k_end, m0, m_lim, n0, n_lim);
+      }
+      cp_async_commit();
+    }
+    const double* sA = smem + (kt % STAGES) * Cf::STAGE_ELEMS;
+    const double* sB = sA + Cf::A_ELEMS;
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      double af[WTM], bf[WTN];
+#pragma unroll
+      for (int i = 0; i < WTM; ++i) {
+        int m = wm * WTM * 8 + i * 8 + lr;
+        int k = kk * 4 + lc;
+        af[i] = TN ? sA[k * Cf::A_LD + m] : sA[m * Cf::A_LD + k];
+      }
+#pragma unroll
+      for (int j = 0; j < WTN; ++j) {
+        int n = wn * WTN * 8 + j * 8 + lr;
+        int k = kk * 4 + lc;
+        bf[j] = sB[k * Cf::B_LD + n];
+      }
+#pragma unroll
+      for (int i = 0; i < WTM; ++i)
+#pragma unroll
+        for (int j = 0; j < WTN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
+// NN kernel
+// ---------------------------------------------------------------------------
+template <int WARPS_M, int WARPS_N, int WTM, int WTN, int STAGES>
+__global__ void __launch_bounds__(WARPS_M * WARPS_N * 32)
+gemm_nn_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
+               int64_t ldb, int64_t rows, int64_t K, int64_t M2, double* __restrict__ out,
+               int64_t ldo, int accumulate, double alpha, int n_tiles_n) {
+  using Cf = Cfg<WARPS_M, WARPS_N, WTM, WTN, STAGES, false>;
+  extern __shared__ __align__(16) double smem[];
+  const int64_t tile = blockIdx.x;
+  const int64_t bm = tile / n_tiles_n;
+  const int bn = static_cast<int>(tile % n_tiles_n);
+  const int64_t m0 = bm * Cf::BM;
+  const int64_t n0 = int64_t(bn) * Cf::BN;
+
+  double acc[WTM][WTN][2];
+#pragma unroll
+  for (int i = 0; i < WTM; ++i)
+#pragma unroll
+    for (int j = 0; j < WTN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  mainloop<WARPS_M, WARPS_N, WTM, WTN, STAGES, false>(acc, smem, A, lda, B, ldb, 0, K, m0, rows,
+                                                      n0, M2);
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp / WARPS_N, wn = warp % WARPS_N;
+#pragma unroll
+  for (int i = 0; i < WTM; ++i) {
+    int64_t r = m0 + wm * WTM * 8 + i * 8 + (lane >> 2);
+    if (r >= rows) continue;
+    double* orow = out + r * ldo;
+#pragma unroll
+    for (int j = 0; j < WTN; ++j) {
+      int64_t c = n0 + wn * WTN * 8 + j * 8 + 2 * (lane & 3);
+      double v0 = alpha * acc[i][j][0], v1 = alpha * acc[i][j][1];
+      if (c + 1 < M2) {
+        double2* p = reinterpret_cast<double2*>(orow + c);
+        if (accumulate) { double2 o = *p; v0 += o.x; v1 += o.y; }
+        *p = make_double2(v0, v1);
+      } else if (c < M2) {
+        if (accumulate) v0 += orow[c];
+        orow[c] = v0;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TN kernel: one CTA = (tile, row chunk); partial tile -> workspace
+// ---------------------------------------------------------------------------
+template <int WARPS_M, int WARPS_N, int WTM, int WTN, int STAGES>
+__global__ void __launch_bounds__(WARPS_M * WARPS_N * 32)
+gemm_tn_kernel(const double* __restrict__ X, int64_t ldx, const double* __restrict__ Y,
+               int64_t ldy, int64_t rows, int64_t M1, int64_t M2, int tn, int symmetric,
+               int n_tiles, int64_t chunk_rows, double* __restrict__ partial) {
+  using Cf = Cfg<WARPS_M, WARPS_N, WTM, WTN, STAGES, true>;
+  extern __shared__ __align__(16) double smem[];
+  const int t = blockIdx.x;
+  const int chunk = blockIdx.y;
+  const int2 tt = decode_tile(t, tn, symmetric);
+  const int64_t m0 = int64_t(tt.x) * Cf::BM, n0 = int64_t(tt.y) * Cf::BN;
+  const int64_t k_begin = int64_t(chunk) * chunk_rows;
+  const int64_t k_end = min(rows, k_begin + chunk_rows);
+
+  double acc[WTM][WTN][2];
+#pragma unroll
+  for (int i = 0; i < WTM; ++i)
+#pragma unroll
+    for (int j = 0; j < WTN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  if (k_begin < k_end)
+    mainloop<WARPS_M, WARPS_N, WTM, WTN, STAGES, true>(acc, smem, X, ldx, Y, ldy, k_begin, k_end,
+                                                       m0, M1, n0, M2);
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp / WARPS_N, wn = warp % WARPS_N;
+  double* dst = partial + (int64_t(chunk) * n_tiles + t) * (Cf::BM * Cf::BN);
+#pragma unroll
+  for (int i = 0; i < WTM; ++i) {
+    int r = wm * WTM * 8 + i * 8 + (lane >> 2);
+#pragma unroll
+    for (int j = 0; j < WTN; ++j) {
+      int c = wn * WTN * 8 + j * 8 + 2 * (lane & 3);
+      *reinterpret_cast<double2*>(dst + r * Cf::BN + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+    }
+  }
+}
+
+template <int BM, int BN>
+__global__ void tn_reduce_kernel(const double* __restrict__ partial, int tn, int symmetric,
+                                 int n_tiles, int n_chunks, int64_t M1, int64_t M2,
+                                 double* __restrict__ out, int64_t ldo) {
+  const int64_t total = int64_t(n_tiles) * BM * BN;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int t = static_cast<int>(e / (BM * BN));
+    const int rc = static_cast<int>(e % (BM * BN));
+    const int2 tt = decode_tile(t, tn, symmetric);
+    const int64_t i = int64_t(tt.x) * BM + rc / BN;
+    const int64_t j = int64_t(tt.y) * BN + rc % BN;
+    if (i >= M1 || j >= M2) continue;
+    if (symmetric && j < i) continue;  // diagonal tiles: keep the upper half
+    double s = 0.0;
+    for (int c = 0; c < n_chunks; ++c) s += partial[(int64_t(c) * n_tiles + t) * (BM * BN) + rc];
+    out[i * ldo + j] = s;
+    if (symmetric && j != i) out[j * ldo + i] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host-side dispatch
+// ---------------------------------------------------------------------------
+template <int WARPS_M, int WARPS_N, int WTM, int WTN, int STAGES>
+int launch_nn(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows, int64_t K,
+              int64_t M2, double* out, int64_t ldo, int accumulate, double alpha, cudaStream_t st) {
+  using Cf = Cfg<WARPS_M, WARPS_N, WTM, WTN, STAGES, false>;
+  auto kern = gemm_nn_kernel<WARPS_M, WARPS_N, WTM, WTN, STAGES>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    SWB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(Cf::SMEM)));
+    attr_done = true;
+  }
+  const int64_t tm = (rows + Cf::BM - 1) / Cf::BM;
+  const int tn = static_cast<int>((M2 + Cf::BN - 1) / Cf::BN);
+  const int64_t grid = tm * tn;
+  if (grid <= 0) return SWB_OK;
+  if (grid > 0x7fffffffLL) return SWB_INVALID_PARAM;
+  kern<<<static_cast<unsigned>(grid), Cf::THREADS, Cf::SMEM, st>>>(A, lda, B, ldb, rows, K, M2, out,
+                                                                     ldo, accumulate, alpha, tn);
+  SWB_CHECK_LAUNCH();
+  return SWB_OK;
+}
+
+// TN plan: tile list + chunking
+struct TnPlan {
+  int bm, bn, n_tiles, n_chunks, tn;
+  int64_t chunk_rows;
+};
+
+template <int BM, int BN>
+TnPlan plan_tn(int64_t rows, int64_t M1, int64_t M2, int symmetric, int ctas_per_sm) {
+  TnPlan p{};
+  p.bm = BM; p.bn = BN;
+  const int tm = static_cast<int>((M1 + BM - 1) / BM), tn = static_cast<int>((M2 + BN - 1) / BN);
+  static_assert(BM == BN || BN < BM, "tile shapes");
+  const int n = symmetric ? tm * (tm + 1) / 2 : tm * tn;  // symmetric => BM == BN, tm == tn
+  p.n_tiles = n;
+  p.tn = tn;
+  const int64_t target = int64_t(swb_sm_count()) * ctas_per_sm;
+  int64_t chunks = (target + n - 1) / n;
+  const int64_t max_chunks = (rows + 511) / 512;  // >= 512 rows per chunk
+  if (chunks > max_chunks) chunks = max_chunks;
+  if (chunks < 1) chunks = 1;
+  int64_t cr = (rows + chunks - 1) / chunks;
+  cr = (cr + BK - 1) / BK * BK;
+  p.chunk_rows = cr > 0 ? cr : BK;
+  p.n_chunks = static_cast<int>((rows + p.chunk_rows - 1) / p.chunk_rows);
+  if (p.n_chunks < 1) p.n_chunks = 1;
+  return p;
+}
+
+enum TnKind { TN_80x80 = 0, TN_64x64 = 1, TN_80x16 = 2 };
+
+TnKind choose_tn(int64_t M1, int64_t M2) {
+  if (M2 <= 16) return TN_80x16;
+  auto waste = [&](int b) { return ((M1 + b - 1) / b) * b * ((M2 + b - 1) / b) * b; };
+  return waste(80) <= waste(64) ? TN_80x80 : TN_64x64;
+}
+
+constexpr int TN_STAGES = 3;
+
+template <int WARPS_M, int WARPS_N, int WTM, int WTN>
+int run_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t rows, int64_t M1,
+           int64_t M2, int symmetric, double* out, int64_t ldo, void* ws, size_t ws_bytes,
+           cudaStream_t st, bool size_only, size_t* need) {
+  using Cf = Cfg<WARPS_M, WARPS_N, WTM, WTN, TN_STAGES, true>;
+  TnPlan p = plan_tn<Cf::BM, Cf::BN>(rows, M1, M2, symmetric, 2);
+  const size_t part_bytes = sizeof(double) * size_t(p.n_chunks) * p.n_tiles * Cf::BM * Cf::BN;
+  *need = part_bytes;
+  if (size_only) return SWB_OK;
+  if (ws_bytes < *need || ws == nullptr) return SWB_WORKSPACE_TOO_SMALL;
+  double* partial = reinterpret_cast<double*>(ws);
+  auto kern = gemm_tn_kernel<WARPS_M, WARPS_N, WTM, WTN, TN_STAGES>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    SWB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(Cf::SMEM)));
+    attr_done = true;
+  }
+  dim3 grid(p.n_tiles, p.n_chunks);
+  kern<<<grid, Cf::THREADS, Cf::SMEM, st>>>(X, ldx, Y, ldy, rows, M1, M2, p.tn, symmetric, p.n_tiles,
+                                            p.chunk_rows, partial);
+  SWB_CHECK_LAUNCH();
+  const int64_t total = int64_t(p.n_tiles) * Cf::BM * Cf::BN;
+  int rb = static_cast<int>(std::min<int64_t>((total + 255) / 256, int64_t(swb_sm_count()) * 8));
+  tn_reduce_kernel<Cf::BM, Cf::BN><<<rb, 256, 0, st>>>(partial, p.tn, symmetric, p.n_tiles, p.n_chunks,
+                                                       M1, M2, out, ldo);
+  SWB_CHECK_LAUNCH();
+  return SWB_OK;
+}
+
+int dispatch_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t rows, int64_t M1,
+                int64_t M2, int symmetric, double* out, int64_t ldo, void* ws, size_t ws_bytes,
+                cudaStream_t st, bool size_only, size_t* need) {
+  switch (choose_tn(M1, M2)) {
+    case TN_80x80:
+      return run_tn<2, 2, 5, 5>(X, ldx, Y, ldy, rows, M1, M2, symmetric, out, ldo, ws, ws_bytes, st,
+                                size_only, need);
+    case TN_64x64:
+      return run_tn<2, 2, 4, 4>(X, ldx, Y, ldy, rows, M1, M2, symmetric, out, ldo, ws, ws_bytes, st,
+                                size_only, need);
+    default:
+      return run_tn<2, 2, 5, 1>(X, ldx, Y, ldy, rows, M1, M2, 0, out, ldo, ws, ws_bytes, st,
+                                size_only, need);
+  }
+}
+
+}  // namespace
+
+extern "C" size_t swb_gemm_tn_workspace_bytes(int64_t rows, int64_t M1, int64_t M2) {
+  size_t need = 0;
+  if (rows <= 0 || M1 <= 0 || M2 <= 0) return 0;
+  dispatch_tn(nullptr, 0, nullptr, 0, rows, M1, M2, 1, nullptr, 0, nullptr, 0, nullptr, true, &need);
+  size_t need2 = 0;
+  dispatch_tn(nullptr, 0, nullptr, 0, rows, M1, M2, 0, nullptr, 0, nullptr, 0, nullptr, true, &need2);
+  return need > need2 ? need : need2;
+}
+
+extern "C" int swb_gemm_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t rows,
+                           int64_t M1, int64_t M2, int symmetric, double* out, int64_t ldo,
+                           void* workspace, size_t workspace_bytes, void* stream) {
+  if (M1 <= 0 || M2 <= 0 || rows < 0 || !out) return SWB_INVALID_PARAM;
+  if (ldx < M1 || ldy < M2 || ldo < M2 || (ldx & 1) || (ldy & 1)) return SWB_INVALID_PARAM;
+  if (symmetric && M1 != M2) return SWB_INVALID_PARAM;
+  if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 15) return SWB_INVALID_PARAM;
+  cudaStream_t st = swb_stream(stream);
+  if (rows == 0) {
+    for (int64_t i = 0; i < M1; ++i)
+      SWB_CUDA_TRY(cudaMemsetAsync(out + i * ldo, 0, sizeof(double) * M2, st));
+    return SWB_OK;
+  }
+  size_t need = 0;
+  return dispatch_tn(X, ldx, Y, ldy, rows, M1, M2, symmetric, out, ldo, workspace, workspace_bytes, st,
+                     false, &need);
+}
+
+int swb_gemm_nn_alpha(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows, int64_t K,
+                      int64_t M2, double* out, int64_t ldo, int accumulate, double alpha, cudaStream_t st) {
+  if (rows < 0 || K <= 0 || M2 <= 0 || !A || !B || !out) return SWB_INVALID_PARAM;
+  if (lda < K || ldb < M2 || ldo < M2 || (lda & 1) || (ldo & 1)) return SWB_INVALID_PARAM;
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(out)) & 15) return SWB_INVALID_PARAM;
+  if (reinterpret_cast<uintptr_t>(B) & 7) return SWB_INVALID_PARAM;
+  if (rows == 0) return SWB_OK;
+  // pick the column tile that wastes the least of M2
+  auto padded = [&](int64_t b) { return (M2 + b - 1) / b * b; };
+  const int64_t p80 = padded(80), p64 = padded(64), p128 = padded(128), p32 = padded(32);
+  int64_t best = p80;
+  int which = 80;
+  if (p128 < best) { best = p128; which = 128; }
+  if (p64 < best) { best = p64; which = 64; }
+  if (p32 < best) { best = p32; which = 32; }
+  switch (which) {
+    case 128: return launch_nn<4, 2, 4, 8, 3>(A, lda, B, ldb, rows, K, M2, out, ldo, accumulate, alpha, st);
+    case 64: return launch_nn<4, 2, 4, 4, 3>(A, lda, B, ldb, rows, K, M2, out, ldo, accumulate, alpha, st);
+    case 32: return launch_nn<4, 2, 4, 2, 3>(A, lda, B, ldb, rows, K, M2, out, ldo, accumulate, alpha, st);
+    default: return launch_nn<4, 2, 4, 5, 3>(A, lda, B, ldb, rows, K, M2, out, ldo, accumulate, alpha, st);
+  }
+}
+
+extern "C" int swb_gemm_nn(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows,
+                           int64_t K, int64_t M2, double* out, int64_t ldo, int accumulate,
+                           void* stream) {
+  return swb_gemm_nn_alpha(A, lda, B, ldb, rows, K, M2, out, ldo, accumulate, 1.0, swb_stream(stream));
+}

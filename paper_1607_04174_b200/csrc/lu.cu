@@ -1,0 +1,432 @@
+// Dense FP64 LU with partial pivoting, 1-norm condition estimate and solve:
+// the seed system of the fast random walker (reference fastrw.py:332-344,
+// which calls LAPACK getrf / gecon / getrs through scipy).
+//
+// Row-major storage.  Right-looking blocked LU (panel width 32):
+//   panel  : one CTA factors rows [k,n) x cols [k,k+32) (the panel lives in
+//            shared memory when it fits, the tail rows stay in global)
+//   swaps  : the panel's row interchanges applied to the other columns
+//   trsm   : U12 = L11^-1 A12
+//   update : A22 -= L21 U12 on the DMMA tensor-core GEMM
+// rcond follows LAPACK dgecon: Higham's dlacn2 estimator of
+// ||U^-1 L^-1||_1 (single CTA), rcond = 1/(anorm * est).
+#include "swb_common.cuh"
+
+namespace {
+
+constexpr int NB = 32;           // panel width
+constexpr int PANEL_THREADS = 1024;
+constexpr int PANEL_LD = NB + 1;  // smem panel row stride (doubles)
+constexpr int PANEL_SMEM_ROWS = 840;  // 840*33*8 = 221,760 B
+
+struct ArgMax { double v; int i; };
+
+__device__ __forceinline__ ArgMax argmax_merge(ArgMax a, ArgMax b) {
+  // idamax semantics: larger |value|, ties -> smaller index
+  if (b.v > a.v || (b.v == a.v && b.i < a.i)) return b;
+  return a;
+}
+
+__device__ ArgMax block_argmax(ArgMax a, ArgMax* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ArgMax b;
+    b.v = __shfl_xor_sync(0xffffffffu, a.v, o);
+    b.i = __shfl_xor_sync(0xffffffffu, a.i, o);
+    a = argmax_merge(a, b);
+  }
+  if (lane == 0) sh[warp] = a;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    a = lane < nw ? sh[lane] : ArgMax{-1.0, 0x7fffffff};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ArgMax b;
+      b.v = __shfl_xor_sync(0xffffffffu, a.v, o);
+      b.i = __shfl_xor_sync(0xffffffffu, a.i, o);
+      a = argmax_merge(a, b);
+    }
+    if (lane == 0) sh[0] = a;
+  }
+  __syncthreads();
+  ArgMax r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+// column sums of |A| (for the 1-norm)
+__global__ void colabs_kernel(const double* __restrict__ A, int64_t n, int64_t lda, double* __restrict__ cs) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j >= n) return;
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) s += fabs(A[i * lda + j]);
+  cs[j] = s;
+}
+
+__global__ void max_kernel(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
+  __shared__ double red[1024];
+  double m = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double x = v[i];
+    m = (x > m || x != x) ? x : m;  // NaN propagates like np.linalg.norm
+  }
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double b = red[threadIdx.x + o];
+      if (b > red[threadIdx.x] || b != b) red[threadIdx.x] = b;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+// Factor the panel rows [k,n) x cols [k,k+w).  piv[k+jj] = global pivot row.
+__global__ void __launch_bounds__(PANEL_THREADS)
+panel_kernel(double* __restrict__ A, int64_t n, int64_t lda, int64_t k, int w, int32_t* __restrict__ piv,
+             int32_t* __restrict__ zero_pivot) {
+  extern __shared__ double sp[];
+  __shared__ ArgMax sh[32];
+  __shared__ double prow[NB];
+  const int64_t rows = n - k;
+  const int64_t srows = rows < PANEL_SMEM_ROWS ? rows : PANEL_SMEM_ROWS;
+  auto row = [&](int64_t i) -> double* { return i < srows ? sp + i * PANEL_LD : A + (k + i) * lda + k; };
+  for (int64_t e = threadIdx.x; e < srows * w; e += blockDim.x) {
+    const int64_t i = e / w, c = e % w;
+    sp[i * PANEL_LD + c] = A[(k + i) * lda + k + c];
+  }
+  __syncthreads();
+  for (int jj = 0; jj < w; ++jj) {
+    ArgMax a{-1.0, 0x7fffffff};
+    for (int64_t i = jj + threadIdx.x; i < rows; i += blockDim.x) {
+      const double v = fabs(row(i)[jj]);
+      a = argmax_merge(a, ArgMax{v != v ? __longlong_as_double(0x7ff0000000000000LL) : v, static_cast<int>(i)});
+    }
+    const ArgMax best = block_argmax(a, sh);
+    const int p = best.i;
+    if (threadIdx.x == 0) piv[k + jj] = static_cast<int32_t>(k + p);
+    if (p != jj) {
+      for (int c = threadIdx.x; c < w; c += blockDim.x) {
+        double* rj = row(jj);
+        double* rp = row(p);
+        const double t = rj[c]; rj[c] = rp[c]; rp[c] = t;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < w) prow[threadIdx.x] = row(jj)[threadIdx.x];
+    __syncthreads();
+    const double pv = prow[jj];
+    if (pv == 0.0) {
+      if (threadIdx.x == 0) atomicExch(zero_pivot, 1);
+      continue;  // LAPACK: column left unscaled, info > 0
+    }
+    for (int64_t i = jj + 1 + threadIdx.x; i < rows; i += blockDim.x) {
+      double* ri = row(i);
+      const double l = ri[jj] / pv;
+      ri[jj] = l;
+      for (int c = jj + 1; c < w; ++c) ri[c] -= l * prow[c];
+    }
+    __syncthreads();
+  }
+  for (int64_t e = threadIdx.x; e < srows * w; e += blockDim.x) {
+    const int64_t i = e / w, c = e % w;
+    A[(k + i) * lda + k + c] = sp[i * PANEL_LD + c];
+  }
+}
+
+// apply the panel's interchanges to columns outside [k, k+w)
+__global__ void swap_kernel(double* __restrict__ A, int64_t n, int64_t lda, int64_t k, int w,
+                            const int32_t* __restrict__ piv) {
+  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int64_t ncols = n - w;
+  if (t >= ncols) return;
+  const int64_t c = t < k ? t : t + w;
+  for (int jj = 0; jj < w; ++jj) {
+    const int64_t p = piv[k + jj];
+    if (p != k + jj) {
+      double* a = A + (k + jj) * lda + c;
+      double* b = A + p * lda + c;
+      const double x = *a; *a = *b; *b = x;
+    }
+  }
+}
+
+// U12 = L11^-1 A12 for columns [k+w, n)
+__global__ void trsm_kernel(double* __restrict__ A, int64_t n, int64_t lda, int64_t k, int w) {
+  __shared__ double L[NB][NB + 1];
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) L[e / w][e % w] = A[(k + e / w) * lda + k + e % w];
+  __syncthreads();
+  const int64_t c = k + w + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (c >= n) return;
+  double x[NB];
+#pragma unroll
+  for (int r = 0; r < NB; ++r)
+    if (r < w) x[r] = A[(k + r) * lda + c];
+#pragma unroll
+  for (int r = 0; r < NB; ++r) {
+    if (r >= w) break;
+    double s = x[r];
+#pragma unroll
+    for (int q = 0; q < NB; ++q)
+      if (q < r) s -= L[r][q] * x[q];
+    x[r] = s;
+    A[(k + r) * lda + c] = s;
+  }
+}
+
+// ---- triangular solves on the LU factors (single CTA, blocked by 32) ----
+// op: 0 = L (unit lower), 1 = U (upper), 2 = U^T (lower), 3 = L^T (unit upper)
+// B is n x nrhs (ldb) in global memory.
+__device__ void tri_solve(const double* __restrict__ LU, int64_t n, int64_t lda, double* B, int64_t nrhs,
+                          int64_t ldb, int op) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const bool forward = (op == 0 || op == 2);
+  const bool unit = (op == 0 || op == 3);
+  // element (i, j) of the triangular operator T
+  auto T = [&](int64_t i, int64_t j) -> double { return (op == 2 || op == 3) ? LU[j * lda + i] : LU[i * lda + j]; };
+  const int64_t nblk = (n + 31) / 32;
+  for (int64_t bb = 0; bb < nblk; ++bb) {
+    const int64_t blk = forward ? bb : nblk - 1 - bb;
+    const int64_t b0 = blk * 32, b1 = min(n, b0 + 32);
+    const int bs = static_cast<int>(b1 - b0);
+    // diagonal block: warp per rhs column, lane per row
+    for (int64_t c = warp; c < nrhs; c += nw) {
+      double x = lane < bs ? B[(b0 + lane) * ldb + c] : 0.0;
+      for (int s = 0; s < bs; ++s) {
+        const int r = forward ? s : bs - 1 - s;
+        double xr = __shfl_sync(0xffffffffu, x, r);
+        if (!unit) xr = xr / T(b0 + r, b0 + r);
+        if (lane == r) x = xr;
+        const bool below = forward ? (lane > r) : (lane < r);
+        if (below && lane < bs) x -= T(b0 + lane, b0 + r) * xr;
+      }
+      if (lane < bs) B[(b0 + lane) * ldb + c] = x;
+    }
+    __syncthreads();
+    // trailing update of the remaining rows
+    const int64_t r_lo = forward ? b1 : 0, r_hi = forward ? n : b0;
+    const int64_t cnt = (r_hi - r_lo) * nrhs;
+    for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) {
+      const int64_t i = r_lo + e / nrhs, c = e % nrhs;
+      double s = B[i * ldb + c];
+      for (int64_t q = b0; q < b1; ++q) s -= T(i, q) * B[q * ldb + c];
+      B[i * ldb + c] = s;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(1024)
+getrs_kernel(const double* __restrict__ LU, int64_t n, int64_t lda, const int32_t* __restrict__ piv,
+             double* B, int64_t nrhs, int64_t ldb) {
+  // B <- P^T B (LAPACK dlaswp forward)
+  for (int64_t j = 0; j < n; ++j) {
+    const int64_t p = piv[j];
+    if (p != j)
+      for (int64_t c = threadIdx.x; c < nrhs; c += blockDim.x) {
+        const double t = B[j * ldb + c]; B[j * ldb + c] = B[p * ldb + c]; B[p * ldb + c] = t;
+      }
+    __syncthreads();
+  }
+  tri_solve(LU, n, lda, B, nrhs, ldb, 0);
+  tri_solve(LU, n, lda, B, nrhs, ldb, 1);
+}
+
+__device__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < static_cast<int>(blockDim.x >> 5) ? red[lane] : 0.0;
+    v = warp_sum(v);
+    if (lane == 0) red[0] = v;
+  }
+  __syncthreads();
+  const double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+__device__ int block_idamax(const double* x, int64_t n, ArgMax* sh) {
+  ArgMax a{-1.0, 0x7fffffff};
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a = argmax_merge(a, ArgMax{fabs(x[i]), static_cast<int>(i)});
+  return block_argmax(a, sh).i;
+}
+
+// dgecon (norm '1') with dlacn2; x, xs = 2n doubles + isgn n ints of scratch.
+__global__ void __launch_bounds__(1024)
+gecon_kernel(const double* __restrict__ LU, int64_t n, int64_t lda, const double* __restrict__ anorm_p,
+             double* __restrict__ x, int32_t* __restrict__ isgn, double* __restrict__ rcond_out) {
+  __shared__ double red[32];
+  __shared__ ArgMax sh[32];
+  __shared__ int flag;
+  const double anorm = *anorm_p;
+  if (n == 0) { if (threadIdx.x == 0) *rcond_out = 1.0; return; }
+  if (!(anorm > 0.0)) { if (threadIdx.x == 0) *rcond_out = (anorm == 0.0) ? 0.0 : anorm; return; }
+  // exactly singular U -> rcond 0 (dlatrs would return scale 0)
+  if (threadIdx.x == 0) flag = 0;
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+    if (LU[i * lda + i] == 0.0) flag = 1;
+  __syncthreads();
+  if (flag) { if (threadIdx.x == 0) *rcond_out = 0.0; return; }
+
+  auto apply_inv = [&]() { tri_solve(LU, n, lda, x, 1, 1, 0); tri_solve(LU, n, lda, x, 1, 1, 1); };
+  auto apply_inv_t = [&]() { tri_solve(LU, n, lda, x, 1, 1, 2); tri_solve(LU, n, lda, x, 1, 1, 3); };
+
+  // dlacn2, kase loop unrolled into straight-line code
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x[i] = 1.0 / double(n);
+  __syncthreads();
+  apply_inv();
+  double est;
+  if (n == 1) {
+    est = fabs(x[0]);
+  } else {
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += fabs(x[i]);
+    est = block_sum(s, red);
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const bool pos = x[i] >= 0.0;
+      x[i] = pos ? 1.0 : -1.0;
+      isgn[i] = pos ? 1 : -1;
+    }
+    __syncthreads();
+    apply_inv_t();
+    int j = block_idamax(x, n, sh);
+    int iter = 2;
+    bool alt = false;
+    while (true) {
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x[i] = (i == j) ? 1.0 : 0.0;
+      __syncthreads();
+      apply_inv();
+      const double estold = est;
+      s = 0.0;
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += fabs(x[i]);
+      est = block_sum(s, red);
+      if (threadIdx.x == 0) flag = 0;
+      __syncthreads();
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+        if ((x[i] >= 0.0 ? 1 : -1) != isgn[i]) flag = 1;
+      __syncthreads();
+      const bool changed = flag != 0;
+      __syncthreads();
+      if (!changed || est <= estold) { alt = true; break; }
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const bool pos = x[i] >= 0.0;
+        x[i] = pos ? 1.0 : -1.0;
+        isgn[i] = pos ? 1 : -1;
+      }
+      __syncthreads();
+      apply_inv_t();
+      const int jlast = j;
+      j = block_idamax(x, n, sh);
+      if (x[jlast] != fabs(x[j]) && iter < 5) { ++iter; continue; }
+      alt = true;
+      break;
+    }
+    if (alt) {
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double sgn = (i & 1) ? -1.0 : 1.0;
+        x[i] = sgn * (1.0 + double(i) / double(n - 1));
+      }
+      __syncthreads();
+      apply_inv();
+      s = 0.0;
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += fabs(x[i]);
+      const double temp = 2.0 * (block_sum(s, red) / double(3 * n));
+      if (temp > est) est = temp;
+    }
+  }
+  if (threadIdx.x == 0) *rcond_out = est != 0.0 ? (1.0 / est) / anorm : 0.0;
+}
+
+}  // namespace
+
+// internal: out = alpha*A*B (+ out), see dgemm.cu
+int swb_gemm_nn_alpha(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows, int64_t K,
+                      int64_t M2, double* out, int64_t ldo, int accumulate, double alpha, cudaStream_t st);
+
+extern "C" size_t swb_lu_workspace_bytes(int64_t n) {
+  // column sums (n) + zero-pivot flag + gecon scratch (x: n, isgn: n)
+  return swb_align_up(sizeof(double) * size_t(n + 1), 256) + 256 +
+         swb_align_up(sizeof(double) * size_t(n + 1), 256) + swb_align_up(sizeof(int32_t) * size_t(n + 1), 256);
+}
+
+extern "C" int swb_lu_factor(double* A, int64_t n, int64_t lda, int32_t* piv, double* anorm_out, void* ws,
+                             size_t ws_bytes, void* stream) {
+  if (n < 0 || (n > 0 && (!A || !piv || lda < n || (lda & 1)))) return SWB_INVALID_PARAM;
+  if (n > 0x7fffffff) return SWB_INVALID_PARAM;
+  if (!ws || ws_bytes < swb_lu_workspace_bytes(n)) return SWB_WORKSPACE_TOO_SMALL;
+  cudaStream_t st = swb_stream(stream);
+  double* cs = static_cast<double*>(ws);
+  int32_t* zp = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + swb_align_up(sizeof(double) * size_t(n + 1), 256));
+  SWB_CUDA_TRY(cudaMemsetAsync(zp, 0, sizeof(int32_t), st));
+  if (n == 0) {
+    if (anorm_out) SWB_CUDA_TRY(cudaMemsetAsync(anorm_out, 0, sizeof(double), st));
+    return SWB_OK;
+  }
+  if (anorm_out) {
+    colabs_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(A, n, lda, cs);
+    SWB_CHECK_LAUNCH();
+    max_kernel<<<1, 1024, 0, st>>>(cs, n, anorm_out);
+    SWB_CHECK_LAUNCH();
+  }
+  static bool attr = false;
+  const int smem = PANEL_SMEM_ROWS * PANEL_LD * sizeof(double);
+  if (!attr) {
+    SWB_CUDA_TRY(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  for (int64_t k = 0; k < n; k += NB) {
+    const int w = static_cast<int>(std::min<int64_t>(NB, n - k));
+    panel_kernel<<<1, PANEL_THREADS, smem, st>>>(A, n, lda, k, w, piv, zp);
+    SWB_CHECK_LAUNCH();
+    const int64_t others = n - w;
+    if (others > 0) {
+      swap_kernel<<<static_cast<unsigned>((others + 255) / 256), 256, 0, st>>>(A, n, lda, k, w, piv);
+      SWB_CHECK_LAUNCH();
+    }
+    const int64_t rest = n - k - w;
+    if (rest > 0) {
+      trsm_kernel<<<static_cast<unsigned>((rest + 127) / 128), 128, 0, st>>>(A, n, lda, k, w);
+      SWB_CHECK_LAUNCH();
+      int rc = swb_gemm_nn_alpha(A + (k + w) * lda + k, lda, A + k * lda + k + w, lda, rest, w, rest,
+                                 A + (k + w) * lda + k + w, lda, 1, -1.0, st);
+      if (rc) return rc;
+    }
+  }
+  return SWB_OK;
+}
+
+extern "C" int swb_lu_rcond(const double* LU, int64_t n, int64_t lda, const int32_t* piv, const double* anorm,
+                            double* rcond_out, void* ws, size_t ws_bytes, void* stream) {
+  (void)piv;  // ||A^-1||_1 == ||U^-1 L^-1||_1: the row permutation does not change column sums
+  if (n < 0 || !anorm || !rcond_out || (n > 0 && (!LU || lda < n))) return SWB_INVALID_PARAM;
+  if (!ws || ws_bytes < swb_lu_workspace_bytes(n)) return SWB_WORKSPACE_TOO_SMALL;
+  cudaStream_t st = swb_stream(stream);
+  char* base = static_cast<char*>(ws) + swb_align_up(sizeof(double) * size_t(n + 1), 256) + 256;
+  double* x = reinterpret_cast<double*>(base);
+  int32_t* isgn = reinterpret_cast<int32_t*>(base + swb_align_up(sizeof(double) * size_t(n + 1), 256));
+  gecon_kernel<<<1, 1024, 0, st>>>(LU, n, lda, anorm, x, isgn, rcond_out);
+  SWB_CHECK_LAUNCH();
+  return SWB_OK;
+}
+
+extern "C" int swb_lu_solve(const double* LU, int64_t n, int64_t lda, const int32_t* piv, double* B,
+                            int64_t nrhs, int64_t ldb, void* stream) {
+  if (n < 0 || nrhs < 0 || (n > 0 && (!LU || !piv || !B || lda < n || ldb < nrhs))) return SWB_INVALID_PARAM;
+  if (n == 0 || nrhs == 0) return SWB_OK;
+  getrs_kernel<<<1, 1024, 0, swb_stream(stream)>>>(LU, n, lda, piv, B, nrhs, ldb);
+  SWB_CHECK_LAUNCH();
+  return SWB_OK;
+}
+
+extern "C" int swb_check_rcond(double rcond) {
+  // fastrw.py:340: not finite or < 1e-14 -> SingularSmallSystem
+  if (!(rcond == rcond) || rcond == __builtin_inf() || rcond < 1e-14) return SWB_SINGULAR_SMALL_SYSTEM;
+  return SWB_OK;
+}

@@ -1,0 +1,410 @@
+"""GPU-resident state of the hot path: lattice, graph stencil, spectral pack.
+
+PyTorch is used only to own device memory and to pick the current CUDA
+stream; every computation is a call into libspecwalk_b200.so.
+
+Device layout:
+  * V            row-major N x ldv float64 (ldv = round_up(m, 8), zero pad)
+  * what         N x ndir float64: normalised forward-edge weights of L^
+  * diag, d_sqrt N float64
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import BackendUnavailable, DegenerateGraph, InvalidParam
+from .types import PackProvenance, num_voxels
+
+WEIGHT_MODES = {"abs": 0, "sq": 1}
+
+
+def torch_mod():
+    import torch
+    return torch
+
+
+def require_cuda():
+    torch = torch_mod()
+    if not torch.cuda.is_available():
+        raise BackendUnavailable("no CUDA device: the B200 path has no CPU fallback")
+    _lib.load()
+    return torch
+
+
+def stream_handle():
+    torch = torch_mod()
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t) -> C.c_void_p:
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def round_up(x: int, a: int) -> int:
+    return (x + a - 1) // a * a
+
+
+class Workspace:
+    """Grow-only scratch buffers keyed by purpose (one set per process)."""
+
+    def __init__(self):
+        self._bufs = {}
+
+    def get(self, key: str, nbytes: int):
+        torch = torch_mod()
+        nbytes = max(int(nbytes), 256)
+        buf = self._bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(round_up(nbytes, 1 << 20), dtype=torch.uint8, device="cuda")
+            self._bufs[key] = buf
+        return buf
+
+    def clear(self):
+        self._bufs.clear()
+
+
+WORKSPACE = Workspace()
+
+
+# ---------------------------------------------------------------------------
+# lattice
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class LatticeSpec:
+    """Grid + neighbourhood + weight formula (see include/specwalk_b200.h)."""
+
+    dims: tuple
+    connectivity: int
+    weight_mode: str = "abs"
+
+    @staticmethod
+    def make(dims, connectivity=None, weight_mode="abs") -> "LatticeSpec":
+        dims = tuple(int(d) for d in dims)
+        if connectivity is None:
+            connectivity = 4 if len(dims) == 2 else 6
+        if len(dims) == 2 and connectivity not in (4, 8):
+            raise InvalidParam("2-D lattices support 4- or 8-connectivity")
+        if len(dims) == 3 and connectivity != 6:
+            raise InvalidParam("3-D lattices support 6-connectivity")
+        if weight_mode not in WEIGHT_MODES:
+            raise InvalidParam(f"unknown weight mode {weight_mode!r}")
+        return LatticeSpec(dims, int(connectivity), weight_mode)
+
+    @property
+    def n(self) -> int:
+        return num_voxels(self.dims)
+
+    @property
+    def nx(self) -> int:
+        return self.dims[0]
+
+    @property
+    def ndir(self) -> int:
+        return {4: 2, 8: 4, 6: 3}[self.connectivity]
+
+    def c_struct(self) -> _lib.Lattice:
+        nz = self.dims[2] if len(self.dims) == 3 else 1
+        return _lib.Lattice(self.dims[0], self.dims[1], nz, self.connectivity, WEIGHT_MODES[self.weight_mode])
+
+    def forward_offsets(self):
+        if self.connectivity == 4:
+            return [(1, 0), (0, 1)]
+        if self.connectivity == 8:
+            return [(1, 0), (0, 1), (1, 1), (-1, 1)]
+        return [(1, 0, 0), (0, 1, 0), (0, 0, 1)]
+
+    def edge_mask_to_voxel_mask(self, edge_mask) -> np.ndarray:
+        """Edge-list mask (order of oracle.lattice_edges / reference
+        lattice_edges: direction-major, heads in Fortran order) -> N x ndir."""
+        edge_mask = np.asarray(edge_mask, dtype=bool).ravel()
+        dims = self.dims
+        nd = len(dims)
+        grid = np.arange(self.n, dtype=np.int64).reshape(dims, order="F")
+        out = np.zeros((self.n, self.ndir), dtype=np.uint8)
+        pos = 0
+        for d, off in enumerate(self.forward_offsets()):
+            src = [slice(None)] * nd
+            for ax, o in enumerate(off):
+                if o > 0:
+                    src[ax] = slice(None, -o)
+                elif o < 0:
+                    src[ax] = slice(-o, None)
+            heads = grid[tuple(src)].ravel(order="F")
+            out[heads, d] = edge_mask[pos:pos + heads.size]
+            pos += heads.size
+        if pos != edge_mask.size:
+            raise InvalidParam(f"cut mask has {edge_mask.size} edges, lattice has {pos}")
+        return out
+
+
+# ---------------------------------------------------------------------------
+# graph (normalised Laplacian stencil)
+# ---------------------------------------------------------------------------
+
+class DeviceGraph:
+    """Normalised Laplacian L^ at one beta, as a device stencil.
+
+    Replaces build_graph + laplacian(NORMALIZED) (graphs.py:127-159).  The
+    reference ``Laplacian`` surface used by callers (``mode``, ``n_vertices``,
+    ``d_sqrt``, ``matrix``) is provided lazily on the host for compatibility;
+    the device path never materialises the CSR.
+    """
+
+    def __init__(self, lattice: LatticeSpec, beta: float, what, diag, d_sqrt, dnorm: float, cut_mask=None):
+        self.lattice = lattice
+        self.beta = float(beta)
+        self.what = what
+        self.diag = diag
+        self.d_sqrt_dev = d_sqrt
+        self.dnorm = float(dnorm)
+        self.cut_mask = cut_mask
+        self._host_d_sqrt = None
+        self._csr = None
+
+    @classmethod
+    def build(cls, intensities_dev, lattice: LatticeSpec, beta: float, cut_mask_dev=None) -> "DeviceGraph":
+        torch = require_cuda()
+        if beta < 0:
+            raise InvalidParam(f"beta must be >= 0, got {beta}")
+        n = lattice.n
+        what = torch.empty(n * lattice.ndir, dtype=torch.float64, device="cuda")
+        diag = torch.empty(n, dtype=torch.float64, device="cuda")
+        d_sqrt = torch.empty(n, dtype=torch.float64, device="cuda")
+        flag = torch.zeros(2, dtype=torch.int32, device="cuda")
+        lat = lattice.c_struct()
+        st = stream_handle()
+        _lib.call("swb_graph_build", C.byref(lat), ptr(intensities_dev), float(beta), ptr(cut_mask_dev),
+                  ptr(what), ptr(diag), ptr(d_sqrt), ptr(flag), st)
+        ss = torch.empty(1, dtype=torch.float64, device="cuda")
+        ws = WORKSPACE.get("sumsq", 256 * 8)
+        _lib.call("swb_sumsq", ptr(d_sqrt), n, ptr(ss), ptr(ws), ws.numel(), st)
+        # one small D2H for the degenerate flag and ||d_sqrt|| (host scalars)
+        host = torch.cat([ss, flag[:1].to(torch.float64)]).cpu().numpy()
+        if host[1] != 0:
+            raise DegenerateGraph("graph has an isolated vertex (zero degree)")
+        return cls(lattice, beta, what, diag, d_sqrt, float(np.sqrt(host[0])), cut_mask_dev)
+
+    # --- reference Laplacian surface (host, lazy) --------------------------
+    @property
+    def mode(self):
+        from .types import LaplacianMode
+        return LaplacianMode.NORMALIZED
+
+    @property
+    def n_vertices(self) -> int:
+        return self.lattice.n
+
+    @property
+    def d_sqrt(self) -> np.ndarray:
+        if self._host_d_sqrt is None:
+            self._host_d_sqrt = self.d_sqrt_dev.cpu().numpy()
+        return self._host_d_sqrt
+
+    @property
+    def matrix(self):
+        """Host CSR of L^ (compatibility only; assembled from the stencil)."""
+        if self._csr is None:
+            import scipy.sparse as sp
+            lat = self.lattice
+            what = self.what.cpu().numpy().reshape(lat.n, lat.ndir)
+            diag = self.diag.cpu().numpy()
+            dims = lat.dims
+            nd = len(dims)
+            grid = np.arange(lat.n, dtype=np.int64).reshape(dims, order="F")
+            rows, cols, vals = [np.arange(lat.n)], [np.arange(lat.n)], [diag]
+            for d, off in enumerate(lat.forward_offsets()):
+                src = [slice(None)] * nd
+                dst = [slice(None)] * nd
+                for ax, o in enumerate(off):
+                    if o > 0:
+                        src[ax], dst[ax] = slice(None, -o), slice(o, None)
+                    elif o < 0:
+                        src[ax], dst[ax] = slice(-o, None), slice(None, o)
+                h = grid[tuple(src)].ravel(order="F")
+                t = grid[tuple(dst)].ravel(order="F")
+                v = -what[h, d]
+                rows += [h, t]
+                cols += [t, h]
+                vals += [v, v]
+            mat = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                                shape=(lat.n, lat.n)).tocsr()
+            mat.sort_indices()
+            self._csr = mat
+        return self._csr
+
+
+# ---------------------------------------------------------------------------
+# spectral pack on the device
+# ---------------------------------------------------------------------------
+
+class DevicePack:
+    """GPU-resident spectral pack (the reference pack protocol, on device).
+
+    Exposes the duck-typed surface the reference solve uses (``eigen``,
+    ``d_sqrt``, ``dims``, ``m``; fastrw.py:352-360) — the host views are
+    materialised lazily and only for compatibility.
+    """
+
+    def __init__(self, V, m: int, values, d_sqrt_dev, dnorm: float, dims, spacing, beta: float,
+                 provenance, lattice: LatticeSpec, image_dev=None, graph: DeviceGraph | None = None,
+                 vtg=None, col_map=None, mr: int | None = None):
+        self.V = V
+        self.ldv = V.shape[1]
+        self._m = int(m)
+        self.values_dev = values
+        self.d_sqrt_dev = d_sqrt_dev
+        self.dnorm = float(dnorm)
+        self.dims = tuple(dims)
+        self.spacing = tuple(spacing) if spacing else (1.0,) * len(self.dims)
+        self.beta = float(beta)
+        self.provenance = provenance
+        self.lattice = lattice
+        self.image_dev = image_dev
+        self.graph = graph
+        self.vtg = vtg
+        self.col_map = col_map
+        self.mr = int(mr) if mr is not None else int(m)
+        self._host_values = None
+        self._host_d_sqrt = None
+
+    # --- reference pack surface -----------------------------------------
+    @property
+    def m(self) -> int:
+        return self._m
+
+    @property
+    def n_vertices(self) -> int:
+        return self.V.shape[0]
+
+    @property
+    def values(self) -> np.ndarray:
+        if self._host_values is None:
+            self._host_values = self.values_dev.cpu().numpy()
+        return self._host_values
+
+    @property
+    def d_sqrt(self) -> np.ndarray:
+        if self._host_d_sqrt is None:
+            self._host_d_sqrt = self.d_sqrt_dev.cpu().numpy()
+        return self._host_d_sqrt
+
+    @property
+    def eigen(self):
+        """Host EigenBasis (N x m, column order of this pack).  Compatibility
+        only — a full D2H copy of V."""
+        from .types import EigenBasis
+        torch = torch_mod()
+        if self.col_map is not None:
+            v = self.V.index_select(1, self.col_map.long())
+        else:
+            v = self.V[:, :self.m]
+        return EigenBasis(vectors=np.asfortranarray(v.cpu().numpy()), values=self.values)
+
+    @property
+    def laplacian_mode(self):
+        from .types import LaplacianMode
+        return LaplacianMode.NORMALIZED
+
+    def ensure_graph(self) -> DeviceGraph:
+        if self.graph is None:
+            if self.image_dev is None:
+                raise InvalidParam("this pack has no image attached; pass image= to to_device()")
+            self.graph = DeviceGraph.build(self.image_dev, self.lattice, self.beta)
+        return self.graph
+
+    def ensure_vtg(self):
+        """V^T g for g = d_sqrt/||d_sqrt|| in this pack's column order
+        (the per-basis part of fastrw.py:426, reused by every gamma=0 solve)."""
+        if self.vtg is None:
+            torch = torch_mod()
+            vt = column_dot(self.V, self.mr, self.d_sqrt_dev) / self.dnorm
+            if self.col_map is not None:
+                vt = gather_vector(vt, self.col_map)
+            self.vtg = vt
+        return self.vtg
+
+
+def column_dot(V, mr: int, x):
+    """out[j] = sum_r V[r, j] x[r] for j < mr (one HBM pass over V)."""
+    torch = torch_mod()
+    n = V.shape[0]
+    line = 64 if n % 64 == 0 else 1
+    lat = _lib.Lattice(line, n // line, 1, 4, 0)
+    # an empty stencil: the swb_stencil_rayleigh pass with zero coefficients
+    # reduces to the column sums norm2 = sum v^2 and vtd = sum v x
+    zeros = WORKSPACE.get("zero_coeffs", n * 2 * 8 + n * 8)
+    z = zeros[: n * 3 * 8].view(torch.float64)
+    z.zero_()
+    quad = torch.empty(mr, dtype=torch.float64, device="cuda")
+    norm2 = torch.empty_like(quad)
+    out = torch.empty_like(quad)
+    ws = WORKSPACE.get("stencil", _lib.size("swb_stencil_workspace_bytes", mr))
+    _lib.call("swb_stencil_rayleigh", C.byref(lat), ptr(V), V.shape[1], 0, 0, n, mr,
+              ptr(z[: 2 * n]), ptr(z[2 * n:]), ptr(x), ptr(quad), ptr(norm2), ptr(out),
+              ptr(ws), ws.numel(), stream_handle())
+    return out
+
+
+def device_norm(x) -> float:
+    """||x||_2 with the deterministic device reduction (one host scalar)."""
+    torch = torch_mod()
+    ss = torch.empty(1, dtype=torch.float64, device="cuda")
+    ws = WORKSPACE.get("sumsq", 256 * 8)
+    _lib.call("swb_sumsq", ptr(x), x.numel(), ptr(ss), ptr(ws), ws.numel(), stream_handle())
+    return float(np.sqrt(ss.item()))
+
+
+def gather_vector(v, idx):
+    """out[j] = v[idx[j]] via the row-gather kernel (1 column)."""
+    torch = torch_mod()
+    m = idx.numel()
+    out = torch.empty(m, dtype=torch.float64, device="cuda")
+    _lib.call("swb_gather_rows", ptr(v), 1, ptr(idx), m, 1, ptr(out), 1, stream_handle())
+    return out
+
+
+def upload_basis(vectors, m: int | None = None):
+    """Host N x m basis (any order, f32/f64) -> device row-major f64, ld = round_up(m, 8)."""
+    torch = require_cuda()
+    vec = np.asarray(vectors)
+    n, mm = vec.shape
+    if m is None:
+        m = mm
+    ldv = round_up(max(m, 1), 8)
+    V = torch.zeros((n, ldv), dtype=torch.float64, device="cuda")
+    if vec.flags.f_contiguous:
+        # column-major on the host == row-major (m x N): upload, then transpose on device
+        dev = torch.from_numpy(np.ascontiguousarray(vec[:, :m].T)).to("cuda")
+        V[:, :m].copy_(dev.t().to(torch.float64))
+    else:
+        V[:, :m].copy_(torch.from_numpy(np.ascontiguousarray(vec[:, :m])).to("cuda").to(torch.float64))
+    return V
+
+
+def to_device(pack, image=None, connectivity=None, weight_mode="abs") -> DevicePack:
+    """Host pack (reference SpectralPack or ours, or any duck-typed pack) ->
+    DevicePack.  ``image`` (optional) is kept on the device for beta updates."""
+    if isinstance(pack, DevicePack):
+        return pack
+    torch = require_cuda()
+    eigen = pack.eigen
+    values = np.asarray(eigen.values, dtype=np.float64)
+    m = values.size
+    V = upload_basis(eigen.vectors, m)
+    d_sqrt = np.asarray(pack.d_sqrt, dtype=np.float64)
+    d_dev = torch.from_numpy(d_sqrt.copy()).to("cuda")
+    dims = tuple(int(d) for d in pack.dims)
+    lattice = LatticeSpec.make(dims, connectivity, weight_mode)
+    img_dev = None
+    if image is not None:
+        img_dev = torch.from_numpy(np.asarray(image.intensities, dtype=np.float64).copy()).to("cuda")
+    prov = getattr(pack, "provenance", None) or PackProvenance(image_hash=b"")
+    return DevicePack(V, m, torch.from_numpy(values.copy()).to("cuda"), d_dev,
+                      device_norm(d_dev), dims, getattr(pack, "spacing", ()),
+                      float(getattr(pack, "beta", 0.0)), prov, lattice, image_dev=img_dev)

@@ -1,0 +1,75 @@
+"""CPU-side checks of the C ABI: the library loads without a GPU and exports
+every symbol declared in include/specwalk_b200.h (no compute calls)."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_1607_04174_b200 import _lib
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "specwalk_b200.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"\b(swb_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(str(_lib.library_path()))
+    missing = [s for s in declared_symbols() if not hasattr(lib, s)]
+    assert not missing, missing
+
+
+def test_binding_table_matches_header():
+    assert sorted(_lib.SIGNATURES) == declared_symbols()
+
+
+def test_status_strings_match_reference_taxonomy():
+    lib = _lib.load()
+    names = {i: lib.swb_status_string(i).decode() for i in range(7)}
+    assert names[0] == "ok"
+    assert names[1] == "InvalidParam"
+    assert names[2] == "InsufficientBasis"
+    assert names[3] == "SingularSmallSystem"
+    assert names[4] == "DegenerateGraph"
+    assert lib.swb_abi_version() == 1
+
+
+def test_status_maps_to_exceptions():
+    from paper_1607_04174_b200 import errors
+    with pytest.raises(errors.InvalidParam):
+        _lib.check(1)
+    with pytest.raises(errors.InsufficientBasis):
+        _lib.check(2)
+    with pytest.raises(errors.SingularSmallSystem):
+        _lib.check(3)
+    with pytest.raises(errors.DegenerateGraph):
+        _lib.check(4)
+
+
+def test_host_side_validation_without_device():
+    lib = _lib.load()
+    lat = _lib.Lattice(4, 4, 1, 5, 0)        # no such neighbourhood
+    assert lib.swb_num_directions(ctypes.byref(lat)) == -1
+    lat = _lib.Lattice(4, 4, 1, 8, 0)
+    assert lib.swb_num_directions(ctypes.byref(lat)) == 4
+    lat = _lib.Lattice(4, 4, 4, 6, 1)
+    assert lib.swb_num_directions(ctypes.byref(lat)) == 3
+    # rcond gate of fastrw.py:340
+    assert lib.swb_check_rcond(1e-3) == 0
+    assert lib.swb_check_rcond(1e-15) == 3
+    assert lib.swb_check_rcond(float("nan")) == 3
+    # invalid arguments are rejected before any device work
+    assert lib.swb_gemm_nn(None, 0, None, 0, 10, 4, 4, None, 4, 0, None) == 1
+    assert lib.swb_update_coeffs(7, None, 0, None, None, None, 4, 0.5, None, 0, None, None, None) == 1
+
+
+def test_workspace_queries():
+    lib = _lib.load()
+    assert lib.swb_gemm_tn_workspace_bytes(16_777_216, 400, 400) > 0
+    assert lib.swb_small_solve_workspace_bytes(800, 400, 4) > 801 * 801 * 8
+    assert lib.swb_lu_workspace_bytes(801) >= 801 * 8
