@@ -1,0 +1,435 @@
+"""Benchmark of the online hot path on B200 (one JSON line on rank 0).
+
+One *step* = one interaction of the BASELINE config-4 workload (256^3 volume,
+K = 400 eigenvectors, V = 54 GB FP64 resident in HBM):
+  1. first-order basis update for beta 80 -> 110 (alternating 110 -> 80 on
+     odd steps so every step is a valid update of the previous one):
+     graph coefficients, difference stencil dL V, DMMA symmetric projection
+     P = V^T dL V, refresh eigenvalues + gap-guarded coefficients C,
+     DMMA rotation V' = V C;
+  2. 4-label reduced-basis random-walker solve with 200 seeds per label
+     (gamma = 0): seed projections, (S+1)^2 LU + rcond, reconstruction +
+     finalize + per-voxel argmax.
+value = N*K / step time (whole job, all ranks).  e2e = the same through the
+public API with host seeds in and host labels out every step.
+
+--impl reference times the reference algorithm's CPU restatement
+(oracle/rw_oracle.py, numpy/scipy on all host cores) on a bounded z-slab
+sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "basis-update N·K/s and RW-solve voxels/s; % HBM / FP64-tensor roofline"
+UNIT = "N·K/s"
+CPU_SLAB_PLANES = 4
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--dims", default=None, help="override volume dims, e.g. 64,64,64")
+    ap.add_argument("--m", type=int, default=None, help="override K")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=0, help="ncu helper: run N steps, no timing")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle restatement on a bounded z-slab sample
+# ---------------------------------------------------------------------------
+
+def cpu_sample(cfg: str, dims, m: int, planes: int = CPU_SLAB_PLANES):
+    from paper_1607_04174_b200 import workloads as W
+    w = W.make_image(cfg, dims)
+    d3 = len(w.dims) == 3
+    sdims = (w.dims[0], w.dims[1], planes) if d3 else w.dims
+    n = int(np.prod(sdims))
+    z0 = 0
+    if d3:  # the slab window that sees the most labelled objects
+        plane = w.dims[0] * w.dims[1]
+        t3 = w.truth.reshape(w.dims[2], plane)
+        best = (-1, -1)
+        for z in range(0, w.dims[2] - planes + 1):
+            win = t3[z:z + planes]
+            score = (len(np.unique(win[win >= 0])), int((win >= 0).sum()))
+            if score > best:
+                best, z0 = score, z
+        z0 *= plane
+    img = w.intensities[z0:z0 + n]
+    truth = w.truth[z0:z0 + n]
+    rng = np.random.default_rng([W.CFG_INDEX[cfg], 9])
+    G = rng.standard_normal((n, m))
+    for _ in range(2):  # CholeskyQR2
+        R = np.linalg.cholesky(G.T @ G).T
+        G = np.linalg.solve(R.T, G.T).T
+    lam = W.synthetic_lambda(cfg, m)
+    seeds, labs = W.sample_region_seeds(truth, w.params["labels"], w.params["seeds_per_label"], rng)
+    return dict(dims=sdims, img=img, V=np.asfortranarray(G), lam=lam, seeds=seeds, labs=labs, n=n,
+                params=w.params)
+
+
+def cpu_step(s, beta0, beta1, labels):
+    from oracle import rw_oracle as O
+    p = s["params"]
+    lap0 = O.build_laplacian(s["img"], s["dims"], beta0, p["weight_mode"], p["connectivity"])
+    lap1 = O.build_laplacian(s["img"], s["dims"], beta1, p["weight_mode"], p["connectivity"])
+    V1, lam1, _, _, _ = O.first_order_update(s["V"], s["lam"], lap0, lap1)
+    u = O.solve_fast(V1, lam1, lap1.d_sqrt, lap1.matrix, s["seeds"], s["labs"], labels)
+    return O.hard_labels(u)
+
+
+def cpu_baseline(cfg, dims, m, steps=2):
+    s = cpu_sample(cfg, dims, m)
+    p = s["params"]
+    cpu_step(s, p["beta0"], p["beta1"], p["labels"])  # warm
+    t = []
+    for i in range(steps):
+        t0 = time.perf_counter()
+        b0, b1 = (p["beta0"], p["beta1"]) if i % 2 == 0 else (p["beta1"], p["beta0"])
+        cpu_step(s, b0, b1, p["labels"])
+        t.append(time.perf_counter() - t0)
+    sec = min(t)
+    return {"value": s["n"] * m / sec, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{cfg} z-slab {'x'.join(map(str, s['dims']))} ({s['n']} voxels) x K={m}: oracle "
+                      f"first-order update + gamma=0 solve + labels, best of {steps}, {sec:.2f} s/step"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_1607_04174_b200 import workloads as W
+    cfg = args.config
+    dims = tuple(int(x) for x in args.dims.split(",")) if args.dims else None
+    m = args.m or W.CONFIGS[cfg]["m"]
+    s = cpu_sample(cfg, dims, m)
+    p = s["params"]
+    for i in range(args.warmup):
+        cpu_step(s, p["beta0"], p["beta1"], p["labels"])
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        b0, b1 = (p["beta0"], p["beta1"]) if i % 2 == 0 else (p["beta1"], p["beta0"])
+        cpu_step(s, b0, b1, p["labels"])
+    sec = (time.perf_counter() - t0) / max(args.steps, 1)
+    value = s["n"] * m / sec
+    dims_full = dims or W.CONFIGS[cfg]["dims"]
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg} {'x'.join(map(str, dims_full))} K={m}", "K": m,
+                       "sample_voxels": s["n"]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                             "sample": f"z-slab {'x'.join(map(str, s['dims']))} of {cfg} ({s['n']} voxels)"
+                                       f" x K={m}, oracle/rw_oracle.py on numpy/scipy"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def setup_gpu(cfg, dims, m, rank):
+    import torch
+
+    import paper_1607_04174_b200 as swb
+    from paper_1607_04174_b200 import workloads as W
+    from paper_1607_04174_b200.device import DevicePack, LatticeSpec, round_up
+    w = W.make_image(cfg, dims)
+    p = w.params
+    n = int(np.prod(w.dims))
+    image = swb.Image(w.dims, w.intensities)
+    lattice = LatticeSpec.make(w.dims, p["connectivity"], p["weight_mode"])
+    V = W.orthonormal_basis_device(n, m, seed=W.CFG_INDEX[cfg] * 1000 + 17 + rank)
+    lam = torch.from_numpy(W.synthetic_lambda(cfg, m)).cuda()
+    img_dev = torch.from_numpy(np.array(w.intensities)).cuda()
+    g0 = swb.DeviceGraph.build(img_dev, lattice, p["beta0"])
+    prov = swb.PackProvenance(image_hash=image.content_hash())
+    pack = DevicePack(V, m, lam, g0.d_sqrt_dev, g0.dnorm, w.dims, (), p["beta0"], prov, lattice,
+                      image_dev=img_dev, graph=g0)
+    # the API caches the device copy of the image per Image object
+    from paper_1607_04174_b200 import api
+    api._image_entry(image)[2] = img_dev
+    seeds, labs = W.seeds_for(w)
+    prob = swb.LabelProblem(num_labels=p["labels"], seeds=swb.SeedPartition(n, seeds, labs))
+    return dict(w=w, image=image, pack=pack, prob=prob, n=n, m=m, params=p)
+
+
+def gpu_step(state, i):
+    import paper_1607_04174_b200 as swb
+    p = state["params"]
+    beta = p["beta1"] if i % 2 == 0 else p["beta0"]
+    pack = swb.update_basis(state["pack"], state["image"], beta, method="first_order")
+    state["pack"] = pack
+    field = swb.solve_fast(pack, pack.laplacian, state["prob"])
+    return field
+
+
+def e2e_step(state, i, host_labels):
+    """Public API with host buffers: host seeds in (H2D inside solve_fast),
+    host label map out (D2H into pinned memory) every step."""
+    import paper_1607_04174_b200 as swb
+    p = state["params"]
+    beta = p["beta1"] if i % 2 == 0 else p["beta0"]
+    seeds = state["prob"].seeds
+    prob = swb.LabelProblem(num_labels=p["labels"],
+                            seeds=swb.SeedPartition(state["n"], seeds.seed_indices.copy(), seeds.seed_labels.copy()))
+    pack = swb.update_basis(state["pack"], state["image"], beta, method="first_order")
+    state["pack"] = pack
+    field = swb.solve_fast(pack, pack.laplacian, prob)
+    host_labels.copy_(field.labels_dev, non_blocking=True)
+    return field
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1607_04174_b200 as swb
+    from paper_1607_04174_b200 import _lib, api
+    from paper_1607_04174_b200 import workloads as W
+    from paper_1607_04174_b200.device import stream_handle
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = args.config
+    dims = tuple(int(x) for x in args.dims.split(",")) if args.dims else None
+    m = args.m or W.CONFIGS[cfg]["m"]
+    lib = _lib.load()
+
+    state = setup_gpu(cfg, dims, m, rank)
+    n = state["n"]
+    if args.profile_steps:
+        for i in range(args.profile_steps):
+            gpu_step(state, i)
+        torch.cuda.synchronize()
+        return
+
+    # live FP64 tensor-core peak (DMMA probe), best of 5
+    sink = torch.zeros(1, dtype=torch.float64, device="cuda")
+    flops = _lib.c_dbl()
+    best = 0.0
+    for it in range(6):
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        _lib.check(lib.swb_fp64_peak_probe(20000, _lib.c_vp(sink.data_ptr()), _lib.C.byref(flops),
+                                           stream_handle()))
+        e1.record()
+        torch.cuda.synchronize()
+        if it:
+            best = max(best, flops.value / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    fp64_peak = best
+
+    for i in range(args.warmup):
+        gpu_step(state, i)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- device-resident timed region -------------------------------------
+    api.TIMER = api.PhaseTimer()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = lib.swb_launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for i in range(args.steps):
+        gpu_step(state, args.warmup + i)
+    e1.record()
+    barrier()
+    torch.cuda.synchronize()
+    launches = lib.swb_launch_count() - launches0
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    phases = {k: float(np.mean(v)) for k, v in api.TIMER.durations().items()}
+    api.TIMER = None
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    value = world * n * m / (ms * 1e-3)
+
+    # ---- end-to-end through the public API with host buffers ---------------
+    e2e = None
+    if not args.no_e2e:
+        host_labels = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        barrier()
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        a0.record()
+        for i in range(args.steps):
+            e2e_step(state, args.warmup + args.steps + i, host_labels)
+        a1.record()
+        barrier()
+        torch.cuda.synchronize()
+        ems = a0.elapsed_time(a1) / args.steps
+        et = torch.tensor([ems], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        ems = float(et.item())
+        s = state["prob"].seeds.n_seeds
+        e2e = {"value": world * n * m / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(s * (8 + 4)),
+               "d2h_bytes_per_step": int(n * 4 + 8), "ms_per_step": ems}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (rotation GEMM, DMMA) ------------
+    rot_ms = phases.get("rotate")
+    rot_flops = 2.0 * n * m * m
+    achieved = rot_flops / (rot_ms * 1e-3) / 1e12 if rot_ms else None
+    peaks = {}
+    mp = ROOT / "MEASURED_PEAKS.json"
+    if mp.exists():
+        peaks = json.loads(mp.read_text())
+    hbm = float(peaks.get("hbm_gbs", 6544.3))
+    proj_ms = phases.get("project")
+    st_ms = phases.get("stencil")
+    rc_ms = phases.get("solve_reconstruct")
+    upd_ms = sum(v for k, v in phases.items() if not k.startswith("solve"))
+    solve_ms = sum(v for k, v in phases.items() if k.startswith("solve"))
+    kernels = {
+        "rotation_dmma": {"ms": rot_ms, "tflops": achieved, "frac_fp64": achieved / fp64_peak if achieved else None},
+        "projection_dmma": {"ms": proj_ms, "tflops": (n * m * (m + 1)) / (proj_ms * 1e-3) / 1e12 if proj_ms else None},
+        "stencil_delta": {"ms": st_ms, "gbs": (16.0 * n * m + 72.0 * n) / (st_ms * 1e-3) / 1e9 if st_ms else None},
+        "reconstruct_argmax": {"ms": rc_ms, "gbs": (8.0 * n * m + 20.0 * n) / (rc_ms * 1e-3) / 1e9 if rc_ms else None},
+    }
+    for k in ("projection_dmma",):
+        if kernels[k]["tflops"]:
+            kernels[k]["frac_fp64"] = kernels[k]["tflops"] / fp64_peak
+    for k in ("stencil_delta", "reconstruct_argmax"):
+        if kernels[k]["gbs"]:
+            kernels[k]["frac_hbm"] = kernels[k]["gbs"] / hbm
+
+    cpu = None
+    if not args.no_cpu:
+        try:
+            cpu = cpu_baseline(cfg, dims, m)
+        except Exception as exc:  # noqa: BLE001 - reported, never fatal
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {exc}"}
+
+    dims_full = tuple(state["w"].dims)
+    s = state["prob"].seeds.n_seeds
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg}: {'x'.join(map(str, dims_full))} volume, K={m}, first-order beta update "
+                               f"{state['params']['beta0']}<->{state['params']['beta1']} + {state['params']['labels']}-"
+                               f"label RW solve, S={s}",
+                   "N": n, "K": m, "labels": state["params"]["labels"], "seeds": int(s),
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (V = %.1f GB)" % (n * m * 8 / 1e9)},
+        "roofline": {"bound": "tensor", "kernel": "rotation V*C (DMMA NN GEMM)", "achieved": achieved,
+                     "peak": fp64_peak, "unit": "TFLOP/s", "frac": (achieved / fp64_peak) if achieved else None,
+                     "peak_source": "live DMMA.8x8x4 probe (swb_fp64_peak_probe) in this run; MEASURED_PEAKS.json "
+                                    "has no FP64 entry",
+                     "traffic": None},
+        "kernels": kernels,
+        "update": {"ms": upd_ms, "value": n * m / (upd_ms * 1e-3) if upd_ms else None, "unit": UNIT},
+        "solve": {"ms": solve_ms, "value": n / (solve_ms * 1e-3) if solve_ms else None, "unit": "voxels/s"},
+        "phases_ms": phases,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

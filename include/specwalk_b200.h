@@ -60,6 +60,9 @@ int swb_abi_version(void);
 const char* swb_status_string(int status);
 const char* swb_last_cuda_error(void);
 int swb_num_directions(const swb_lattice* lat);
+/* Number of kernels this library has launched in the process (bench
+ * accounting: gpu_launches). */
+unsigned long long swb_launch_count(void);
 
 /* ---- graph (replaces graphs.py:127-140 build_graph + :143-159
  *      laplacian_from_weights, NORMALIZED mode) ------------------------ */
@@ -78,7 +81,7 @@ int swb_graph_build(const swb_lattice* lat, const double* intensities, double be
  *   quad_j = sum_x v_xj (L^ v_j)_x,  norm2_j = sum_x v_xj^2,
  *   vtd_j  = sum_x v_xj d_sqrt_x.
  * Deterministic (fixed reduction order). */
-size_t swb_stencil_workspace_bytes(int64_t M);
+size_t swb_stencil_workspace_bytes(const swb_lattice* lat, int64_t M);
 int swb_stencil_rayleigh(const swb_lattice* lat, const double* V, int64_t ldv, int64_t row_base,
                          int64_t r_begin, int64_t r_end, int64_t M,
                          const double* what, const double* diag, const double* d_sqrt,
@@ -201,6 +204,12 @@ int swb_prior_hat(const double* priors, int64_t ldp, int64_t row_begin, int64_t 
 /* hard_labels of an existing field (images.py:128-130). */
 int swb_argmax_rows(const double* U, int64_t ldu, int64_t N, int64_t L, int32_t* labels,
                     double* top2, void* stream);
+
+/* FP64 tensor-core peak probe: launches back-to-back DMMA.8x8x4 work on
+ * every SM; *flops_out = flops of the launch (host value) for the caller to
+ * divide by its event-timed duration.  sink: device double (never written
+ * in practice). */
+int swb_fp64_peak_probe(int iters, double* sink, double* flops_out, void* stream);
 
 /* ---- small helpers used by the host layer --------------------------- */
 /* out = sum_x v[x]^2 over n entries (deterministic). */

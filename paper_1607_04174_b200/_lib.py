@@ -33,9 +33,10 @@ SIGNATURES = {
     "swb_abi_version": (C.c_int, []),
     "swb_status_string": (C.c_char_p, [C.c_int]),
     "swb_last_cuda_error": (C.c_char_p, []),
+    "swb_launch_count": (C.c_ulonglong, []),
     "swb_num_directions": (C.c_int, [C.POINTER(Lattice)]),
     "swb_graph_build": (C.c_int, [C.POINTER(Lattice), c_vp, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
-    "swb_stencil_workspace_bytes": (c_sz, [c_i64]),
+    "swb_stencil_workspace_bytes": (c_sz, [C.POINTER(Lattice), c_i64]),
     "swb_stencil_rayleigh": (C.c_int, [C.POINTER(Lattice), c_vp, c_i64, c_i64, c_i64, c_i64, c_i64,
                                        c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "swb_stencil_delta": (C.c_int, [C.POINTER(Lattice), c_vp, c_i64, c_i64, c_i64, c_i64, c_i64,
@@ -68,6 +69,7 @@ SIGNATURES = {
                                   c_vp]),
     "swb_prior_hat": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp]),
     "swb_argmax_rows": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
+    "swb_fp64_peak_probe": (C.c_int, [C.c_int, c_vp, C.POINTER(c_dbl), c_vp]),
     "swb_sumsq": (C.c_int, [c_vp, c_i64, c_vp, c_vp, c_sz, c_vp]),
     "swb_gather_columns": (C.c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp]),
 }

@@ -30,6 +30,38 @@ from .errors import (ImageMismatch, InsufficientBasis, InvalidParam, SingularSma
 from .types import MAX_SEEDS, LabelMap, LaplacianMode, ProbabilityField, content_hash
 
 # ---------------------------------------------------------------------------
+# optional phase timing (CUDA events on the launching stream; bench.py)
+# ---------------------------------------------------------------------------
+
+class PhaseTimer:
+    """Records a CUDA event at each named phase boundary on the current
+    stream.  ``durations()`` (after a synchronize) gives per-phase ms."""
+
+    def __init__(self):
+        self.marks = []
+
+    def mark(self, name: str):
+        torch = torch_mod()
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self.marks.append((name, ev))
+
+    def durations(self) -> dict:
+        out: dict = {}
+        for (name, ev), (_, nxt) in zip(self.marks, self.marks[1:]):
+            out.setdefault(name, []).append(ev.elapsed_time(nxt))
+        return out
+
+
+TIMER: PhaseTimer | None = None
+
+
+def _mark(name: str):
+    if TIMER is not None:
+        TIMER.mark(name)
+
+
+# ---------------------------------------------------------------------------
 # image plumbing (hash check of refresh.py:71-72, device copy cache)
 # ---------------------------------------------------------------------------
 
@@ -130,8 +162,9 @@ class UpdatedPack(RefreshedPack):
     P = None
 
 
-def _stencil_ws(m):
-    return WORKSPACE.get("stencil", _lib.size("swb_stencil_workspace_bytes", m))
+def _stencil_ws(lattice, m):
+    lat = lattice.c_struct()
+    return WORKSPACE.get("stencil", _lib.size("swb_stencil_workspace_bytes", C.byref(lat), m))
 
 
 def refresh(pack, image, new_beta: float, *, connectivity=None, weight_mode=None) -> RefreshedPack:
@@ -149,7 +182,7 @@ def refresh(pack, image, new_beta: float, *, connectivity=None, weight_mode=None
     quad = torch.empty(m, dtype=torch.float64, device="cuda")
     norm2 = torch.empty_like(quad)
     vtd = torch.empty_like(quad)
-    ws = _stencil_ws(m)
+    ws = _stencil_ws(dp.lattice, m)
     lat = dp.lattice.c_struct()
     st = stream_handle()
     n = dp.n_vertices
@@ -210,9 +243,11 @@ def update_basis(pack, image, new_beta: float | None = None, cut_edges=None, met
                   dp.ldv, stream_handle())
         dp = DevicePack(V2, dp.m, dp.values_dev, dp.d_sqrt_dev, dp.dnorm, dp.dims, dp.spacing, dp.beta,
                         dp.provenance, dp.lattice, image_dev=dp.image_dev, graph=dp.graph, vtg=dp.vtg)
+    _mark("graph")
     g_old = dp.ensure_graph()
     cut = _cut_mask_device(dp.lattice, cut_edges)
     g_new = DeviceGraph.build(dp.image_dev, dp.lattice, beta, cut)
+    _mark("alloc")
     m, n, ldv = dp.m, dp.n_vertices, dp.ldv
     st = stream_handle()
     lat = dp.lattice.c_struct()
@@ -222,7 +257,7 @@ def update_basis(pack, image, new_beta: float | None = None, cut_edges=None, met
     lam = torch.empty(m, dtype=torch.float64, device="cuda")
     order = torch.empty(m, dtype=torch.int64, device="cuda")
     if method == "rayleigh":  # cut edges, no rotation
-        ws = _stencil_ws(m)
+        ws = _stencil_ws(dp.lattice, m)
         _lib.call("swb_stencil_rayleigh", C.byref(lat), ptr(dp.V), ldv, 0, 0, n, m, ptr(g_new.what),
                   ptr(g_new.diag), ptr(g_new.d_sqrt_dev), ptr(quad), ptr(norm2), ptr(vtd), ptr(ws),
                   ws.numel(), st)
@@ -234,21 +269,26 @@ def update_basis(pack, image, new_beta: float | None = None, cut_edges=None, met
                             vtg=gather_vector(vtd, col_map) / g_new.dnorm, col_map=col_map, mr=dp.mr)
     else:
         W = torch.empty((n, ldv), dtype=torch.float64, device="cuda")   # becomes V' below
-        ws = _stencil_ws(m)
+        ws = _stencil_ws(dp.lattice, m)
+        _mark("stencil")
         _lib.call("swb_stencil_delta", C.byref(lat), ptr(dp.V), ldv, 0, 0, n, m, ptr(g_old.what),
                   ptr(g_old.diag), ptr(g_new.what), ptr(g_new.diag), ptr(g_new.d_sqrt_dev), ptr(W), ldv,
                   ptr(quad), ptr(norm2), ptr(vtd), ptr(ws), ws.numel(), st)
         ldp = round_up(m, 2)
         P = torch.empty((m, ldp), dtype=torch.float64, device="cuda")
         tws = WORKSPACE.get("gemm_tn", _lib.size("swb_gemm_tn_workspace_bytes", n, m, m))
+        _mark("project")
         _lib.call("swb_gemm_tn", ptr(dp.V), ldv, ptr(W), ldv, n, m, m, 1, ptr(P), ldp, ptr(tws), tws.numel(), st)
         Cm = torch.empty((m, ldp), dtype=torch.float64, device="cuda")
+        _mark("coeffs")
         _lib.call("swb_update_coeffs", 1, ptr(P), ldp, ptr(dp.values_dev), ptr(quad), ptr(norm2), m,
                   float(gap_guard), ptr(Cm), ldp, ptr(lam), ptr(order), st)
         Vn = W  # W is dead after the projection: the rotation writes V' into its buffer
         if ldv > m:
             Vn[:, m:].zero_()
+        _mark("rotate")
         _lib.call("swb_gemm_nn", ptr(dp.V), ldv, ptr(Cm), ldp, n, m, m, ptr(Vn), ldv, 0, st)
+        _mark("update_tail")
         # V'^T d = C^T (V^T d): a 1-row NN product
         vtd_row = torch.zeros((1, ldp), dtype=torch.float64, device="cuda")
         vtd_row[0, :m].copy_(vtd)
@@ -259,9 +299,10 @@ def update_basis(pack, image, new_beta: float | None = None, cut_edges=None, met
         out.C = Cm
         if keep_P:
             out.P = P
-    out.base = pack
+    out.base = pack if method == "rayleigh" else None   # an updated pack owns new memory: no strong ref
     out.new_beta = beta
     out.order_dev = order
+    _mark("update_end")
     return out
 
 
@@ -355,6 +396,7 @@ def solve_fast(pack, lap, prob, m_use: int | None = None, streaming_block: int |
         raise InvalidParam(f"at most {MAX_SEEDS} seeds supported, got {s}")
     gamma = float(prob.gamma)
     st = stream_handle()
+    _mark("solve_seeds")
     sidx = torch.from_numpy(np.ascontiguousarray(seeds.seed_indices, dtype=np.int64)).to("cuda")
     slab = torch.from_numpy(np.ascontiguousarray(seeds.seed_labels, dtype=np.int32)).to("cuda")
     labels = torch.empty(n, dtype=torch.int32, device="cuda")
@@ -415,6 +457,7 @@ def solve_fast(pack, lap, prob, m_use: int | None = None, streaming_block: int |
     coeff = torch.empty((m_use, k), dtype=torch.float64, device="cuda")
     extra = torch.empty(k, dtype=torch.float64, device="cuda") if gamma == 0 else None
     rcond = torch.empty(1, dtype=torch.float64, device="cuda")
+    _mark("solve_system")
     sws = WORKSPACE.get("small_solve", _lib.size("swb_small_solve_workspace_bytes", s, m_use, k))
     _lib.call("swb_small_solve", gamma, s, m_use, k, ptr(q_s), ptr(b_qn), ldq, ptr(bg), ptr(lsu), ptr(dsq_s),
               dp.dnorm, ptr(slab), ptr(values), ptr(vtg), ptr(t_p), ldt, ptr(coeff), ptr(extra), ptr(rcond),
@@ -434,7 +477,9 @@ def solve_fast(pack, lap, prob, m_use: int | None = None, streaming_block: int |
                   stream_handle())
         return U
 
+    _mark("solve_reconstruct")
     U = reconstruct(want_field or k > 8)
+    _mark("solve_end")
     if check:
         rc = float(rcond.item())
         if _lib.load().swb_check_rcond(rc) != 0:

@@ -5,9 +5,13 @@
 namespace {
 thread_local cudaError_t g_last = cudaSuccess;
 std::atomic<int> g_sms{0};
+std::atomic<unsigned long long> g_launches{0};
 }  // namespace
 
 void swb_set_last_cuda(cudaError_t e) { g_last = e; }
+void swb_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+extern "C" unsigned long long swb_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int swb_sm_count() {
   int v = g_sms.load(std::memory_order_relaxed);

@@ -204,49 +204,60 @@ gemm_nn_kernel(const double* __restrict__ A, int64_t lda, const double* __restri
 }
 
 // ---------------------------------------------------------------------------
-// TN kernel: one CTA = (tile, row chunk); partial tile -> workspace
+// TN kernel: balanced persistent split-K.  The work is n_tiles x nk units
+// (one unit = one BK-row k-step of one output tile); CTA c takes the
+// contiguous unit range [c*upc, (c+1)*upc), which spans at most a few tiles,
+// and writes one partial tile per tile it touched.  Every CTA does the same
+// amount of DMMA work, so one wave of (SMs x occupancy) CTAs finishes
+// together; CTAs at the same position of consecutive tiles read the same
+// rows of X / Y at the same time (L2 reuse).
 // ---------------------------------------------------------------------------
 template <int WARPS_M, int WARPS_N, int WTM, int WTN, int STAGES>
 __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32)
 gemm_tn_kernel(const double* __restrict__ X, int64_t ldx, const double* __restrict__ Y,
                int64_t ldy, int64_t rows, int64_t M1, int64_t M2, int tn, int symmetric,
-               int n_tiles, int64_t chunk_rows, double* __restrict__ partial) {
+               int64_t nk, int64_t total_units, int64_t upc, int max_slots, double* __restrict__ partial) {
   using Cf = Cfg<WARPS_M, WARPS_N, WTM, WTN, STAGES, true>;
   extern __shared__ __align__(16) double smem[];
-  const int t = blockIdx.x;
-  const int chunk = blockIdx.y;
-  const int2 tt = decode_tile(t, tn, symmetric);
-  const int64_t m0 = int64_t(tt.x) * Cf::BM, n0 = int64_t(tt.y) * Cf::BN;
-  const int64_t k_begin = int64_t(chunk) * chunk_rows;
-  const int64_t k_end = min(rows, k_begin + chunk_rows);
-
-  double acc[WTM][WTN][2];
-#pragma unroll
-  for (int i = 0; i < WTM; ++i)
-#pragma unroll
-    for (int j = 0; j < WTN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-  if (k_begin < k_end)
-    mainloop<WARPS_M, WARPS_N, WTM, WTN, STAGES, true>(acc, smem, X, ldx, Y, ldy, k_begin, k_end,
-                                                       m0, M1, n0, M2);
-
+  const int64_t c = blockIdx.x;
+  int64_t u = c * upc;
+  const int64_t u_end = min(total_units, u + upc);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm = warp / WARPS_N, wn = warp % WARPS_N;
-  double* dst = partial + (int64_t(chunk) * n_tiles + t) * (Cf::BM * Cf::BN);
+  int slot = 0;
+  while (u < u_end) {
+    const int t = static_cast<int>(u / nk);
+    const int64_t ks = u % nk;
+    const int64_t ke = min(nk, ks + (u_end - u));
+    const int2 tt = decode_tile(t, tn, symmetric);
+    const int64_t m0 = int64_t(tt.x) * Cf::BM, n0 = int64_t(tt.y) * Cf::BN;
+    double acc[WTM][WTN][2];
 #pragma unroll
-  for (int i = 0; i < WTM; ++i) {
-    int r = wm * WTM * 8 + i * 8 + (lane >> 2);
+    for (int i = 0; i < WTM; ++i)
 #pragma unroll
-    for (int j = 0; j < WTN; ++j) {
-      int c = wn * WTN * 8 + j * 8 + 2 * (lane & 3);
-      *reinterpret_cast<double2*>(dst + r * Cf::BN + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+      for (int j = 0; j < WTN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    mainloop<WARPS_M, WARPS_N, WTM, WTN, STAGES, true>(acc, smem, X, ldx, Y, ldy, ks * BK,
+                                                       min(rows, ke * BK), m0, M1, n0, M2);
+    double* dst = partial + (c * max_slots + slot) * (Cf::BM * Cf::BN);
+#pragma unroll
+    for (int i = 0; i < WTM; ++i) {
+      int r = wm * WTM * 8 + i * 8 + (lane >> 2);
+#pragma unroll
+      for (int j = 0; j < WTN; ++j) {
+        int cc = wn * WTN * 8 + j * 8 + 2 * (lane & 3);
+        *reinterpret_cast<double2*>(dst + r * Cf::BN + cc) = make_double2(acc[i][j][0], acc[i][j][1]);
+      }
     }
+    __syncthreads();  // smem stages are reused by the next segment
+    u += ke - ks;
+    ++slot;
   }
 }
 
+// out[i, j] = sum over the CTAs that touched the tile, in CTA order
 template <int BM, int BN>
 __global__ void tn_reduce_kernel(const double* __restrict__ partial, int tn, int symmetric,
-                                 int n_tiles, int n_chunks, int64_t M1, int64_t M2,
+                                 int n_tiles, int64_t nk, int64_t upc, int max_slots, int64_t M1, int64_t M2,
                                  double* __restrict__ out, int64_t ldo) {
   const int64_t total = int64_t(n_tiles) * BM * BN;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
@@ -258,8 +269,12 @@ __global__ void tn_reduce_kernel(const double* __restrict__ partial, int tn, int
     const int64_t j = int64_t(tt.y) * BN + rc % BN;
     if (i >= M1 || j >= M2) continue;
     if (symmetric && j < i) continue;  // diagonal tiles: keep the upper half
+    const int64_t c_lo = (int64_t(t) * nk) / upc, c_hi = ((int64_t(t) + 1) * nk - 1) / upc;
     double s = 0.0;
-    for (int c = 0; c < n_chunks; ++c) s += partial[(int64_t(c) * n_tiles + t) * (BM * BN) + rc];
+    for (int64_t c = c_lo; c <= c_hi; ++c) {
+      const int64_t first_tile = (c * upc) / nk;
+      s += partial[(c * max_slots + (t - first_tile)) * (BM * BN) + rc];
+    }
     out[i * ldo + j] = s;
     if (symmetric && j != i) out[j * ldo + i] = s;
   }
@@ -290,31 +305,26 @@ int launch_nn(const double* A, int64_t lda, const double* B, int64_t ldb, int64_
   return SWB_OK;
 }
 
-// TN plan: tile list + chunking
+// TN plan: tiles x k-steps split evenly over one wave of CTAs
 struct TnPlan {
-  int bm, bn, n_tiles, n_chunks, tn;
-  int64_t chunk_rows;
+  int n_tiles, tn, n_ctas, max_slots;
+  int64_t nk, total_units, upc;
 };
 
 template <int BM, int BN>
-TnPlan plan_tn(int64_t rows, int64_t M1, int64_t M2, int symmetric, int ctas_per_sm) {
+TnPlan plan_tn(int64_t rows, int64_t M1, int64_t M2, int symmetric, int slots) {
   TnPlan p{};
-  p.bm = BM; p.bn = BN;
   const int tm = static_cast<int>((M1 + BM - 1) / BM), tn = static_cast<int>((M2 + BN - 1) / BN);
-  static_assert(BM == BN || BN < BM, "tile shapes");
-  const int n = symmetric ? tm * (tm + 1) / 2 : tm * tn;  // symmetric => BM == BN, tm == tn
-  p.n_tiles = n;
+  p.n_tiles = symmetric ? tm * (tm + 1) / 2 : tm * tn;  // symmetric => BM == BN, tm == tn
   p.tn = tn;
-  const int64_t target = int64_t(swb_sm_count()) * ctas_per_sm;
-  int64_t chunks = (target + n - 1) / n;
-  const int64_t max_chunks = (rows + 511) / 512;  // >= 512 rows per chunk
-  if (chunks > max_chunks) chunks = max_chunks;
-  if (chunks < 1) chunks = 1;
-  int64_t cr = (rows + chunks - 1) / chunks;
-  cr = (cr + BK - 1) / BK * BK;
-  p.chunk_rows = cr > 0 ? cr : BK;
-  p.n_chunks = static_cast<int>((rows + p.chunk_rows - 1) / p.chunk_rows);
-  if (p.n_chunks < 1) p.n_chunks = 1;
+  p.nk = std::max<int64_t>(1, (rows + BK - 1) / BK);
+  p.total_units = p.nk * p.n_tiles;
+  int64_t ctas = std::max(1, slots);
+  const int64_t min_units = 32;  // >= 512 rows per CTA
+  if (ctas > p.total_units / min_units) ctas = std::max<int64_t>(1, p.total_units / min_units);
+  p.upc = (p.total_units + ctas - 1) / ctas;
+  p.n_ctas = static_cast<int>((p.total_units + p.upc - 1) / p.upc);
+  p.max_slots = static_cast<int>((p.upc + p.nk - 1) / p.nk) + 1;
   return p;
 }
 
@@ -333,27 +343,30 @@ int run_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t r
            int64_t M2, int symmetric, double* out, int64_t ldo, void* ws, size_t ws_bytes,
            cudaStream_t st, bool size_only, size_t* need) {
   using Cf = Cfg<WARPS_M, WARPS_N, WTM, WTN, TN_STAGES, true>;
-  TnPlan p = plan_tn<Cf::BM, Cf::BN>(rows, M1, M2, symmetric, 2);
-  const size_t part_bytes = sizeof(double) * size_t(p.n_chunks) * p.n_tiles * Cf::BM * Cf::BN;
+  auto kern = gemm_tn_kernel<WARPS_M, WARPS_N, WTM, WTN, TN_STAGES>;
+  static int occ = 0;
+  if (occ == 0 && !size_only) {
+    SWB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(Cf::SMEM)));
+    SWB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cf::THREADS, Cf::SMEM));
+    if (occ < 1) occ = 1;
+  }
+  // size queries may run before any device call: bound the occupancy by 8
+  // (the partial workspace grows with the CTA count)
+  const int occ_used = occ > 0 ? occ : 8;
+  TnPlan p = plan_tn<Cf::BM, Cf::BN>(rows, M1, M2, symmetric, swb_sm_count() * occ_used);
+  const size_t part_bytes = sizeof(double) * size_t(p.n_ctas) * p.max_slots * Cf::BM * Cf::BN;
   *need = part_bytes;
   if (size_only) return SWB_OK;
   if (ws_bytes < *need || ws == nullptr) return SWB_WORKSPACE_TOO_SMALL;
   double* partial = reinterpret_cast<double*>(ws);
-  auto kern = gemm_tn_kernel<WARPS_M, WARPS_N, WTM, WTN, TN_STAGES>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    SWB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(Cf::SMEM)));
-    attr_done = true;
-  }
-  dim3 grid(p.n_tiles, p.n_chunks);
-  kern<<<grid, Cf::THREADS, Cf::SMEM, st>>>(X, ldx, Y, ldy, rows, M1, M2, p.tn, symmetric, p.n_tiles,
-                                            p.chunk_rows, partial);
+  kern<<<p.n_ctas, Cf::THREADS, Cf::SMEM, st>>>(X, ldx, Y, ldy, rows, M1, M2, p.tn, symmetric, p.nk,
+                                                p.total_units, p.upc, p.max_slots, partial);
   SWB_CHECK_LAUNCH();
   const int64_t total = int64_t(p.n_tiles) * Cf::BM * Cf::BN;
   int rb = static_cast<int>(std::min<int64_t>((total + 255) / 256, int64_t(swb_sm_count()) * 8));
-  tn_reduce_kernel<Cf::BM, Cf::BN><<<rb, 256, 0, st>>>(partial, p.tn, symmetric, p.n_tiles, p.n_chunks,
-                                                       M1, M2, out, ldo);
+  tn_reduce_kernel<Cf::BM, Cf::BN><<<rb, 256, 0, st>>>(partial, p.tn, symmetric, p.n_tiles, p.nk, p.upc,
+                                                       p.max_slots, M1, M2, out, ldo);
   SWB_CHECK_LAUNCH();
   return SWB_OK;
 }
@@ -430,4 +443,34 @@ extern "C" int swb_gemm_nn(const double* A, int64_t lda, const double* B, int64_
                            int64_t K, int64_t M2, double* out, int64_t ldo, int accumulate,
                            void* stream) {
   return swb_gemm_nn_alpha(A, lda, B, ldb, rows, K, M2, out, ldo, accumulate, 1.0, swb_stream(stream));
+}
+
+// ---------------------------------------------------------------------------
+// FP64 tensor-core peak probe (measurement only): back-to-back independent
+// DMMA.8x8x4 on every SM; bench.py times it to get the live FP64 roofline.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void __launch_bounds__(256) dmma_probe_kernel(double* out, int iters) {
+  double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dmma_8x8x4(c[i][0], c[i][1], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.0) out[0] = s;
+}
+}  // namespace
+
+extern "C" int swb_fp64_peak_probe(int iters, double* sink, double* flops_out, void* stream) {
+  if (iters <= 0 || !sink || !flops_out) return SWB_INVALID_PARAM;
+  const int blocks = swb_sm_count() * 2;
+  dmma_probe_kernel<<<blocks, 256, 0, swb_stream(stream)>>>(sink, iters);
+  SWB_CHECK_LAUNCH();
+  *flops_out = 2.0 * 256.0 * 8.0 * double(iters) * double(blocks) * 8.0;  // 8 warps per block
+  return SWB_OK;
 }

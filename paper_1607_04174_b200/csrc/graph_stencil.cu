@@ -144,80 +144,187 @@ __global__ void normalize_kernel(const StencilGeom g, double* __restrict__ w, co
 // --- stencil passes --------------------------------------------------------
 
 constexpr int ST_WARPS = 8;
-constexpr int ST_CTAS_PER_SM = 4;
+constexpr int ST_CTAS_PER_SM = 2;
 
-// One warp: column block cb (32 columns, lane = column), one x-line.
-// Accumulates per-column partials in registers; flushes them into
-// slots[warp][col][3] whenever the warp moves to another column block.
-template <bool DELTA>
-__global__ void __launch_bounds__(ST_WARPS * 32)
+// Compile-time neighbour tables, sorted by flat offset (the reference CSR
+// column order): kind 0 = diagonal, 1 = forward edge `dir` of this voxel,
+// 2 = backward edge `dir` (stored at the neighbour).
+struct NbC { int dx, dy, dz, dir, kind; };
+
+__host__ __device__ constexpr int nb_count(int conn) { return conn == 4 ? 5 : (conn == 8 ? 9 : 7); }
+__host__ __device__ constexpr int nb_ndir(int conn) { return conn == 4 ? 2 : (conn == 8 ? 4 : 3); }
+__host__ __device__ constexpr NbC nb_entry(int conn, int i) {
+  // 4-conn: -y -x diag +x +y        dirs {+x, +y}
+  // 8-conn: (-1,-1) -y (+1,-1) -x diag +x (-1,+1) +y (+1,+1)
+  //         dirs {+x, +y, (+1,+1), (-1,+1)}
+  // 6-conn: -z -y -x diag +x +y +z  dirs {+x, +y, +z}
+  return conn == 4
+             ? (i == 0 ? NbC{0, -1, 0, 1, 2} : i == 1 ? NbC{-1, 0, 0, 0, 2} : i == 2 ? NbC{0, 0, 0, -1, 0}
+                : i == 3 ? NbC{1, 0, 0, 0, 1} : NbC{0, 1, 0, 1, 1})
+         : conn == 8
+             ? (i == 0 ? NbC{-1, -1, 0, 2, 2} : i == 1 ? NbC{0, -1, 0, 1, 2} : i == 2 ? NbC{1, -1, 0, 3, 2}
+                : i == 3 ? NbC{-1, 0, 0, 0, 2} : i == 4 ? NbC{0, 0, 0, -1, 0} : i == 5 ? NbC{1, 0, 0, 0, 1}
+                : i == 6 ? NbC{-1, 1, 0, 3, 1} : i == 7 ? NbC{0, 1, 0, 1, 1} : NbC{1, 1, 0, 2, 1})
+             : (i == 0 ? NbC{0, 0, -1, 2, 2} : i == 1 ? NbC{0, -1, 0, 1, 2} : i == 2 ? NbC{-1, 0, 0, 0, 2}
+                : i == 3 ? NbC{0, 0, 0, -1, 0} : i == 4 ? NbC{1, 0, 0, 0, 1} : i == 5 ? NbC{0, 1, 0, 1, 1}
+                : NbC{0, 0, 1, 2, 1});
+}
+
+// One warp: one x-line (nx consecutive voxel rows) of one 64-column block
+// (lane = 2 adjacent columns, 16-byte loads).  Per line the warp sets up one
+// row pointer per stencil entry (off-grid lines point at the centre row with
+// a zero coefficient) and then walks x with pointer increments only; the
+// first / last voxel of a line clamp their +-x neighbours.  Per-column
+// partial sums live in registers and are flushed to slots[warp][col][3]
+// whenever the warp moves to another column block.
+// Coefficient element of the stencil pass: the new L^ entry, or for the
+// difference pass the (new, old) pair interleaved by pair_coeffs_kernel so
+// one 16-byte load serves both.
+template <bool DELTA> struct CoefT { using T = double; };
+template <> struct CoefT<true> { using T = double2; };
+
+__device__ __forceinline__ void coef_split(double c, double& n, double& o) { n = c; o = 0.0; }
+__device__ __forceinline__ void coef_split(double2 c, double& n, double& o) { n = c.x; o = c.y; }
+
+// Row kernel.  vp[e] / cp[e] point at the current row's entry-e neighbour
+// row of V / coefficient; the caller advances them by ldv / stride per row.
+// EDGE rows (x = 0, nx-1) drop their off-grid +-x entries.
+template <int CONN, bool DELTA, bool EDGE>
+__device__ __forceinline__ void stencil_row(const double* (&vp)[nb_count(CONN)],
+                                            const typename CoefT<DELTA>::T* (&cp)[nb_count(CONN)], int64_t x,
+                                            int64_t nx, const double* __restrict__ dsq, double* __restrict__ wrow,
+                                            bool active, double2& q, double2& s2, double2& sd) {
+  constexpr int R = nb_count(CONN);
+  double2 v[R];
+  double cn[R], co[R];
+#pragma unroll
+  for (int e = 0; e < R; ++e) {
+    const NbC t = nb_entry(CONN, e);
+    const bool x_ok = !EDGE || t.dx == 0 || ((x + t.dx >= 0) && (x + t.dx < nx));
+    if (x_ok) {
+      v[e] = *reinterpret_cast<const double2*>(vp[e]);
+      coef_split(*cp[e], cn[e], co[e]);
+    } else {
+      v[e] = make_double2(0.0, 0.0);
+      cn[e] = 0.0;
+      co[e] = 0.0;
+    }
+  }
+  const double d = *dsq;
+  double2 c = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int e = 0; e < R; ++e)
+    if (nb_entry(CONN, e).kind == 0) c = v[e];
+  double lx = 0.0, ly = 0.0, dx = 0.0, dy = 0.0;
+#pragma unroll
+  for (int e = 0; e < R; ++e) {
+    if (nb_entry(CONN, e).kind == 0) {
+      lx = __dadd_rn(lx, __dmul_rn(cn[e], c.x));
+      ly = __dadd_rn(ly, __dmul_rn(cn[e], c.y));
+      if (DELTA) {
+        const double gg = cn[e] - co[e];
+        dx = fma(gg, c.x, dx);
+        dy = fma(gg, c.y, dy);
+      }
+    } else {
+      lx = __dadd_rn(lx, __dmul_rn(-cn[e], v[e].x));
+      ly = __dadd_rn(ly, __dmul_rn(-cn[e], v[e].y));
+      if (DELTA) {
+        const double gg = co[e] - cn[e];
+        dx = fma(gg, v[e].x, dx);
+        dy = fma(gg, v[e].y, dy);
+      }
+    }
+  }
+  if (active) {
+    q.x = fma(c.x, lx, q.x);
+    q.y = fma(c.y, ly, q.y);
+    s2.x = fma(c.x, c.x, s2.x);
+    s2.y = fma(c.y, c.y, s2.y);
+    sd.x = fma(c.x, d, sd.x);
+    sd.y = fma(c.y, d, sd.y);
+    if (DELTA) *reinterpret_cast<double2*>(wrow) = make_double2(dx, dy);
+  }
+}
+
+// (new, old) pairs: pw[r*ND + d] = {what_new, what_old}, pd[r] = {diag_new, diag_old}
+__global__ void pair_coeffs_kernel(const double* __restrict__ wn, const double* __restrict__ wo,
+                                   const double* __restrict__ dn, const double* __restrict__ dold, int64_t nw,
+                                   int64_t nd, double2* __restrict__ pw, double2* __restrict__ pd) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nw + nd; i += int64_t(gridDim.x) * blockDim.x) {
+    if (i < nw) pw[i] = make_double2(wn[i], wo[i]);
+    else pd[i - nw] = make_double2(dn[i - nw], dold[i - nw]);
+  }
+}
+
+template <int CONN, bool DELTA>
+__global__ void __launch_bounds__(ST_WARPS * 32, ST_CTAS_PER_SM)
 stencil_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, int64_t row_base, int64_t line_begin,
-               int64_t n_lines, int64_t M, int n_cb,
-               const double* __restrict__ what_new, const double* __restrict__ diag_new,
-               const double* __restrict__ what_old, const double* __restrict__ diag_old,
-               const double* __restrict__ d_sqrt, double* __restrict__ W, int64_t ldw,
-               int64_t w_row0, double* __restrict__ slots, int64_t slot_ld) {
+               int64_t n_lines, int64_t M, int n_cb, const typename CoefT<DELTA>::T* __restrict__ cwhat,
+               const typename CoefT<DELTA>::T* __restrict__ cdiag, const typename CoefT<DELTA>::T* __restrict__ czero,
+               const double* __restrict__ d_sqrt, double* __restrict__ W, int64_t ldw, int64_t w_row0,
+               double* __restrict__ slots, int64_t slot_ld) {
+  using T = typename CoefT<DELTA>::T;
+  constexpr int R = nb_count(CONN);
+  constexpr int ND = nb_ndir(CONN);
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   const int64_t n_items = int64_t(n_cb) * n_lines;
-  const int64_t nx = g.lat.nx;
-  const int nd = g.lat.ndir;
-  const int nn = g.nbr.n;
+  const int64_t nx = g.lat.nx, ny = g.lat.ny, nz = g.lat.nz;
 
-  double q = 0.0, s2 = 0.0, sd = 0.0;
+  double2 q = make_double2(0.0, 0.0), s2 = q, sd = q;
   int cur_cb = -1;
+  auto flush = [&](int cb) {
+    double* sl = slots + gwarp * slot_ld * 3 + (int64_t(cb) * 64 + 2 * lane) * 3;
+    sl[0] = q.x; sl[1] = s2.x; sl[2] = sd.x;
+    sl[3] = q.y; sl[4] = s2.y; sl[5] = sd.y;
+  };
   for (int64_t it = gwarp; it < n_items; it += n_warps) {
     const int cb = static_cast<int>(it / n_lines);
     const int64_t line = line_begin + it % n_lines;
     if (cb != cur_cb) {
-      if (cur_cb >= 0) {
-        double* sl = slots + gwarp * slot_ld * 3 + int64_t(cur_cb * 32 + lane) * 3;
-        sl[0] = q; sl[1] = s2; sl[2] = sd;
-      }
-      q = s2 = sd = 0.0;
+      if (cur_cb >= 0) flush(cur_cb);
+      q = make_double2(0.0, 0.0); s2 = q; sd = q;
       cur_cb = cb;
     }
-    const int64_t col = int64_t(cb) * 32 + lane;
-    const bool active = col < M;
+    const int64_t col_raw = int64_t(cb) * 64 + 2 * lane;
+    const bool active = col_raw < M;
+    const int64_t col = active ? col_raw : 0;  // idle lanes read column 0, never store
     const int64_t r0 = line * nx;
-    const int64_t yz = line;  // y + ny*z
-    const int64_t y = yz % g.lat.ny, z = yz / g.lat.ny;
-#pragma unroll 2
-    for (int64_t xi = 0; xi < nx; ++xi) {
-      const int64_t r = r0 + xi;
-      const double* vrow = V + (r - row_base) * ldv;
-      const double c = active ? vrow[col] : 0.0;
-      double lv = 0.0, dw = 0.0;
-      for (int e = 0; e < nn; ++e) {
-        const int kind = g.nbr.kind[e];
-        if (kind == 0) {
-          const double dn = diag_new[r];
-          lv = __dadd_rn(lv, __dmul_rn(dn, c));
-          if (DELTA) dw += (dn - diag_old[r]) * c;
-          continue;
-        }
-        const int64_t x2 = xi + g.nbr.dx[e], y2 = y + g.nbr.dy[e], z2 = z + g.nbr.dz[e];
-        if (!in_grid(g.lat, x2, y2, z2)) continue;
-        const int d = g.nbr.dir[e];
-        const int64_t cidx = (kind == 1 ? r : r + g.nbr.off[e]) * nd + d;
-        const double an = what_new[cidx];
-        const double ao = DELTA ? what_old[cidx] : 0.0;
-        if (an == 0.0 && ao == 0.0) continue;
-        const double vn = active ? V[(r + g.nbr.off[e] - row_base) * ldv + col] : 0.0;
-        lv = __dadd_rn(lv, __dmul_rn(-an, vn));
-        if (DELTA) dw -= (an - ao) * vn;
-      }
-      q += c * lv;
-      s2 += c * c;
-      sd += c * d_sqrt[r];
-      if (DELTA && active) W[(r - w_row0) * ldw + col] = dw;
+    const int64_t y = line % ny, z = line / ny;
+    const double* vp[R];
+    const T* cp[R];
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      const NbC t = nb_entry(CONN, e);
+      const bool line_ok = (y + t.dy >= 0) && (y + t.dy < ny) && (z + t.dz >= 0) && (z + t.dz < nz);
+      const int64_t lo = line_ok ? nx * (t.dy + ny * int64_t(t.dz)) + t.dx : 0;  // row offset of the entry
+      vp[e] = V + (r0 + lo - row_base) * ldv + col;
+      if (t.kind == 0) cp[e] = cdiag + r0;
+      else if (t.kind == 1) cp[e] = cwhat + r0 * ND + t.dir;        // forward entries are 0 off-grid
+      else cp[e] = line_ok ? cwhat + (r0 + lo) * ND + t.dir : czero;  // backward entry of an off-grid line
     }
+    const double* dsq = d_sqrt + r0;
+    double* wrow = DELTA ? W + (r0 - w_row0) * ldw + col : nullptr;
+    auto advance = [&]() {
+#pragma unroll
+      for (int e = 0; e < R; ++e) {
+        vp[e] += ldv;
+        cp[e] += nb_entry(CONN, e).kind == 0 ? 1 : ND;
+      }
+      ++dsq;
+      if (DELTA) wrow += ldw;
+    };
+    stencil_row<CONN, DELTA, true>(vp, cp, 0, nx, dsq, wrow, active, q, s2, sd);
+    advance();
+    for (int64_t x = 1; x < nx - 1; ++x) {
+      stencil_row<CONN, DELTA, false>(vp, cp, x, nx, dsq, wrow, active, q, s2, sd);
+      advance();
+    }
+    if (nx > 1) stencil_row<CONN, DELTA, true>(vp, cp, nx - 1, nx, dsq, wrow, active, q, s2, sd);
   }
-  if (cur_cb >= 0) {
-    double* sl = slots + gwarp * slot_ld * 3 + int64_t(cur_cb * 32 + lane) * 3;
-    sl[0] = q; sl[1] = s2; sl[2] = sd;
-  }
+  if (cur_cb >= 0) flush(cur_cb);
 }
 
 // out[col] = sum over warps (fixed order) of slots[w][col][k]
@@ -243,12 +350,29 @@ __global__ void slot_reduce_kernel(const double* __restrict__ slots, int64_t slo
 
 int64_t stencil_grid() { return int64_t(swb_sm_count()) * ST_CTAS_PER_SM; }
 
+// workspace layout: slots | zeros (nx*ND + 1 coefficient elements) | pairs (DELTA)
+struct StencilWs {
+  size_t slots, zeros, pairs, total;
+};
+
+StencilWs stencil_ws_layout(const LatticeDev& L, int64_t M) {
+  StencilWs w{};
+  const int64_t n_cb = (M + 63) / 64;
+  const int64_t N = L.nx * L.ny * L.nz;
+  w.slots = swb_align_up(sizeof(double) * size_t(stencil_grid() * ST_WARPS) * size_t(n_cb * 64) * 3, 256);
+  w.zeros = swb_align_up(sizeof(double2) * size_t(L.nx * L.ndir + 1), 256);
+  w.pairs = swb_align_up(sizeof(double2) * size_t(N * (L.ndir + 1)), 256);
+  w.total = w.slots + w.zeros + w.pairs;
+  return w;
+}
+
 template <bool DELTA>
 int run_stencil(const swb_lattice* lat, const double* V, int64_t ldv, int64_t row_base,
                 int64_t r_begin, int64_t r_end, int64_t M, const double* what_new,
                 const double* diag_new, const double* what_old, const double* diag_old,
                 const double* d_sqrt, double* W, int64_t ldw, double* quad, double* norm2, double* vtd,
                 void* ws, size_t ws_bytes, void* stream) {
+  using T = typename CoefT<DELTA>::T;
   cudaStream_t st = swb_stream(stream);
   StencilGeom g;
   int rc = make_geom(lat, &g);
@@ -256,20 +380,42 @@ int run_stencil(const swb_lattice* lat, const double* V, int64_t ldv, int64_t ro
   const LatticeDev& L = g.lat;
   if (!V || M <= 0 || ldv < M || r_begin < row_base || r_end < r_begin) return SWB_INVALID_PARAM;
   if (r_begin % L.nx || r_end % L.nx) return SWB_INVALID_PARAM;  // whole x-lines
-  if (r_end > L.nx * L.ny * L.nz) return SWB_INVALID_PARAM;
-  const size_t need = swb_stencil_workspace_bytes(M);
-  if (!ws || ws_bytes < need) return SWB_WORKSPACE_TOO_SMALL;
-  const int n_cb = static_cast<int>((M + 31) / 32);
-  const int64_t slot_ld = int64_t(n_cb) * 32;
+  const int64_t N = L.nx * L.ny * L.nz;
+  if (r_end > N) return SWB_INVALID_PARAM;
+  if (ldv & 1) return SWB_INVALID_PARAM;                              // 16-byte row access
+  if ((reinterpret_cast<uintptr_t>(V) | reinterpret_cast<uintptr_t>(W)) & 15) return SWB_INVALID_PARAM;
+  if (W && (ldw & 1)) return SWB_INVALID_PARAM;
+  const StencilWs lay = stencil_ws_layout(L, M);
+  if (!ws || ws_bytes < lay.total) return SWB_WORKSPACE_TOO_SMALL;
+  const int n_cb = static_cast<int>((M + 63) / 64);
+  const int64_t slot_ld = int64_t(n_cb) * 64;
   const int64_t grid = stencil_grid();
   const int64_t n_warps = grid * ST_WARPS;
-  double* slots = static_cast<double*>(ws);
-  SWB_CUDA_TRY(cudaMemsetAsync(slots, 0, sizeof(double) * n_warps * slot_ld * 3, st));
+  char* base = static_cast<char*>(ws);
+  double* slots = reinterpret_cast<double*>(base);
+  T* zeros = reinterpret_cast<T*>(base + lay.slots);
+  SWB_CUDA_TRY(cudaMemsetAsync(slots, 0, lay.slots + lay.zeros, st));
+  const T* cwhat;
+  const T* cdiag;
+  if (DELTA) {
+    double2* pw = reinterpret_cast<double2*>(base + lay.slots + lay.zeros);
+    double2* pd = pw + N * L.ndir;
+    pair_coeffs_kernel<<<swb_sm_count() * 8, 256, 0, st>>>(what_new, what_old, diag_new, diag_old, N * L.ndir, N,
+                                                           pw, pd);
+    SWB_CHECK_LAUNCH();
+    cwhat = reinterpret_cast<const T*>(pw);
+    cdiag = reinterpret_cast<const T*>(pd);
+  } else {
+    cwhat = reinterpret_cast<const T*>(what_new);
+    cdiag = reinterpret_cast<const T*>(diag_new);
+  }
   const int64_t n_lines = (r_end - r_begin) / L.nx;
   if (n_lines > 0) {
-    stencil_kernel<DELTA><<<static_cast<unsigned>(grid), ST_WARPS * 32, 0, st>>>(
-        g, V, ldv, row_base, r_begin / L.nx, n_lines, M, n_cb, what_new, diag_new, what_old, diag_old,
-        d_sqrt, W, ldw, r_begin, slots, slot_ld);
+    auto kern = L.conn == 4 ? stencil_kernel<4, DELTA> : (L.conn == 8 ? stencil_kernel<8, DELTA>
+                                                                       : stencil_kernel<6, DELTA>);
+    kern<<<static_cast<unsigned>(grid), ST_WARPS * 32, 0, st>>>(g, V, ldv, row_base, r_begin / L.nx, n_lines, M, n_cb,
+                                                                cwhat, cdiag, zeros, d_sqrt, W, ldw, r_begin, slots,
+                                                                slot_ld);
     SWB_CHECK_LAUNCH();
   }
   dim3 rg(static_cast<unsigned>(M), 3);
@@ -345,9 +491,10 @@ extern "C" int swb_graph_build(const swb_lattice* lat, const double* intensities
   return SWB_OK;
 }
 
-extern "C" size_t swb_stencil_workspace_bytes(int64_t M) {
-  const int64_t n_cb = (M + 31) / 32;
-  return sizeof(double) * size_t(stencil_grid() * ST_WARPS) * size_t(n_cb * 32) * 3;
+extern "C" size_t swb_stencil_workspace_bytes(const swb_lattice* lat, int64_t M) {
+  LatticeDev L;
+  if (swb_make_lattice(lat, &L) || M <= 0) return 0;
+  return stencil_ws_layout(L, M).total;
 }
 
 extern "C" int swb_stencil_rayleigh(const swb_lattice* lat, const double* V, int64_t ldv,

@@ -16,11 +16,13 @@
 
 #define SWB_CHECK_LAUNCH()                                   \
   do {                                                       \
+    swb_count_launch();                                      \
     cudaError_t _e = cudaGetLastError();                     \
     if (_e != cudaSuccess) { swb_set_last_cuda(_e); return SWB_CUDA_ERROR; } \
   } while (0)
 
 void swb_set_last_cuda(cudaError_t e);
+void swb_count_launch();
 int swb_sm_count();
 
 static inline cudaStream_t swb_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }

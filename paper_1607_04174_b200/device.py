@@ -344,7 +344,7 @@ def column_dot(V, mr: int, x):
     quad = torch.empty(mr, dtype=torch.float64, device="cuda")
     norm2 = torch.empty_like(quad)
     out = torch.empty_like(quad)
-    ws = WORKSPACE.get("stencil", _lib.size("swb_stencil_workspace_bytes", mr))
+    ws = WORKSPACE.get("stencil", _lib.size("swb_stencil_workspace_bytes", C.byref(lat), mr))
     _lib.call("swb_stencil_rayleigh", C.byref(lat), ptr(V), V.shape[1], 0, 0, n, mr,
               ptr(z[: 2 * n]), ptr(z[2 * n:]), ptr(x), ptr(quad), ptr(norm2), ptr(out),
               ptr(ws), ws.numel(), stream_handle())
