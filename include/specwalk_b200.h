@@ -106,11 +106,15 @@ size_t swb_gemm_tn_workspace_bytes(int64_t rows, int64_t M1, int64_t M2);
 int swb_gemm_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t rows,
                 int64_t M1, int64_t M2, int symmetric, double* out, int64_t ldo,
                 void* workspace, size_t workspace_bytes, void* stream);
-/* out[rows x M2] = A[rows x K] B[K x M2] (+ beta_acc * out when
- * accumulate != 0).  A row-major (lda), B row-major (ldb), out (ldo);
+/* out[rows x M2] = A[rows x K] B[K x M2] (+ out when accumulate != 0).  A row-major (lda), B row-major (ldb), out (ldo);
  * out must not alias A. */
 int swb_gemm_nn(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows,
                 int64_t K, int64_t M2, double* out, int64_t ldo, int accumulate, void* stream);
+/* out = alpha * A B (+ out when accumulate != 0) — e.g. the prior residual
+ * update r -= V_new (V_new^T r) of adaptive.py:129. */
+int swb_gemm_nn_ex(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows,
+                   int64_t K, int64_t M2, double* out, int64_t ldo, int accumulate, double alpha,
+                   void* stream);
 
 /* ---- eigen update coefficients (refresh.py:78-79 + first-order) ------ */
 /* method 0 (rayleigh, reference refresh): lam_new = sort(max(quad/norm2,0)),
@@ -195,6 +199,19 @@ int swb_scatter_rows(const double* src, int64_t m, int64_t L, const int32_t* col
 int swb_apply_seeds(const int64_t* seed_idx, const int32_t* seed_lab, int64_t S,
                     int64_t r_begin, int64_t r_end, int64_t L, double* U, int64_t ldu,
                     int32_t* labels, double* top2, void* stream);
+
+/* ---- dynamic basis size (adaptive.py:72-185) ------------------------ */
+/* f_out[t*K + k] = seed_fit(q_s[:, :steps[t]], u_k, bound) for every
+ * scheduled prefix steps[t] <= max_step <= M and label k, where
+ * q_s[i, j] = V[s_i, col(j)] (col_map nullable) and u_k = [lab == k] d_sqrt[s].
+ * One Householder QR of q_s, then per step (in parallel) a one-sided Jacobi
+ * SVD of R[:m, :m], the 1e-13 sigma_0 cutoff and the ridge bisection. */
+size_t swb_seed_fit_workspace_bytes(int64_t S, int64_t M, int64_t K, int64_t n_steps);
+int swb_seed_fit_schedule(const double* V, int64_t ldv, const int32_t* col_map,
+                          const int64_t* seed_idx, const int32_t* seed_lab, int64_t S,
+                          const double* d_sqrt, int64_t M, int64_t K, const int32_t* steps,
+                          int64_t n_steps, int32_t max_step, double bound, double* f_out,
+                          void* workspace, size_t workspace_bytes, void* stream);
 
 /* P^_masked (fastrw.py:395-397): out[r] = priors[r] * d_sqrt[r] for rows
  * [row_begin, row_end) (out row 0 = row_begin), seed rows zeroed. */

@@ -46,6 +46,8 @@ SIGNATURES = {
     "swb_gemm_tn": (C.c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, C.c_int, c_vp, c_i64,
                               c_vp, c_sz, c_vp]),
     "swb_gemm_nn": (C.c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, C.c_int, c_vp]),
+    "swb_gemm_nn_ex": (C.c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, C.c_int, c_dbl,
+                                 c_vp]),
     "swb_update_coeffs": (C.c_int, [C.c_int, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_dbl, c_vp, c_i64,
                                     c_vp, c_vp, c_vp]),
     "swb_seed_rows": (C.c_int, [C.POINTER(Lattice), c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
@@ -67,6 +69,9 @@ SIGNATURES = {
     "swb_scatter_rows": (C.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp]),
     "swb_apply_seeds": (C.c_int, [c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp,
                                   c_vp]),
+    "swb_seed_fit_workspace_bytes": (c_sz, [c_i64, c_i64, c_i64, c_i64]),
+    "swb_seed_fit_schedule": (C.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64,
+                                        c_i32, c_dbl, c_vp, c_vp, c_sz, c_vp]),
     "swb_prior_hat": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp]),
     "swb_argmax_rows": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "swb_fp64_peak_probe": (C.c_int, [C.c_int, c_vp, C.POINTER(c_dbl), c_vp]),

@@ -502,3 +502,96 @@ def hard_labels(field) -> LabelMap:
     labels = torch.empty(n, dtype=torch.int32, device="cuda")
     _lib.call("swb_argmax_rows", ptr(U), k, n, k, ptr(labels), None, stream_handle())
     return LabelMap(field.dims, labels.cpu().numpy())
+
+
+# ---------------------------------------------------------------------------
+# dynamic basis size (adaptive.py:133-185)
+# ---------------------------------------------------------------------------
+
+def select_m(pack, prob, policy=None):
+    """Smallest scheduled m whose seed-fit and prior-residual criteria all
+    pass, else (pack.m, saturated) — adaptive.py:133-185 on the device.
+
+    Seed criterion: swb_seed_fit_schedule evaluates seed_fit for every
+    scheduled m at once (one QR, per-step Jacobi SVDs in parallel).  Prior
+    criterion: the incremental residual r <- r - V_new (V_new^T r) on the
+    DMMA GEMMs (adaptive.py:113-130).  Returns (m_use, info) with the same
+    info layout as the reference (steps up to the decision only).
+    """
+    from .types import AdaptivePolicy
+    torch = require_cuda()
+    policy = policy or AdaptivePolicy()
+    dp = _as_device(pack)
+    k = prob.K
+    n = dp.n_vertices
+    M = dp.m
+    bound = dp.dnorm  # norm_bound(NORMALIZED, d_sqrt**2) = sqrt(sum d_sqrt^2) (adaptive.py:65-69)
+    seeds = prob.seeds
+    s = int(seeds.n_seeds)
+    sched = policy.schedule(M, k)
+    st = stream_handle()
+    f_tab = None
+    if s:
+        sidx = torch.from_numpy(np.ascontiguousarray(seeds.seed_indices, dtype=np.int64)).to("cuda")
+        slab = torch.from_numpy(np.ascontiguousarray(seeds.seed_labels, dtype=np.int32)).to("cuda")
+        steps = torch.tensor(sched, dtype=torch.int32, device="cuda")
+        f_dev = torch.empty((len(sched), k), dtype=torch.float64, device="cuda")
+        ws = WORKSPACE.get("seed_fit", _lib.size("swb_seed_fit_workspace_bytes", s, M, k, len(sched)))
+        _lib.call("swb_seed_fit_schedule", ptr(dp.V), dp.ldv, ptr(dp.col_map), ptr(sidx), ptr(slab), s,
+                  ptr(dp.d_sqrt_dev), M, k, ptr(steps), len(sched), int(max(sched)), float(bound), ptr(f_dev),
+                  ptr(ws), ws.numel(), st)
+        f_tab = f_dev.cpu().numpy()
+    g_tab = None
+    if prob.priors is not None:
+        tl = policy.label_subset(k)
+        T = int(tl.size)
+        ldt = round_up(T, 2)
+        pri = prob.priors
+        if hasattr(pri, "is_cuda"):
+            pri = pri[:, torch.as_tensor(tl, device=pri.device)].contiguous()
+        else:
+            pri = torch.from_numpy(np.ascontiguousarray(np.asarray(pri, dtype=np.float64)[:, tl])).to("cuda")
+        R = torch.empty((n, ldt), dtype=torch.float64, device="cuda")
+        _lib.call("swb_prior_hat", ptr(pri), pri.stride(0), 0, n, T, ptr(dp.d_sqrt_dev), None, 0, ptr(R), ldt, st)
+        cmap = dp.col_map if dp.col_map is not None else torch.arange(M, dtype=torch.int32, device="cuda")
+        g_rows = []
+        prev = 0
+        G = torch.empty((T, ldt), dtype=torch.float64, device="cuda")
+        for m in sched:
+            dm = m - prev
+            if dm > 0:
+                ldn = round_up(dm, 2)
+                Vn = torch.zeros((n, ldn), dtype=torch.float64, device="cuda")
+                _lib.call("swb_gather_columns", ptr(dp.V), dp.ldv, n, ptr(cmap[prev:m]), dm, ptr(Vn), ldn, st)
+                coef = torch.empty((dm, ldt), dtype=torch.float64, device="cuda")
+                tws = WORKSPACE.get("gemm_tn", _lib.size("swb_gemm_tn_workspace_bytes", n, max(dm, T), T))
+                _lib.call("swb_gemm_tn", ptr(Vn), ldn, ptr(R), ldt, n, dm, T, 0, ptr(coef), ldt, ptr(tws),
+                          tws.numel(), st)
+                # r -= V_new coef
+                _lib.call("swb_gemm_nn_ex", ptr(Vn), ldn, ptr(coef), ldt, n, dm, T, ptr(R), ldt, 1, -1.0, st)
+            tws = WORKSPACE.get("gemm_tn", _lib.size("swb_gemm_tn_workspace_bytes", n, T, T))
+            _lib.call("swb_gemm_tn", ptr(R), ldt, ptr(R), ldt, n, T, T, 1, ptr(G), ldt, ptr(tws), tws.numel(), st)
+            g_rows.append(torch.diagonal(G[:, :T]).clone())
+            prev = m
+        g_tab = torch.stack(g_rows).cpu().numpy()
+    f_max = policy.seed_threshold(s) if s else None
+    g_max = policy.prior_threshold(n) if prob.priors is not None else None
+    info = {"steps": [], "saturated": False}
+    for t, m in enumerate(sched):
+        step = {"m": m, "f": [], "g": []}
+        ok = True
+        if f_tab is not None:
+            for col in range(k):
+                f = float(f_tab[t, col])
+                step["f"].append(f)
+                ok = ok and f <= f_max
+        if g_tab is not None:
+            for j in range(g_tab.shape[1]):
+                g = float(g_tab[t, j])
+                step["g"].append(g)
+                ok = ok and g <= g_max
+        info["steps"].append(step)
+        if ok:
+            return m, info
+    info["saturated"] = True
+    return M, info

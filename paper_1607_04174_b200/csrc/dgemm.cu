@@ -445,6 +445,12 @@ extern "C" int swb_gemm_nn(const double* A, int64_t lda, const double* B, int64_
   return swb_gemm_nn_alpha(A, lda, B, ldb, rows, K, M2, out, ldo, accumulate, 1.0, swb_stream(stream));
 }
 
+extern "C" int swb_gemm_nn_ex(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows,
+                              int64_t K, int64_t M2, double* out, int64_t ldo, int accumulate, double alpha,
+                              void* stream) {
+  return swb_gemm_nn_alpha(A, lda, B, ldb, rows, K, M2, out, ldo, accumulate, alpha, swb_stream(stream));
+}
+
 // ---------------------------------------------------------------------------
 // FP64 tensor-core peak probe (measurement only): back-to-back independent
 // DMMA.8x8x4 on every SM; bench.py times it to get the live FP64 roofline.
