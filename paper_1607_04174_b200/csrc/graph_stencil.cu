@@ -183,70 +183,6 @@ __host__ __device__ constexpr NbC nb_entry(int conn, int i) {
 template <bool DELTA> struct CoefT { using T = double; };
 template <> struct CoefT<true> { using T = double2; };
 
-__device__ __forceinline__ void coef_split(double c, double& n, double& o) { n = c; o = 0.0; }
-__device__ __forceinline__ void coef_split(double2 c, double& n, double& o) { n = c.x; o = c.y; }
-
-// Row kernel.  vp[e] / cp[e] point at the current row's entry-e neighbour
-// row of V / coefficient; the caller advances them by ldv / stride per row.
-// EDGE rows (x = 0, nx-1) drop their off-grid +-x entries.
-template <int CONN, bool DELTA, bool EDGE>
-__device__ __forceinline__ void stencil_row(const double* (&vp)[nb_count(CONN)],
-                                            const typename CoefT<DELTA>::T* (&cp)[nb_count(CONN)], int64_t x,
-                                            int64_t nx, const double* __restrict__ dsq, double* __restrict__ wrow,
-                                            bool active, double2& q, double2& s2, double2& sd) {
-  constexpr int R = nb_count(CONN);
-  double2 v[R];
-  double cn[R], co[R];
-#pragma unroll
-  for (int e = 0; e < R; ++e) {
-    const NbC t = nb_entry(CONN, e);
-    const bool x_ok = !EDGE || t.dx == 0 || ((x + t.dx >= 0) && (x + t.dx < nx));
-    if (x_ok) {
-      v[e] = *reinterpret_cast<const double2*>(vp[e]);
-      coef_split(*cp[e], cn[e], co[e]);
-    } else {
-      v[e] = make_double2(0.0, 0.0);
-      cn[e] = 0.0;
-      co[e] = 0.0;
-    }
-  }
-  const double d = *dsq;
-  double2 c = make_double2(0.0, 0.0);
-#pragma unroll
-  for (int e = 0; e < R; ++e)
-    if (nb_entry(CONN, e).kind == 0) c = v[e];
-  double lx = 0.0, ly = 0.0, dx = 0.0, dy = 0.0;
-#pragma unroll
-  for (int e = 0; e < R; ++e) {
-    if (nb_entry(CONN, e).kind == 0) {
-      lx = __dadd_rn(lx, __dmul_rn(cn[e], c.x));
-      ly = __dadd_rn(ly, __dmul_rn(cn[e], c.y));
-      if (DELTA) {
-        const double gg = cn[e] - co[e];
-        dx = fma(gg, c.x, dx);
-        dy = fma(gg, c.y, dy);
-      }
-    } else {
-      lx = __dadd_rn(lx, __dmul_rn(-cn[e], v[e].x));
-      ly = __dadd_rn(ly, __dmul_rn(-cn[e], v[e].y));
-      if (DELTA) {
-        const double gg = co[e] - cn[e];
-        dx = fma(gg, v[e].x, dx);
-        dy = fma(gg, v[e].y, dy);
-      }
-    }
-  }
-  if (active) {
-    q.x = fma(c.x, lx, q.x);
-    q.y = fma(c.y, ly, q.y);
-    s2.x = fma(c.x, c.x, s2.x);
-    s2.y = fma(c.y, c.y, s2.y);
-    sd.x = fma(c.x, d, sd.x);
-    sd.y = fma(c.y, d, sd.y);
-    if (DELTA) *reinterpret_cast<double2*>(wrow) = make_double2(dx, dy);
-  }
-}
-
 // (new, old) pairs: pw[r*ND + d] = {what_new, what_old}, pd[r] = {diag_new, diag_old}
 __global__ void pair_coeffs_kernel(const double* __restrict__ wn, const double* __restrict__ wo,
                                    const double* __restrict__ dn, const double* __restrict__ dold, int64_t nw,
@@ -257,74 +193,202 @@ __global__ void pair_coeffs_kernel(const double* __restrict__ wn, const double* 
   }
 }
 
+__device__ __forceinline__ void coef_split(double c, double& n, double& o) { n = c; o = 0.0; }
+__device__ __forceinline__ void coef_split(double2 c, double& n, double& o) { n = c.x; o = c.y; }
+
+// ---------------------------------------------------------------------------
+// Stencil pass v4: one warp = one x-line of one 64-column block (lane = 2
+// adjacent columns).  Rows stream through a per-warp cp.async ring of
+// RING stages, PREF rows ahead.  A stage holds, for voxel row x of the line:
+//   V rows     : centre, y-1 line, y+1 line [, z-1 line, z+1 line]  (512 B each)
+//   coefficients: centre row (ND forward + diag), y-1 line row (ND)
+//                [, z-1 line row (ND)]  ((new, old) pairs for the difference pass)
+//   d_sqrt of the centre row.
+// +-x neighbours (and the 8-connected diagonals) come from the adjacent
+// stages; every backward coefficient is the forward coefficient of the row
+// it starts from, found in the stage of that row.  Off-grid lines are
+// zero-filled by the predicated copies (coefficient 0, value 0).
+// ---------------------------------------------------------------------------
+template <int CONN, bool DELTA>
+struct StencilRing {
+  static constexpr bool D3 = CONN == 6;
+  static constexpr int ND = nb_ndir(CONN);
+  static constexpr int NV = D3 ? 5 : 3;                         // V rows per stage
+  static constexpr int NCL = D3 ? 3 : 2;                        // coefficient rows per stage
+  static constexpr int CW = DELTA ? 2 : 1;                      // doubles per coefficient
+  static constexpr int COEF = (ND + 1) + ND * (NCL - 1);        // coefficients per stage
+  static constexpr int PREF = 3;                                // rows prefetched ahead
+  static constexpr int RING = PREF + 2;
+  static constexpr int V_DBL = NV * 64;
+  static constexpr int C_DBL = ((COEF * CW + 1) + 1) / 2 * 2;   // + d_sqrt, 16-B aligned
+  static constexpr int STAGE_DBL = V_DBL + C_DBL;
+  static constexpr int WARP_DBL = RING * STAGE_DBL;
+};
+
 template <int CONN, bool DELTA>
 __global__ void __launch_bounds__(ST_WARPS * 32, ST_CTAS_PER_SM)
-stencil_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, int64_t row_base, int64_t line_begin,
-               int64_t n_lines, int64_t M, int n_cb, const typename CoefT<DELTA>::T* __restrict__ cwhat,
-               const typename CoefT<DELTA>::T* __restrict__ cdiag, const typename CoefT<DELTA>::T* __restrict__ czero,
-               const double* __restrict__ d_sqrt, double* __restrict__ W, int64_t ldw, int64_t w_row0,
-               double* __restrict__ slots, int64_t slot_ld) {
-  using T = typename CoefT<DELTA>::T;
-  constexpr int R = nb_count(CONN);
-  constexpr int ND = nb_ndir(CONN);
+stencil4_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, int64_t row_base, int64_t blk_begin,
+                int64_t blk_end, int64_t M, int n_cb, const double* __restrict__ cwhat, const double* __restrict__ cdiag,
+                const double* __restrict__ d_sqrt, double* __restrict__ W, int64_t ldw, int64_t w_row0,
+                double* __restrict__ slots, int64_t slot_ld) {
+  using Rg = StencilRing<CONN, DELTA>;
+  constexpr int ND = Rg::ND, NV = Rg::NV, CW = Rg::CW, RING = Rg::RING, PREF = Rg::PREF;
+  constexpr int SD = Rg::STAGE_DBL;
+  extern __shared__ __align__(16) double ring_all[];
   const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  double* ring = ring_all + warp * Rg::WARP_DBL;
+  double* zst = ring_all + ST_WARPS * Rg::WARP_DBL;  // shared all-zero stage for x-1 < 0 / x+1 >= nx
+  for (int i = threadIdx.x; i < SD; i += blockDim.x) zst[i] = 0.0;
+  __syncthreads();
   const int64_t gwarp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t n_warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  const int64_t n_items = int64_t(n_cb) * n_lines;
   const int64_t nx = g.lat.nx, ny = g.lat.ny, nz = g.lat.nz;
+  const int64_t plane = nx * ny;
+  const int nxi = static_cast<int>(nx);
+  // CTA item = (column block, block of 8 lines along the slowest axis, other
+  // axis): 3-D -> warp w takes z = 8*zb + w at a common y, so every warp's
+  // +-z neighbour lines are its sibling warps' lines, streamed in lockstep;
+  // consecutive CTAs take consecutive y.  2-D -> warp w takes y = 8*yb + w.
+  const bool d3 = Rg::D3;
+  const int64_t inner = d3 ? ny : 1;
+  const int64_t nblk = (blk_end - blk_begin + ST_WARPS - 1) / ST_WARPS;
+  const int64_t per_cb = nblk * inner;
+  const int64_t n_items = int64_t(n_cb) * per_cb;
 
   double2 q = make_double2(0.0, 0.0), s2 = q, sd = q;
   int cur_cb = -1;
-  auto flush = [&](int cb) {
-    double* sl = slots + gwarp * slot_ld * 3 + (int64_t(cb) * 64 + 2 * lane) * 3;
-    sl[0] = q.x; sl[1] = s2.x; sl[2] = sd.x;
-    sl[3] = q.y; sl[4] = s2.y; sl[5] = sd.y;
-  };
-  for (int64_t it = gwarp; it < n_items; it += n_warps) {
-    const int cb = static_cast<int>(it / n_lines);
-    const int64_t line = line_begin + it % n_lines;
+  for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const int cb = static_cast<int>(it / per_cb);
+    const int64_t rem = it % per_cb;
+    const int64_t slow = blk_begin + (rem / inner) * ST_WARPS + warp;  // z (3-D) or y (2-D)
+    if (slow >= blk_end) continue;
+    const int64_t line = d3 ? (slow * ny + rem % inner) : slow;
     if (cb != cur_cb) {
-      if (cur_cb >= 0) flush(cur_cb);
+      if (cur_cb >= 0) {
+        double* sl = slots + gwarp * slot_ld * 3 + (int64_t(cur_cb) * 64 + 2 * lane) * 3;
+        sl[0] = q.x; sl[1] = s2.x; sl[2] = sd.x; sl[3] = q.y; sl[4] = s2.y; sl[5] = sd.y;
+      }
       q = make_double2(0.0, 0.0); s2 = q; sd = q;
       cur_cb = cb;
     }
     const int64_t col_raw = int64_t(cb) * 64 + 2 * lane;
     const bool active = col_raw < M;
-    const int64_t col = active ? col_raw : 0;  // idle lanes read column 0, never store
+    const int64_t col = active ? col_raw : 0;
     const int64_t r0 = line * nx;
     const int64_t y = line % ny, z = line / ny;
-    const double* vp[R];
-    const T* cp[R];
+    // per-line copy sources (advanced by one row per prefetch)
+    const double* vsrc[NV];
+    bool vok[NV];
+    {
+      const int64_t off[5] = {0, -nx, nx, -plane, plane};
+      const bool okk[5] = {true, y > 0, y + 1 < ny, z > 0, z + 1 < nz};
 #pragma unroll
-    for (int e = 0; e < R; ++e) {
-      const NbC t = nb_entry(CONN, e);
-      const bool line_ok = (y + t.dy >= 0) && (y + t.dy < ny) && (z + t.dz >= 0) && (z + t.dz < nz);
-      const int64_t lo = line_ok ? nx * (t.dy + ny * int64_t(t.dz)) + t.dx : 0;  // row offset of the entry
-      vp[e] = V + (r0 + lo - row_base) * ldv + col;
-      if (t.kind == 0) cp[e] = cdiag + r0;
-      else if (t.kind == 1) cp[e] = cwhat + r0 * ND + t.dir;        // forward entries are 0 off-grid
-      else cp[e] = line_ok ? cwhat + (r0 + lo) * ND + t.dir : czero;  // backward entry of an off-grid line
-    }
-    const double* dsq = d_sqrt + r0;
-    double* wrow = DELTA ? W + (r0 - w_row0) * ldw + col : nullptr;
-    auto advance = [&]() {
-#pragma unroll
-      for (int e = 0; e < R; ++e) {
-        vp[e] += ldv;
-        cp[e] += nb_entry(CONN, e).kind == 0 ? 1 : ND;
+      for (int v = 0; v < NV; ++v) {
+        vok[v] = okk[v];
+        vsrc[v] = V + (r0 + (okk[v] ? off[v] : 0) - row_base) * ldv + col;
       }
-      ++dsq;
-      if (DELTA) wrow += ldw;
-    };
-    stencil_row<CONN, DELTA, true>(vp, cp, 0, nx, dsq, wrow, active, q, s2, sd);
-    advance();
-    for (int64_t x = 1; x < nx - 1; ++x) {
-      stencil_row<CONN, DELTA, false>(vp, cp, x, nx, dsq, wrow, active, q, s2, sd);
-      advance();
     }
-    if (nx > 1) stencil_row<CONN, DELTA, true>(vp, cp, nx - 1, nx, dsq, wrow, active, q, s2, sd);
+    // lane s < COEF + 1 copies coefficient slot s (or d_sqrt for s == COEF)
+    const double* csrc = d_sqrt + r0;
+    int64_t cstride = 1;
+    bool cok = lane <= Rg::COEF;
+    int cbytes = 8;
+    if (lane < ND) {
+      csrc = cwhat + (r0 * ND + lane) * CW; cstride = ND * CW; cbytes = 8 * CW;
+    } else if (lane == ND) {
+      csrc = cdiag + r0 * CW; cstride = CW; cbytes = 8 * CW;
+    } else if (lane < 2 * ND + 1) {
+      const bool ok = y > 0;
+      csrc = cwhat + ((r0 - (ok ? nx : 0)) * ND + (lane - ND - 1)) * CW; cstride = ND * CW; cbytes = 8 * CW;
+      cok = ok;
+    } else if (lane < Rg::COEF) {
+      const bool ok = z > 0;
+      csrc = cwhat + ((r0 - (ok ? plane : 0)) * ND + (lane - 2 * ND - 1)) * CW; cstride = ND * CW; cbytes = 8 * CW;
+      cok = ok;
+    }
+    const bool c_issue = lane <= Rg::COEF;
+    const int cslot = lane < Rg::COEF ? lane * CW : Rg::COEF * CW;
+
+    int pst = 0;  // ring stage of the next prefetched row
+    int xp = 0;   // next row to prefetch
+    auto prefetch = [&]() {
+      if (xp < nxi) {
+        double* stg = ring + pst * SD;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) cp_async16(stg + v * 64 + 2 * lane, vsrc[v], vok[v]);
+        if (c_issue) {
+          if (cbytes == 16) cp_async16(stg + Rg::V_DBL + cslot, csrc, cok);
+          else cp_async8(stg + Rg::V_DBL + cslot, csrc, cok);
+        }
+#pragma unroll
+        for (int v = 0; v < NV; ++v) vsrc[v] += ldv;
+        csrc += cstride;
+        ++xp;
+        pst = pst + 1 == RING ? 0 : pst + 1;
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int i = 0; i <= PREF; ++i) prefetch();
+
+    double* wrow = DELTA ? W + (r0 - w_row0) * ldw + col : nullptr;
+    int sc_i = 0;
+    const double* sm1 = zst;
+    for (int x = 0; x < nxi; ++x) {
+      cp_async_wait<PREF - 1>();  // rows <= x+1 have landed
+      __syncwarp();
+      const double* sc = ring + sc_i * SD;
+      const int sp_i = sc_i + 1 == RING ? 0 : sc_i + 1;
+      const double* sp1 = x + 1 < nxi ? ring + sp_i * SD : zst;
+      const double2 c = *reinterpret_cast<const double2*>(sc + 2 * lane);
+      const double d = sc[Rg::V_DBL + Rg::COEF * CW];
+      double lx = 0.0, ly = 0.0, dx = 0.0, dy = 0.0;
+#pragma unroll
+      for (int e = 0; e < nb_count(CONN); ++e) {
+        const NbC t = nb_entry(CONN, e);
+        const double* vs = t.dx < 0 ? sm1 : t.dx > 0 ? sp1 : sc;
+        const int v = t.dz < 0 ? 3 : t.dz > 0 ? 4 : t.dy < 0 ? 1 : t.dy > 0 ? 2 : 0;
+        const double2 val = *reinterpret_cast<const double2*>(vs + v * 64 + 2 * lane);
+        int slot;
+        const double* cs;
+        if (t.kind == 0) { slot = ND; cs = sc; }
+        else if (t.kind == 1) { slot = t.dir; cs = sc; }
+        else { slot = t.dz < 0 ? 2 * ND + 1 + t.dir : t.dy < 0 ? ND + 1 + t.dir : t.dir; cs = vs; }
+        const double* cp = cs + Rg::V_DBL + slot * CW;
+        const double cn = cp[0];
+        const double co = DELTA ? cp[1] : 0.0;
+        if (t.kind == 0) {
+          lx = __dadd_rn(lx, __dmul_rn(cn, val.x));
+          ly = __dadd_rn(ly, __dmul_rn(cn, val.y));
+          if (DELTA) { const double gg = cn - co; dx = fma(gg, val.x, dx); dy = fma(gg, val.y, dy); }
+        } else {
+          lx = __dadd_rn(lx, __dmul_rn(-cn, val.x));
+          ly = __dadd_rn(ly, __dmul_rn(-cn, val.y));
+          if (DELTA) { const double gg = co - cn; dx = fma(gg, val.x, dx); dy = fma(gg, val.y, dy); }
+        }
+      }
+      if (active) {
+        q.x = fma(c.x, lx, q.x);
+        q.y = fma(c.y, ly, q.y);
+        s2.x = fma(c.x, c.x, s2.x);
+        s2.y = fma(c.y, c.y, s2.y);
+        sd.x = fma(c.x, d, sd.x);
+        sd.y = fma(c.y, d, sd.y);
+        if (DELTA) *reinterpret_cast<double2*>(wrow) = make_double2(dx, dy);
+      }
+      if (DELTA) wrow += ldw;
+      __syncwarp();
+      prefetch();  // fills the stage of row x-1 (RING = PREF + 2)
+      sm1 = sc;
+      sc_i = sp_i;
+    }
+    cp_async_wait<0>();
+    __syncwarp();
   }
-  if (cur_cb >= 0) flush(cur_cb);
+  if (cur_cb >= 0) {
+    double* sl = slots + gwarp * slot_ld * 3 + (int64_t(cur_cb) * 64 + 2 * lane) * 3;
+    sl[0] = q.x; sl[1] = s2.x; sl[2] = sd.x; sl[3] = q.y; sl[4] = s2.y; sl[5] = sd.y;
+  }
 }
 
 // out[col] = sum over warps (fixed order) of slots[w][col][k]
@@ -349,6 +413,25 @@ __global__ void slot_reduce_kernel(const double* __restrict__ slots, int64_t slo
 }
 
 int64_t stencil_grid() { return int64_t(swb_sm_count()) * ST_CTAS_PER_SM; }
+
+template <int CONN, bool DELTA>
+int launch_stencil4(const StencilGeom& g, const double* V, int64_t ldv, int64_t row_base, int64_t blk_begin,
+                    int64_t blk_end, int64_t M, int n_cb, const double* cw, const double* cd, const double* d_sqrt,
+                    double* W, int64_t ldw, int64_t w_row0, double* slots, int64_t slot_ld, int64_t grid,
+                    cudaStream_t st) {
+  using Rg = StencilRing<CONN, DELTA>;
+  const size_t smem = sizeof(double) * (size_t(Rg::WARP_DBL) * ST_WARPS + Rg::STAGE_DBL);
+  auto kern = stencil4_kernel<CONN, DELTA>;
+  static bool attr = false;
+  if (!attr) {
+    SWB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr = true;
+  }
+  kern<<<static_cast<unsigned>(grid), ST_WARPS * 32, smem, st>>>(g, V, ldv, row_base, blk_begin, blk_end, M, n_cb, cw,
+                                                                 cd, d_sqrt, W, ldw, w_row0, slots, slot_ld);
+  SWB_CHECK_LAUNCH();
+  return SWB_OK;
+}
 
 // workspace layout: slots | zeros (nx*ND + 1 coefficient elements) | pairs (DELTA)
 struct StencilWs {
@@ -411,12 +494,18 @@ int run_stencil(const swb_lattice* lat, const double* V, int64_t ldv, int64_t ro
   }
   const int64_t n_lines = (r_end - r_begin) / L.nx;
   if (n_lines > 0) {
-    auto kern = L.conn == 4 ? stencil_kernel<4, DELTA> : (L.conn == 8 ? stencil_kernel<8, DELTA>
-                                                                       : stencil_kernel<6, DELTA>);
-    kern<<<static_cast<unsigned>(grid), ST_WARPS * 32, 0, st>>>(g, V, ldv, row_base, r_begin / L.nx, n_lines, M, n_cb,
-                                                                cwhat, cdiag, zeros, d_sqrt, W, ldw, r_begin, slots,
-                                                                slot_ld);
-    SWB_CHECK_LAUNCH();
+    (void)zeros;
+    const double* cw = reinterpret_cast<const double*>(cwhat);
+    const double* cd = reinterpret_cast<const double*>(cdiag);
+    int rc2 = SWB_OK;
+    // 3-D: blocks along z (whole planes); 2-D: along y (whole lines)
+    const int64_t unit = L.conn == 6 ? L.nx * L.ny : L.nx;
+    if (r_begin % unit || r_end % unit) return SWB_INVALID_PARAM;
+    const int64_t b0 = r_begin / unit, b1 = r_end / unit;
+    if (L.conn == 4) rc2 = launch_stencil4<4, DELTA>(g, V, ldv, row_base, b0, b1, M, n_cb, cw, cd, d_sqrt, W, ldw, r_begin, slots, slot_ld, grid, st);
+    else if (L.conn == 8) rc2 = launch_stencil4<8, DELTA>(g, V, ldv, row_base, b0, b1, M, n_cb, cw, cd, d_sqrt, W, ldw, r_begin, slots, slot_ld, grid, st);
+    else rc2 = launch_stencil4<6, DELTA>(g, V, ldv, row_base, b0, b1, M, n_cb, cw, cd, d_sqrt, W, ldw, r_begin, slots, slot_ld, grid, st);
+    if (rc2) return rc2;
   }
   dim3 rg(static_cast<unsigned>(M), 3);
   slot_reduce_kernel<<<rg, 256, 0, st>>>(slots, slot_ld, n_warps, M, quad, norm2, vtd);

@@ -5,6 +5,7 @@
 //   pass 2   reconstruction V*coeff (+ g c), finalize (solver.py:55-66) and
 //            hard labels (images.py:128-130) fused in one HBM-bound kernel
 #include "swb_common.cuh"
+#include "dmma_core.cuh"
 
 namespace {
 
@@ -406,6 +407,85 @@ __global__ void scatter_rows_kernel(const double* __restrict__ src, int64_t m, i
   }
 }
 
+// DMMA-fed reconstruction for L <= 8 labels: a 128-row tile of V times the
+// coefficient block (mr x L, zero-padded to 8 columns by the loader) on the
+// FP64 tensor pipe (the K=400 reduction costs 2*8*K flops per voxel, far
+// below the FP64 roof, so the kernel stays HBM-bound), 4-stage cp.async
+// stream of V, and the finalize + argmax epilogue per row in registers.
+constexpr int RD_WARPS = 8, RD_WTM = 2, RD_STAGES = 4;
+using RdCfg = swb_core::Cfg<RD_WARPS, 1, RD_WTM, 1, RD_STAGES, false>;
+
+__global__ void __launch_bounds__(RD_WARPS * 32)
+reconstruct_dmma_kernel(const double* __restrict__ V, int64_t ldv, int64_t rows, int64_t mr,
+                        const double* __restrict__ coeff, int64_t L, const double* __restrict__ extra, double dnorm,
+                        const double* __restrict__ d_sqrt, double* __restrict__ U, int64_t ldu,
+                        int32_t* __restrict__ labels, double* __restrict__ top2) {
+  extern __shared__ __align__(16) double smem[];
+  const int64_t m0 = int64_t(blockIdx.x) * RdCfg::BM;
+  double acc[RD_WTM][1][2];
+#pragma unroll
+  for (int i = 0; i < RD_WTM; ++i) acc[i][0][0] = acc[i][0][1] = 0.0;
+  swb_core::mainloop<RD_WARPS, 1, RD_WTM, 1, RD_STAGES, false>(acc, smem, V, ldv, coeff, L, 0, mr, m0, rows, 0, L);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q = lane & 3;             // this lane holds labels 2q, 2q+1 of its row
+  double ex0 = 0.0, ex1 = 0.0;
+  if (extra) {
+    if (2 * q < L) ex0 = extra[2 * q];
+    if (2 * q + 1 < L) ex1 = extra[2 * q + 1];
+  }
+#pragma unroll
+  for (int i = 0; i < RD_WTM; ++i) {
+    const int64_t r = m0 + warp * RD_WTM * 8 + i * 8 + (lane >> 2);
+    const bool row_ok = r < rows;
+    // gather the row's 8 values into the quad leader (lane & 3 == 0)
+    double v[8];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      v[2 * t] = __shfl_sync(0xffffffffu, acc[i][0][0], (lane & ~3) | t);
+      v[2 * t + 1] = __shfl_sync(0xffffffffu, acc[i][0][1], (lane & ~3) | t);
+    }
+    double e[8];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      e[2 * t] = __shfl_sync(0xffffffffu, ex0, (lane & ~3) | t);
+      e[2 * t + 1] = __shfl_sync(0xffffffffu, ex1, (lane & ~3) | t);
+    }
+    if (q != 0 || !row_ok) continue;
+    const double ds = d_sqrt[r];
+    const double g = ds / dnorm;
+    double sum = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k >= L) break;
+      double u = (v[k] + g * e[k]) / ds;                  // fastrw.py:462-464
+      u = u > 0.0 ? u : (u != u ? u : 0.0);                // np.clip(u, 0, None)
+      v[k] = u;
+      sum += u;                                            // row sum in label order
+    }
+    if (sum == 0.0) {                                      // solver.py:63-65
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = 1.0 / double(L);
+      sum = 1.0;
+    }
+    int best = 0;
+    double p1 = -1.0, p2 = -1.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k >= L) break;
+      const double p = v[k] / sum;
+      v[k] = p;
+      if (p > p1) { p2 = p1; p1 = p; best = k; } else if (p > p2) p2 = p;
+    }
+    labels[r] = best;
+    if (top2) top2[r] = L > 1 ? p1 - p2 : 1.0;
+    if (U) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < L) U[r * ldu + k] = v[k];
+    }
+  }
+}
+
 template <int L>
 int launch_reconstruct(const double* V, int64_t ldv, int64_t row_base, int64_t r_begin, int64_t r_end, int64_t mr,
                        const double* coeff, const double* extra, double dnorm, const double* d_sqrt, double* U,
@@ -588,6 +668,20 @@ extern "C" int swb_reconstruct_label(const double* V, int64_t ldv, int64_t row_b
   if (r_end == r_begin) return SWB_OK;
   cudaStream_t st = swb_stream(stream);
   const size_t smem = sizeof(double) * size_t(mr) * L;
+  if (L <= 8 && (ldv % 2) == 0 && (reinterpret_cast<uintptr_t>(V) & 15) == 0) {
+    static bool attr = false;
+    if (!attr) {
+      SWB_CUDA_TRY(cudaFuncSetAttribute(reconstruct_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(RdCfg::SMEM)));
+      attr = true;
+    }
+    const int64_t rows = r_end - r_begin;
+    const int64_t grid = (rows + RdCfg::BM - 1) / RdCfg::BM;
+    reconstruct_dmma_kernel<<<static_cast<unsigned>(grid), RdCfg::THREADS, RdCfg::SMEM, st>>>(
+        V + (r_begin - row_base) * ldv, ldv, rows, mr, coeff, L, extra, dnorm, d_sqrt + r_begin, U, ldu, labels, top2);
+    SWB_CHECK_LAUNCH();
+    return SWB_OK;
+  }
   if (L <= 8 && smem <= 200 * 1024) {
     switch (L) {
 #define SWB_RC(n) case n: return launch_reconstruct<n>(V, ldv, row_base, r_begin, r_end, mr, coeff, extra, dnorm, d_sqrt, U, ldu, labels, top2, st);
