@@ -35,6 +35,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+
 METRIC = "basis-update N·K/s and RW-solve voxels/s; % HBM / FP64-tensor roofline"
 UNIT = "N·K/s"
 CPU_SLAB_PLANES = 4
@@ -52,6 +53,7 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=0, help="ncu helper: run N steps, no timing")
+    ap.add_argument("--sharded", action="store_true", help="use the z-slab sharded path even at N=1")
     return ap.parse_args()
 
 
@@ -229,12 +231,23 @@ def setup_gpu(cfg, dims, m, rank):
     return dict(w=w, image=image, pack=pack, prob=prob, n=n, m=m, params=p)
 
 
+def _next_pack(state, beta):
+    """Chained update in ping-pong mode: V' goes into the previous step's
+    (retired) basis buffer, so no 54 GB allocation happens per step."""
+    import paper_1607_04174_b200 as swb
+    spare = state.pop("spare", None)
+    old = state["pack"]
+    pack = swb.update_basis(old, state["image"], beta, method="first_order", out=spare)
+    state["spare"] = old.V
+    state["pack"] = pack
+    return pack
+
+
 def gpu_step(state, i):
     import paper_1607_04174_b200 as swb
     p = state["params"]
     beta = p["beta1"] if i % 2 == 0 else p["beta0"]
-    pack = swb.update_basis(state["pack"], state["image"], beta, method="first_order")
-    state["pack"] = pack
+    pack = _next_pack(state, beta)
     field = swb.solve_fast(pack, pack.laplacian, state["prob"])
     return field
 
@@ -248,11 +261,107 @@ def e2e_step(state, i, host_labels):
     seeds = state["prob"].seeds
     prob = swb.LabelProblem(num_labels=p["labels"],
                             seeds=swb.SeedPartition(state["n"], seeds.seed_indices.copy(), seeds.seed_labels.copy()))
-    pack = swb.update_basis(state["pack"], state["image"], beta, method="first_order")
-    state["pack"] = pack
+    pack = _next_pack(state, beta)
     field = swb.solve_fast(pack, pack.laplacian, prob)
     host_labels.copy_(field.labels_dev, non_blocking=True)
     return field
+
+
+def run_sharded(args):
+    """N > 1 ranks (torchrun): the c4 volume split into z-slabs, one per GPU
+    (strong scaling).  Step = sharded first-order update (halo exchange +
+    one all-reduce) + sharded RW solve (one all-reduce)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1607_04174_b200 as swb
+    from paper_1607_04174_b200 import _lib
+    from paper_1607_04174_b200 import workloads as W
+    from paper_1607_04174_b200.device import LatticeSpec
+    from paper_1607_04174_b200.sharded import (CudaBackend, DistComm, Shard, SlabPlan, sharded_init_vtg,
+                                                sharded_solve, sharded_update)
+
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = args.config
+    dims = tuple(int(x) for x in args.dims.split(",")) if args.dims else None
+    m = args.m or W.CONFIGS[cfg]["m"]
+    lib = _lib.load()
+    w = W.make_image(cfg, dims)
+    p = w.params
+    n = int(np.prod(w.dims))
+    lattice = LatticeSpec.make(w.dims, p["connectivity"], p["weight_mode"])
+    plan = SlabPlan.make(w.dims, world, rank)
+    comm = DistComm()
+    be = CudaBackend()
+    V = W.orthonormal_basis_slab(plan, m, W.CFG_INDEX[cfg] * 1000 + 17, comm)
+    lam = torch.from_numpy(W.synthetic_lambda(cfg, m)).cuda()
+    img = torch.from_numpy(np.array(w.intensities)).cuda()
+    sh = Shard(plan, V, m, lam, lattice, img, be.graph(img, lattice, p["beta0"]), p["beta0"])
+    sharded_init_vtg([sh], comm, be)
+    seeds, labs = W.seeds_for(w)
+
+    def step(i):
+        beta = p["beta1"] if i % 2 == 0 else p["beta0"]
+        sharded_update([sh], comm, be, beta)
+        (labels, _, _, rc), = sharded_solve([sh], comm, be, seeds, labs, p["labels"])
+        return labels, rc
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    from paper_1607_04174_b200 import api
+    api.TIMER = api.PhaseTimer()
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = lib.swb_launch_count()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for i in range(args.steps):
+        labels, rc = step(args.warmup + i)
+    e1.record()
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches = lib.swb_launch_count() - l0
+    clk = clocks.stop()
+    phases = {k: float(np.mean(v)) for k, v in api.TIMER.durations().items()}
+    api.TIMER = None
+    ms_t = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device="cuda")
+    dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    # e2e: host seeds in, host labels out (each rank its slab) every step
+    host = torch.empty(plan.own_end - plan.own_begin, dtype=torch.int32, pin_memory=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    a0, a1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    a0.record()
+    for i in range(args.steps):
+        labels, rc = step(args.warmup + args.steps + i)
+        host.copy_(labels, non_blocking=True)
+    a1.record()
+    dist.barrier()
+    torch.cuda.synchronize()
+    et = torch.tensor([a0.elapsed_time(a1) / args.steps], dtype=torch.float64, device="cuda")
+    dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    ems = float(et.item())
+    if rank == 0:
+        line = {"metric": METRIC, "value": n * m / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"{cfg}: {'x'.join(map(str, w.dims))} volume, K={m}, sharded first-order "
+                                       f"update + {p['labels']}-label RW solve, S={len(seeds)}",
+                           "N": n, "K": m, "parallelism": f"z-slab x{world} (halo Send/Recv + all-reduce, NCCL)",
+                           "l2": "inputs larger than L2"},
+                "e2e": {"value": n * m / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(len(seeds) * 12),
+                        "d2h_bytes_per_step": int(n * 4 // world), "ms_per_step": ems},
+                "gpu_launches": int(launches), "clocks": clk, "phases_ms": phases}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
 
 
 def run_gpu(args):
@@ -427,6 +536,11 @@ def main():
     args = parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.sharded:
+        for k, v in (("RANK", "0"), ("WORLD_SIZE", "1"), ("LOCAL_RANK", "0"), ("MASTER_ADDR", "127.0.0.1"),
+                     ("MASTER_PORT", "29533")):
+            os.environ.setdefault(k, v)
+        run_sharded(args)
     else:
         run_gpu(args)
 

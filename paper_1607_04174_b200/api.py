@@ -217,14 +217,16 @@ def refresh_from_set(packs, image, new_beta: float, **kw) -> RefreshedPack:
 
 
 def update_basis(pack, image, new_beta: float | None = None, cut_edges=None, method: str = "first_order",
-                 gap_guard: float = 0.5, *, connectivity=None, weight_mode=None, keep_P: bool = False):
+                 gap_guard: float = 0.5, *, connectivity=None, weight_mode=None, keep_P: bool = False, out=None):
     """Update the eigenbasis for a new beta and/or cut edges (north-star (a)).
 
     method="rayleigh": exactly the reference refresh (no rotation).
     method="first_order": P = V^T (L^' - L^) V (difference stencil + DMMA
     symmetric projection), gap-guarded divided differences C, rotation
     V' = V C (DMMA GEMM), eigenvalues = refresh Rayleigh quotients, columns
-    stably sorted.  The old pack stays valid.
+    stably sorted.  The old pack stays valid unless ``out``
+    (an N x ldv float64 device buffer, e.g. a retired pack's V) is given to
+    receive V' — the ping-pong mode of chained interactive updates.
     """
     if method not in ("first_order", "rayleigh"):
         raise InvalidParam(f"unknown method {method!r}")
@@ -268,7 +270,12 @@ def update_basis(pack, image, new_beta: float | None = None, cut_edges=None, met
                             dp.provenance, dp.lattice, image_dev=dp.image_dev, graph=g_new,
                             vtg=gather_vector(vtd, col_map) / g_new.dnorm, col_map=col_map, mr=dp.mr)
     else:
-        W = torch.empty((n, ldv), dtype=torch.float64, device="cuda")   # becomes V' below
+        if out is not None:
+            if tuple(out.shape) != (n, ldv) or out.dtype != torch.float64 or out.data_ptr() == dp.V.data_ptr():
+                raise InvalidParam("out must be a distinct N x ldv float64 device buffer")
+            W = out
+        else:
+            W = torch.empty((n, ldv), dtype=torch.float64, device="cuda")   # becomes V' below
         ws = _stencil_ws(dp.lattice, m)
         _mark("stencil")
         _lib.call("swb_stencil_delta", C.byref(lat), ptr(dp.V), ldv, 0, 0, n, m, ptr(g_old.what),

@@ -305,39 +305,60 @@ class Shard:
         return self.V[self.plan.own_slice()]
 
 
+def _mark(name):
+    from . import api
+    if api.TIMER is not None:
+        api.TIMER.mark(name)
+
+
 def sharded_update(shards: list, comm, backend, new_beta: float, gap_guard: float = 0.5, cut_mask=None):
     """First-order basis update of every local shard (one all-reduce)."""
+    _mark("halo")
     comm.halo_exchange(shards)
     parts = []
     for sh in shards:
+        _mark("graph")
         g_new = backend.graph(sh.image, sh.lattice, new_beta, cut_mask)
-        W = backend.empty((sh.plan.own_end - sh.plan.own_begin, sh.V.shape[1]))
+        # ping-pong: the spare local buffer holds W = dL V in its owned rows,
+        # then V' (W is dead after P); the old V becomes the next spare
+        buf = sh.extra.pop("spare", None)
+        if buf is None or tuple(buf.shape) != tuple(sh.V.shape):
+            buf = backend.empty(tuple(sh.V.shape))
+        W = buf[sh.plan.own_slice()]
+        _mark("stencil")
         quad, norm2, vtd = backend.stencil_delta(sh.lattice, sh.V, sh.plan, sh.m, sh.graph, g_new, W)
+        _mark("project")
         P = backend.gram_sym(sh.own(), W, sh.plan.own_end - sh.plan.own_begin, sh.m)
+        _mark("pack")
         m = sh.m
         flat = backend.zeros((m * m + 3 * m,))
         flat[: m * m] = P.reshape(-1)
         flat[m * m: m * m + m] = quad
         flat[m * m + m: m * m + 2 * m] = norm2
         flat[m * m + 2 * m:] = vtd
-        parts.append((sh, g_new, W, flat))
+        parts.append((sh, g_new, buf, flat))
+    _mark("allreduce")
     comm.allreduce_sum([p[3] for p in parts])
-    for sh, g_new, W, flat in parts:
+    for sh, g_new, buf, flat in parts:
+        _mark("coeffs")
         m = sh.m
         P = flat[: m * m].reshape(m, m)
         quad, norm2, vtd = flat[m * m: m * m + m], flat[m * m + m: m * m + 2 * m], flat[m * m + 2 * m:]
         Cm, lam, order = backend.update_coeffs(P, sh.values, quad, norm2, m, gap_guard)
-        V_new = backend.zeros(tuple(sh.V.shape))
-        # W is dead after the projection; the rotation writes the owned rows of the new buffer
+        V_new = buf
+        _mark("rotate")
         backend.rotate(sh.own(), Cm, m, V_new[sh.plan.own_slice()])
+        _mark("update_tail")
+        if V_new.shape[1] > m:
+            V_new[:, m:] = 0.0
         sh.vtg = backend.rotate_vector(vtd, Cm, m) / g_new.dnorm
+        sh.extra["spare"] = sh.V
         sh.V = V_new
         sh.values = lam
         sh.graph = g_new
         sh.beta = float(new_beta)
         sh.extra["order"] = order
         sh.extra["C"] = Cm
-        del W
     return shards
 
 
@@ -360,6 +381,7 @@ def sharded_solve(shards: list, comm, backend, seed_idx, seed_lab, k: int, gamma
     Returns per shard (labels_own, top2_own, U_own or None, rcond)."""
     s = int(len(seed_idx))
     staged = []
+    _mark("solve_seeds")
     for i, sh in enumerate(shards):
         m = sh.m
         sidx, slab = backend.seeds(seed_idx, seed_lab)
@@ -376,7 +398,9 @@ def sharded_solve(shards: list, comm, backend, seed_idx, seed_lab, k: int, gamma
             flat[o:o + n] = x.reshape(-1)
             o += n
         staged.append((sh, sidx, slab, parts, sizes, flat))
+    _mark("solve_allreduce")
     comm.allreduce_sum([st[5] for st in staged])
+    _mark("solve_system")
     out = []
     for sh, sidx, slab, parts, sizes, flat in staged:
         o = 0
@@ -389,9 +413,11 @@ def sharded_solve(shards: list, comm, backend, seed_idx, seed_lab, k: int, gamma
         m = sh.m
         coeff, extra, rcond = backend.small_solve(gamma, s, m, k, q_s, b_qn, bg, lsu, dsq, sh.graph.dnorm, slab,
                                                   sh.values, sh.vtg, tp)
+        _mark("solve_reconstruct")
         labels, top2, U = backend.reconstruct(sh.V, sh.plan, m, coeff, extra, sh.graph.dnorm, sh.graph.d_sqrt_dev,
                                               k, sidx, slab, s, want_u)
         out.append((labels, top2, U, rcond))
+    _mark("solve_end")
     return out
 
 

@@ -177,3 +177,37 @@ def orthonormal_basis_device(n: int, m: int, seed: int, ldv: int | None = None):
         V, W = W, V
     del W
     return V
+
+
+def orthonormal_basis_slab(plan, m: int, seed: int, comm, ldv: int | None = None):
+    """Rows [row_base, row_base + local_rows) of the same global orthonormal
+    basis for any rank count: a per-plane seeded Gaussian, orthonormalised by
+    a distributed CholeskyQR2 (local DMMA Gram + one all-reduce).  Halo rows
+    are left zero (the update's halo exchange fills them)."""
+    import torch
+
+    from . import _lib
+    from .device import WORKSPACE, ptr, round_up, stream_handle
+    ldv = ldv or round_up(m, 8)
+    V = torch.zeros((plan.local_rows, ldv), dtype=torch.float64, device="cuda")
+    own = V[plan.own_slice()]
+    g = torch.Generator(device="cuda")
+    for k, u in enumerate(range(plan.u0, plan.u1)):
+        g.manual_seed(int(seed) * 1_000_003 + u)
+        own[k * plan.unit:(k + 1) * plan.unit, :m].normal_(generator=g)
+    rows = plan.own_end - plan.own_begin
+    W = torch.zeros_like(own)
+    st = stream_handle()
+    ldg = round_up(m, 2)
+    for _ in range(2):
+        G = torch.zeros((m, ldg), dtype=torch.float64, device="cuda")
+        ws = WORKSPACE.get("gemm_tn", _lib.size("swb_gemm_tn_workspace_bytes", rows, m, m))
+        _lib.call("swb_gemm_tn", ptr(own), ldv, ptr(own), ldv, rows, m, m, 1, ptr(G), ldg, ptr(ws), ws.numel(), st)
+        comm.allreduce_sum([G])
+        R = torch.linalg.cholesky(G[:, :m], upper=True)
+        Rinv = torch.zeros((m, ldg), dtype=torch.float64, device="cuda")
+        Rinv[:, :m] = torch.linalg.solve_triangular(R, torch.eye(m, dtype=torch.float64, device="cuda"), upper=True)
+        _lib.call("swb_gemm_nn", ptr(own), ldv, ptr(Rinv), ldg, rows, m, m, ptr(W), ldv, 0, st)
+        own.copy_(W)
+    del W
+    return V
