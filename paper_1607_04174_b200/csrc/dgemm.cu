@@ -21,7 +21,7 @@ using namespace swb_core;
 // NN kernel
 // ---------------------------------------------------------------------------
 template <int WARPS_M, int WARPS_N, int WTM, int WTN, int STAGES>
-__global__ void __launch_bounds__(WARPS_M * WARPS_N * 32)
+__global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 2)
 gemm_nn_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
                int64_t ldb, int64_t rows, int64_t K, int64_t M2, double* __restrict__ out,
                int64_t ldo, int accumulate, double alpha, int n_tiles_n) {
@@ -75,7 +75,7 @@ gemm_nn_kernel(const double* __restrict__ A, int64_t lda, const double* __restri
 // rows of X / Y at the same time (L2 reuse).
 // ---------------------------------------------------------------------------
 template <int WARPS_M, int WARPS_N, int WTM, int WTN, int STAGES>
-__global__ void __launch_bounds__(WARPS_M * WARPS_N * 32)
+__global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 3)
 gemm_tn_kernel(const double* __restrict__ X, int64_t ldx, const double* __restrict__ Y,
                int64_t ldy, int64_t rows, int64_t M1, int64_t M2, int tn, int symmetric,
                int64_t nk, int64_t total_units, int64_t upc, int max_slots, double* __restrict__ partial) {

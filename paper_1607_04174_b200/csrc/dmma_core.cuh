@@ -38,53 +38,56 @@ __host__ __device__ __forceinline__ int2 decode_tile(int t, int tn, int symmetri
   return make_int2(i, i + t);
 }
 
+// One pipeline stage: copy the A tile and the B tile of one BK-deep k-slice
+// into shared memory.  Tile bases are 64-bit pointers computed once per
+// stage; per-chunk offsets are 32-bit (tile extents are small), and the
+// chunk loops have compile-time trip counts.
+//   NN: A tile = BM rows x BK cols at A_t (ld lda), B tile = BK rows x BN cols
+//   TN: A tile = BK rows x BM cols at A_t (ld lda) (k-major), B tile as NN
+// *_rows / *_cols: valid extent of each tile (rest zero-filled).
 template <int WARPS_M, int WARPS_N, int WTM, int WTN, int STAGES, bool TN>
-__device__ __forceinline__ void load_stage(double* sA, double* sB, const double* A, int64_t lda,
-                                           const double* B, int64_t ldb, int64_t k0,
-                                           int64_t k_end, int64_t m0, int64_t m_lim,
-                                           int64_t n0, int64_t n_lim) {
+__device__ __forceinline__ void load_stage(double* sA, double* sB, const double* A_t, int lda, int a_rows,
+                                           int a_cols, const double* B_t, int ldb, int b_rows, int b_cols,
+                                           bool b_vec) {
   using Cf = Cfg<WARPS_M, WARPS_N, WTM, WTN, STAGES, TN>;
+  constexpr int T = Cf::THREADS;
   const int tid = threadIdx.x;
-  if (TN) {
-    // X tile: BK rows (k) x BM cols, rows k0.., cols m0..
-    constexpr int CH = Cf::BM / 2;              // 16B chunks per row
-    for (int c = tid; c < BK * CH; c += Cf::THREADS) {
-      int kr = c / CH, cc = (c % CH) * 2;
-      int64_t gk = k0 + kr, gm = m0 + cc;
-      bool p = (gk < k_end) && (gm < m_lim);
-      const double* src = p ? (A + gk * lda + gm) : A;
-      cp_async16(sA + kr * Cf::A_LD + cc, src, p);
-    }
-  } else {
-    // A tile: BM rows x BK cols (k), rows m0.., cols k0..
-    constexpr int CH = BK / 2;
-    for (int c = tid; c < Cf::BM * CH; c += Cf::THREADS) {
-      int mr = c / CH, cc = (c % CH) * 2;
-      int64_t gm = m0 + mr, gk = k0 + cc;
-      bool p = (gm < m_lim) && (gk < k_end);
-      const double* src = p ? (A + gm * lda + gk) : A;
-      cp_async16(sA + mr * Cf::A_LD + cc, src, p);
+  {
+    constexpr int ROWS = TN ? BK : Cf::BM;
+    constexpr int CH = (TN ? Cf::BM : BK) / 2;  // 16-byte chunks per row
+    constexpr int TOTAL = ROWS * CH;
+#pragma unroll
+    for (int i = 0; i < (TOTAL + T - 1) / T; ++i) {
+      const int c = tid + i * T;
+      if (TOTAL % T != 0 && c >= TOTAL) break;
+      const int r = c / CH, cc = (c % CH) * 2;
+      const bool p = (r < a_rows) && (cc < a_cols);
+      cp_async16(sA + r * Cf::A_LD + cc, p ? A_t + r * lda + cc : A_t, p);
     }
   }
-  if (((ldb & 1) == 0) && ((reinterpret_cast<uintptr_t>(B) & 15) == 0)) {
+  if (b_vec) {
     constexpr int CH = Cf::BN / 2;
-    for (int c = tid; c < BK * CH; c += Cf::THREADS) {
-      int kr = c / CH, cc = (c % CH) * 2;
-      int64_t gk = k0 + kr, gn = n0 + cc;
-      bool p = (gk < k_end) && (gn < n_lim);
-      const double* src = p ? (B + gk * ldb + gn) : B;
-      cp_async16(sB + kr * Cf::B_LD + cc, src, p);
+    constexpr int TOTAL = BK * CH;
+#pragma unroll
+    for (int i = 0; i < (TOTAL + T - 1) / T; ++i) {
+      const int c = tid + i * T;
+      if (TOTAL % T != 0 && c >= TOTAL) break;
+      const int r = c / CH, cc = (c % CH) * 2;
+      const bool p = (r < b_rows) && (cc < b_cols);
+      cp_async16(sB + r * Cf::B_LD + cc, p ? B_t + r * ldb + cc : B_t, p);
     }
-  } else {  // odd leading dimension (small label counts): 8-byte copies
-    for (int c = tid; c < BK * Cf::BN; c += Cf::THREADS) {
-      int kr = c / Cf::BN, cc = c % Cf::BN;
-      int64_t gk = k0 + kr, gn = n0 + cc;
-      bool p = (gk < k_end) && (gn < n_lim);
-      const double* src = p ? (B + gk * ldb + gn) : B;
-      cp_async8(sB + kr * Cf::B_LD + cc, src, p);
+  } else {  // odd leading dimension / 8-byte alignment (small label counts)
+    constexpr int TOTAL = BK * Cf::BN;
+#pragma unroll 4
+    for (int c = tid; c < TOTAL; c += T) {
+      const int r = c / Cf::BN, cc = c % Cf::BN;
+      const bool p = (r < b_rows) && (cc < b_cols);
+      cp_async8(sB + r * Cf::B_LD + cc, p ? B_t + r * ldb + cc : B_t, p);
     }
   }
 }
+
+__device__ __forceinline__ int clamp_int(int64_t v, int hi) { return v < 0 ? 0 : (v > hi ? hi : static_cast<int>(v)); }
 
 template <int WARPS_M, int WARPS_N, int WTM, int WTN, int STAGES, bool TN>
 __device__ __forceinline__ void mainloop(double (&acc)[WTM][WTN][2], double* smem,
@@ -95,46 +98,61 @@ __device__ __forceinline__ void mainloop(double (&acc)[WTM][WTN][2], double* sme
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int wm = warp / WARPS_N, wn = warp % WARPS_N;
-  const int64_t nk = (k_end - k_begin + BK - 1) / BK;
+  const int nk = static_cast<int>((k_end - k_begin + BK - 1) / BK);
+  const bool b_vec = ((ldb & 1) == 0) && ((reinterpret_cast<uintptr_t>(B) & 15) == 0);
+  // tile-base pointers of the first k-slice and their per-stage advance
+  const double* a_t = TN ? A + k_begin * lda + m0 : A + m0 * lda + k_begin;
+  const int64_t a_step = TN ? BK * lda : BK;
+  const double* b_t = B + k_begin * ldb + n0;
+  const int64_t b_step = BK * ldb;
+  const int m_rows = clamp_int(m_lim - m0, TN ? Cf::BM : Cf::BM);
+  const int n_cols = clamp_int(n_lim - n0, Cf::BN);
+  int k_left = static_cast<int>(k_end - k_begin);  // fits: k extents are per-CTA row chunks (< 2^31)
+
+  auto issue = [&](int slot, int kt) {
+    double* st = smem + slot * Cf::STAGE_ELEMS;
+    const int kl = k_left - kt * BK;
+    if (TN)
+      load_stage<WARPS_M, WARPS_N, WTM, WTN, STAGES, TN>(st, st + Cf::A_ELEMS, a_t + kt * a_step,
+                                                         static_cast<int>(lda), kl, m_rows, b_t + kt * b_step,
+                                                         static_cast<int>(ldb), kl, n_cols, b_vec);
+    else
+      load_stage<WARPS_M, WARPS_N, WTM, WTN, STAGES, TN>(st, st + Cf::A_ELEMS, a_t + kt * a_step,
+                                                         static_cast<int>(lda), m_rows, kl, b_t + kt * b_step,
+                                                         static_cast<int>(ldb), kl, n_cols, b_vec);
+  };
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk) {
-      double* st = smem + s * Cf::STAGE_ELEMS;
-      load_stage<WARPS_M, WARPS_N, WTM, WTN, STAGES, TN>(st, st + Cf::A_ELEMS, A, lda, B, ldb,
-                                                         k_begin + s * BK, k_end, m0, m_lim, n0, n_lim);
-    }
+    if (s < nk) issue(s, s);
     cp_async_commit();
   }
 
   const int lr = lane >> 2, lc = lane & 3;
-  for (int64_t kt = 0; kt < nk; ++kt) {
+  int slot = 0;                 // stage being consumed
+  int fill = STAGES - 1;        // stage being filled next
+  for (int kt = 0; kt < nk; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
-    {
-      int64_t nt = kt + STAGES - 1;
-      if (nt < nk) {
-        double* st = smem + (nt % STAGES) * Cf::STAGE_ELEMS;
-        load_stage<WARPS_M, WARPS_N, WTM, WTN, STAGES, TN>(st, st + Cf::A_ELEMS, A, lda, B, ldb,
-                                                           k_begin + nt * BK, k_end, m0, m_lim, n0, n_lim);
-      }
-      cp_async_commit();
-    }
-    const double* sA = smem + (kt % STAGES) * Cf::STAGE_ELEMS;
+    if (kt + STAGES - 1 < nk) issue(fill, kt + STAGES - 1);
+    cp_async_commit();
+    fill = fill + 1 == STAGES ? 0 : fill + 1;
+    const double* sA = smem + slot * Cf::STAGE_ELEMS;
     const double* sB = sA + Cf::A_ELEMS;
+    slot = slot + 1 == STAGES ? 0 : slot + 1;
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
       double af[WTM], bf[WTN];
 #pragma unroll
       for (int i = 0; i < WTM; ++i) {
-        int m = wm * WTM * 8 + i * 8 + lr;
-        int k = kk * 4 + lc;
+        const int m = wm * WTM * 8 + i * 8 + lr;
+        const int k = kk * 4 + lc;
         af[i] = TN ? sA[k * Cf::A_LD + m] : sA[m * Cf::A_LD + k];
       }
 #pragma unroll
       for (int j = 0; j < WTN; ++j) {
-        int n = wn * WTN * 8 + j * 8 + lr;
-        int k = kk * 4 + lc;
+        const int n = wn * WTN * 8 + j * 8 + lr;
+        const int k = kk * 4 + lc;
         bf[j] = sB[k * Cf::B_LD + n];
       }
 #pragma unroll
@@ -145,6 +163,5 @@ __device__ __forceinline__ void mainloop(double (&acc)[WTM][WTN][2], double* sme
   }
   cp_async_wait<0>();
 }
-
 
 }  // namespace swb_core
