@@ -197,72 +197,92 @@ __device__ __forceinline__ void coef_split(double c, double& n, double& o) { n =
 __device__ __forceinline__ void coef_split(double2 c, double& n, double& o) { n = c.x; o = c.y; }
 
 // ---------------------------------------------------------------------------
-// Stencil pass v4: one warp = one x-line of one 64-column block (lane = 2
-// adjacent columns).  Rows stream through a per-warp cp.async ring of
-// RING stages, PREF rows ahead.  A stage holds, for voxel row x of the line:
-//   V rows     : centre, y-1 line, y+1 line [, z-1 line, z+1 line]  (512 B each)
-//   coefficients: centre row (ND forward + diag), y-1 line row (ND)
-//                [, z-1 line row (ND)]  ((new, old) pairs for the difference pass)
-//   d_sqrt of the centre row.
-// +-x neighbours (and the 8-connected diagonals) come from the adjacent
-// stages; every backward coefficient is the forward coefficient of the row
-// it starts from, found in the stage of that row.  Off-grid lines are
-// zero-filled by the predicated copies (coefficient 0, value 0).
+// Stencil pass v5: CTA-shared ring.  A CTA's 8 warps own a block of
+// ZB x YB x-lines (3-D: 4 z x 2 y; 2-D: 8 y) of one 64-column block; warp w
+// takes line (zi, yi) = (w / YB, w % YB).  Each ring stage holds, for voxel
+// row x, every V line the block needs exactly once -- the 8 centre lines plus
+// the one-line halo around the block (no corners) -- together with each
+// centre line's coefficients (forward + diag, and the forward coefficients
+// of its y-1 / z-1 source rows) and d_sqrt.  Lines shared by sibling warps
+// (their +-y / +-z neighbours) are therefore fetched from L2 once instead of
+// once per warp; +-x comes from the adjacent stages as before.  One CTA
+// barrier per row; RING = PREF + 3 so the stage being refilled is never one
+// a warp can still read.
 // ---------------------------------------------------------------------------
 template <int CONN, bool DELTA>
-struct StencilRing {
+struct Ring5 {
   static constexpr bool D3 = CONN == 6;
   static constexpr int ND = nb_ndir(CONN);
-  static constexpr int NV = D3 ? 5 : 3;                         // V rows per stage
-  static constexpr int NCL = D3 ? 3 : 2;                        // coefficient rows per stage
-  static constexpr int CW = DELTA ? 2 : 1;                      // doubles per coefficient
-  static constexpr int COEF = (ND + 1) + ND * (NCL - 1);        // coefficients per stage
-  static constexpr int PREF = 3;                                // rows prefetched ahead
-  static constexpr int RING = PREF + 2;
-  static constexpr int V_DBL = NV * 64;
-  static constexpr int C_DBL = ((COEF * CW + 1) + 1) / 2 * 2;   // + d_sqrt, 16-B aligned
+  static constexpr int ZB = D3 ? 4 : 1;
+  static constexpr int YB = D3 ? 2 : 8;
+  static constexpr int NL = ZB * YB;                                   // centre lines (= warps)
+  // extended grid (ZB+2) x (YB+2) without corners (3-D); 2-D: 1 x (YB+2)
+  static constexpr int NS = D3 ? NL + 2 * ZB + 2 * YB : YB + 2;        // V line slots
+  static constexpr int CW = DELTA ? 2 : 1;
+  static constexpr int NCL = D3 ? 3 : 2;                               // coefficient rows per line
+  static constexpr int COEF = (ND + 1) + ND * (NCL - 1);
+  static constexpr int LCD = (COEF * CW + 1 + 1) / 2 * 2;              // doubles per line (+ d_sqrt), 16-B aligned
+  static constexpr int V_DBL = NS * 64;
+  static constexpr int C_DBL = (NL * LCD + 1) / 2 * 2;
   static constexpr int STAGE_DBL = V_DBL + C_DBL;
-  static constexpr int WARP_DBL = RING * STAGE_DBL;
+  static constexpr int PREF = 3;
+  static constexpr int RING = PREF + 2;
+  // slot of extended line (zi, yi), zi in [-1, ZB], yi in [-1, YB]; -1 = unused corner
+  __host__ __device__ static constexpr int slot(int zi, int yi) {
+    return !D3 ? (yi + 1)
+                 : (zi >= 0 && zi < ZB && yi >= 0 && yi < YB) ? zi * YB + yi
+                 : (zi >= 0 && zi < ZB && yi == -1) ? NL + zi
+                 : (zi >= 0 && zi < ZB && yi == YB) ? NL + ZB + zi
+                 : (yi >= 0 && yi < YB && zi == -1) ? NL + 2 * ZB + yi
+                 : (yi >= 0 && yi < YB && zi == ZB) ? NL + 2 * ZB + YB + yi
+                 : -1;
+  }
 };
 
 template <int CONN, bool DELTA>
 __global__ void __launch_bounds__(ST_WARPS * 32, ST_CTAS_PER_SM)
-stencil4_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, int64_t row_base, int64_t blk_begin,
+stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, int64_t row_base, int64_t blk_begin,
                 int64_t blk_end, int64_t M, int n_cb, const double* __restrict__ cwhat, const double* __restrict__ cdiag,
                 const double* __restrict__ d_sqrt, double* __restrict__ W, int64_t ldw, int64_t w_row0,
                 double* __restrict__ slots, int64_t slot_ld) {
-  using Rg = StencilRing<CONN, DELTA>;
-  constexpr int ND = Rg::ND, NV = Rg::NV, CW = Rg::CW, RING = Rg::RING, PREF = Rg::PREF;
-  constexpr int SD = Rg::STAGE_DBL;
-  extern __shared__ __align__(16) double ring_all[];
+  using Rg = Ring5<CONN, DELTA>;
+  constexpr int ND = Rg::ND, CW = Rg::CW, RING = Rg::RING, PREF = Rg::PREF, SD = Rg::STAGE_DBL;
+  constexpr int ZB = Rg::ZB, YB = Rg::YB, NS = Rg::NS, NL = Rg::NL, LCD = Rg::LCD;
+  static_assert(NL == ST_WARPS, "one warp per centre line");
+  extern __shared__ __align__(16) double ring[];
+  double* zst = ring + RING * SD;  // zero stage for x-1 < 0 / x+1 >= nx
+  for (int i = threadIdx.x; i < SD; i += blockDim.x) zst[i] = 0.0;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  double* ring = ring_all + warp * Rg::WARP_DBL;
-  double* zst = ring_all + ST_WARPS * Rg::WARP_DBL;  // shared all-zero stage for x-1 < 0 / x+1 >= nx
-  for (int i = threadIdx.x; i < SD; i += blockDim.x) zst[i] = 0.0;
-  __syncthreads();
+  const int zi = warp / YB, yi = warp % YB;
   const int64_t gwarp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nx = g.lat.nx, ny = g.lat.ny, nz = g.lat.nz;
   const int64_t plane = nx * ny;
   const int nxi = static_cast<int>(nx);
-  // CTA item = (column block, block of 8 lines along the slowest axis, other
-  // axis): 3-D -> warp w takes z = 8*zb + w at a common y, so every warp's
-  // +-z neighbour lines are its sibling warps' lines, streamed in lockstep;
-  // consecutive CTAs take consecutive y.  2-D -> warp w takes y = 8*yb + w.
-  const bool d3 = Rg::D3;
-  const int64_t inner = d3 ? ny : 1;
-  const int64_t nblk = (blk_end - blk_begin + ST_WARPS - 1) / ST_WARPS;
-  const int64_t per_cb = nblk * inner;
+  // items: (column block, block along the slowest axis, block along y) -- y fastest
+  const int64_t n_slow = Rg::D3 ? (blk_end - blk_begin + ZB - 1) / ZB : 1;
+  const int64_t n_yb = Rg::D3 ? (ny + YB - 1) / YB : (blk_end - blk_begin + YB - 1) / YB;
+  const int64_t per_cb = n_slow * n_yb;
   const int64_t n_items = int64_t(n_cb) * per_cb;
+
+  // copy assignment of this thread (fixed per kernel): V chunks j = tid + i*256
+  constexpr int VCH = NS * 32;                       // 16-byte chunks per stage (32 per line)
+  constexpr int VPT = (VCH + ST_WARPS * 32 - 1) / (ST_WARPS * 32);
+  constexpr int CSL = NL * (Rg::COEF + 1);           // coefficient / d_sqrt slots per stage
+  __syncthreads();
 
   double2 q = make_double2(0.0, 0.0), s2 = q, sd = q;
   int cur_cb = -1;
   for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
     const int cb = static_cast<int>(it / per_cb);
     const int64_t rem = it % per_cb;
-    const int64_t slow = blk_begin + (rem / inner) * ST_WARPS + warp;  // z (3-D) or y (2-D)
-    if (slow >= blk_end) continue;
-    const int64_t line = d3 ? (slow * ny + rem % inner) : slow;
+    const int64_t z0 = Rg::D3 ? blk_begin + (rem / n_yb) * ZB : 0;
+    const int64_t y0 = Rg::D3 ? (rem % n_yb) * YB : blk_begin + (rem % n_yb) * YB;
+    const int64_t z_end = Rg::D3 ? blk_end : 1;
+    const int64_t y_end = Rg::D3 ? ny : blk_end;
+    // my centre line
+    const int64_t my_z = z0 + zi, my_y = y0 + yi;
+    const bool line_live = (Rg::D3 ? my_z < z_end : true) && my_y < y_end;
     if (cb != cur_cb) {
       if (cur_cb >= 0) {
         double* sl = slots + gwarp * slot_ld * 3 + (int64_t(cur_cb) * 64 + 2 * lane) * 3;
@@ -271,119 +291,138 @@ stencil4_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
       q = make_double2(0.0, 0.0); s2 = q; sd = q;
       cur_cb = cb;
     }
-    const int64_t col_raw = int64_t(cb) * 64 + 2 * lane;
-    const bool active = col_raw < M;
-    const int64_t col = active ? col_raw : 0;
-    const int64_t r0 = line * nx;
-    const int64_t y = line % ny, z = line / ny;
-    // per-line copy sources (advanced by one row per prefetch)
-    const double* vsrc[NV];
-    bool vok[NV];
-    {
-      const int64_t off[5] = {0, -nx, nx, -plane, plane};
-      const bool okk[5] = {true, y > 0, y + 1 < ny, z > 0, z + 1 < nz};
+    const int64_t col0 = int64_t(cb) * 64;
+    // per-thread copy sources for this item: V chunks
+    const double* vsrc[VPT];
+    int vdst[VPT];
+    bool vok[VPT];
 #pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        vok[v] = okk[v];
-        vsrc[v] = V + (r0 + (okk[v] ? off[v] : 0) - row_base) * ldv + col;
+    for (int i = 0; i < VPT; ++i) {
+      const int j = threadIdx.x + i * ST_WARPS * 32;
+      vok[i] = false; vsrc[i] = V; vdst[i] = 0;
+      if (j < VCH) {
+        const int s = j >> 5, ch = j & 31;
+        // decode slot -> extended (zi, yi)
+        int ez = 0, ey = 0;
+        if (!Rg::D3) { ey = s - 1; }
+        else if (s < NL) { ez = s / YB; ey = s % YB; }
+        else if (s < NL + ZB) { ez = s - NL; ey = -1; }
+        else if (s < NL + 2 * ZB) { ez = s - NL - ZB; ey = YB; }
+        else if (s < NL + 2 * ZB + YB) { ey = s - NL - 2 * ZB; ez = -1; }
+        else { ey = s - NL - 2 * ZB - YB; ez = ZB; }
+        const int64_t lz = z0 + ez, ly = y0 + ey;
+        const int64_t col = col0 + 2 * ch;
+        const bool ok = lz >= 0 && lz < nz && ly >= 0 && ly < ny && col < M &&
+                        (Rg::D3 ? true : ly < ny);
+        vok[i] = ok;
+        vsrc[i] = ok ? V + ((lz * ny + ly) * nx - row_base) * ldv + col : V;
+        vdst[i] = s * 64 + 2 * ch;
       }
     }
-    // lane s < COEF + 1 copies coefficient slot s (or d_sqrt for s == COEF)
-    const double* csrc = d_sqrt + r0;
-    int64_t cstride = 1;
-    bool cok = lane <= Rg::COEF;
-    int cbytes = 8;
-    if (lane < ND) {
-      csrc = cwhat + (r0 * ND + lane) * CW; cstride = ND * CW; cbytes = 8 * CW;
-    } else if (lane == ND) {
-      csrc = cdiag + r0 * CW; cstride = CW; cbytes = 8 * CW;
-    } else if (lane < 2 * ND + 1) {
-      const bool ok = y > 0;
-      csrc = cwhat + ((r0 - (ok ? nx : 0)) * ND + (lane - ND - 1)) * CW; cstride = ND * CW; cbytes = 8 * CW;
-      cok = ok;
-    } else if (lane < Rg::COEF) {
-      const bool ok = z > 0;
-      csrc = cwhat + ((r0 - (ok ? plane : 0)) * ND + (lane - 2 * ND - 1)) * CW; cstride = ND * CW; cbytes = 8 * CW;
-      cok = ok;
+    // coefficient slot: line l = cs / (COEF+1), k = cs % (COEF+1) (k == COEF -> d_sqrt)
+    const double* csrc = d_sqrt;
+    int64_t cstride = 0;
+    int cdst = 0, cbytes = 0;
+    bool cok = false;
+    if (threadIdx.x < CSL) {
+      const int l = threadIdx.x / (Rg::COEF + 1), k = threadIdx.x % (Rg::COEF + 1);
+      const int lzi = l / YB, lyi = l % YB;
+      const int64_t lz = z0 + lzi, ly = y0 + lyi;
+      const bool live = (lz < nz) && (ly < ny);
+      const int64_t r0 = (lz * ny + ly) * nx;
+      cdst = Rg::V_DBL + l * LCD + (k < Rg::COEF ? k * CW : Rg::COEF * CW);
+      if (!live) {
+        cok = false; csrc = d_sqrt; cstride = 0; cbytes = 8 * CW;
+      } else if (k < ND) {
+        csrc = cwhat + (r0 * ND + k) * CW; cstride = ND * CW; cbytes = 8 * CW; cok = true;
+      } else if (k == ND) {
+        csrc = cdiag + r0 * CW; cstride = CW; cbytes = 8 * CW; cok = true;
+      } else if (k < 2 * ND + 1) {
+        cok = ly > 0;
+        csrc = cwhat + ((r0 - (cok ? nx : 0)) * ND + (k - ND - 1)) * CW; cstride = ND * CW; cbytes = 8 * CW;
+      } else if (k < Rg::COEF) {
+        cok = lz > 0;
+        csrc = cwhat + ((r0 - (cok ? plane : 0)) * ND + (k - 2 * ND - 1)) * CW; cstride = ND * CW; cbytes = 8 * CW;
+      } else {
+        csrc = d_sqrt + r0; cstride = 1; cbytes = 8; cok = true;
+      }
     }
-    const bool c_issue = lane <= Rg::COEF;
-    const int cslot = lane < Rg::COEF ? lane * CW : Rg::COEF * CW;
-
-    int pst = 0;  // ring stage of the next prefetched row
-    int xp = 0;   // next row to prefetch
+    int pst = 0, xp = 0;
     auto prefetch = [&]() {
       if (xp < nxi) {
         double* stg = ring + pst * SD;
 #pragma unroll
-        for (int v = 0; v < NV; ++v) cp_async16(stg + v * 64 + 2 * lane, vsrc[v], vok[v]);
-        if (c_issue) {
-          if (cbytes == 16) cp_async16(stg + Rg::V_DBL + cslot, csrc, cok);
-          else cp_async8(stg + Rg::V_DBL + cslot, csrc, cok);
+        for (int i = 0; i < VPT; ++i)
+          if (threadIdx.x + i * ST_WARPS * 32 < VCH) cp_async16(stg + vdst[i], vsrc[i] + int64_t(xp) * ldv, vok[i]);
+        if (threadIdx.x < CSL) {
+          if (cbytes == 16) cp_async16(stg + cdst, csrc + int64_t(xp) * cstride, cok);
+          else cp_async8(stg + cdst, csrc + int64_t(xp) * cstride, cok);
         }
-#pragma unroll
-        for (int v = 0; v < NV; ++v) vsrc[v] += ldv;
-        csrc += cstride;
         ++xp;
         pst = pst + 1 == RING ? 0 : pst + 1;
       }
       cp_async_commit();
     };
 #pragma unroll
-    for (int i = 0; i <= PREF; ++i) prefetch();
+    for (int i = 0; i < PREF; ++i) prefetch();
 
-    double* wrow = DELTA ? W + (r0 - w_row0) * ldw + col : nullptr;
+    const bool active = line_live && (col0 + 2 * lane < M);
+    const int64_t my_r0 = (my_z * ny + my_y) * nx;
+    double* wrow = (DELTA && line_live) ? W + (my_r0 - w_row0) * ldw + col0 + 2 * lane : nullptr;
+    const int my_slot = Rg::slot(zi, yi);
     int sc_i = 0;
-    const double* sm1 = zst;
     for (int x = 0; x < nxi; ++x) {
-      cp_async_wait<PREF - 1>();  // rows <= x+1 have landed
-      __syncwarp();
+      cp_async_wait<PREF - 2>();   // rows <= x+1 have landed (this thread's copies)
+      __syncthreads();             // ... every thread's; compute(x-1) finished everywhere
+      prefetch();                  // row x+PREF -> stage (x+PREF) % RING == stage of row x-2
       const double* sc = ring + sc_i * SD;
       const int sp_i = sc_i + 1 == RING ? 0 : sc_i + 1;
+      const int sm_i = sc_i == 0 ? RING - 1 : sc_i - 1;
+      const double* sm1 = x > 0 ? ring + sm_i * SD : zst;
       const double* sp1 = x + 1 < nxi ? ring + sp_i * SD : zst;
-      const double2 c = *reinterpret_cast<const double2*>(sc + 2 * lane);
-      const double d = sc[Rg::V_DBL + Rg::COEF * CW];
-      double lx = 0.0, ly = 0.0, dx = 0.0, dy = 0.0;
+      if (line_live) {
+        const double* cme = sc + Rg::V_DBL + warp * LCD;
+        const double2 c = *reinterpret_cast<const double2*>(sc + my_slot * 64 + 2 * lane);
+        const double d = cme[Rg::COEF * CW];
+        double lx = 0.0, ly = 0.0, dx = 0.0, dy = 0.0;
 #pragma unroll
-      for (int e = 0; e < nb_count(CONN); ++e) {
-        const NbC t = nb_entry(CONN, e);
-        const double* vs = t.dx < 0 ? sm1 : t.dx > 0 ? sp1 : sc;
-        const int v = t.dz < 0 ? 3 : t.dz > 0 ? 4 : t.dy < 0 ? 1 : t.dy > 0 ? 2 : 0;
-        const double2 val = *reinterpret_cast<const double2*>(vs + v * 64 + 2 * lane);
-        int slot;
-        const double* cs;
-        if (t.kind == 0) { slot = ND; cs = sc; }
-        else if (t.kind == 1) { slot = t.dir; cs = sc; }
-        else { slot = t.dz < 0 ? 2 * ND + 1 + t.dir : t.dy < 0 ? ND + 1 + t.dir : t.dir; cs = vs; }
-        const double* cp = cs + Rg::V_DBL + slot * CW;
-        const double cn = cp[0];
-        const double co = DELTA ? cp[1] : 0.0;
-        if (t.kind == 0) {
-          lx = __dadd_rn(lx, __dmul_rn(cn, val.x));
-          ly = __dadd_rn(ly, __dmul_rn(cn, val.y));
-          if (DELTA) { const double gg = cn - co; dx = fma(gg, val.x, dx); dy = fma(gg, val.y, dy); }
-        } else {
-          lx = __dadd_rn(lx, __dmul_rn(-cn, val.x));
-          ly = __dadd_rn(ly, __dmul_rn(-cn, val.y));
-          if (DELTA) { const double gg = co - cn; dx = fma(gg, val.x, dx); dy = fma(gg, val.y, dy); }
+        for (int e = 0; e < nb_count(CONN); ++e) {
+          const NbC t = nb_entry(CONN, e);
+          const double* vs = t.dx < 0 ? sm1 : t.dx > 0 ? sp1 : sc;
+          const int vsl = Rg::slot(zi + t.dz, yi + t.dy);
+          const double2 val = *reinterpret_cast<const double2*>(vs + vsl * 64 + 2 * lane);
+          int slot;
+          const double* cs;
+          if (t.kind == 0) { slot = ND; cs = sc; }
+          else if (t.kind == 1) { slot = t.dir; cs = sc; }
+          else { slot = t.dz < 0 ? 2 * ND + 1 + t.dir : t.dy < 0 ? ND + 1 + t.dir : t.dir; cs = vs; }
+          const double* cp = cs + Rg::V_DBL + warp * LCD + slot * CW;
+          const double cn = cp[0];
+          const double co = DELTA ? cp[1] : 0.0;
+          if (t.kind == 0) {
+            lx = __dadd_rn(lx, __dmul_rn(cn, val.x));
+            ly = __dadd_rn(ly, __dmul_rn(cn, val.y));
+            if (DELTA) { const double gg = cn - co; dx = fma(gg, val.x, dx); dy = fma(gg, val.y, dy); }
+          } else {
+            lx = __dadd_rn(lx, __dmul_rn(-cn, val.x));
+            ly = __dadd_rn(ly, __dmul_rn(-cn, val.y));
+            if (DELTA) { const double gg = co - cn; dx = fma(gg, val.x, dx); dy = fma(gg, val.y, dy); }
+          }
+        }
+        if (active) {
+          q.x = fma(c.x, lx, q.x);
+          q.y = fma(c.y, ly, q.y);
+          s2.x = fma(c.x, c.x, s2.x);
+          s2.y = fma(c.y, c.y, s2.y);
+          sd.x = fma(c.x, d, sd.x);
+          sd.y = fma(c.y, d, sd.y);
+          if (DELTA) *reinterpret_cast<double2*>(wrow + int64_t(x) * ldw) = make_double2(dx, dy);
         }
       }
-      if (active) {
-        q.x = fma(c.x, lx, q.x);
-        q.y = fma(c.y, ly, q.y);
-        s2.x = fma(c.x, c.x, s2.x);
-        s2.y = fma(c.y, c.y, s2.y);
-        sd.x = fma(c.x, d, sd.x);
-        sd.y = fma(c.y, d, sd.y);
-        if (DELTA) *reinterpret_cast<double2*>(wrow) = make_double2(dx, dy);
-      }
-      if (DELTA) wrow += ldw;
-      __syncwarp();
-      prefetch();  // fills the stage of row x-1 (RING = PREF + 2)
-      sm1 = sc;
       sc_i = sp_i;
     }
     cp_async_wait<0>();
-    __syncwarp();
+    __syncthreads();
   }
   if (cur_cb >= 0) {
     double* sl = slots + gwarp * slot_ld * 3 + (int64_t(cur_cb) * 64 + 2 * lane) * 3;
@@ -415,13 +454,13 @@ __global__ void slot_reduce_kernel(const double* __restrict__ slots, int64_t slo
 int64_t stencil_grid() { return int64_t(swb_sm_count()) * ST_CTAS_PER_SM; }
 
 template <int CONN, bool DELTA>
-int launch_stencil4(const StencilGeom& g, const double* V, int64_t ldv, int64_t row_base, int64_t blk_begin,
+int launch_stencil5(const StencilGeom& g, const double* V, int64_t ldv, int64_t row_base, int64_t blk_begin,
                     int64_t blk_end, int64_t M, int n_cb, const double* cw, const double* cd, const double* d_sqrt,
                     double* W, int64_t ldw, int64_t w_row0, double* slots, int64_t slot_ld, int64_t grid,
                     cudaStream_t st) {
-  using Rg = StencilRing<CONN, DELTA>;
-  const size_t smem = sizeof(double) * (size_t(Rg::WARP_DBL) * ST_WARPS + Rg::STAGE_DBL);
-  auto kern = stencil4_kernel<CONN, DELTA>;
+  using Rg = Ring5<CONN, DELTA>;
+  const size_t smem = sizeof(double) * size_t(Rg::RING + 1) * Rg::STAGE_DBL;
+  auto kern = stencil5_kernel<CONN, DELTA>;
   static bool attr = false;
   if (!attr) {
     SWB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -502,9 +541,9 @@ int run_stencil(const swb_lattice* lat, const double* V, int64_t ldv, int64_t ro
     const int64_t unit = L.conn == 6 ? L.nx * L.ny : L.nx;
     if (r_begin % unit || r_end % unit) return SWB_INVALID_PARAM;
     const int64_t b0 = r_begin / unit, b1 = r_end / unit;
-    if (L.conn == 4) rc2 = launch_stencil4<4, DELTA>(g, V, ldv, row_base, b0, b1, M, n_cb, cw, cd, d_sqrt, W, ldw, r_begin, slots, slot_ld, grid, st);
-    else if (L.conn == 8) rc2 = launch_stencil4<8, DELTA>(g, V, ldv, row_base, b0, b1, M, n_cb, cw, cd, d_sqrt, W, ldw, r_begin, slots, slot_ld, grid, st);
-    else rc2 = launch_stencil4<6, DELTA>(g, V, ldv, row_base, b0, b1, M, n_cb, cw, cd, d_sqrt, W, ldw, r_begin, slots, slot_ld, grid, st);
+    if (L.conn == 4) rc2 = launch_stencil5<4, DELTA>(g, V, ldv, row_base, b0, b1, M, n_cb, cw, cd, d_sqrt, W, ldw, r_begin, slots, slot_ld, grid, st);
+    else if (L.conn == 8) rc2 = launch_stencil5<8, DELTA>(g, V, ldv, row_base, b0, b1, M, n_cb, cw, cd, d_sqrt, W, ldw, r_begin, slots, slot_ld, grid, st);
+    else rc2 = launch_stencil5<6, DELTA>(g, V, ldv, row_base, b0, b1, M, n_cb, cw, cd, d_sqrt, W, ldw, r_begin, slots, slot_ld, grid, st);
     if (rc2) return rc2;
   }
   dim3 rg(static_cast<unsigned>(M), 3);
