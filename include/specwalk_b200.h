@@ -164,6 +164,17 @@ int swb_small_solve(double gamma, int64_t S, int64_t m, int64_t L, const double*
                     const double* values, const double* vtg, const double* t_p, int64_t ldt,
                     double* coeff, double* extra, double* rcond_out,
                     void* workspace, size_t workspace_bytes, void* stream);
+/* Same, with the condition estimate enqueued on rcond_stream after
+ * rcond_event (a cudaEvent_t) is recorded on stream, so it overlaps the
+ * caller's next work (the reconstruction).  The caller must join
+ * rcond_stream before reading rcond_out or reusing the workspace. */
+int swb_small_solve_ex(double gamma, int64_t S, int64_t m, int64_t L, const double* q_s,
+                       const double* b_qn, int64_t ldq, const double* bg, const double* lsu,
+                       const double* dsq_s, double dnorm, const int32_t* seed_lab,
+                       const double* values, const double* vtg, const double* t_p, int64_t ldt,
+                       double* coeff, double* extra, double* rcond_out,
+                       void* workspace, size_t workspace_bytes, void* stream,
+                       void* rcond_stream, void* rcond_event);
 int swb_check_rcond(double rcond);
 
 /* Dense LU with partial pivoting, 1-norm rcond (Hager/Higham) and solve.
@@ -174,8 +185,9 @@ int swb_lu_factor(double* A, int64_t n, int64_t lda, int32_t* piv, double* anorm
 int swb_lu_rcond(const double* LU, int64_t n, int64_t lda, const int32_t* piv,
                  const double* anorm, double* rcond_out, void* workspace,
                  size_t workspace_bytes, void* stream);
+size_t swb_lu_solve_workspace_bytes(int64_t n, int64_t nrhs);
 int swb_lu_solve(const double* LU, int64_t n, int64_t lda, const int32_t* piv, double* B,
-                 int64_t nrhs, int64_t ldb, void* stream);
+                 int64_t nrhs, int64_t ldb, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Pass 2 + finalize + hard labels (fastrw.py:456-466, solver.py:55-66,
  * images.py:128-130) for rows [r_begin, r_end):

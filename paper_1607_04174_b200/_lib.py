@@ -58,11 +58,15 @@ SIGNATURES = {
     "swb_small_solve": (C.c_int, [c_dbl, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,
                                   c_dbl, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_sz,
                                   c_vp]),
+    "swb_small_solve_ex": (C.c_int, [c_dbl, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,
+                                     c_dbl, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_sz,
+                                     c_vp, c_vp, c_vp]),
     "swb_check_rcond": (C.c_int, [c_dbl]),
     "swb_lu_workspace_bytes": (c_sz, [c_i64]),
     "swb_lu_factor": (C.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "swb_lu_rcond": (C.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
-    "swb_lu_solve": (C.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp]),
+    "swb_lu_solve_workspace_bytes": (c_sz, [c_i64, c_i64]),
+    "swb_lu_solve": (C.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp, c_sz, c_vp]),
     "swb_reconstruct_label": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_dbl,
                                         c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "swb_gather_rows": (C.c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp]),

@@ -162,6 +162,18 @@ class UpdatedPack(RefreshedPack):
     P = None
 
 
+_SIDE = {}
+
+
+def _side_stream():
+    """Per-device side stream + event for work that overlaps the main stream."""
+    torch = torch_mod()
+    dev = torch.cuda.current_device()
+    if dev not in _SIDE:
+        _SIDE[dev] = (torch.cuda.Stream(), torch.cuda.Event())
+    return _SIDE[dev]
+
+
 def _stencil_ws(lattice, m):
     lat = lattice.c_struct()
     return WORKSPACE.get("stencil", _lib.size("swb_stencil_workspace_bytes", C.byref(lat), m))
@@ -466,9 +478,13 @@ def solve_fast(pack, lap, prob, m_use: int | None = None, streaming_block: int |
     rcond = torch.empty(1, dtype=torch.float64, device="cuda")
     _mark("solve_system")
     sws = WORKSPACE.get("small_solve", _lib.size("swb_small_solve_workspace_bytes", s, m_use, k))
-    _lib.call("swb_small_solve", gamma, s, m_use, k, ptr(q_s), ptr(b_qn), ldq, ptr(bg), ptr(lsu), ptr(dsq_s),
+    # the 1-norm condition estimate runs on a side stream, overlapping the
+    # reconstruction; the current stream joins it before returning
+    side, ev = _side_stream()
+    ev.record()
+    _lib.call("swb_small_solve_ex", gamma, s, m_use, k, ptr(q_s), ptr(b_qn), ldq, ptr(bg), ptr(lsu), ptr(dsq_s),
               dp.dnorm, ptr(slab), ptr(values), ptr(vtg), ptr(t_p), ldt, ptr(coeff), ptr(extra), ptr(rcond),
-              ptr(sws), sws.numel(), st)
+              ptr(sws), sws.numel(), st, C.c_void_p(side.cuda_stream), C.c_void_p(ev.cuda_event))
     if col_map is not None:
         mr = dp.mr
         cf = torch.empty((mr, k), dtype=torch.float64, device="cuda")
@@ -486,6 +502,7 @@ def solve_fast(pack, lap, prob, m_use: int | None = None, streaming_block: int |
 
     _mark("solve_reconstruct")
     U = reconstruct(want_field or k > 8)
+    torch.cuda.current_stream().wait_stream(side)
     _mark("solve_end")
     if check:
         rc = float(rcond.item())

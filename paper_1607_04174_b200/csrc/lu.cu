@@ -221,16 +221,27 @@ __device__ void tri_solve(const double* __restrict__ LU, int64_t n, int64_t lda,
 
 __global__ void __launch_bounds__(1024)
 getrs_kernel(const double* __restrict__ LU, int64_t n, int64_t lda, const int32_t* __restrict__ piv,
-             double* B, int64_t nrhs, int64_t ldb) {
-  // B <- P^T B (LAPACK dlaswp forward)
-  for (int64_t j = 0; j < n; ++j) {
-    const int64_t p = piv[j];
-    if (p != j)
-      for (int64_t c = threadIdx.x; c < nrhs; c += blockDim.x) {
-        const double t = B[j * ldb + c]; B[j * ldb + c] = B[p * ldb + c]; B[p * ldb + c] = t;
-      }
-    __syncthreads();
+             double* B, int64_t nrhs, int64_t ldb, int32_t* __restrict__ perm, double* __restrict__ tmp) {
+  // B <- P^T B (LAPACK dlaswp forward): compose the interchanges into one
+  // permutation (thread 0, O(n)), then gather the rows in parallel
+  if (threadIdx.x == 0) {
+    for (int64_t j = 0; j < n; ++j) perm[j] = static_cast<int32_t>(j);
+    for (int64_t j = 0; j < n; ++j) {
+      const int64_t p = piv[j];
+      if (p != j) { const int32_t t = perm[j]; perm[j] = perm[p]; perm[p] = t; }
+    }
   }
+  __syncthreads();
+  for (int64_t e = threadIdx.x; e < n * nrhs; e += blockDim.x) {
+    const int64_t i = e / nrhs, c = e % nrhs;
+    tmp[e] = B[int64_t(perm[i]) * ldb + c];
+  }
+  __syncthreads();
+  for (int64_t e = threadIdx.x; e < n * nrhs; e += blockDim.x) {
+    const int64_t i = e / nrhs, c = e % nrhs;
+    B[i * ldb + c] = tmp[e];
+  }
+  __syncthreads();
   tri_solve(LU, n, lda, B, nrhs, ldb, 0);
   tri_solve(LU, n, lda, B, nrhs, ldb, 1);
 }
@@ -416,11 +427,19 @@ extern "C" int swb_lu_rcond(const double* LU, int64_t n, int64_t lda, const int3
   return SWB_OK;
 }
 
+extern "C" size_t swb_lu_solve_workspace_bytes(int64_t n, int64_t nrhs) {
+  return swb_align_up(sizeof(int32_t) * size_t(n + 1), 256) + sizeof(double) * size_t(n) * size_t(nrhs > 0 ? nrhs : 1);
+}
+
 extern "C" int swb_lu_solve(const double* LU, int64_t n, int64_t lda, const int32_t* piv, double* B,
-                            int64_t nrhs, int64_t ldb, void* stream) {
+                            int64_t nrhs, int64_t ldb, void* workspace, size_t workspace_bytes, void* stream) {
   if (n < 0 || nrhs < 0 || (n > 0 && (!LU || !piv || !B || lda < n || ldb < nrhs))) return SWB_INVALID_PARAM;
   if (n == 0 || nrhs == 0) return SWB_OK;
-  getrs_kernel<<<1, 1024, 0, swb_stream(stream)>>>(LU, n, lda, piv, B, nrhs, ldb);
+  if (!workspace || workspace_bytes < swb_lu_solve_workspace_bytes(n, nrhs)) return SWB_WORKSPACE_TOO_SMALL;
+  int32_t* perm = static_cast<int32_t*>(workspace);
+  double* tmp = reinterpret_cast<double*>(static_cast<char*>(workspace) +
+                                          swb_align_up(sizeof(int32_t) * size_t(n + 1), 256));
+  getrs_kernel<<<1, 1024, 0, swb_stream(stream)>>>(LU, n, lda, piv, B, nrhs, ldb, perm, tmp);
   SWB_CHECK_LAUNCH();
   return SWB_OK;
 }

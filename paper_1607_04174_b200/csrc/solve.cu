@@ -547,7 +547,7 @@ extern "C" int swb_seed_project(const double* V, int64_t ldv, int64_t row_base, 
 namespace {
 struct SmallLayout {
   int64_t n, lda, ldr, ldm, lds;
-  size_t off_A, off_rhs, off_bw, off_qt, off_piv, off_anorm, off_lu, off_tn, off_proj, off_w, total;
+  size_t off_A, off_rhs, off_bw, off_qt, off_piv, off_anorm, off_lu, off_tn, off_proj, off_w, off_rs, total;
 };
 
 SmallLayout small_layout(int64_t S, int64_t m, int64_t L, int gamma_zero) {
@@ -568,11 +568,19 @@ SmallLayout small_layout(int64_t S, int64_t m, int64_t L, int gamma_zero) {
   Ly.off_lu = take(swb_lu_workspace_bytes(Ly.n));
   Ly.off_proj = take(sizeof(double) * size_t(m) * Ly.ldr);
   Ly.off_w = take(sizeof(double) * size_t(2 * m + S + 1));
+  Ly.off_rs = take(swb_lu_solve_workspace_bytes(Ly.n, L));
   Ly.off_tn = take(S > 0 ? swb_gemm_tn_workspace_bytes(S, m, L) : 0);
   Ly.total = o;
   return Ly;
 }
 }  // namespace
+
+extern "C" int swb_small_solve_ex(double gamma, int64_t S, int64_t m, int64_t L, const double* q_s,
+                                  const double* b_qn, int64_t ldq, const double* bg, const double* lsu,
+                                  const double* dsq_s, double dnorm, const int32_t* seed_lab, const double* values,
+                                  const double* vtg, const double* t_p, int64_t ldt, double* coeff, double* extra,
+                                  double* rcond_out, void* workspace, size_t workspace_bytes, void* stream,
+                                  void* rcond_stream, void* rcond_event);
 
 extern "C" size_t swb_small_solve_workspace_bytes(int64_t S, int64_t m, int64_t L) {
   const SmallLayout a = small_layout(S, m, L, 1), b = small_layout(S, m, L, 0);
@@ -584,6 +592,16 @@ extern "C" int swb_small_solve(double gamma, int64_t S, int64_t m, int64_t L, co
                                const int32_t* seed_lab, const double* values, const double* vtg, const double* t_p,
                                int64_t ldt, double* coeff, double* extra, double* rcond_out, void* workspace,
                                size_t workspace_bytes, void* stream) {
+  return swb_small_solve_ex(gamma, S, m, L, q_s, b_qn, ldq, bg, lsu, dsq_s, dnorm, seed_lab, values, vtg, t_p, ldt,
+                            coeff, extra, rcond_out, workspace, workspace_bytes, stream, nullptr, nullptr);
+}
+
+extern "C" int swb_small_solve_ex(double gamma, int64_t S, int64_t m, int64_t L, const double* q_s,
+                                  const double* b_qn, int64_t ldq, const double* bg, const double* lsu,
+                                  const double* dsq_s, double dnorm, const int32_t* seed_lab, const double* values,
+                                  const double* vtg, const double* t_p, int64_t ldt, double* coeff, double* extra,
+                                  double* rcond_out, void* workspace, size_t workspace_bytes, void* stream,
+                                  void* rcond_stream, void* rcond_event) {
   if (!(gamma >= 0.0) || S < 0 || m <= 0 || L <= 0 || !values || !coeff || !rcond_out) return SWB_INVALID_PARAM;
   if (!(dnorm > 0.0)) return SWB_INVALID_PARAM;
   const int g0 = gamma == 0.0;
@@ -644,7 +662,8 @@ extern "C" int swb_small_solve(double gamma, int64_t S, int64_t m, int64_t L, co
   }
   rc = swb_lu_factor(A, Ly.n, Ly.lda, piv, anorm, luws, swb_lu_workspace_bytes(Ly.n), stream);
   if (rc) return rc;
-  rc = swb_lu_solve(A, Ly.n, Ly.lda, piv, rhs, L, Ly.ldr, stream);
+  rc = swb_lu_solve(A, Ly.n, Ly.lda, piv, rhs, L, Ly.ldr, base + Ly.off_rs, swb_lu_solve_workspace_bytes(Ly.n, L),
+                    stream);
   if (rc) return rc;
   // proj = q_s^T f_s (m x L), reduction over the S seed rows
   rc = swb_gemm_tn(q_s, ldq, rhs, Ly.ldr, S, m, L, 0, proj, Ly.ldr, tnws, swb_gemm_tn_workspace_bytes(S, m, L), stream);
@@ -654,6 +673,14 @@ extern "C" int swb_small_solve(double gamma, int64_t S, int64_t m, int64_t L, co
   if (g0) {
     copy_row_kernel<<<1, 128, 0, st>>>(rhs + S * Ly.ldr, L, extra);
     SWB_CHECK_LAUNCH();
+  }
+  if (rcond_stream && rcond_event) {
+    // condition estimate concurrently with whatever the caller enqueues next
+    // (the reconstruction); the caller joins rcond_stream before reusing the
+    // workspace or reading rcond_out
+    SWB_CUDA_TRY(cudaEventRecord(reinterpret_cast<cudaEvent_t>(rcond_event), st));
+    SWB_CUDA_TRY(cudaStreamWaitEvent(swb_stream(rcond_stream), reinterpret_cast<cudaEvent_t>(rcond_event), 0));
+    return swb_lu_rcond(A, Ly.n, Ly.lda, piv, anorm, rcond_out, luws, swb_lu_workspace_bytes(Ly.n), rcond_stream);
   }
   return swb_lu_rcond(A, Ly.n, Ly.lda, piv, anorm, rcond_out, luws, swb_lu_workspace_bytes(Ly.n), stream);
 }

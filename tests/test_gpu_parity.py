@@ -284,7 +284,8 @@ def test_lu_solve_and_rcond_match_lapack(cuda_ok, n):
     ws = torch.empty(_lib.size("swb_lu_workspace_bytes", n), dtype=torch.uint8, device="cuda")
     st = stream_handle()
     _lib.call("swb_lu_factor", ptr(Ad), n, lda, ptr(piv), ptr(anorm), ptr(ws), ws.numel(), st)
-    _lib.call("swb_lu_solve", ptr(Ad), n, lda, ptr(piv), ptr(Bd), 4, 4, st)
+    rws = torch.empty(_lib.size("swb_lu_solve_workspace_bytes", n, 4), dtype=torch.uint8, device="cuda")
+    _lib.call("swb_lu_solve", ptr(Ad), n, lda, ptr(piv), ptr(Bd), 4, 4, ptr(rws), rws.numel(), st)
     _lib.call("swb_lu_rcond", ptr(Ad), n, lda, ptr(piv), ptr(anorm), ptr(rc), ptr(ws), ws.numel(), st)
     x = np.linalg.solve(A, B)
     np.testing.assert_allclose(Bd.cpu().numpy(), x, rtol=1e-11, atol=1e-12)
