@@ -267,6 +267,18 @@ def e2e_step(state, i, host_labels):
     return field
 
 
+def _ncu_traffic(kernel: str, cfg, dims, m):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture of the
+    same workload (profiles/r1_c4_kernel_metrics.json), else None."""
+    f = ROOT / "profiles" / "r1_c4_kernel_metrics.json"
+    if cfg != "c4" or dims is not None or m != 400 or not f.exists():
+        return None
+    try:
+        return json.loads(f.read_text())["kernels"][kernel]["traffic_bytes"]
+    except (KeyError, ValueError):
+        return None
+
+
 def run_sharded(args):
     """N > 1 ranks (torchrun): the c4 volume split into z-slabs, one per GPU
     (strong scaling).  Step = sharded first-order update (halo exchange +
@@ -517,7 +529,8 @@ def run_gpu(args):
                      "peak": fp64_peak, "unit": "TFLOP/s", "frac": (achieved / fp64_peak) if achieved else None,
                      "peak_source": "live DMMA.8x8x4 probe (swb_fp64_peak_probe) in this run; MEASURED_PEAKS.json "
                                     "has no FP64 entry",
-                     "traffic": None},
+                     "traffic": _ncu_traffic("rotation_nn", cfg, dims, m),
+                     "algorithmic_bytes": 16.0 * n * m},
         "kernels": kernels,
         "update": {"ms": upd_ms, "value": n * m / (upd_ms * 1e-3) if upd_ms else None, "unit": UNIT},
         "solve": {"ms": solve_ms, "value": n / (solve_ms * 1e-3) if solve_ms else None, "unit": "voxels/s"},

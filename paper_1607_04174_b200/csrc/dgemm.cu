@@ -66,61 +66,50 @@ gemm_nn_kernel(const double* __restrict__ A, int64_t lda, const double* __restri
 }
 
 // ---------------------------------------------------------------------------
-// TN kernel: balanced persistent split-K.  The work is n_tiles x nk units
-// (one unit = one BK-row k-step of one output tile); CTA c takes the
-// contiguous unit range [c*upc, (c+1)*upc), which spans at most a few tiles,
-// and writes one partial tile per tile it touched.  Every CTA does the same
-// amount of DMMA work, so one wave of (SMs x occupancy) CTAs finishes
-// together; CTAs at the same position of consecutive tiles read the same
-// rows of X / Y at the same time (L2 reuse).
+// TN kernel: split-K with an integer number of CTAs per output tile.  CTA
+// c = t * per_tile + q computes tile t over row chunk q; every tile uses the
+// same row chunks and the whole grid is one wave, so the CTAs of all tiles
+// stream the same rows of X / Y at the same time and each row is fetched
+// from HBM once (L2 serves the other tiles).  Partial tiles are summed in
+// chunk order (deterministic).
 // ---------------------------------------------------------------------------
 template <int WARPS_M, int WARPS_N, int WTM, int WTN, int STAGES>
 __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 3)
 gemm_tn_kernel(const double* __restrict__ X, int64_t ldx, const double* __restrict__ Y,
                int64_t ldy, int64_t rows, int64_t M1, int64_t M2, int tn, int symmetric,
-               int64_t nk, int64_t total_units, int64_t upc, int max_slots, double* __restrict__ partial) {
+               int per_tile, int64_t chunk_rows, double* __restrict__ partial) {
   using Cf = Cfg<WARPS_M, WARPS_N, WTM, WTN, STAGES, true>;
   extern __shared__ __align__(16) double smem[];
-  const int64_t c = blockIdx.x;
-  int64_t u = c * upc;
-  const int64_t u_end = min(total_units, u + upc);
+  const int c = blockIdx.x;
+  const int t = c / per_tile, q = c % per_tile;
+  const int2 tt = decode_tile(t, tn, symmetric);
+  const int64_t m0 = int64_t(tt.x) * Cf::BM, n0 = int64_t(tt.y) * Cf::BN;
+  const int64_t k_begin = int64_t(q) * chunk_rows;
+  const int64_t k_end = min(rows, k_begin + chunk_rows);
+  double acc[WTM][WTN][2];
+#pragma unroll
+  for (int i = 0; i < WTM; ++i)
+#pragma unroll
+    for (int j = 0; j < WTN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if (k_begin < k_end)
+    mainloop<WARPS_M, WARPS_N, WTM, WTN, STAGES, true>(acc, smem, X, ldx, Y, ldy, k_begin, k_end, m0, M1, n0, M2);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm = warp / WARPS_N, wn = warp % WARPS_N;
-  int slot = 0;
-  while (u < u_end) {
-    const int t = static_cast<int>(u / nk);
-    const int64_t ks = u % nk;
-    const int64_t ke = min(nk, ks + (u_end - u));
-    const int2 tt = decode_tile(t, tn, symmetric);
-    const int64_t m0 = int64_t(tt.x) * Cf::BM, n0 = int64_t(tt.y) * Cf::BN;
-    double acc[WTM][WTN][2];
+  double* dst = partial + int64_t(c) * (Cf::BM * Cf::BN);
 #pragma unroll
-    for (int i = 0; i < WTM; ++i)
+  for (int i = 0; i < WTM; ++i) {
+    const int r = wm * WTM * 8 + i * 8 + (lane >> 2);
 #pragma unroll
-      for (int j = 0; j < WTN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    mainloop<WARPS_M, WARPS_N, WTM, WTN, STAGES, true>(acc, smem, X, ldx, Y, ldy, ks * BK,
-                                                       min(rows, ke * BK), m0, M1, n0, M2);
-    double* dst = partial + (c * max_slots + slot) * (Cf::BM * Cf::BN);
-#pragma unroll
-    for (int i = 0; i < WTM; ++i) {
-      int r = wm * WTM * 8 + i * 8 + (lane >> 2);
-#pragma unroll
-      for (int j = 0; j < WTN; ++j) {
-        int cc = wn * WTN * 8 + j * 8 + 2 * (lane & 3);
-        *reinterpret_cast<double2*>(dst + r * Cf::BN + cc) = make_double2(acc[i][j][0], acc[i][j][1]);
-      }
+    for (int j = 0; j < WTN; ++j) {
+      const int cc = wn * WTN * 8 + j * 8 + 2 * (lane & 3);
+      *reinterpret_cast<double2*>(dst + r * Cf::BN + cc) = make_double2(acc[i][j][0], acc[i][j][1]);
     }
-    __syncthreads();  // smem stages are reused by the next segment
-    u += ke - ks;
-    ++slot;
   }
 }
 
-// out[i, j] = sum over the CTAs that touched the tile, in CTA order
 template <int BM, int BN>
-__global__ void tn_reduce_kernel(const double* __restrict__ partial, int tn, int symmetric,
-                                 int n_tiles, int64_t nk, int64_t upc, int max_slots, int64_t M1, int64_t M2,
-                                 double* __restrict__ out, int64_t ldo) {
+__global__ void tn_reduce_kernel(const double* __restrict__ partial, int tn, int symmetric, int n_tiles, int per_tile,
+                                 int64_t M1, int64_t M2, double* __restrict__ out, int64_t ldo) {
   const int64_t total = int64_t(n_tiles) * BM * BN;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
@@ -131,12 +120,8 @@ __global__ void tn_reduce_kernel(const double* __restrict__ partial, int tn, int
     const int64_t j = int64_t(tt.y) * BN + rc % BN;
     if (i >= M1 || j >= M2) continue;
     if (symmetric && j < i) continue;  // diagonal tiles: keep the upper half
-    const int64_t c_lo = (int64_t(t) * nk) / upc, c_hi = ((int64_t(t) + 1) * nk - 1) / upc;
     double s = 0.0;
-    for (int64_t c = c_lo; c <= c_hi; ++c) {
-      const int64_t first_tile = (c * upc) / nk;
-      s += partial[(c * max_slots + (t - first_tile)) * (BM * BN) + rc];
-    }
+    for (int q = 0; q < per_tile; ++q) s += partial[(int64_t(t) * per_tile + q) * (BM * BN) + rc];
     out[i * ldo + j] = s;
     if (symmetric && j != i) out[j * ldo + i] = s;
   }
@@ -167,10 +152,10 @@ int launch_nn(const double* A, int64_t lda, const double* B, int64_t ldb, int64_
   return SWB_OK;
 }
 
-// TN plan: tiles x k-steps split evenly over one wave of CTAs
+// TN plan: per_tile CTAs per output tile, one wave when possible
 struct TnPlan {
-  int n_tiles, tn, n_ctas, max_slots;
-  int64_t nk, total_units, upc;
+  int n_tiles, tn, per_tile, n_ctas;
+  int64_t chunk_rows;
 };
 
 template <int BM, int BN>
@@ -179,14 +164,14 @@ TnPlan plan_tn(int64_t rows, int64_t M1, int64_t M2, int symmetric, int slots) {
   const int tm = static_cast<int>((M1 + BM - 1) / BM), tn = static_cast<int>((M2 + BN - 1) / BN);
   p.n_tiles = symmetric ? tm * (tm + 1) / 2 : tm * tn;  // symmetric => BM == BN, tm == tn
   p.tn = tn;
-  p.nk = std::max<int64_t>(1, (rows + BK - 1) / BK);
-  p.total_units = p.nk * p.n_tiles;
-  int64_t ctas = std::max(1, slots);
-  const int64_t min_units = 32;  // >= 512 rows per CTA
-  if (ctas > p.total_units / min_units) ctas = std::max<int64_t>(1, p.total_units / min_units);
-  p.upc = (p.total_units + ctas - 1) / ctas;
-  p.n_ctas = static_cast<int>((p.total_units + p.upc - 1) / p.upc);
-  p.max_slots = static_cast<int>((p.upc + p.nk - 1) / p.nk) + 1;
+  int per = std::max(1, slots / p.n_tiles);
+  const int64_t max_per = std::max<int64_t>(1, rows / 512);  // >= 512 rows per chunk
+  if (per > max_per) per = static_cast<int>(max_per);
+  int64_t cr = (rows + per - 1) / per;
+  cr = std::max<int64_t>(BK, (cr + BK - 1) / BK * BK);
+  p.chunk_rows = cr;
+  p.per_tile = static_cast<int>(std::max<int64_t>(1, (rows + cr - 1) / cr));
+  p.n_ctas = p.n_tiles * p.per_tile;
   return p;
 }
 
@@ -217,18 +202,18 @@ int run_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t r
   // (the partial workspace grows with the CTA count)
   const int occ_used = occ > 0 ? occ : 8;
   TnPlan p = plan_tn<Cf::BM, Cf::BN>(rows, M1, M2, symmetric, swb_sm_count() * occ_used);
-  const size_t part_bytes = sizeof(double) * size_t(p.n_ctas) * p.max_slots * Cf::BM * Cf::BN;
+  const size_t part_bytes = sizeof(double) * size_t(p.n_ctas) * Cf::BM * Cf::BN;
   *need = part_bytes;
   if (size_only) return SWB_OK;
   if (ws_bytes < *need || ws == nullptr) return SWB_WORKSPACE_TOO_SMALL;
   double* partial = reinterpret_cast<double*>(ws);
-  kern<<<p.n_ctas, Cf::THREADS, Cf::SMEM, st>>>(X, ldx, Y, ldy, rows, M1, M2, p.tn, symmetric, p.nk,
-                                                p.total_units, p.upc, p.max_slots, partial);
+  kern<<<p.n_ctas, Cf::THREADS, Cf::SMEM, st>>>(X, ldx, Y, ldy, rows, M1, M2, p.tn, symmetric, p.per_tile,
+                                                p.chunk_rows, partial);
   SWB_CHECK_LAUNCH();
   const int64_t total = int64_t(p.n_tiles) * Cf::BM * Cf::BN;
   int rb = static_cast<int>(std::min<int64_t>((total + 255) / 256, int64_t(swb_sm_count()) * 8));
-  tn_reduce_kernel<Cf::BM, Cf::BN><<<rb, 256, 0, st>>>(partial, p.tn, symmetric, p.n_tiles, p.nk, p.upc,
-                                                       p.max_slots, M1, M2, out, ldo);
+  tn_reduce_kernel<Cf::BM, Cf::BN><<<rb, 256, 0, st>>>(partial, p.tn, symmetric, p.n_tiles, p.per_tile, M1, M2,
+                                                       out, ldo);
   SWB_CHECK_LAUNCH();
   return SWB_OK;
 }
