@@ -240,6 +240,20 @@ int swb_argmax_rows(const double* U, int64_t ldu, int64_t N, int64_t L, int32_t*
  * in practice). */
 int swb_fp64_peak_probe(int iters, double* sink, double* flops_out, void* stream);
 
+/* ---- .rwpk pack ingest (fastrw.py:228-325) ----------------------------- */
+/* Streaming XXH64 on the host (state: swb_xxh64_state_bytes() bytes). */
+size_t swb_xxh64_state_bytes(void);
+void swb_xxh64_init(void* state, uint64_t seed);
+void swb_xxh64_update(void* state, const void* data, size_t len);
+uint64_t swb_xxh64_digest(const void* state);
+/* f32 column-major N x m eigenvector block (as stored in a pack) ->
+ * row-major f64 device basis (ld >= m). */
+int swb_f32_colmajor_to_f64_rowmajor(const float* src, int64_t n, int64_t m, double* dst, int64_t ld,
+                                     void* stream);
+/* and back (save_pack): first m columns (through col_map if given). */
+int swb_f64_rowmajor_to_f32_colmajor(const double* src, int64_t n, int64_t ld, int64_t m,
+                                     const int32_t* col_map, float* dst, void* stream);
+
 /* ---- small helpers used by the host layer --------------------------- */
 /* out = sum_x v[x]^2 over n entries (deterministic). */
 int swb_sumsq(const double* v, int64_t n, double* out, void* workspace,

@@ -16,7 +16,8 @@ from .types import (AdaptivePolicy, EigenBasis, Image, LabelMap, LabelProblem, L
                     PackSet, ProbabilityField, SeedPartition, SpectralPack, SENTINEL_UNLABELED)
 from .device import DeviceGraph, DevicePack, LatticeSpec, to_device
 from .api import (DeviceField, RefreshedPack, UpdatedPack, hard_labels, nearest_pack, refresh,
-                  refresh_from_set, select_m, solve_fast, update_basis)
+                  refresh_from_set, segment, select_m, solve_fast, update_basis)
+from .packs import load_pack, save_pack, xxh64
 
 __version__ = "0.1.0"
 

@@ -79,6 +79,12 @@ SIGNATURES = {
     "swb_prior_hat": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp]),
     "swb_argmax_rows": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "swb_fp64_peak_probe": (C.c_int, [C.c_int, c_vp, C.POINTER(c_dbl), c_vp]),
+    "swb_xxh64_state_bytes": (c_sz, []),
+    "swb_xxh64_init": (None, [c_vp, C.c_uint64]),
+    "swb_xxh64_update": (None, [c_vp, c_vp, c_sz]),
+    "swb_xxh64_digest": (C.c_uint64, [c_vp]),
+    "swb_f32_colmajor_to_f64_rowmajor": (C.c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp]),
+    "swb_f64_rowmajor_to_f32_colmajor": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "swb_sumsq": (C.c_int, [c_vp, c_i64, c_vp, c_vp, c_sz, c_vp]),
     "swb_gather_columns": (C.c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp]),
 }

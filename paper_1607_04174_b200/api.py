@@ -520,7 +520,7 @@ def hard_labels(field) -> LabelMap:
     if isinstance(field, DeviceField):
         return LabelMap(field.dims, field.labels_dev.cpu().numpy())
     torch = require_cuda()
-    vals = np.ascontiguousarray(np.asarray(field.values, dtype=np.float64))
+    vals = np.array(field.values, dtype=np.float64)
     n, k = vals.shape
     U = torch.from_numpy(vals).to("cuda")
     labels = torch.empty(n, dtype=torch.int32, device="cuda")
@@ -619,3 +619,51 @@ def select_m(pack, prob, policy=None):
             return m, info
     info["saturated"] = True
     return M, info
+
+
+# ---------------------------------------------------------------------------
+# segment: the CLI "segment" flow as one library call (cli.py:126-163)
+# ---------------------------------------------------------------------------
+
+def segment(image, packs, seeds, gamma: float = 0.0, beta_online: float | None = None, adaptive: bool = False,
+            m_use: int | None = None, epsilon: float = 0.1, method: str = "rayleigh", want_field: bool = False):
+    """Library form of ``specwalk segment`` (cli.py:126-163).
+
+    ``packs``: a PackSet / sequence of host or device packs of ``image``;
+    ``seeds``: a SeedPartition.  With ``beta_online`` the nearest pack (log
+    beta) is refreshed (``method="rayleigh"``, the reference) or updated to
+    first order (``method="first_order"``).  gamma > 0 uses uniform priors
+    like the CLI.  Returns (LabelMap, field, report dict)."""
+    from .types import AdaptivePolicy, LabelProblem, PackSet
+    if not isinstance(packs, PackSet):
+        packs = PackSet(tuple(sorted(packs, key=lambda p: p.beta)))
+    h = image_hash(image)
+    for p in packs.packs:
+        if p.provenance.image_hash != h:
+            raise ImageMismatch("pack was not built from this image")
+    k = seeds.num_labels
+    n = image.n_voxels
+    priors = None if gamma == 0 else np.full((n, k), 1.0 / k)
+    prob = LabelProblem(num_labels=k, seeds=seeds, gamma=gamma, priors=priors)
+    refreshed = False
+    if beta_online is not None:
+        base = nearest_pack(packs, beta_online)
+        if method == "rayleigh":
+            pack = refresh(base, image, beta_online)
+        else:
+            pack = update_basis(base, image, beta_online, method=method)
+        lap = pack.laplacian
+        refreshed = True
+        base_beta = base.beta
+    else:
+        pack = _as_device(packs.packs[0], image)
+        lap = pack.ensure_graph()
+        base_beta = pack.beta
+    if adaptive:
+        m_use, _ = select_m(pack, prob, AdaptivePolicy(epsilon=epsilon))
+    elif m_use is None:
+        m_use = pack.m
+    field = solve_fast(pack, lap, prob, m_use=m_use, want_field=want_field)
+    labels = hard_labels(field)
+    report = {"m_use": int(m_use), "refreshed": refreshed, "base_beta": float(base_beta), "num_labels": k}
+    return labels, field, report

@@ -299,6 +299,25 @@ def case_errors():
     np.savez_compressed(OUT / "errors.npz", **out)
 
 
+def case_pack_file():
+    """A reference-written .rwpk file + what the reference loads from it."""
+    ph = sw.make_phantom("blobs2d", (12, 10), rng_seed=2, noise_sigma=0.05, num_regions=2)
+    pack = sw.precompute(ph.image, 15.0, m=12)
+    path = OUT / "small.rwpk"
+    sw.save_pack(pack, path)
+    loaded = sw.load_pack(path)
+    seeds = seeds_of(ph, 3, 4)
+    lap = sw.laplacian(sw.build_graph(ph.image, 15.0), LaplacianMode.NORMALIZED)
+    prob = sw.LabelProblem(num_labels=2, seeds=seeds, gamma=0.0)
+    u = sw.solve_fast(loaded, lap, prob)
+    np.savez_compressed(OUT / "pack_file.npz", V=np.asarray(loaded.eigen.vectors), lam=loaded.eigen.values,
+                        d_sqrt=loaded.d_sqrt, beta=loaded.beta, dims=np.array(loaded.dims),
+                        intensities=ph.image.intensities, image_hash=np.frombuffer(loaded.provenance.image_hash,
+                                                                                    dtype=np.uint8),
+                        seeds_idx=seeds.seed_indices, seeds_lab=seeds.seed_labels, U=u.values,
+                        xxh_empty=sw.xxh64(b""), xxh_a=sw.xxh64(b"a"))
+
+
 if __name__ == "__main__":
     case_path3()
     case_phantom16()
@@ -306,5 +325,6 @@ if __name__ == "__main__":
     case_modes()
     case_adaptive_kats()
     case_errors()
+    case_pack_file()
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size)
