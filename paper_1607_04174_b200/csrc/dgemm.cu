@@ -280,9 +280,11 @@ int swb_gemm_nn_alpha(const double* A, int64_t lda, const double* B, int64_t ldb
   if (p32 < best) { best = p32; which = 32; }
   switch (which) {
     case 128: return launch_nn<4, 2, 4, 8, 3>(A, lda, B, ldb, rows, K, M2, out, ldo, accumulate, alpha, st);
-    case 64: return launch_nn<4, 2, 4, 4, 3>(A, lda, B, ldb, rows, K, M2, out, ldo, accumulate, alpha, st);
+    case 64: return launch_nn<2, 2, 8, 4, 3>(A, lda, B, ldb, rows, K, M2, out, ldo, accumulate, alpha, st);
     case 32: return launch_nn<4, 2, 4, 2, 3>(A, lda, B, ldb, rows, K, M2, out, ldo, accumulate, alpha, st);
-    default: return launch_nn<4, 2, 4, 5, 3>(A, lda, B, ldb, rows, K, M2, out, ldo, accumulate, alpha, st);
+    // 4 warps x (64 x 40) warp tiles: 40 independent DMMAs per k-step per warp
+    // measured best on B200 (tools/gemm_tune.cu: 33.5 vs 32.9 TFLOP/s for 8 x (32 x 40))
+    default: return launch_nn<2, 2, 8, 5, 3>(A, lda, B, ldb, rows, K, M2, out, ldo, accumulate, alpha, st);
   }
 }
 
