@@ -225,7 +225,7 @@ struct Ring5 {
   static constexpr int V_DBL = NS * 64;
   static constexpr int C_DBL = (NL * LCD + 1) / 2 * 2;
   static constexpr int STAGE_DBL = V_DBL + C_DBL;
-  static constexpr int PREF = 3;
+  static constexpr int PREF = 5;
   static constexpr int RING = PREF + 2;
   // slot of extended line (zi, yi), zi in [-1, ZB], yi in [-1, YB]; -1 = unused corner
   __host__ __device__ static constexpr int slot(int zi, int yi) {
@@ -352,11 +352,14 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
       if (xp < nxi) {
         double* stg = ring + pst * SD;
 #pragma unroll
-        for (int i = 0; i < VPT; ++i)
-          if (threadIdx.x + i * ST_WARPS * 32 < VCH) cp_async16(stg + vdst[i], vsrc[i] + int64_t(xp) * ldv, vok[i]);
+        for (int i = 0; i < VPT; ++i) {
+          if (threadIdx.x + i * ST_WARPS * 32 < VCH) cp_async16(stg + vdst[i], vsrc[i], vok[i]);
+          if (vok[i]) vsrc[i] += ldv;  // next row (pointer increments only)
+        }
         if (threadIdx.x < CSL) {
-          if (cbytes == 16) cp_async16(stg + cdst, csrc + int64_t(xp) * cstride, cok);
-          else cp_async8(stg + cdst, csrc + int64_t(xp) * cstride, cok);
+          if (cbytes == 16) cp_async16(stg + cdst, csrc, cok);
+          else cp_async8(stg + cdst, csrc, cok);
+          if (cok) csrc += cstride;
         }
         ++xp;
         pst = pst + 1 == RING ? 0 : pst + 1;
@@ -397,8 +400,15 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
           else if (t.kind == 1) { slot = t.dir; cs = sc; }
           else { slot = t.dz < 0 ? 2 * ND + 1 + t.dir : t.dy < 0 ? ND + 1 + t.dir : t.dir; cs = vs; }
           const double* cp = cs + Rg::V_DBL + warp * LCD + slot * CW;
-          const double cn = cp[0];
-          const double co = DELTA ? cp[1] : 0.0;
+          double cn, co;
+          if (DELTA) {
+            const double2 pr = *reinterpret_cast<const double2*>(cp);  // (new, old) in one 16-B load
+            cn = pr.x;
+            co = pr.y;
+          } else {
+            cn = cp[0];
+            co = 0.0;
+          }
           if (t.kind == 0) {
             lx = __dadd_rn(lx, __dmul_rn(cn, val.x));
             ly = __dadd_rn(ly, __dmul_rn(cn, val.y));
