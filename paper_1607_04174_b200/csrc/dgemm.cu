@@ -128,6 +128,190 @@ __global__ void tn_reduce_kernel(const double* __restrict__ partial, int tn, int
 }
 
 // ---------------------------------------------------------------------------
+// Symmetric TN (P = V^T W, upper triangle only).  Off-diagonal tiles run the
+// regular 4-warp (W x W cells of 8x8 per warp) tile; a diagonal tile needs
+// only the G(G+1)/2 upper cells of its G x G cell grid (G = 2W), split over
+// the 4 warps by pairing rows, so it costs ~60 % of a full tile and gets
+// proportionally longer row chunks.  One launch, one wave: CTAs
+// [0, n_full*per_full) do off-diagonal tiles, the rest diagonal tiles.
+// ---------------------------------------------------------------------------
+// row lists per warp (-1 = none): G = 10 -> {0,7,9} {1,6} {2,5} {3,4,8}
+//                                 G =  8 -> {0,7}   {1,6} {2,5} {3,4}
+__host__ __device__ constexpr int diag_row(int G, int w, int k) {
+  return G == 10 ? (w == 0 ? (k == 0 ? 0 : k == 1 ? 7 : 9)
+                  : w == 1 ? (k == 0 ? 1 : k == 1 ? 6 : -1)
+                  : w == 2 ? (k == 0 ? 2 : k == 1 ? 5 : -1)
+                           : (k == 0 ? 3 : k == 1 ? 4 : 8))
+                 : (k == 2 ? -1 : w == 0 ? (k == 0 ? 0 : 7) : w == 1 ? (k == 0 ? 1 : 6)
+                                : w == 2 ? (k == 0 ? 2 : 5) : (k == 0 ? 3 : 4));
+}
+__host__ __device__ constexpr int diag_cells(int G, int w) {
+  int n = 0;
+  for (int k = 0; k < 3; ++k)
+    if (diag_row(G, w, k) >= 0) n += G - diag_row(G, w, k);
+  return n;
+}
+__host__ __device__ constexpr int diag_max_cells(int G) {
+  int m = 0;
+  for (int w = 0; w < 4; ++w) m = diag_cells(G, w) > m ? diag_cells(G, w) : m;
+  return m;
+}
+
+template <int G, int WID, int A_LD, int B_LD>
+__device__ __forceinline__ void diag_compute(double (&acc)[diag_max_cells(G)][2], const double* sA, const double* sB,
+                                             int lr, int lc) {
+#pragma unroll
+  for (int kk = 0; kk < BK / 4; ++kk) {
+    const int k = kk * 4 + lc;
+    double af[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      constexpr int dummy = 0;
+      (void)dummy;
+      const int r = diag_row(G, WID, q);
+      af[q] = r >= 0 ? sA[k * A_LD + r * 8 + lr] : 0.0;
+    }
+    int cell = 0;
+#pragma unroll
+    for (int c = 0; c < G; ++c) {
+      bool need = false;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) need |= (diag_row(G, WID, q) >= 0 && diag_row(G, WID, q) <= c);
+      if (!need) continue;
+      const double bf = sB[k * B_LD + c * 8 + lr];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int r = diag_row(G, WID, q);
+        if (r < 0 || r > c) continue;
+        // cell index = position of (r, c) in the warp's row-major cell list
+        int idx = 0;
+#pragma unroll
+        for (int q2 = 0; q2 < q; ++q2)
+          if (diag_row(G, WID, q2) >= 0) idx += G - diag_row(G, WID, q2);
+        idx += c - r;
+        dmma_8x8x4(acc[idx][0], acc[idx][1], af[q], bf);
+        (void)cell;
+      }
+    }
+  }
+}
+
+template <int G, int WID>
+__device__ __forceinline__ void diag_store(const double (&acc)[diag_max_cells(G)][2], double* dst, int BN, int lane) {
+  int idx = 0;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const int r = diag_row(G, WID, q);
+    if (r < 0) continue;
+#pragma unroll
+    for (int c = 0; c < G; ++c) {
+      if (c < r) continue;
+      const int row = r * 8 + (lane >> 2), col = c * 8 + 2 * (lane & 3);
+      *reinterpret_cast<double2*>(dst + row * BN + col) = make_double2(acc[idx][0], acc[idx][1]);
+      ++idx;
+    }
+  }
+}
+
+template <int W, int STAGES>
+__global__ void __launch_bounds__(128, 3)
+gemm_tn_sym_kernel(const double* __restrict__ X, int64_t ldx, const double* __restrict__ Y, int64_t ldy,
+                   int64_t rows, int64_t M, int T, int per_full, int64_t chunk_full, int per_diag,
+                   int64_t chunk_diag, double* __restrict__ partial) {
+  using Cf = Cfg<2, 2, W, W, STAGES, true>;
+  constexpr int G = 2 * W;
+  extern __shared__ __align__(16) double smem[];
+  const int c = blockIdx.x;
+  const int n_full = T * (T - 1) / 2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* dst = partial + int64_t(c) * (Cf::BM * Cf::BN);
+  if (c < n_full * per_full) {
+    // off-diagonal tile f -> (i, j), i < j
+    int f = c / per_full;
+    const int q = c % per_full;
+    int i = 0;
+    while (f >= T - 1 - i) { f -= T - 1 - i; ++i; }
+    const int j = i + 1 + f;
+    const int64_t kb = int64_t(q) * chunk_full, ke = min(rows, kb + chunk_full);
+    double acc[W][W][2];
+#pragma unroll
+    for (int a = 0; a < W; ++a)
+#pragma unroll
+      for (int b = 0; b < W; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    if (kb < ke)
+      mainloop<2, 2, W, W, STAGES, true>(acc, smem, X, ldx, Y, ldy, kb, ke, int64_t(i) * Cf::BM, M,
+                                         int64_t(j) * Cf::BN, M);
+    const int wm = warp / 2, wn = warp % 2;
+#pragma unroll
+    for (int a = 0; a < W; ++a) {
+      const int r = wm * W * 8 + a * 8 + (lane >> 2);
+#pragma unroll
+      for (int b = 0; b < W; ++b) {
+        const int cc = wn * W * 8 + b * 8 + 2 * (lane & 3);
+        *reinterpret_cast<double2*>(dst + r * Cf::BN + cc) = make_double2(acc[a][b][0], acc[a][b][1]);
+      }
+    }
+    return;
+  }
+  const int d = c - n_full * per_full;
+  const int i = d / per_diag, q = d % per_diag;
+  const int64_t kb = int64_t(q) * chunk_diag, ke = min(rows, kb + chunk_diag);
+  double acc[diag_max_cells(G)][2];
+#pragma unroll
+  for (int a = 0; a < diag_max_cells(G); ++a) acc[a][0] = acc[a][1] = 0.0;
+  const int lr = lane >> 2, lc = lane & 3;
+  if (kb < ke) {
+    pipeline<2, 2, W, W, STAGES, true>(
+        smem, X, ldx, Y, ldy, kb, ke, int64_t(i) * Cf::BM, M, int64_t(i) * Cf::BN, M,
+        [&](const double* sA, const double* sB) {
+          switch (warp) {
+            case 0: diag_compute<G, 0, Cf::A_LD, Cf::B_LD>(acc, sA, sB, lr, lc); break;
+            case 1: diag_compute<G, 1, Cf::A_LD, Cf::B_LD>(acc, sA, sB, lr, lc); break;
+            case 2: diag_compute<G, 2, Cf::A_LD, Cf::B_LD>(acc, sA, sB, lr, lc); break;
+            default: diag_compute<G, 3, Cf::A_LD, Cf::B_LD>(acc, sA, sB, lr, lc); break;
+          }
+        });
+  }
+  switch (warp) {
+    case 0: diag_store<G, 0>(acc, dst, Cf::BN, lane); break;
+    case 1: diag_store<G, 1>(acc, dst, Cf::BN, lane); break;
+    case 2: diag_store<G, 2>(acc, dst, Cf::BN, lane); break;
+    default: diag_store<G, 3>(acc, dst, Cf::BN, lane); break;
+  }
+}
+
+// out[i, j] (i <= j) = sum of the tile's CTA partials (fixed order), mirrored
+template <int BM>
+__global__ void tn_sym_reduce_kernel(const double* __restrict__ partial, int T, int per_full, int per_diag, int64_t M,
+                                     double* __restrict__ out, int64_t ldo) {
+  const int n_tiles = T * (T + 1) / 2;
+  const int n_full = T * (T - 1) / 2;
+  const int64_t total = int64_t(n_tiles) * BM * BM;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int t = static_cast<int>(e / (BM * BM));
+    const int rc = static_cast<int>(e % (BM * BM));
+    const int2 tt = decode_tile(t, T, 1);
+    const int64_t i = int64_t(tt.x) * BM + rc / BM, j = int64_t(tt.y) * BM + rc % BM;
+    if (i >= M || j >= M || j < i) continue;
+    int c0, cnt;
+    if (tt.x == tt.y) {
+      c0 = n_full * per_full + tt.x * per_diag;
+      cnt = per_diag;
+    } else {
+      int f = 0;
+      for (int a = 0; a < tt.x; ++a) f += T - 1 - a;
+      f += tt.y - tt.x - 1;
+      c0 = f * per_full;
+      cnt = per_full;
+    }
+    double s = 0.0;
+    for (int q = 0; q < cnt; ++q) s += partial[int64_t(c0 + q) * (BM * BM) + rc];
+    out[i * ldo + j] = s;
+    if (j != i) out[j * ldo + i] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host-side dispatch
 // ---------------------------------------------------------------------------
 template <int WARPS_M, int WARPS_N, int WTM, int WTN, int STAGES>
@@ -218,14 +402,59 @@ int run_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t r
   return SWB_OK;
 }
 
+template <int W>
+int run_tn_sym(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t rows, int64_t M, double* out,
+               int64_t ldo, void* ws, size_t ws_bytes, cudaStream_t st, bool size_only, size_t* need) {
+  using Cf = Cfg<2, 2, W, W, TN_STAGES, true>;
+  constexpr int G = 2 * W;
+  auto kern = gemm_tn_sym_kernel<W, TN_STAGES>;
+  static int occ = 0;
+  if (occ == 0 && !size_only) {
+    SWB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cf::SMEM)));
+    SWB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cf::THREADS, Cf::SMEM));
+    if (occ < 1) occ = 1;
+  }
+  const int slots = swb_sm_count() * (occ > 0 ? occ : 8);
+  const int T = static_cast<int>((M + Cf::BM - 1) / Cf::BM);
+  const int n_full = T * (T - 1) / 2;
+  const double ratio = double(diag_max_cells(G)) / double(W * W);  // diagonal / full tile cost
+  int per_full = std::max(1, static_cast<int>(slots / (n_full + ratio * T)));
+  const int64_t max_per = std::max<int64_t>(1, rows / 512);
+  if (per_full > max_per) per_full = static_cast<int>(max_per);
+  int per_diag = std::max(1, static_cast<int>(ratio * per_full + 0.5));
+  int64_t chunk_full = std::max<int64_t>(BK, ((rows + per_full - 1) / per_full + BK - 1) / BK * BK);
+  int64_t chunk_diag = std::max<int64_t>(BK, ((rows + per_diag - 1) / per_diag + BK - 1) / BK * BK);
+  per_full = static_cast<int>((rows + chunk_full - 1) / chunk_full);
+  per_diag = static_cast<int>((rows + chunk_diag - 1) / chunk_diag);
+  if (per_full < 1) per_full = 1;
+  if (per_diag < 1) per_diag = 1;
+  const int n_ctas = n_full * per_full + T * per_diag;
+  *need = sizeof(double) * size_t(n_ctas) * Cf::BM * Cf::BN;
+  if (size_only) return SWB_OK;
+  if (ws_bytes < *need || ws == nullptr) return SWB_WORKSPACE_TOO_SMALL;
+  double* partial = reinterpret_cast<double*>(ws);
+  kern<<<n_ctas, Cf::THREADS, Cf::SMEM, st>>>(X, ldx, Y, ldy, rows, M, T, per_full, chunk_full, per_diag, chunk_diag,
+                                              partial);
+  SWB_CHECK_LAUNCH();
+  const int64_t total = int64_t(T * (T + 1) / 2) * Cf::BM * Cf::BN;
+  int rb = static_cast<int>(std::min<int64_t>((total + 255) / 256, int64_t(swb_sm_count()) * 8));
+  tn_sym_reduce_kernel<Cf::BM><<<rb, 256, 0, st>>>(partial, T, per_full, per_diag, M, out, ldo);
+  SWB_CHECK_LAUNCH();
+  return SWB_OK;
+}
+
 int dispatch_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t rows, int64_t M1,
                 int64_t M2, int symmetric, double* out, int64_t ldo, void* ws, size_t ws_bytes,
                 cudaStream_t st, bool size_only, size_t* need) {
   switch (choose_tn(M1, M2)) {
     case TN_80x80:
+      if (symmetric)
+        return run_tn_sym<5>(X, ldx, Y, ldy, rows, M1, out, ldo, ws, ws_bytes, st, size_only, need);
       return run_tn<2, 2, 5, 5>(X, ldx, Y, ldy, rows, M1, M2, symmetric, out, ldo, ws, ws_bytes, st,
                                 size_only, need);
     case TN_64x64:
+      if (symmetric)
+        return run_tn_sym<4>(X, ldx, Y, ldy, rows, M1, out, ldo, ws, ws_bytes, st, size_only, need);
       return run_tn<2, 2, 4, 4>(X, ldx, Y, ldy, rows, M1, M2, symmetric, out, ldo, ws, ws_bytes, st,
                                 size_only, need);
     default:

@@ -89,15 +89,12 @@ __device__ __forceinline__ void load_stage(double* sA, double* sB, const double*
 
 __device__ __forceinline__ int clamp_int(int64_t v, int hi) { return v < 0 ? 0 : (v > hi ? hi : static_cast<int>(v)); }
 
-template <int WARPS_M, int WARPS_N, int WTM, int WTN, int STAGES, bool TN>
-__device__ __forceinline__ void mainloop(double (&acc)[WTM][WTN][2], double* smem,
-                                         const double* A, int64_t lda, const double* B,
-                                         int64_t ldb, int64_t k_begin, int64_t k_end,
-                                         int64_t m0, int64_t m_lim, int64_t n0, int64_t n_lim) {
+// Pipelined k-loop; `compute(sA, sB)` consumes one BK-deep stage.
+template <int WARPS_M, int WARPS_N, int WTM, int WTN, int STAGES, bool TN, class Compute>
+__device__ __forceinline__ void pipeline(double* smem, const double* A, int64_t lda, const double* B, int64_t ldb,
+                                         int64_t k_begin, int64_t k_end, int64_t m0, int64_t m_lim, int64_t n0,
+                                         int64_t n_lim, Compute&& compute) {
   using Cf = Cfg<WARPS_M, WARPS_N, WTM, WTN, STAGES, TN>;
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int wm = warp / WARPS_N, wn = warp % WARPS_N;
   const int nk = static_cast<int>((k_end - k_begin + BK - 1) / BK);
   const bool b_vec = ((ldb & 1) == 0) && ((reinterpret_cast<uintptr_t>(B) & 15) == 0);
   // tile-base pointers of the first k-slice and their per-stage advance
@@ -105,9 +102,9 @@ __device__ __forceinline__ void mainloop(double (&acc)[WTM][WTN][2], double* sme
   const int64_t a_step = TN ? BK * lda : BK;
   const double* b_t = B + k_begin * ldb + n0;
   const int64_t b_step = BK * ldb;
-  const int m_rows = clamp_int(m_lim - m0, TN ? Cf::BM : Cf::BM);
+  const int m_rows = clamp_int(m_lim - m0, Cf::BM);
   const int n_cols = clamp_int(n_lim - n0, Cf::BN);
-  int k_left = static_cast<int>(k_end - k_begin);  // fits: k extents are per-CTA row chunks (< 2^31)
+  const int k_left = static_cast<int>(k_end - k_begin);  // per-CTA row chunks (< 2^31)
 
   auto issue = [&](int slot, int kt) {
     double* st = smem + slot * Cf::STAGE_ELEMS;
@@ -127,8 +124,6 @@ __device__ __forceinline__ void mainloop(double (&acc)[WTM][WTN][2], double* sme
     if (s < nk) issue(s, s);
     cp_async_commit();
   }
-
-  const int lr = lane >> 2, lc = lane & 3;
   int slot = 0;                 // stage being consumed
   int fill = STAGES - 1;        // stage being filled next
   for (int kt = 0; kt < nk; ++kt) {
@@ -138,30 +133,45 @@ __device__ __forceinline__ void mainloop(double (&acc)[WTM][WTN][2], double* sme
     cp_async_commit();
     fill = fill + 1 == STAGES ? 0 : fill + 1;
     const double* sA = smem + slot * Cf::STAGE_ELEMS;
-    const double* sB = sA + Cf::A_ELEMS;
     slot = slot + 1 == STAGES ? 0 : slot + 1;
-#pragma unroll
-    for (int kk = 0; kk < BK / 4; ++kk) {
-      double af[WTM], bf[WTN];
-#pragma unroll
-      for (int i = 0; i < WTM; ++i) {
-        const int m = wm * WTM * 8 + i * 8 + lr;
-        const int k = kk * 4 + lc;
-        af[i] = TN ? sA[k * Cf::A_LD + m] : sA[m * Cf::A_LD + k];
-      }
-#pragma unroll
-      for (int j = 0; j < WTN; ++j) {
-        const int n = wn * WTN * 8 + j * 8 + lr;
-        const int k = kk * 4 + lc;
-        bf[j] = sB[k * Cf::B_LD + n];
-      }
-#pragma unroll
-      for (int i = 0; i < WTM; ++i)
-#pragma unroll
-        for (int j = 0; j < WTN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-    }
+    compute(sA, sA + Cf::A_ELEMS);
   }
   cp_async_wait<0>();
+}
+
+template <int WARPS_M, int WARPS_N, int WTM, int WTN, int STAGES, bool TN>
+__device__ __forceinline__ void mainloop(double (&acc)[WTM][WTN][2], double* smem,
+                                         const double* A, int64_t lda, const double* B,
+                                         int64_t ldb, int64_t k_begin, int64_t k_end,
+                                         int64_t m0, int64_t m_lim, int64_t n0, int64_t n_lim) {
+  using Cf = Cfg<WARPS_M, WARPS_N, WTM, WTN, STAGES, TN>;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int wm = warp / WARPS_N, wn = warp % WARPS_N;
+  const int lr = lane >> 2, lc = lane & 3;
+  pipeline<WARPS_M, WARPS_N, WTM, WTN, STAGES, TN>(
+      smem, A, lda, B, ldb, k_begin, k_end, m0, m_lim, n0, n_lim, [&](const double* sA, const double* sB) {
+#pragma unroll
+        for (int kk = 0; kk < BK / 4; ++kk) {
+          double af[WTM], bf[WTN];
+#pragma unroll
+          for (int i = 0; i < WTM; ++i) {
+            const int m = wm * WTM * 8 + i * 8 + lr;
+            const int k = kk * 4 + lc;
+            af[i] = TN ? sA[k * Cf::A_LD + m] : sA[m * Cf::A_LD + k];
+          }
+#pragma unroll
+          for (int j = 0; j < WTN; ++j) {
+            const int n = wn * WTN * 8 + j * 8 + lr;
+            const int k = kk * 4 + lc;
+            bf[j] = sB[k * Cf::B_LD + n];
+          }
+#pragma unroll
+          for (int i = 0; i < WTM; ++i)
+#pragma unroll
+            for (int j = 0; j < WTN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+      });
 }
 
 }  // namespace swb_core
