@@ -240,6 +240,16 @@ int swb_argmax_rows(const double* U, int64_t ldu, int64_t N, int64_t L, int32_t*
  * in practice). */
 int swb_fp64_peak_probe(int iters, double* sink, double* flops_out, void* stream);
 
+/* ---- registration data term (registration.py:95-129) ------------------ */
+/* priors[x*ldp + k] = softmax_k(-(s_k(x)/sigma)^2), s_k = edge-clamped mean
+ * |F - M shifted by disp_k| over the (2r+1)^d patch, sigma = max(mean_x
+ * min_k s_k, 1e-8) (device double *sigma_out).  disp: K x 3 int32 (x, y, z). */
+size_t swb_similarity_priors_workspace_bytes(int64_t N, int64_t K);
+int swb_similarity_priors(const double* fixed, const double* moving, int64_t nx, int64_t ny, int64_t nz,
+                          int32_t ndim, const int32_t* disp, int64_t K, int32_t patch_radius,
+                          double* priors, int64_t ldp, double* sigma_out, void* workspace,
+                          size_t workspace_bytes, void* stream);
+
 /* ---- .rwpk pack ingest (fastrw.py:228-325) ----------------------------- */
 /* Streaming XXH64 on the host (state: swb_xxh64_state_bytes() bytes). */
 size_t swb_xxh64_state_bytes(void);

@@ -511,3 +511,49 @@ def nearest_beta(betas, new_beta: float) -> int:
         return abs(math.log(new_beta) - math.log(b))
     best = min(range(len(betas)), key=lambda i: dist(betas[i]))
     return best
+
+
+# ---------------------------------------------------------------------------
+# registration data term (registration.py:27-136)
+# ---------------------------------------------------------------------------
+
+def grid_vectors(extents, step: int = 1) -> np.ndarray:
+    """registration.py:44-48: displacement table, x offset fastest."""
+    extents = tuple(int(e) for e in extents)
+    k = int(np.prod(extents))
+    out = np.empty((k, len(extents)), dtype=np.int64)
+    rem = np.arange(k)
+    for a, e in enumerate(extents):
+        out[:, a] = rem % e
+        rem = rem // e
+    return (out - np.array([(e - 1) // 2 for e in extents])) * step
+
+
+def similarity_priors(fixed, moving, dims, vectors, patch_radius: int = 2):
+    """registration.py:95-129: returns (priors N x K, sigma)."""
+    dims = tuple(dims)
+    d = len(dims)
+    f = np.asarray(fixed, dtype=np.float64).reshape(dims, order="F")
+    m = np.asarray(moving, dtype=np.float64).reshape(dims, order="F")
+
+    def shifted(g, off):
+        out = g
+        for axis, o in enumerate(off):
+            idx = np.clip(np.arange(g.shape[axis]) + int(o), 0, g.shape[axis] - 1)
+            out = np.take(out, idx, axis=axis)
+        return out
+
+    offs = np.stack(np.meshgrid(*([np.arange(-patch_radius, patch_radius + 1)] * d), indexing="ij"),
+                    axis=-1).reshape(-1, d)
+    scores = np.empty((f.size, len(vectors)))
+    for k, disp in enumerate(vectors):
+        acc = np.zeros(dims)
+        for off in offs:
+            acc += np.abs(shifted(f, off) - shifted(m, off + disp))
+        scores[:, k] = (acc / len(offs)).reshape(-1, order="F")
+    sigma = max(scores.min(axis=1).mean(), 1e-8)
+    logits = -((scores / sigma) ** 2)
+    logits -= logits.max(axis=1, keepdims=True)
+    vals = np.exp(logits)
+    vals /= vals.sum(axis=1, keepdims=True)
+    return vals, sigma

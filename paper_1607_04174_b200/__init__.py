@@ -18,6 +18,7 @@ from .device import DeviceGraph, DevicePack, LatticeSpec, to_device
 from .api import (DeviceField, RefreshedPack, UpdatedPack, hard_labels, nearest_pack, refresh,
                   refresh_from_set, segment, select_m, solve_fast, update_basis)
 from .packs import load_pack, save_pack, xxh64
+from .registration import DevicePriors, DisplacementGrid, expected_displacement, similarity_priors
 
 __version__ = "0.1.0"
 

@@ -407,7 +407,7 @@ def solve_fast(pack, lap, prob, m_use: int | None = None, streaming_block: int |
         raise InsufficientBasis(f"m_use={m_use} cannot represent {k} labels")
     if getattr(prob.laplacian_mode, "value", "normalized") != LaplacianMode.NORMALIZED.value:
         raise InvalidParam("the fast path requires the normalized mode")
-    if lap is not None and lap.n_vertices != n:
+    if lap is not None and (lap.n_vertices if hasattr(lap, "n_vertices") else lap.shape[0]) != n:
         raise InvalidParam("Laplacian size does not match the pack")
     seeds = prob.seeds
     s = int(seeds.n_seeds)

@@ -318,6 +318,33 @@ def case_pack_file():
                         xxh_empty=sw.xxh64(b""), xxh_a=sw.xxh64(b"a"))
 
 
+def case_registration():
+    """Reference similarity_priors + a full registration-style solve."""
+    from specwalk.registration import DisplacementGrid, expected_displacement, similarity_priors
+    out = {}
+    ph = sw.make_phantom("shifted_pair", (14, 12), rng_seed=4, noise_sigma=0.02, num_regions=2, shift=(1, 0))
+    grid = DisplacementGrid((3, 3))
+    pri = similarity_priors(ph.image, ph.moving, grid, patch_radius=1)
+    out.update(f2=ph.image.intensities, m2=ph.moving.intensities, dims2=np.array(ph.image.dims),
+               pri2=pri.values, vec2=grid.vectors())
+    ph3 = sw.make_phantom("shifted_pair", (8, 7, 6), rng_seed=5, noise_sigma=0.02, num_regions=2, shift=(1, 0, 0))
+    grid3 = DisplacementGrid((3, 3, 3))
+    pri3 = similarity_priors(ph3.image, ph3.moving, grid3, patch_radius=1)
+    out.update(f3=ph3.image.intensities, m3=ph3.moving.intensities, dims3=np.array(ph3.image.dims),
+               pri3=pri3.values, vec3=grid3.vectors())
+    # solve with the priors on an eigen pack and read out the displacement
+    pack = sw.precompute(ph3.image, 50.0, m=60)
+    lap = sw.laplacian(sw.build_graph(ph3.image, 50.0), LaplacianMode.NORMALIZED)
+    n = ph3.image.n_voxels
+    prob = sw.LabelProblem(num_labels=grid3.K, seeds=sw.SeedPartition(n, [], []), priors=pri3.values, gamma=1.0)
+    u = sw.solve_fast(pack, lap, prob, m_use=50)
+    disp = expected_displacement(u, grid3)
+    out.update(V3=np.asarray(pack.eigen.vectors), lam3=pack.eigen.values, d3=pack.d_sqrt, U3=u.values,
+               disp3=disp.vectors)
+    csr_parts("lap3", lap.matrix, out)
+    np.savez_compressed(OUT / "registration.npz", **out)
+
+
 if __name__ == "__main__":
     case_path3()
     case_phantom16()
@@ -326,5 +353,6 @@ if __name__ == "__main__":
     case_adaptive_kats()
     case_errors()
     case_pack_file()
+    case_registration()
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size)

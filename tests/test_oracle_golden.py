@@ -172,3 +172,21 @@ def test_error_kinds_and_all_seeded():
     u = O.solve_fast(z["V"], z["lam"], z["d_sqrt"], lap, np.arange(64), np.arange(64) % 2, 2, m_use=4)
     np.testing.assert_array_equal(u, z["allseed_U"])
     np.testing.assert_array_equal(O.hard_labels(z["ties_in"]), z["ties_out"])
+
+
+@pytest.mark.parametrize("tag", ["2", "3"])
+def test_similarity_priors_matches_reference(tag):
+    z = load_golden("registration")
+    vec = z["vec" + tag]
+    np.testing.assert_array_equal(O.grid_vectors((3,) * len(z["dims" + tag])), vec)
+    pri, sigma = O.similarity_priors(z["f" + tag], z["m" + tag], tuple(z["dims" + tag]), vec, patch_radius=1)
+    np.testing.assert_allclose(pri, z["pri" + tag], rtol=1e-12, atol=1e-15)
+    assert sigma > 0
+
+
+def test_registration_solve_matches_reference():
+    z = load_golden("registration")
+    lap = csr_from(z, "lap3")
+    u = O.solve_fast(z["V3"], z["lam3"], z["d3"], lap, [], [], 27, gamma=1.0, priors=z["pri3"], m_use=50)
+    np.testing.assert_allclose(u, z["U3"], rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(u @ z["vec3"].astype(float), z["disp3"], rtol=1e-9, atol=1e-12)
