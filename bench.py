@@ -133,6 +133,7 @@ def cpu_sample(cfg: str, dims, m: int, planes: int = CPU_SLAB_PLANES):
         z0 *= plane
     img = w.intensities[z0:z0 + n]
     truth = w.truth[z0:z0 + n]
+    moving = w.params["moving"][z0:z0 + n] if "moving" in w.params else None
     rng = np.random.default_rng([W.CFG_INDEX[cfg], 9])
     G = rng.standard_normal((n, m))
     for _ in range(2):  # CholeskyQR2
@@ -141,7 +142,7 @@ def cpu_sample(cfg: str, dims, m: int, planes: int = CPU_SLAB_PLANES):
     lam = W.synthetic_lambda(cfg, m)
     seeds, labs = W.sample_region_seeds(truth, w.params["labels"], w.params["seeds_per_label"], rng)
     return dict(dims=sdims, img=img, V=np.asfortranarray(G), lam=lam, seeds=seeds, labs=labs, n=n,
-                params=w.params)
+                params=w.params, moving=moving)
 
 
 def cpu_step(s, beta0, beta1, labels):
@@ -150,6 +151,11 @@ def cpu_step(s, beta0, beta1, labels):
     lap0 = O.build_laplacian(s["img"], s["dims"], beta0, p["weight_mode"], p["connectivity"])
     lap1 = O.build_laplacian(s["img"], s["dims"], beta1, p["weight_mode"], p["connectivity"])
     V1, lam1, _, _, _ = O.first_order_update(s["V"], s["lam"], lap0, lap1)
+    if s["moving"] is not None:  # c5: registration data term + gamma > 0 solve + expected displacement
+        vec = O.grid_vectors(p["grid"])
+        pri, _ = O.similarity_priors(s["img"], s["moving"], s["dims"], vec, p["patch_radius"])
+        u = O.solve_fast(V1, lam1, lap1.d_sqrt, lap1.matrix, [], [], labels, gamma=p["gamma"], priors=pri)
+        return O.hard_labels(u), u @ vec
     u = O.solve_fast(V1, lam1, lap1.d_sqrt, lap1.matrix, s["seeds"], s["labs"], labels)
     return O.hard_labels(u)
 
@@ -167,7 +173,8 @@ def cpu_baseline(cfg, dims, m, steps=2):
     sec = min(t)
     return {"value": s["n"] * m / sec, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
             "sample": f"{cfg} z-slab {'x'.join(map(str, s['dims']))} ({s['n']} voxels) x K={m}: oracle "
-                      f"first-order update + gamma=0 solve + labels, best of {steps}, {sec:.2f} s/step"}
+                      f"first-order update + " + ("priors + gamma=1 solve + labels + displacement" if cfg == "c5" else
+                                                  "gamma=0 solve + labels") + f", best of {steps}, {sec:.2f} s/step"}
 
 
 def run_reference(args):
@@ -226,9 +233,14 @@ def setup_gpu(cfg, dims, m, rank):
     # the API caches the device copy of the image per Image object
     from paper_1607_04174_b200 import api
     api._image_entry(image)[2] = img_dev
+    if cfg == "c5":
+        from paper_1607_04174_b200 import registration as R
+        moving = swb.Image(w.dims, p["moving"])
+        return dict(w=w, image=image, moving=moving, grid=R.DisplacementGrid(p["grid"]), pack=pack, prob=None, n=n,
+                    m=m, params=p, seeds_n=0)
     seeds, labs = W.seeds_for(w)
     prob = swb.LabelProblem(num_labels=p["labels"], seeds=swb.SeedPartition(n, seeds, labs))
-    return dict(w=w, image=image, pack=pack, prob=prob, n=n, m=m, params=p)
+    return dict(w=w, image=image, pack=pack, prob=prob, n=n, m=m, params=p, seeds_n=len(seeds))
 
 
 def _next_pack(state, beta):
@@ -243,11 +255,27 @@ def _next_pack(state, beta):
     return pack
 
 
+def registration_solve(state, pack, fixed, moving):
+    """c5: data term -> 125-label gamma > 0 solve -> expected displacement,
+    all on the device (registration.py:153-229, fast branch)."""
+    import paper_1607_04174_b200 as swb
+    from paper_1607_04174_b200 import registration as R
+    p = state["params"]
+    pri = R.similarity_priors(fixed, moving, state["grid"], p["patch_radius"])
+    prob = swb.LabelProblem(num_labels=p["labels"], seeds=swb.SeedPartition(state["n"], [], []),
+                            priors=pri.values_dev, gamma=p["gamma"])
+    field = swb.solve_fast(pack, pack.laplacian, prob)
+    field.displacement_dev = R.expected_displacement_device(field, state["grid"])
+    return field
+
+
 def gpu_step(state, i):
     import paper_1607_04174_b200 as swb
     p = state["params"]
     beta = p["beta1"] if i % 2 == 0 else p["beta0"]
     pack = _next_pack(state, beta)
+    if state["prob"] is None:
+        return registration_solve(state, pack, state["image"], state["moving"])
     field = swb.solve_fast(pack, pack.laplacian, state["prob"])
     return field
 
@@ -258,6 +286,16 @@ def e2e_step(state, i, host_labels):
     import paper_1607_04174_b200 as swb
     p = state["params"]
     beta = p["beta1"] if i % 2 == 0 else p["beta0"]
+    if state["prob"] is None:
+        # host fixed / moving images in (fresh Image objects: H2D every
+        # step), host label map + displacement field out
+        fixed = swb.Image(state["w"].dims, state["w"].intensities)
+        moving = swb.Image(state["w"].dims, p["moving"])
+        pack = _next_pack(state, beta)
+        field = registration_solve(state, pack, fixed, moving)
+        host_labels.copy_(field.labels_dev, non_blocking=True)
+        state["host_disp"].copy_(field.displacement_dev, non_blocking=True)
+        return field
     seeds = state["prob"].seeds
     prob = swb.LabelProblem(num_labels=p["labels"],
                             seeds=swb.SeedPartition(state["n"], seeds.seed_indices.copy(), seeds.seed_labels.copy()))
@@ -456,6 +494,8 @@ def run_gpu(args):
     e2e = None
     if not args.no_e2e:
         host_labels = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        if state["prob"] is None:
+            state["host_disp"] = torch.empty((n, 4), dtype=torch.float64, pin_memory=True)
         barrier()
         torch.cuda.synchronize()
         a0, a1 = torch.cuda.Event(True), torch.cuda.Event(True)
@@ -470,9 +510,13 @@ def run_gpu(args):
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         ems = float(et.item())
-        s = state["prob"].seeds.n_seeds
-        e2e = {"value": world * n * m / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(s * (8 + 4)),
-               "d2h_bytes_per_step": int(n * 4 + 8), "ms_per_step": ems}
+        s = state["seeds_n"]
+        if state["prob"] is None:
+            h2d, d2h = 2 * n * 8, n * 4 + n * 4 * 8
+        else:
+            h2d, d2h = s * (8 + 4), n * 4 + 8
+        e2e = {"value": world * n * m / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": ems}
 
     if rank != 0:
         if world > 1:
@@ -491,8 +535,8 @@ def run_gpu(args):
     proj_ms = phases.get("project")
     st_ms = phases.get("stencil")
     rc_ms = phases.get("solve_reconstruct")
-    upd_ms = sum(v for k, v in phases.items() if not k.startswith("solve"))
-    solve_ms = sum(v for k, v in phases.items() if k.startswith("solve"))
+    upd_ms = sum(v for k, v in phases.items() if not k.startswith("solve") and k not in ("priors", "displacement"))
+    solve_ms = sum(v for k, v in phases.items() if k.startswith("solve") or k in ("priors", "displacement"))
     kernels = {
         "rotation_dmma": {"ms": rot_ms, "tflops": achieved, "frac_fp64": achieved / fp64_peak if achieved else None},
         "projection_dmma": {"ms": proj_ms, "tflops": (n * m * (m + 1)) / (proj_ms * 1e-3) / 1e12 if proj_ms else None},
@@ -514,14 +558,17 @@ def run_gpu(args):
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {exc}"}
 
     dims_full = tuple(state["w"].dims)
-    s = state["prob"].seeds.n_seeds
+    s = state["seeds_n"]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{cfg}: {'x'.join(map(str, dims_full))} volume, K={m}, first-order beta update "
-                               f"{state['params']['beta0']}<->{state['params']['beta1']} + {state['params']['labels']}-"
-                               f"label RW solve, S={s}",
+                               f"{state['params']['beta0']}<->{state['params']['beta1']} + " + (
+                                   f"{state['params']['labels']}-label RW solve, S={s}" if cfg != "c5" else
+                                   f"similarity priors (grid {state['params']['grid']}, patch radius "
+                                   f"{state['params']['patch_radius']}) + {state['params']['labels']}-label "
+                                   f"gamma={state['params']['gamma']} RW solve + expected displacement"),
                    "N": n, "K": m, "labels": state["params"]["labels"], "seeds": int(s),
                    "parallelism": "replicas" if world > 1 else "single",
                    "l2": "inputs larger than L2 (V = %.1f GB)" % (n * m * 8 / 1e9)},

@@ -4,6 +4,7 @@ registration.py:27-136) — the c5 caller of the hot path.
   DisplacementGrid       registration.py:27-55 (odd extents, x-fastest labels)
   similarity_priors      registration.py:95-129 -> swb_similarity_priors
   expected_displacement  registration.py:132-136 (U @ grid vectors, DMMA GEMM)
+  register               registration.py:153-229, the pack (fast) branch
 """
 
 from __future__ import annotations
@@ -13,6 +14,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
+from .api import _mark, image_device
 from .device import WORKSPACE, ptr, require_cuda, round_up, stream_handle
 from .errors import DimsMismatch, InvalidParam
 from .types import num_voxels
@@ -82,16 +84,14 @@ def similarity_priors(fixed, moving, grid: DisplacementGrid, patch_radius: int =
     nd = len(dims)
     nx, ny = dims[0], dims[1]
     nz = dims[2] if nd == 3 else 1
-    vec = grid.vectors()
-    if vec.shape[1] != nd:
+    if len(grid.extents) != nd:
         raise InvalidParam("grid dimensionality does not match the images")
-    disp = np.zeros((grid.K, 3), dtype=np.int32)
-    disp[:, :nd] = vec
     n = nx * ny * nz
     k = grid.K
-    F = torch.from_numpy(np.array(fixed.intensities, dtype=np.float64)).to("cuda")
-    M = torch.from_numpy(np.array(moving.intensities, dtype=np.float64)).to("cuda")
-    D = torch.from_numpy(disp).to("cuda")
+    _mark("priors")
+    F = image_device(fixed)
+    M = image_device(moving)
+    D = _grid_table(grid, nd)
     out = torch.empty((n, k), dtype=torch.float64, device="cuda")
     sigma = torch.empty(1, dtype=torch.float64, device="cuda")
     ws = WORKSPACE.get("priors", _lib.size("swb_similarity_priors_workspace_bytes", n, k))
@@ -100,8 +100,28 @@ def similarity_priors(fixed, moving, grid: DisplacementGrid, patch_radius: int =
     return DevicePriors(dims, out, sigma)
 
 
-def expected_displacement(field, grid: DisplacementGrid) -> np.ndarray:
-    """registration.py:132-136: probability-weighted mean displacement (N, d)."""
+def _grid_table(grid: DisplacementGrid, nd: int):
+    """Device int32 (K, 3) displacement table and (K, round_up(d, 2)) f64
+    vectors, cached per grid."""
+    ent = _GRID_CACHE.get(grid)
+    if ent is None:
+        torch = require_cuda()
+        vec = grid.vectors()
+        disp = np.zeros((grid.K, 3), dtype=np.int32)
+        disp[:, :nd] = vec
+        B = np.zeros((grid.K, round_up(nd, 2)))
+        B[:, :nd] = vec
+        ent = (torch.from_numpy(disp).to("cuda"), torch.from_numpy(B).to("cuda"))
+        _GRID_CACHE[grid] = ent
+    return ent[0]
+
+
+_GRID_CACHE: dict = {}
+
+
+def expected_displacement_device(field, grid: DisplacementGrid):
+    """U @ vectors on the DMMA NN GEMM; (N, round_up(d, 2)) device tensor,
+    columns >= d zero."""
     torch = require_cuda()
     if field.K != grid.K:
         raise DimsMismatch("probability columns do not match grid labels")
@@ -109,13 +129,69 @@ def expected_displacement(field, grid: DisplacementGrid) -> np.ndarray:
         U = field._u()
     else:                                         # host ProbabilityField
         U = torch.from_numpy(np.ascontiguousarray(field.values, dtype=np.float64)).to("cuda")
-    vec = grid.vectors().astype(np.float64)
-    d = vec.shape[1]
-    ldb = round_up(d, 2)
-    B = torch.zeros((grid.K, ldb), dtype=torch.float64, device="cuda")
-    B[:, :d] = torch.from_numpy(vec)
+    _mark("displacement")
+    d = len(grid.extents)
+    _grid_table(grid, d)
+    B = _GRID_CACHE[grid][1]
+    ldb = B.shape[1]
     n = U.shape[0]
     out = torch.empty((n, ldb), dtype=torch.float64, device="cuda")
     Uc = U if U.stride(1) == 1 else U.contiguous()
     _lib.call("swb_gemm_nn", ptr(Uc), Uc.stride(0), ptr(B), ldb, n, grid.K, ldb, ptr(out), ldb, 0, stream_handle())
-    return out[:, :d].cpu().numpy()
+    return out
+
+
+def expected_displacement(field, grid: DisplacementGrid) -> np.ndarray:
+    """registration.py:132-136: probability-weighted mean displacement (N, d)."""
+    return expected_displacement_device(field, grid)[:, :len(grid.extents)].cpu().numpy()
+
+
+@dataclass
+class RegisterReport:
+    """registration.py:58-82 (the fields the fast branch fills)."""
+    method: str = "fast"
+    m_use: int = 0
+    adaptive_saturated: bool = False
+    priors_s: float = 0.0
+    solve_s: float = 0.0
+
+
+def register(fixed, moving, pack, grid: DisplacementGrid | None = None, gamma: float = 1.0,
+             patch_radius: int = 2, adaptive: bool = False, m_use: int | None = None, landmarks=None,
+             policy=None):
+    """registration.py:153-229, fast branch: priors -> (select_m) -> solve_fast
+    -> expected displacement, all on the GPU.  The basic (no pack) and
+    aggregation branches are outside the hot path."""
+    import time
+    from dataclasses import replace
+
+    from .api import select_m, solve_fast
+    from .types import AdaptivePolicy, LabelProblem, LaplacianMode, SeedPartition
+    if pack is None:
+        raise InvalidParam("register() on the GPU needs a spectral pack (the basic solver is out of scope)")
+    if grid is None:
+        grid = DisplacementGrid((7,) * len(fixed.dims))
+    rep = RegisterReport()
+    t0 = time.perf_counter()
+    pri = similarity_priors(fixed, moving, grid, patch_radius)
+    rep.priors_s = time.perf_counter() - t0
+    n = num_voxels(fixed.dims)
+    seeds = landmarks if landmarks is not None else SeedPartition(n, [], [])
+    prob = LabelProblem(num_labels=grid.K, seeds=seeds, priors=pri.values_dev, gamma=gamma,
+                        laplacian_mode=LaplacianMode.NORMALIZED)
+    policy = replace(policy, grid_extents=grid.extents) if policy is not None else \
+        AdaptivePolicy(grid_extents=grid.extents)
+    t0 = time.perf_counter()
+    lap = getattr(pack, "laplacian", None)
+    chosen = m_use if m_use is not None else pack.m
+    if adaptive:
+        chosen, info = select_m(pack, prob, policy)
+        rep.adaptive_saturated = info["saturated"]
+    if lap is None:
+        from .device import DeviceGraph, LatticeSpec
+        lap = DeviceGraph.build(image_device(fixed), LatticeSpec.make(tuple(fixed.dims)), float(pack.beta))
+    u = solve_fast(pack, lap, prob, m_use=chosen, want_field=True)
+    rep.m_use = chosen
+    rep.solve_s = time.perf_counter() - t0
+    return u, expected_displacement(u, grid), rep
+

@@ -12,6 +12,14 @@ config index as the seed and sub-streams ``[cfg, purpose]``:
       beta 100 -> 140, M<=150, L=2, 5 rounds of +100 seeds / label
   c4  3-D 256^3, 4 spheres r~U(20,50), I~U(0.2,0.9) + N(0, 0.05^2), 6-conn,
       beta 80 -> 110, M=400, L=4, 200 seeds / label
+  c5  3-D 96^3 registration pair: fixed = trilinear upsampling of 8^3 U(0,1)
+      noise; moving = fixed sampled at x + u(x), u a smooth seeded field
+      (trilinear 4^3 U(-1,1) per component, scaled to max |u_i| = 3);
+      6-conn, reference default |dI| weights, beta 50 -> 70, M=300, 125
+      labels (5x5x5 displacement grid, spacing 1), gamma 1, patch radius 2,
+      the reference data term (mean |f - m| over the patch; BASELINE's text
+      says "SSD", the reference registration.py:95-129 uses the absolute
+      difference, which parity follows)
 Labels for seeding: the objects (disks / spheres / ellipsoid+background);
 voxels outside every object carry label -1 when the config's label count
 names only the objects (c2, c4) and are never seeded.
@@ -38,6 +46,8 @@ CONFIGS = {
                labels=2, seeds_per_label=100, rounds=5, epsilon=1e-3),
     "c4": dict(dims=(256, 256, 256), connectivity=6, weight_mode="sq", beta0=80.0, beta1=110.0, m=400,
                labels=4, seeds_per_label=200),
+    "c5": dict(dims=(96, 96, 96), connectivity=6, weight_mode="abs", beta0=50.0, beta1=70.0, m=300, labels=125,
+               seeds_per_label=0, grid=(5, 5, 5), gamma=1.0, patch_radius=2, max_disp=3.0),
 }
 CFG_INDEX = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5}
 
@@ -108,11 +118,56 @@ def make_image(name: str, dims=None) -> Workload:
             img[m] = level
             truth[m] = k
         img = img + rng.normal(0, 0.05, dims)
+    elif name == "c5":
+        coarse = rng.uniform(0.0, 1.0, (8, 8, 8))
+        img = _upsample(coarse, dims)
+        u = np.stack([_upsample(rng.uniform(-1.0, 1.0, (4, 4, 4)), dims) for _ in range(3)], axis=-1)
+        u *= p["max_disp"] / max(np.abs(u).max(), 1e-12)
+        pts = np.stack(_grid(dims), axis=-1) + u
+        moving = _trilinear(coarse, pts, dims)
+        p["moving"] = _flat(moving)
+        p["true_displacement"] = u.reshape(-1, 3, order="F")
+        truth = np.zeros(dims, dtype=np.int64)
     else:
         raise ValueError(name)
     img = np.clip(img, 0.0, 1.0)
     p["dims"] = dims
     return Workload(name, dims, _flat(img), _flat(truth), p)
+
+
+def _axis_weights(n_fine: int, n_coarse: int) -> np.ndarray:
+    """(n_fine, n_coarse) linear-interpolation matrix, corners aligned."""
+    t = np.linspace(0.0, n_coarse - 1.0, n_fine)
+    i0 = np.minimum(np.floor(t).astype(int), n_coarse - 2)
+    f = t - i0
+    w = np.zeros((n_fine, n_coarse))
+    w[np.arange(n_fine), i0] = 1.0 - f
+    w[np.arange(n_fine), i0 + 1] += f
+    return w
+
+
+def _upsample(coarse: np.ndarray, dims) -> np.ndarray:
+    """Trilinear upsampling of a coarse 3-D grid onto dims (corners aligned)."""
+    a, b, c = (_axis_weights(n, m) for n, m in zip(dims, coarse.shape))
+    return np.einsum("ia,jb,kc,abc->ijk", a, b, c, coarse, optimize=True)
+
+
+def _trilinear(coarse: np.ndarray, pts: np.ndarray, dims) -> np.ndarray:
+    """The upsampled field evaluated at continuous fine-grid points (clamped)."""
+    out = np.zeros(pts.shape[:-1])
+    idx, frac = [], []
+    for ax, (n, m) in enumerate(zip(dims, coarse.shape)):
+        t = np.clip(pts[..., ax], 0.0, n - 1.0) * (m - 1.0) / (n - 1.0)
+        i0 = np.minimum(np.floor(t).astype(int), m - 2)
+        idx.append(i0)
+        frac.append(t - i0)
+    for dx in (0, 1):
+        for dy in (0, 1):
+            for dz in (0, 1):
+                w = ((frac[0] if dx else 1 - frac[0]) * (frac[1] if dy else 1 - frac[1]) *
+                     (frac[2] if dz else 1 - frac[2]))
+                out += w * coarse[idx[0] + dx, idx[1] + dy, idx[2] + dz]
+    return out
 
 
 def sample_region_seeds(labels: np.ndarray, num_labels: int, per_region: int, rng):

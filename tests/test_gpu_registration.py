@@ -27,10 +27,11 @@ def test_similarity_priors(cuda_ok, tag):
     assert abs(pri.sigma - sigma) <= 1e-13 * sigma
 
 
-@pytest.mark.parametrize("radius,ext", [(0, (3, 3)), (2, (5, 3)), (3, (3, 5, 3))])
+@pytest.mark.parametrize("radius,ext", [(0, (3, 3)), (2, (5, 3)), (3, (3, 5, 3)), (2, (5, 5, 5)), (7, (3, 3, 3)),
+                                        (20, (3, 3))])
 def test_similarity_priors_radius_and_grid(cuda_ok, radius, ext):
     rng = np.random.default_rng(7 + radius)
-    dims = (9, 8) if len(ext) == 2 else (7, 6, 5)
+    dims = (45, 37) if len(ext) == 2 else ((7, 6, 5) if radius == 7 else (35, 19, 9))
     f = rng.random(int(np.prod(dims)))
     m = rng.random(int(np.prod(dims)))
     grid = R.DisplacementGrid(ext, step=2 if radius == 2 else 1)
@@ -65,3 +66,34 @@ def test_registration_solve_and_displacement(cuda_ok):
     np.testing.assert_allclose(u.values, z["U3"], rtol=1e-9, atol=1e-12)
     disp = R.expected_displacement(u, grid)
     np.testing.assert_allclose(disp, z["disp3"], rtol=1e-9, atol=1e-12)
+
+
+def test_c5_workflow_matches_oracle(cuda_ok):
+    """BASELINE config 5 at reduced size (the bench's c5 step): beta 50 -> 70
+    first-order update of a QR basis, similarity priors on the c5 pair,
+    125-label gamma = 1 solve, argmax + expected displacement."""
+    from paper_1607_04174_b200 import workloads as W
+    w = W.make_image("c5", dims=(14, 12, 10))
+    p = w.params
+    dims, n, m = w.dims, int(np.prod(w.dims)), 160
+    lap0 = O.build_laplacian(w.intensities, dims, p["beta0"], p["weight_mode"], p["connectivity"])
+    lap1 = O.build_laplacian(w.intensities, dims, p["beta1"], p["weight_mode"], p["connectivity"])
+    rng = np.random.default_rng(55)
+    V = np.linalg.qr(rng.standard_normal((n, m)))[0]
+    lam = np.sort(rng.uniform(1e-4, 1e-1, m))
+    image = swb.Image(dims, w.intensities)
+    pack = swb.SpectralPack(dims=dims, spacing=(), beta=p["beta0"], eigen=swb.EigenBasis(np.asfortranarray(V), lam),
+                            d_sqrt=lap0.d_sqrt, provenance=swb.PackProvenance(image.content_hash()))
+    dp = swb.to_device(pack, image=image, connectivity=p["connectivity"], weight_mode=p["weight_mode"])
+    up = swb.update_basis(dp, image, p["beta1"], method="first_order")
+    grid = R.DisplacementGrid(p["grid"])
+    field, disp, rep = R.register(image, swb.Image(dims, p["moving"]), up, grid=grid, gamma=p["gamma"],
+                                  patch_radius=p["patch_radius"])
+    Vo, lamo, _, _, _ = O.first_order_update(V, lam, lap0, lap1)
+    pri, _ = O.similarity_priors(w.intensities, p["moving"], dims, grid.vectors(), p["patch_radius"])
+    u = O.solve_fast(Vo, lamo, lap1.d_sqrt, lap1.matrix, [], [], 125, gamma=p["gamma"], priors=pri)
+    np.testing.assert_allclose(field.values, u, rtol=1e-9, atol=1e-12)
+    gap = O.top2_gap(u)
+    lab = swb.hard_labels(field).labels
+    assert not ((lab != O.hard_labels(u)) & (gap >= 1e-9)).any()
+    np.testing.assert_allclose(disp, u @ grid.vectors(), rtol=1e-9, atol=1e-12)
