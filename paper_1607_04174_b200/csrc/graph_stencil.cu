@@ -143,6 +143,14 @@ __global__ void normalize_kernel(const StencilGeom g, double* __restrict__ w, co
 
 // --- stencil passes --------------------------------------------------------
 
+// cp.async with a precomputed shared-space address
+__device__ __forceinline__ void cp_async16_s(uint32_t s, const void* gmem, bool pred) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" :: "r"(s), "l"(gmem), "r"(pred ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async8_s(uint32_t s, const void* gmem, bool pred) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" :: "r"(s), "l"(gmem), "r"(pred ? 8 : 0));
+}
+
 constexpr int ST_WARPS = 8;
 constexpr int ST_CTAS_PER_SM = 2;
 
@@ -183,18 +191,16 @@ __host__ __device__ constexpr NbC nb_entry(int conn, int i) {
 template <bool DELTA> struct CoefT { using T = double; };
 template <> struct CoefT<true> { using T = double2; };
 
-// (new, old) pairs: pw[r*ND + d] = {what_new, what_old}, pd[r] = {diag_new, diag_old}
+// (new, new - old) pairs: pw[r*ND + d] = {what_new, what_new - what_old}, pd[r] likewise for the diagonal
 __global__ void pair_coeffs_kernel(const double* __restrict__ wn, const double* __restrict__ wo,
                                    const double* __restrict__ dn, const double* __restrict__ dold, int64_t nw,
                                    int64_t nd, double2* __restrict__ pw, double2* __restrict__ pd) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nw + nd; i += int64_t(gridDim.x) * blockDim.x) {
-    if (i < nw) pw[i] = make_double2(wn[i], wo[i]);
-    else pd[i - nw] = make_double2(dn[i - nw], dold[i - nw]);
+    if (i < nw) pw[i] = make_double2(wn[i], wn[i] - wo[i]);
+    else pd[i - nw] = make_double2(dn[i - nw], dn[i - nw] - dold[i - nw]);
   }
 }
 
-__device__ __forceinline__ void coef_split(double c, double& n, double& o) { n = c; o = 0.0; }
-__device__ __forceinline__ void coef_split(double2 c, double& n, double& o) { n = c.x; o = c.y; }
 
 // ---------------------------------------------------------------------------
 // Stencil pass v5: CTA-shared ring.  A CTA's 8 warps own a block of
@@ -239,6 +245,73 @@ struct Ring5 {
   }
 };
 
+// One row of one warp's centre line: (L^' v, dL v) for the lane's two
+// columns, the Rayleigh / norm / d-projection partial sums and the W store.
+template <int CONN, bool DELTA, int WARP>
+__device__ __forceinline__ void row_compute(const double* sc, const double* sm1, const double* sp1, int lane,
+                                            bool active, double2& q, double2& s2, double2& sd, double* wrow) {
+  using Rg = Ring5<CONN, DELTA>;
+  constexpr int ND = Rg::ND, CW = Rg::CW, LCD = Rg::LCD, NB = nb_count(CONN);
+  constexpr int ZI = WARP / Rg::YB, YI = WARP % Rg::YB;
+  constexpr int CBASE = Rg::V_DBL + WARP * LCD;
+  const double* scl = sc + 2 * lane;
+  const double* sml = sm1 + 2 * lane;
+  const double* spl = sp1 + 2 * lane;
+  const double2 c = *reinterpret_cast<const double2*>(scl + Rg::slot(ZI, YI) * 64);
+  const double d = sc[CBASE + Rg::COEF * CW];
+  double lx = 0.0, ly = 0.0, dx = 0.0, dy = 0.0;
+#pragma unroll
+  for (int e = 0; e < NB; ++e) {
+    const NbC t = nb_entry(CONN, e);
+    const double* vl = t.dx < 0 ? sml : t.dx > 0 ? spl : scl;
+    const double* vs = t.dx < 0 ? sm1 : t.dx > 0 ? sp1 : sc;
+    const double2 val = *reinterpret_cast<const double2*>(vl + Rg::slot(ZI + t.dz, YI + t.dy) * 64);
+    const int slot = t.kind == 0 ? ND : t.kind == 1 ? t.dir
+                     : (t.dz < 0 ? 2 * ND + 1 + t.dir : t.dy < 0 ? ND + 1 + t.dir : t.dir);
+    const double* cp = (t.kind == 2 ? vs : sc) + CBASE + slot * CW;
+    double cn, g = 0.0;
+    if (DELTA) {
+      const double2 pr = *reinterpret_cast<const double2*>(cp);  // (new, new - old) in one 16-B load
+      cn = pr.x;
+      g = pr.y;
+    } else {
+      cn = cp[0];
+    }
+    // L^' v in the reference CSR order (exact products and sums); dL v with FMAs
+    if (t.kind == 0) {
+      lx = __dadd_rn(lx, __dmul_rn(cn, val.x));
+      ly = __dadd_rn(ly, __dmul_rn(cn, val.y));
+      if (DELTA) { dx = fma(g, val.x, dx); dy = fma(g, val.y, dy); }
+    } else {
+      lx = __dadd_rn(lx, __dmul_rn(-cn, val.x));
+      ly = __dadd_rn(ly, __dmul_rn(-cn, val.y));
+      if (DELTA) { dx = fma(-g, val.x, dx); dy = fma(-g, val.y, dy); }
+    }
+  }
+  if (active) {
+    q.x = fma(c.x, lx, q.x);
+    q.y = fma(c.y, ly, q.y);
+    s2.x = fma(c.x, c.x, s2.x);
+    s2.y = fma(c.y, c.y, s2.y);
+    sd.x = fma(c.x, d, sd.x);
+    sd.y = fma(c.y, d, sd.y);
+    if (DELTA) *reinterpret_cast<double2*>(wrow) = make_double2(dx, dy);
+  }
+}
+
+// warp-uniform binary dispatch to the compile-time line position
+template <int CONN, bool DELTA, int LO, int HI>
+__device__ __forceinline__ void row_dispatch(int warp, const double* sc, const double* sm1, const double* sp1, int lane,
+                                             bool active, double2& q, double2& s2, double2& sd, double* wrow) {
+  if constexpr (HI - LO == 1) {
+    row_compute<CONN, DELTA, LO>(sc, sm1, sp1, lane, active, q, s2, sd, wrow);
+  } else {
+    constexpr int MID = (LO + HI) / 2;
+    if (warp < MID) row_dispatch<CONN, DELTA, LO, MID>(warp, sc, sm1, sp1, lane, active, q, s2, sd, wrow);
+    else row_dispatch<CONN, DELTA, MID, HI>(warp, sc, sm1, sp1, lane, active, q, s2, sd, wrow);
+  }
+}
+
 template <int CONN, bool DELTA>
 __global__ void __launch_bounds__(ST_WARPS * 32, ST_CTAS_PER_SM)
 stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, int64_t row_base, int64_t blk_begin,
@@ -251,6 +324,8 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
   static_assert(NL == ST_WARPS, "one warp per centre line");
   extern __shared__ __align__(16) double ring[];
   double* zst = ring + RING * SD;  // zero stage for x-1 < 0 / x+1 >= nx
+  const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
+  constexpr uint32_t STAGE_BYTES = 8u * SD;
   for (int i = threadIdx.x; i < SD; i += blockDim.x) zst[i] = 0.0;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -286,7 +361,7 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
     if (cb != cur_cb) {
       if (cur_cb >= 0) {
         double* sl = slots + gwarp * slot_ld * 3 + (int64_t(cur_cb) * 64 + 2 * lane) * 3;
-        sl[0] = q.x; sl[1] = s2.x; sl[2] = sd.x; sl[3] = q.y; sl[4] = s2.y; sl[5] = sd.y;
+        sl[0] += q.x; sl[1] += s2.x; sl[2] += sd.x; sl[3] += q.y; sl[4] += s2.y; sl[5] += sd.y;
       }
       q = make_double2(0.0, 0.0); s2 = q; sd = q;
       cur_cb = cb;
@@ -347,22 +422,30 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
         csrc = d_sqrt + r0; cstride = 1; cbytes = 8; cok = true;
       }
     }
-    int pst = 0, xp = 0;
+    // shared-space byte addresses of this thread's copy destinations in stage 0
+    uint32_t vdst_s[VPT];
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) vdst_s[i] = ring_s + 8u * uint32_t(vdst[i]);
+    const uint32_t cdst_s = ring_s + 8u * uint32_t(cdst);
+    const int64_t vstep = ldv;
+    uint32_t pst_off = 0;  // byte offset of the stage being filled
+    int xp = 0;
     auto prefetch = [&]() {
       if (xp < nxi) {
-        double* stg = ring + pst * SD;
 #pragma unroll
         for (int i = 0; i < VPT; ++i) {
-          if (threadIdx.x + i * ST_WARPS * 32 < VCH) cp_async16(stg + vdst[i], vsrc[i], vok[i]);
-          if (vok[i]) vsrc[i] += ldv;  // next row (pointer increments only)
+          if (i + 1 < VPT || threadIdx.x + i * ST_WARPS * 32 < VCH) {
+            cp_async16_s(vdst_s[i] + pst_off, vsrc[i], vok[i]);
+            vsrc[i] += vok[i] ? vstep : 0;  // next row (pointer increments only)
+          }
         }
         if (threadIdx.x < CSL) {
-          if (cbytes == 16) cp_async16(stg + cdst, csrc, cok);
-          else cp_async8(stg + cdst, csrc, cok);
-          if (cok) csrc += cstride;
+          if (cbytes == 16) cp_async16_s(cdst_s + pst_off, csrc, cok);
+          else cp_async8_s(cdst_s + pst_off, csrc, cok);
+          csrc += cok ? cstride : 0;
         }
         ++xp;
-        pst = pst + 1 == RING ? 0 : pst + 1;
+        pst_off = pst_off + STAGE_BYTES == RING * STAGE_BYTES ? 0u : pst_off + STAGE_BYTES;
       }
       cp_async_commit();
     };
@@ -372,71 +455,28 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
     const bool active = line_live && (col0 + 2 * lane < M);
     const int64_t my_r0 = (my_z * ny + my_y) * nx;
     double* wrow = (DELTA && line_live) ? W + (my_r0 - w_row0) * ldw + col0 + 2 * lane : nullptr;
-    const int my_slot = Rg::slot(zi, yi);
-    int sc_i = 0;
+    const double* sc = ring;
     for (int x = 0; x < nxi; ++x) {
       cp_async_wait<PREF - 2>();   // rows <= x+1 have landed (this thread's copies)
       __syncthreads();             // ... every thread's; compute(x-1) finished everywhere
       prefetch();                  // row x+PREF -> stage (x+PREF) % RING == stage of row x-2
-      const double* sc = ring + sc_i * SD;
-      const int sp_i = sc_i + 1 == RING ? 0 : sc_i + 1;
-      const int sm_i = sc_i == 0 ? RING - 1 : sc_i - 1;
-      const double* sm1 = x > 0 ? ring + sm_i * SD : zst;
-      const double* sp1 = x + 1 < nxi ? ring + sp_i * SD : zst;
+      const double* sp = sc + SD == ring + RING * SD ? ring : sc + SD;
+      const double* sm1 = x > 0 ? (sc == ring ? ring + (RING - 1) * SD : sc - SD) : zst;
+      const double* sp1 = x + 1 < nxi ? sp : zst;
       if (line_live) {
-        const double* cme = sc + Rg::V_DBL + warp * LCD;
-        const double2 c = *reinterpret_cast<const double2*>(sc + my_slot * 64 + 2 * lane);
-        const double d = cme[Rg::COEF * CW];
-        double lx = 0.0, ly = 0.0, dx = 0.0, dy = 0.0;
-#pragma unroll
-        for (int e = 0; e < nb_count(CONN); ++e) {
-          const NbC t = nb_entry(CONN, e);
-          const double* vs = t.dx < 0 ? sm1 : t.dx > 0 ? sp1 : sc;
-          const int vsl = Rg::slot(zi + t.dz, yi + t.dy);
-          const double2 val = *reinterpret_cast<const double2*>(vs + vsl * 64 + 2 * lane);
-          int slot;
-          const double* cs;
-          if (t.kind == 0) { slot = ND; cs = sc; }
-          else if (t.kind == 1) { slot = t.dir; cs = sc; }
-          else { slot = t.dz < 0 ? 2 * ND + 1 + t.dir : t.dy < 0 ? ND + 1 + t.dir : t.dir; cs = vs; }
-          const double* cp = cs + Rg::V_DBL + warp * LCD + slot * CW;
-          double cn, co;
-          if (DELTA) {
-            const double2 pr = *reinterpret_cast<const double2*>(cp);  // (new, old) in one 16-B load
-            cn = pr.x;
-            co = pr.y;
-          } else {
-            cn = cp[0];
-            co = 0.0;
-          }
-          if (t.kind == 0) {
-            lx = __dadd_rn(lx, __dmul_rn(cn, val.x));
-            ly = __dadd_rn(ly, __dmul_rn(cn, val.y));
-            if (DELTA) { const double gg = cn - co; dx = fma(gg, val.x, dx); dy = fma(gg, val.y, dy); }
-          } else {
-            lx = __dadd_rn(lx, __dmul_rn(-cn, val.x));
-            ly = __dadd_rn(ly, __dmul_rn(-cn, val.y));
-            if (DELTA) { const double gg = co - cn; dx = fma(gg, val.x, dx); dy = fma(gg, val.y, dy); }
-          }
-        }
-        if (active) {
-          q.x = fma(c.x, lx, q.x);
-          q.y = fma(c.y, ly, q.y);
-          s2.x = fma(c.x, c.x, s2.x);
-          s2.y = fma(c.y, c.y, s2.y);
-          sd.x = fma(c.x, d, sd.x);
-          sd.y = fma(c.y, d, sd.y);
-          if (DELTA) *reinterpret_cast<double2*>(wrow + int64_t(x) * ldw) = make_double2(dx, dy);
-        }
+        // the warp's line position is a compile-time constant in each
+        // instantiation, so every shared operand is an immediate offset
+        row_dispatch<CONN, DELTA, 0, ST_WARPS>(warp, sc, sm1, sp1, lane, active, q, s2, sd, wrow);
+        if (DELTA) wrow += ldw;
       }
-      sc_i = sp_i;
+      sc = sp;
     }
     cp_async_wait<0>();
     __syncthreads();
   }
   if (cur_cb >= 0) {
     double* sl = slots + gwarp * slot_ld * 3 + (int64_t(cur_cb) * 64 + 2 * lane) * 3;
-    sl[0] = q.x; sl[1] = s2.x; sl[2] = sd.x; sl[3] = q.y; sl[4] = s2.y; sl[5] = sd.y;
+    sl[0] += q.x; sl[1] += s2.x; sl[2] += sd.x; sl[3] += q.y; sl[4] += s2.y; sl[5] += sd.y;
   }
 }
 
