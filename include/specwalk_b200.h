@@ -97,6 +97,16 @@ int swb_stencil_delta(const swb_lattice* lat, const double* V, int64_t ldv, int6
                       double* W, int64_t ldw, double* quad, double* norm2, double* vtd,
                       void* workspace, size_t workspace_bytes, void* stream);
 
+/* Apply pass (polynomial filters of the offline eigensolver):
+ * out = a * (L^ V) + b * V + g * Z over rows [r_begin, r_end) (Z optional,
+ * same row indexing as out: row r at out + (r - r_begin)*ldo); also
+ * returns quad = diag(V^T L^ V) and norm2 = diag(V^T V) over those rows. */
+int swb_stencil_apply(const swb_lattice* lat, const double* V, int64_t ldv, int64_t row_base,
+                      int64_t r_begin, int64_t r_end, int64_t M, const double* what, const double* diag,
+                      const double* d_sqrt, double a, double b, const double* Z, int64_t ldz, double g,
+                      double* out, int64_t ldo, double* quad, double* norm2, void* workspace,
+                      size_t workspace_bytes, void* stream);
+
 /* ---- FP64 tensor-core (DMMA) GEMMs ---------------------------------- */
 /* out[M1 x M2] = X^T Y, X rows x M1 (ldx), Y rows x M2 (ldy), reduction
  * over rows; symmetric != 0 computes the upper triangle blocks only and
@@ -263,6 +273,24 @@ int swb_f32_colmajor_to_f64_rowmajor(const float* src, int64_t n, int64_t m, dou
 /* and back (save_pack): first m columns (through col_map if given). */
 int swb_f64_rowmajor_to_f32_colmajor(const double* src, int64_t n, int64_t ld, int64_t m,
                                      const int32_t* col_map, float* dst, void* stream);
+
+/* ---- offline eigensolver column kernels (fastrw.py:180-221,
+ *      linalg.py:90-175); deterministic fixed-order reductions ------- */
+size_t swb_column_workspace_bytes(int64_t k);
+/* res2[j] = || Y[:, j] - theta[j] X[:, j] ||^2 over N rows */
+int swb_ritz_residuals(const double* X, int64_t ldx, const double* Y, int64_t ldy, const double* theta,
+                       int64_t N, int64_t k, double* res2, void* workspace, size_t workspace_bytes,
+                       void* stream);
+/* out[j] = a^T X[:, j]  (a == NULL: ||X[:, j]||^2) */
+int swb_column_dots(const double* X, int64_t ldx, const double* a, int64_t N, int64_t k, double* out,
+                    void* workspace, size_t workspace_bytes, void* stream);
+/* X[:, j] = (X[:, j] - a * h[j]) * scale[j]   (a / scale optional) */
+int swb_column_update(double* X, int64_t ldx, int64_t N, int64_t k, const double* a, const double* h,
+                      const double* scale, void* stream);
+/* flip columns so the largest-|.| entry (first on ties) is positive
+ * (_canonical_signs, linalg.py:90-95) */
+int swb_canonical_signs(double* X, int64_t ldx, int64_t N, int64_t k, void* workspace,
+                        size_t workspace_bytes, void* stream);
 
 /* ---- small helpers used by the host layer --------------------------- */
 /* out = sum_x v[x]^2 over n entries (deterministic). */

@@ -18,7 +18,8 @@ from .device import DeviceGraph, DevicePack, LatticeSpec, to_device
 from .api import (DeviceField, RefreshedPack, UpdatedPack, hard_labels, nearest_pack, refresh,
                   refresh_from_set, segment, select_m, solve_fast, update_basis)
 from .packs import load_pack, save_pack, xxh64
-from .registration import DevicePriors, DisplacementGrid, expected_displacement, similarity_priors
+from .registration import DevicePriors, DisplacementGrid, expected_displacement, register, similarity_priors
+from .precompute import precompute, smallest_eigs_device
 
 __version__ = "0.1.0"
 

@@ -42,6 +42,14 @@ SIGNATURES = {
     "swb_stencil_delta": (C.c_int, [C.POINTER(Lattice), c_vp, c_i64, c_i64, c_i64, c_i64, c_i64,
                                     c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,
                                     c_vp, c_sz, c_vp]),
+    "swb_stencil_apply": (C.c_int, [C.POINTER(Lattice), c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp,
+                                    c_vp, c_dbl, c_dbl, c_vp, c_i64, c_dbl, c_vp, c_i64, c_vp, c_vp, c_vp,
+                                    c_sz, c_vp]),
+    "swb_column_workspace_bytes": (c_sz, [c_i64]),
+    "swb_ritz_residuals": (C.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp, c_sz, c_vp]),
+    "swb_column_dots": (C.c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp, c_sz, c_vp]),
+    "swb_column_update": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "swb_canonical_signs": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_sz, c_vp]),
     "swb_gemm_tn_workspace_bytes": (c_sz, [c_i64, c_i64, c_i64]),
     "swb_gemm_tn": (C.c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, C.c_int, c_vp, c_i64,
                               c_vp, c_sz, c_vp]),

@@ -245,11 +245,20 @@ struct Ring5 {
   }
 };
 
+// Apply mode of the plain pass (no DELTA, W given): W = a * (L^ v) + b * v + g * Z
+// (Z optional) -- one step of a three-term polynomial recurrence in L^.
+struct ApplyArgs {
+  const double* Z;
+  int64_t ldz;
+  double a, b, g;
+};
+
 // One row of one warp's centre line: (L^' v, dL v) for the lane's two
 // columns, the Rayleigh / norm / d-projection partial sums and the W store.
 template <int CONN, bool DELTA, int WARP>
 __device__ __forceinline__ void row_compute(const double* sc, const double* sm1, const double* sp1, int lane,
-                                            bool active, double2& q, double2& s2, double2& sd, double* wrow) {
+                                            bool active, double2& q, double2& s2, double2& sd, double* wrow,
+                                            const ApplyArgs& ap, const double* zrow) {
   using Rg = Ring5<CONN, DELTA>;
   constexpr int ND = Rg::ND, CW = Rg::CW, LCD = Rg::LCD, NB = nb_count(CONN);
   constexpr int ZI = WARP / Rg::YB, YI = WARP % Rg::YB;
@@ -295,20 +304,31 @@ __device__ __forceinline__ void row_compute(const double* sc, const double* sm1,
     s2.y = fma(c.y, c.y, s2.y);
     sd.x = fma(c.x, d, sd.x);
     sd.y = fma(c.y, d, sd.y);
-    if (DELTA) *reinterpret_cast<double2*>(wrow) = make_double2(dx, dy);
+    if (DELTA) {
+      *reinterpret_cast<double2*>(wrow) = make_double2(dx, dy);
+    } else if (wrow) {
+      double ox = fma(ap.a, lx, ap.b * c.x), oy = fma(ap.a, ly, ap.b * c.y);
+      if (zrow) {
+        const double2 z = *reinterpret_cast<const double2*>(zrow);
+        ox = fma(ap.g, z.x, ox);
+        oy = fma(ap.g, z.y, oy);
+      }
+      *reinterpret_cast<double2*>(wrow) = make_double2(ox, oy);
+    }
   }
 }
 
 // warp-uniform binary dispatch to the compile-time line position
 template <int CONN, bool DELTA, int LO, int HI>
 __device__ __forceinline__ void row_dispatch(int warp, const double* sc, const double* sm1, const double* sp1, int lane,
-                                             bool active, double2& q, double2& s2, double2& sd, double* wrow) {
+                                             bool active, double2& q, double2& s2, double2& sd, double* wrow,
+                                             const ApplyArgs& ap, const double* zrow) {
   if constexpr (HI - LO == 1) {
-    row_compute<CONN, DELTA, LO>(sc, sm1, sp1, lane, active, q, s2, sd, wrow);
+    row_compute<CONN, DELTA, LO>(sc, sm1, sp1, lane, active, q, s2, sd, wrow, ap, zrow);
   } else {
     constexpr int MID = (LO + HI) / 2;
-    if (warp < MID) row_dispatch<CONN, DELTA, LO, MID>(warp, sc, sm1, sp1, lane, active, q, s2, sd, wrow);
-    else row_dispatch<CONN, DELTA, MID, HI>(warp, sc, sm1, sp1, lane, active, q, s2, sd, wrow);
+    if (warp < MID) row_dispatch<CONN, DELTA, LO, MID>(warp, sc, sm1, sp1, lane, active, q, s2, sd, wrow, ap, zrow);
+    else row_dispatch<CONN, DELTA, MID, HI>(warp, sc, sm1, sp1, lane, active, q, s2, sd, wrow, ap, zrow);
   }
 }
 
@@ -317,7 +337,7 @@ __global__ void __launch_bounds__(ST_WARPS * 32, ST_CTAS_PER_SM)
 stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, int64_t row_base, int64_t blk_begin,
                 int64_t blk_end, int64_t M, int n_cb, const double* __restrict__ cwhat, const double* __restrict__ cdiag,
                 const double* __restrict__ d_sqrt, double* __restrict__ W, int64_t ldw, int64_t w_row0,
-                double* __restrict__ slots, int64_t slot_ld) {
+                double* __restrict__ slots, int64_t slot_ld, const ApplyArgs ap) {
   using Rg = Ring5<CONN, DELTA>;
   constexpr int ND = Rg::ND, CW = Rg::CW, RING = Rg::RING, PREF = Rg::PREF, SD = Rg::STAGE_DBL;
   constexpr int ZB = Rg::ZB, YB = Rg::YB, NS = Rg::NS, NL = Rg::NL, LCD = Rg::LCD;
@@ -454,7 +474,8 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
 
     const bool active = line_live && (col0 + 2 * lane < M);
     const int64_t my_r0 = (my_z * ny + my_y) * nx;
-    double* wrow = (DELTA && line_live) ? W + (my_r0 - w_row0) * ldw + col0 + 2 * lane : nullptr;
+    double* wrow = (W && line_live) ? W + (my_r0 - w_row0) * ldw + col0 + 2 * lane : nullptr;
+    const double* zrow = (!DELTA && ap.Z && line_live) ? ap.Z + (my_r0 - w_row0) * ap.ldz + col0 + 2 * lane : nullptr;
     const double* sc = ring;
     for (int x = 0; x < nxi; ++x) {
       cp_async_wait<PREF - 2>();   // rows <= x+1 have landed (this thread's copies)
@@ -466,8 +487,9 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
       if (line_live) {
         // the warp's line position is a compile-time constant in each
         // instantiation, so every shared operand is an immediate offset
-        row_dispatch<CONN, DELTA, 0, ST_WARPS>(warp, sc, sm1, sp1, lane, active, q, s2, sd, wrow);
-        if (DELTA) wrow += ldw;
+        row_dispatch<CONN, DELTA, 0, ST_WARPS>(warp, sc, sm1, sp1, lane, active, q, s2, sd, wrow, ap, zrow);
+        if (wrow) wrow += ldw;
+        if (zrow) zrow += ap.ldz;
       }
       sc = sp;
     }
@@ -507,7 +529,7 @@ template <int CONN, bool DELTA>
 int launch_stencil5(const StencilGeom& g, const double* V, int64_t ldv, int64_t row_base, int64_t blk_begin,
                     int64_t blk_end, int64_t M, int n_cb, const double* cw, const double* cd, const double* d_sqrt,
                     double* W, int64_t ldw, int64_t w_row0, double* slots, int64_t slot_ld, int64_t grid,
-                    cudaStream_t st) {
+                    const ApplyArgs& ap, cudaStream_t st) {
   using Rg = Ring5<CONN, DELTA>;
   const size_t smem = sizeof(double) * size_t(Rg::RING + 1) * Rg::STAGE_DBL;
   auto kern = stencil5_kernel<CONN, DELTA>;
@@ -517,7 +539,7 @@ int launch_stencil5(const StencilGeom& g, const double* V, int64_t ldv, int64_t 
     attr = true;
   }
   kern<<<static_cast<unsigned>(grid), ST_WARPS * 32, smem, st>>>(g, V, ldv, row_base, blk_begin, blk_end, M, n_cb, cw,
-                                                                 cd, d_sqrt, W, ldw, w_row0, slots, slot_ld);
+                                                                 cd, d_sqrt, W, ldw, w_row0, slots, slot_ld, ap);
   SWB_CHECK_LAUNCH();
   return SWB_OK;
 }
@@ -543,7 +565,7 @@ int run_stencil(const swb_lattice* lat, const double* V, int64_t ldv, int64_t ro
                 int64_t r_begin, int64_t r_end, int64_t M, const double* what_new,
                 const double* diag_new, const double* what_old, const double* diag_old,
                 const double* d_sqrt, double* W, int64_t ldw, double* quad, double* norm2, double* vtd,
-                void* ws, size_t ws_bytes, void* stream) {
+                void* ws, size_t ws_bytes, void* stream, const ApplyArgs& ap = ApplyArgs{nullptr, 0, 1.0, 0.0, 0.0}) {
   using T = typename CoefT<DELTA>::T;
   cudaStream_t st = swb_stream(stream);
   StencilGeom g;
@@ -591,9 +613,9 @@ int run_stencil(const swb_lattice* lat, const double* V, int64_t ldv, int64_t ro
     const int64_t unit = L.conn == 6 ? L.nx * L.ny : L.nx;
     if (r_begin % unit || r_end % unit) return SWB_INVALID_PARAM;
     const int64_t b0 = r_begin / unit, b1 = r_end / unit;
-    if (L.conn == 4) rc2 = launch_stencil5<4, DELTA>(g, V, ldv, row_base, b0, b1, M, n_cb, cw, cd, d_sqrt, W, ldw, r_begin, slots, slot_ld, grid, st);
-    else if (L.conn == 8) rc2 = launch_stencil5<8, DELTA>(g, V, ldv, row_base, b0, b1, M, n_cb, cw, cd, d_sqrt, W, ldw, r_begin, slots, slot_ld, grid, st);
-    else rc2 = launch_stencil5<6, DELTA>(g, V, ldv, row_base, b0, b1, M, n_cb, cw, cd, d_sqrt, W, ldw, r_begin, slots, slot_ld, grid, st);
+    if (L.conn == 4) rc2 = launch_stencil5<4, DELTA>(g, V, ldv, row_base, b0, b1, M, n_cb, cw, cd, d_sqrt, W, ldw, r_begin, slots, slot_ld, grid, ap, st);
+    else if (L.conn == 8) rc2 = launch_stencil5<8, DELTA>(g, V, ldv, row_base, b0, b1, M, n_cb, cw, cd, d_sqrt, W, ldw, r_begin, slots, slot_ld, grid, ap, st);
+    else rc2 = launch_stencil5<6, DELTA>(g, V, ldv, row_base, b0, b1, M, n_cb, cw, cd, d_sqrt, W, ldw, r_begin, slots, slot_ld, grid, ap, st);
     if (rc2) return rc2;
   }
   dim3 rg(static_cast<unsigned>(M), 3);
@@ -683,6 +705,18 @@ extern "C" int swb_stencil_rayleigh(const swb_lattice* lat, const double* V, int
   if (!what || !diag || !d_sqrt) return SWB_INVALID_PARAM;
   return run_stencil<false>(lat, V, ldv, row_base, r_begin, r_end, M, what, diag, nullptr, nullptr,
                             d_sqrt, nullptr, 0, quad, norm2, vtd, workspace, workspace_bytes, stream);
+}
+
+extern "C" int swb_stencil_apply(const swb_lattice* lat, const double* V, int64_t ldv, int64_t row_base,
+                                 int64_t r_begin, int64_t r_end, int64_t M, const double* what, const double* diag,
+                                 const double* d_sqrt, double a, double b, const double* Z, int64_t ldz, double g,
+                                 double* out, int64_t ldo, double* quad, double* norm2, void* workspace,
+                                 size_t workspace_bytes, void* stream) {
+  if (!what || !diag || !d_sqrt || !out || ldo < M || (ldo & 1)) return SWB_INVALID_PARAM;
+  if (Z && (ldz < M || (ldz & 1) || (reinterpret_cast<uintptr_t>(Z) & 15))) return SWB_INVALID_PARAM;
+  const ApplyArgs ap{Z, ldz, a, b, g};
+  return run_stencil<false>(lat, V, ldv, row_base, r_begin, r_end, M, what, diag, nullptr, nullptr, d_sqrt, out, ldo,
+                            quad, norm2, nullptr, workspace, workspace_bytes, stream, ap);
 }
 
 extern "C" int swb_stencil_delta(const swb_lattice* lat, const double* V, int64_t ldv, int64_t row_base,
