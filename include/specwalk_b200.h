@@ -284,6 +284,9 @@ int swb_ritz_residuals(const double* X, int64_t ldx, const double* Y, int64_t ld
 /* out[j] = a^T X[:, j]  (a == NULL: ||X[:, j]||^2) */
 int swb_column_dots(const double* X, int64_t ldx, const double* a, int64_t N, int64_t k, double* out,
                     void* workspace, size_t workspace_bytes, void* stream);
+/* out[j] = X[:, j]^T Y[:, j] */
+int swb_column_products(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t N, int64_t k,
+                        double* out, void* workspace, size_t workspace_bytes, void* stream);
 /* X[:, j] = (X[:, j] - a * h[j]) * scale[j]   (a / scale optional) */
 int swb_column_update(double* X, int64_t ldx, int64_t N, int64_t k, const double* a, const double* h,
                       const double* scale, void* stream);
@@ -291,6 +294,27 @@ int swb_column_update(double* X, int64_t ldx, int64_t N, int64_t k, const double
  * (_canonical_signs, linalg.py:90-95) */
 int swb_canonical_signs(double* X, int64_t ldx, int64_t N, int64_t k, void* workspace,
                         size_t workspace_bytes, void* stream);
+
+/* ---- super-vertex aggregation (aggregation.py:89-216) ---------------- */
+/* Greedy region growing (host buffers; sequential by definition):
+ * priors N x L row-major (ldp), dims[ndim] x-fastest -> cluster_ids (N),
+ * n_super. */
+int swb_build_aggregation(const double* priors, int64_t ldp, int64_t L, const int64_t* dims, int32_t ndim,
+                          int32_t max_cluster_radius, double similarity_tol, int32_t* cluster_ids,
+                          int64_t* n_super);
+/* delta[x] = 2 * #lattice neighbours of x in another cluster */
+int swb_delta_weights(const swb_lattice* lat, const int32_t* cluster_ids, double* delta, void* stream);
+/* out[c, :m] = sum_{x in c, ascending} (1/|c|) * (X[x, :m] * w[x])  (w optional);
+ * order = voxels sorted by cluster (stable), offsets[n_super + 1] */
+int swb_cluster_rows(const double* X, int64_t ldx, int64_t m, const double* w, const int64_t* order,
+                     const int64_t* offsets, int64_t n_super, double* out, int64_t ldo, void* stream);
+/* Y = A X for a CSR matrix A (nrows rows), CSR order */
+int swb_csr_spmm(const int64_t* indptr, const int64_t* indices, const double* data, int64_t nrows,
+                 const double* X, int64_t ldx, int64_t m, double* Y, int64_t ldy, void* stream);
+/* raw lattice edge weights w[v * ndir + d] = max(exp(-beta |dI|), 1e-8)
+ * (0 off-grid / cut) -- graphs.py:127-140 before normalisation */
+int swb_edge_weights(const swb_lattice* lat, const double* intensities, double beta, const uint8_t* cut_mask,
+                     double* w, void* stream);
 
 /* ---- small helpers used by the host layer --------------------------- */
 /* out = sum_x v[x]^2 over n entries (deterministic). */

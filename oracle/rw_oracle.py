@@ -557,3 +557,107 @@ def similarity_priors(fixed, moving, dims, vectors, patch_radius: int = 2):
     vals = np.exp(logits)
     vals /= vals.sum(axis=1, keepdims=True)
     return vals, sigma
+
+
+# ---------------------------------------------------------------------------
+# super-vertex aggregation (aggregation.py:89-216)
+# ---------------------------------------------------------------------------
+
+def build_aggregation(priors, dims, max_cluster_radius: int, similarity_tol: float):
+    """aggregation.py:89-127: greedy BFS region growing in flat index order.
+    Returns (cluster_ids int64 (N,), n_super)."""
+    from collections import deque
+    dims = tuple(int(d) for d in dims)
+    p = np.asarray(priors, dtype=np.float64)
+    n = int(np.prod(dims))
+    coords = np.stack(np.unravel_index(np.arange(n), dims, order="F"), axis=1)
+    strides = np.cumprod([1, *dims[:-1]])
+    cluster = np.full(n, -1, dtype=np.int64)
+    nid = 0
+    for start in range(n):
+        if cluster[start] >= 0:
+            continue
+        cluster[start] = nid
+        ps, cs = p[start], coords[start]
+        q = deque([start])
+        while q:
+            x = q.popleft()
+            cx = coords[x]
+            for axis in range(len(dims)):
+                for step in (-1, 1):
+                    if not 0 <= cx[axis] + step < dims[axis]:
+                        continue
+                    y = x + step * strides[axis]
+                    if cluster[y] >= 0:
+                        continue
+                    if np.abs(coords[y] - cs).max() > max_cluster_radius:
+                        continue
+                    if np.abs(p[y] - ps).sum() > similarity_tol:
+                        continue
+                    cluster[y] = nid
+                    q.append(y)
+        nid += 1
+    return cluster, nid
+
+
+def delta_weights(cluster_ids, dims):
+    """aggregation.py:130-139: 2 per lattice neighbour in another cluster."""
+    heads, tails = lattice_edges(dims)
+    differs = cluster_ids[heads] != cluster_ids[tails]
+    delta = np.zeros(int(np.prod(dims)))
+    np.add.at(delta, heads[differs], 2.0)
+    np.add.at(delta, tails[differs], 2.0)
+    return delta
+
+
+def eta_bar_t(cluster_ids, n_super):
+    n = cluster_ids.size
+    sizes = np.bincount(cluster_ids, minlength=n_super)
+    return sp.csr_matrix((1.0 / sizes[cluster_ids], (cluster_ids, np.arange(n))), shape=(n_super, n))
+
+
+def gram_schmidt(v, drop_tol: float = 1e-10):
+    """linalg.py gram_schmidt: modified Gram-Schmidt, two passes, columns
+    with residual norm < drop_tol dropped."""
+    v = np.array(v, dtype=np.float64)
+    kept = []
+    for j in range(v.shape[1]):
+        col = v[:, j].copy()
+        for _ in range(2):
+            for q in kept:
+                col -= q @ col * q
+        nrm = np.linalg.norm(col)
+        if nrm < drop_tol:
+            continue
+        kept.append(col / nrm)
+    return np.column_stack(kept) if kept else np.zeros((v.shape[0], 0))
+
+
+def coarsen_basis(V, cluster_ids, n_super, intensities, dims, beta, variant="delta", m_use=None):
+    """aggregation.py:154-204 -> (q_bar, lambda_bar, d_sqrt_bar, lap_bar)."""
+    V = np.asarray(V, dtype=np.float64)
+    if m_use is not None:
+        V = V[:, :m_use]
+    weighted = V * delta_weights(cluster_ids, dims)[:, None] if variant == "delta" else V
+    raw = eta_bar_t(cluster_ids, n_super) @ weighted
+    if n_super == 1:
+        return np.ones((1, 1)), np.zeros(1), np.ones(1), None
+    q = gram_schmidt(raw)
+    heads, tails = lattice_edges(dims)
+    w = edge_weights(np.asarray(intensities, dtype=np.float64), heads, tails, beta)
+    wmat = symmetric_weights(cluster_ids.size, heads, tails, w).tocoo()
+    ci, cj = cluster_ids[wmat.row], cluster_ids[wmat.col]
+    cross = ci != cj
+    wbar = sp.coo_matrix((wmat.data[cross], (ci[cross], cj[cross])), shape=(n_super, n_super)).tocsr()
+    wbar.sum_duplicates()
+    wbar.sort_indices()
+    lap = normalized_laplacian(wbar)
+    quad = np.einsum("ij,ij->j", q, lap.matrix @ q)
+    lam = np.maximum(quad, 0.0)
+    order = np.argsort(lam, kind="stable")
+    return q[:, order], lam[order], lap.d_sqrt, lap
+
+
+def aggregate_priors(priors, cluster_ids, n_super):
+    """aggregation.py:207-209."""
+    return eta_bar_t(cluster_ids, n_super) @ np.asarray(priors, dtype=np.float64)

@@ -49,6 +49,12 @@ SIGNATURES = {
     "swb_ritz_residuals": (C.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp, c_sz, c_vp]),
     "swb_column_dots": (C.c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp, c_sz, c_vp]),
     "swb_column_update": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "swb_column_products": (C.c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_sz, c_vp]),
+    "swb_build_aggregation": (C.c_int, [c_vp, c_i64, c_i64, c_vp, c_i32, c_i32, c_dbl, c_vp, c_vp]),
+    "swb_delta_weights": (C.c_int, [C.POINTER(Lattice), c_vp, c_vp, c_vp]),
+    "swb_cluster_rows": (C.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp]),
+    "swb_csr_spmm": (C.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp]),
+    "swb_edge_weights": (C.c_int, [C.POINTER(Lattice), c_vp, c_dbl, c_vp, c_vp, c_vp]),
     "swb_canonical_signs": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_sz, c_vp]),
     "swb_gemm_tn_workspace_bytes": (c_sz, [c_i64, c_i64, c_i64]),
     "swb_gemm_tn": (C.c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, C.c_int, c_vp, c_i64,

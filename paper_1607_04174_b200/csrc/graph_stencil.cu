@@ -691,6 +691,19 @@ extern "C" int swb_graph_build(const swb_lattice* lat, const double* intensities
   return SWB_OK;
 }
 
+extern "C" int swb_edge_weights(const swb_lattice* lat, const double* intensities, double beta,
+                                const uint8_t* cut_mask, double* w, void* stream) {
+  if (!(beta >= 0.0) || !intensities || !w) return SWB_INVALID_PARAM;
+  StencilGeom g;
+  int rc = make_geom(lat, &g);
+  if (rc) return rc;
+  const int64_t N = g.lat.nx * g.lat.ny * g.lat.nz;
+  edge_weight_kernel<<<swb_sm_count() * 8, 256, 0, swb_stream(stream)>>>(g, intensities, beta, lat->weight_mode,
+                                                                         cut_mask, w, N);
+  SWB_CHECK_LAUNCH();
+  return SWB_OK;
+}
+
 extern "C" size_t swb_stencil_workspace_bytes(const swb_lattice* lat, int64_t M) {
   LatticeDev L;
   if (swb_make_lattice(lat, &L) || M <= 0) return 0;

@@ -35,6 +35,8 @@ __global__ void col_partial_kernel(const double* __restrict__ X, int64_t ldx, co
         s = fma(d, d, s);
       } else if (MODE == 1) {     // dot with a row vector a[r]
         s = fma(vec[r], x, s);
+      } else if (MODE == 3) {     // column dot of X and Y
+        s = fma(x, Y[r * ldy + j], s);
       } else {                    // sum of squares
         s = fma(x, x, s);
       }
@@ -104,7 +106,8 @@ int col_partials(int mode, const double* X, int64_t ldx, const double* Y, int64_
   double* part = static_cast<double*>(ws);
   if (mode == 0) col_partial_kernel<0><<<CK_BLOCKS, CK_THREADS, 0, st>>>(X, ldx, Y, ldy, vec, N, k, part);
   else if (mode == 1) col_partial_kernel<1><<<CK_BLOCKS, CK_THREADS, 0, st>>>(X, ldx, Y, ldy, vec, N, k, part);
-  else col_partial_kernel<2><<<CK_BLOCKS, CK_THREADS, 0, st>>>(X, ldx, Y, ldy, vec, N, k, part);
+  else if (mode == 2) col_partial_kernel<2><<<CK_BLOCKS, CK_THREADS, 0, st>>>(X, ldx, Y, ldy, vec, N, k, part);
+  else col_partial_kernel<3><<<CK_BLOCKS, CK_THREADS, 0, st>>>(X, ldx, Y, ldy, vec, N, k, part);
   SWB_CHECK_LAUNCH();
   col_reduce_kernel<<<static_cast<unsigned>((k + 255) / 256), 256, 0, st>>>(part, CK_BLOCKS, k, out);
   SWB_CHECK_LAUNCH();
@@ -127,6 +130,12 @@ extern "C" int swb_ritz_residuals(const double* X, int64_t ldx, const double* Y,
 extern "C" int swb_column_dots(const double* X, int64_t ldx, const double* a, int64_t N, int64_t k, double* out,
                                void* workspace, size_t workspace_bytes, void* stream) {
   return col_partials(a ? 1 : 2, X, ldx, nullptr, 0, a, N, k, out, workspace, workspace_bytes, swb_stream(stream));
+}
+
+extern "C" int swb_column_products(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t N, int64_t k,
+                                   double* out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!Y || ldy < k) return SWB_INVALID_PARAM;
+  return col_partials(3, X, ldx, Y, ldy, nullptr, N, k, out, workspace, workspace_bytes, swb_stream(stream));
 }
 
 extern "C" int swb_column_update(double* X, int64_t ldx, int64_t N, int64_t k, const double* a, const double* h,

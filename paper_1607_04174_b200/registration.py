@@ -154,23 +154,44 @@ class RegisterReport:
     adaptive_saturated: bool = False
     priors_s: float = 0.0
     solve_s: float = 0.0
+    aggregate_s: float = 0.0
+    n_super: int = 0
+
+
+def _lift_seeds(seeds, agg):
+    """registration.py:232-246: landmark voxels -> their super-vertices."""
+    from .errors import InvalidParam as _IP
+    from .types import SeedPartition
+    if seeds.n_seeds == 0:
+        return SeedPartition(agg.n_super, [], [])
+    super_ids = agg.cluster_ids[seeds.seed_indices]
+    uniq, first = np.unique(super_ids, return_index=True)
+    labels = seeds.seed_labels[first]
+    clash = {}
+    for sid, lab in zip(super_ids, seeds.seed_labels):
+        if clash.setdefault(sid, lab) != lab:
+            raise _IP("conflicting landmark labels inside one super-vertex")
+    return SeedPartition(agg.n_super, uniq, labels)
 
 
 def register(fixed, moving, pack, grid: DisplacementGrid | None = None, gamma: float = 1.0,
-             patch_radius: int = 2, adaptive: bool = False, m_use: int | None = None, landmarks=None,
-             policy=None):
-    """registration.py:153-229, fast branch: priors -> (select_m) -> solve_fast
-    -> expected displacement, all on the GPU.  The basic (no pack) and
-    aggregation branches are outside the hot path."""
+             patch_radius: int = 2, adaptive: bool = False, aggregate=None, m_use: int | None = None,
+             coarsen_variant=None, landmarks=None, policy=None):
+    """registration.py:153-229 with a pack: priors -> (aggregation) ->
+    (select_m) -> solve_fast -> expected displacement, on the GPU.  The
+    basic (no pack) branch is outside the hot path."""
     import time
     from dataclasses import replace
 
+    from .aggregation import CoarsenVariant, aggregate_priors, build_aggregation, coarsen_basis, propagate
     from .api import select_m, solve_fast
     from .types import AdaptivePolicy, LabelProblem, LaplacianMode, SeedPartition
     if pack is None:
         raise InvalidParam("register() on the GPU needs a spectral pack (the basic solver is out of scope)")
     if grid is None:
         grid = DisplacementGrid((7,) * len(fixed.dims))
+    if coarsen_variant is None:
+        coarsen_variant = CoarsenVariant.DELTA
     rep = RegisterReport()
     t0 = time.perf_counter()
     pri = similarity_priors(fixed, moving, grid, patch_radius)
@@ -182,16 +203,40 @@ def register(fixed, moving, pack, grid: DisplacementGrid | None = None, gamma: f
     policy = replace(policy, grid_extents=grid.extents) if policy is not None else \
         AdaptivePolicy(grid_extents=grid.extents)
     t0 = time.perf_counter()
-    lap = getattr(pack, "laplacian", None)
-    chosen = m_use if m_use is not None else pack.m
-    if adaptive:
-        chosen, info = select_m(pack, prob, policy)
-        rep.adaptive_saturated = info["saturated"]
-    if lap is None:
-        from .device import DeviceGraph, LatticeSpec
-        lap = DeviceGraph.build(image_device(fixed), LatticeSpec.make(tuple(fixed.dims)), float(pack.beta))
-    u = solve_fast(pack, lap, prob, m_use=chosen, want_field=True)
-    rep.m_use = chosen
+    if aggregate is not None:
+        similarity_tol, radius = aggregate
+        t_agg = time.perf_counter()
+        agg = build_aggregation(pri, max_cluster_radius=radius, similarity_tol=similarity_tol)
+        _, pack_bar = coarsen_basis(pack, agg, None, coarsen_variant, m_use=m_use, image=fixed)
+        rep.aggregate_s = time.perf_counter() - t_agg
+        rep.n_super = agg.n_super
+        p_bar = aggregate_priors(pri, agg)
+        p_bar = p_bar / p_bar.sum(dim=1, keepdim=True)
+        if agg.n_super == 1:
+            u = propagate(p_bar, agg)
+            rep.m_use = pack_bar.m
+        else:
+            prob_bar = LabelProblem(num_labels=grid.K, seeds=_lift_seeds(seeds, agg), priors=p_bar.contiguous(),
+                                    gamma=gamma, laplacian_mode=LaplacianMode.NORMALIZED)
+            mb = pack_bar.m
+            if adaptive:
+                mb, info = select_m(pack_bar, prob_bar, policy)
+                rep.adaptive_saturated = info["saturated"]
+            u_bar = solve_fast(pack_bar, pack_bar.laplacian, prob_bar, m_use=mb, want_field=True)
+            rep.m_use = mb
+            u = propagate(u_bar, agg)
+        rep.method = f"aggregate-{coarsen_variant.value}"
+    else:
+        lap = getattr(pack, "laplacian", None)
+        chosen = m_use if m_use is not None else pack.m
+        if adaptive:
+            chosen, info = select_m(pack, prob, policy)
+            rep.adaptive_saturated = info["saturated"]
+        if lap is None:
+            from .device import DeviceGraph, LatticeSpec
+            lap = DeviceGraph.build(image_device(fixed), LatticeSpec.make(tuple(fixed.dims)), float(pack.beta))
+        u = solve_fast(pack, lap, prob, m_use=chosen, want_field=True)
+        rep.m_use = chosen
+        rep.method = "fast"
     rep.solve_s = time.perf_counter() - t0
     return u, expected_displacement(u, grid), rep
-

@@ -345,6 +345,46 @@ def case_registration():
     np.savez_compressed(OUT / "registration.npz", **out)
 
 
+def case_aggregation():
+    """Reference super-vertex aggregation (aggregation.py:89-216): clusters,
+    delta weights, coarsened bases (both variants), aggregate Laplacian,
+    aggregate priors, the coarse solve and the propagated field."""
+    from specwalk.aggregation import (CoarsenVariant, aggregate_priors, build_aggregation,
+                                      coarsen_basis, delta_weights, propagate)
+    from specwalk.registration import DisplacementGrid, similarity_priors
+    out = {}
+    for tag, dims, shift, grid_ext, radius, tol, beta, m, m_use in (
+            ("2", (20, 18), (1, 0), (3, 3), 2, 0.35, 30.0, 40, 30),
+            ("3", (9, 8, 7), (1, 0, 0), (3, 3, 3), 1, 0.5, 20.0, 36, 30)):
+        ph = sw.make_phantom("shifted_pair", dims, rng_seed=7, noise_sigma=0.02, num_regions=2, shift=shift)
+        grid = DisplacementGrid(grid_ext)
+        pri = similarity_priors(ph.image, ph.moving, grid, patch_radius=1)
+        pack = sw.precompute(ph.image, beta, m=m)
+        agg = build_aggregation(pri, max_cluster_radius=radius, similarity_tol=tol)
+        graph = sw.build_graph(ph.image, beta=pack.beta)
+        out.update({f"img{tag}": ph.image.intensities, f"mov{tag}": ph.moving.intensities,
+                    f"dims{tag}": np.array(dims), f"pri{tag}": pri.values, f"V{tag}": np.asarray(pack.eigen.vectors),
+                    f"lam{tag}": pack.eigen.values, f"dsq{tag}": pack.d_sqrt, f"beta{tag}": beta,
+                    f"cid{tag}": agg.cluster_ids, f"nsup{tag}": agg.n_super, f"radius{tag}": radius,
+                    f"tol{tag}": tol, f"muse{tag}": m_use, f"delta{tag}": delta_weights(agg, graph)})
+        for var in (CoarsenVariant.DELTA, CoarsenVariant.NAIVE):
+            v = var.value[0]
+            basis, pbar = coarsen_basis(pack, agg, graph, var, m_use=m_use)
+            out[f"q{v}{tag}"] = basis.q_bar
+            out[f"lb{v}{tag}"] = basis.lambda_bar
+            out[f"dsqbar{v}{tag}"] = pbar.d_sqrt
+            csr_parts(f"lapbar{v}{tag}", pbar.laplacian.matrix, out)
+        p_bar = aggregate_priors(pri.values, agg)
+        p_bar /= p_bar.sum(axis=1, keepdims=True)
+        _, pbar = coarsen_basis(pack, agg, graph, CoarsenVariant.DELTA, m_use=m_use)
+        prob = sw.LabelProblem(num_labels=grid.K, seeds=sw.SeedPartition(agg.n_super, [], []), priors=p_bar,
+                               gamma=1.0)
+        u_bar = sw.solve_fast(pbar, pbar.laplacian, prob, m_use=pbar.m)
+        u = propagate(u_bar.values, agg)
+        out.update({f"pbar{tag}": p_bar, f"ubar{tag}": u_bar.values, f"u{tag}": u.values})
+    np.savez_compressed(OUT / "aggregation.npz", **out)
+
+
 if __name__ == "__main__":
     case_path3()
     case_phantom16()
@@ -354,5 +394,6 @@ if __name__ == "__main__":
     case_errors()
     case_pack_file()
     case_registration()
+    case_aggregation()
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size)

@@ -190,3 +190,28 @@ def test_registration_solve_matches_reference():
     u = O.solve_fast(z["V3"], z["lam3"], z["d3"], lap, [], [], 27, gamma=1.0, priors=z["pri3"], m_use=50)
     np.testing.assert_allclose(u, z["U3"], rtol=1e-9, atol=1e-12)
     np.testing.assert_allclose(u @ z["vec3"].astype(float), z["disp3"], rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("tag", ["2", "3"])
+def test_aggregation_matches_reference(tag):
+    z = load_golden("aggregation")
+    dims = tuple(int(d) for d in z["dims" + tag])
+    cid, ns = O.build_aggregation(z["pri" + tag], dims, int(z["radius" + tag]), float(z["tol" + tag]))
+    np.testing.assert_array_equal(cid, z["cid" + tag])
+    assert ns == int(z["nsup" + tag])
+    np.testing.assert_array_equal(O.delta_weights(cid, dims), z["delta" + tag])
+    for v, var in (("d", "delta"), ("n", "naive")):
+        q, lam, dsq, lap = O.coarsen_basis(z["V" + tag], cid, ns, z["img" + tag], dims, float(z["beta" + tag]), var,
+                                           int(z["muse" + tag]))
+        np.testing.assert_allclose(q, z[f"q{v}{tag}"], atol=1e-12)
+        np.testing.assert_allclose(lam, z[f"lb{v}{tag}"], rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(dsq, z[f"dsqbar{v}{tag}"], rtol=1e-14)
+        np.testing.assert_allclose(lap.matrix.toarray(), csr_from(z, f"lapbar{v}{tag}").toarray(), atol=1e-15)
+    pbar = O.aggregate_priors(z["pri" + tag], cid, ns)
+    pbar /= pbar.sum(axis=1, keepdims=True)
+    np.testing.assert_allclose(pbar, z["pbar" + tag], rtol=1e-14, atol=1e-16)
+    q, lam, dsq, lap = O.coarsen_basis(z["V" + tag], cid, ns, z["img" + tag], dims, float(z["beta" + tag]), "delta",
+                                       int(z["muse" + tag]))
+    ubar = O.solve_fast(q, lam, dsq, lap.matrix, [], [], pbar.shape[1], gamma=1.0, priors=pbar, m_use=q.shape[1])
+    np.testing.assert_allclose(ubar, z["ubar" + tag], rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(ubar[cid], z["u" + tag], rtol=1e-9, atol=1e-12)
