@@ -12,6 +12,8 @@
 // Split-row TN reductions go through a workspace and are summed in a fixed
 // order, so results are bitwise deterministic run to run.
 #include "swb_common.cuh"
+#include <cstdlib>
+
 #include "dmma_core.cuh"
 
 namespace {
@@ -414,7 +416,12 @@ int run_tn_sym(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64
     SWB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cf::THREADS, Cf::SMEM));
     if (occ < 1) occ = 1;
   }
-  const int slots = swb_sm_count() * (occ > 0 ? occ : 8);
+  static const int waves = [] {
+    const char* e = getenv("SWB_TN_WAVES");
+    const int v = e ? atoi(e) : 8;
+    return v >= 1 && v <= 16 ? v : 8;
+  }();
+  const int slots = swb_sm_count() * (occ > 0 ? occ : 8) * waves;
   const int T = static_cast<int>((M + Cf::BM - 1) / Cf::BM);
   const int n_full = T * (T - 1) / 2;
   const double ratio = double(diag_max_cells(G)) / double(W * W);  // diagonal / full tile cost
