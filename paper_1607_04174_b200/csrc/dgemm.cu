@@ -338,7 +338,20 @@ int launch_nn(const double* A, int64_t lda, const double* B, int64_t ldb, int64_
   return SWB_OK;
 }
 
-// TN plan: per_tile CTAs per output tile, one wave when possible
+// Split-K TN launches about this many waves of CTAs: with a single wave
+// the CTAs that finish first leave their SMs idle for the rest of the
+// kernel; several shorter waves keep every SM busy to the end (measured at
+// c4: one wave 95.4 ms, 8 waves 82.9 ms).  SWB_TN_WAVES overrides (1..16).
+int tn_waves() {
+  static const int waves = [] {
+    const char* e = getenv("SWB_TN_WAVES");
+    const int v = e ? atoi(e) : 8;
+    return v >= 1 && v <= 16 ? v : 8;
+  }();
+  return waves;
+}
+
+// TN plan: per_tile CTAs per output tile
 struct TnPlan {
   int n_tiles, tn, per_tile, n_ctas;
   int64_t chunk_rows;
@@ -387,7 +400,7 @@ int run_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t r
   // size queries may run before any device call: bound the occupancy by 8
   // (the partial workspace grows with the CTA count)
   const int occ_used = occ > 0 ? occ : 8;
-  TnPlan p = plan_tn<Cf::BM, Cf::BN>(rows, M1, M2, symmetric, swb_sm_count() * occ_used);
+  TnPlan p = plan_tn<Cf::BM, Cf::BN>(rows, M1, M2, symmetric, swb_sm_count() * occ_used * tn_waves());
   const size_t part_bytes = sizeof(double) * size_t(p.n_ctas) * Cf::BM * Cf::BN;
   *need = part_bytes;
   if (size_only) return SWB_OK;
@@ -416,12 +429,7 @@ int run_tn_sym(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64
     SWB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cf::THREADS, Cf::SMEM));
     if (occ < 1) occ = 1;
   }
-  static const int waves = [] {
-    const char* e = getenv("SWB_TN_WAVES");
-    const int v = e ? atoi(e) : 8;
-    return v >= 1 && v <= 16 ? v : 8;
-  }();
-  const int slots = swb_sm_count() * (occ > 0 ? occ : 8) * waves;
+  const int slots = swb_sm_count() * (occ > 0 ? occ : 8) * tn_waves();
   const int T = static_cast<int>((M + Cf::BM - 1) / Cf::BM);
   const int n_full = T * (T - 1) / 2;
   const double ratio = double(diag_max_cells(G)) / double(W * W);  // diagonal / full tile cost
