@@ -193,11 +193,18 @@ template <> struct CoefT<true> { using T = double2; };
 
 // (new, new - old) pairs: pw[r*ND + d] = {what_new, what_new - what_old}, pd[r] likewise for the diagonal
 __global__ void pair_coeffs_kernel(const double* __restrict__ wn, const double* __restrict__ wo,
-                                   const double* __restrict__ dn, const double* __restrict__ dold, int64_t nw,
-                                   int64_t nd, double2* __restrict__ pw, double2* __restrict__ pd) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nw + nd; i += int64_t(gridDim.x) * blockDim.x) {
-    if (i < nw) pw[i] = make_double2(wn[i], wn[i] - wo[i]);
-    else pd[i - nw] = make_double2(dn[i - nw], dn[i - nw] - dold[i - nw]);
+                                   const double* __restrict__ dn, const double* __restrict__ dold, int nd_dir,
+                                   int64_t r0, int64_t r1, double2* __restrict__ pw, double2* __restrict__ pd) {
+  // rows [r0, r1) only: a range pass needs its own rows and their y-1 / z-1 sources
+  const int64_t nr = r1 - r0, nw = nr * nd_dir;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nw + nr; i += int64_t(gridDim.x) * blockDim.x) {
+    if (i < nw) {
+      const int64_t e = r0 * nd_dir + i;
+      pw[e] = make_double2(wn[e], wn[e] - wo[e]);
+    } else {
+      const int64_t r = r0 + (i - nw);
+      pd[r] = make_double2(dn[r], dn[r] - dold[r]);
+    }
   }
 }
 
@@ -594,8 +601,10 @@ int run_stencil(const swb_lattice* lat, const double* V, int64_t ldv, int64_t ro
   if (DELTA) {
     double2* pw = reinterpret_cast<double2*>(base + lay.slots + lay.zeros);
     double2* pd = pw + N * L.ndir;
-    pair_coeffs_kernel<<<swb_sm_count() * 8, 256, 0, st>>>(what_new, what_old, diag_new, diag_old, N * L.ndir, N,
-                                                           pw, pd);
+    const int64_t back = L.conn == 6 ? L.nx * L.ny : L.nx;   // y-1 / z-1 source rows of the range
+    const int64_t p0 = std::max<int64_t>(0, r_begin - back), p1 = r_end;
+    pair_coeffs_kernel<<<swb_sm_count() * 8, 256, 0, st>>>(what_new, what_old, diag_new, diag_old, L.ndir, p0, p1, pw,
+                                                           pd);
     SWB_CHECK_LAUNCH();
     cwhat = reinterpret_cast<const T*>(pw);
     cdiag = reinterpret_cast<const T*>(pd);
