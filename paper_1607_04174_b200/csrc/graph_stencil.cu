@@ -262,36 +262,64 @@ struct ApplyArgs {
 
 // One row of one warp's centre line: (L^' v, dL v) for the lane's two
 // columns, the Rayleigh / norm / d-projection partial sums and the W store.
+// Register window of a warp's own line along x: the centre value of the
+// previous / current row and the previous row's +x coefficient, so the +-x
+// neighbours and the -x backward coefficient come from registers (5 shared
+// V loads per row instead of 7).
+struct RowWin {
+  double2 prev, cur, f0;
+};
+
 template <int CONN, bool DELTA, int WARP>
 __device__ __forceinline__ void row_compute(const double* sc, const double* sm1, const double* sp1, int lane,
                                             bool active, double2& q, double2& s2, double2& sd, double* wrow,
-                                            const ApplyArgs& ap, const double* zrow) {
+                                            const ApplyArgs& ap, const double* zrow, RowWin& win, bool first) {
   using Rg = Ring5<CONN, DELTA>;
   constexpr int ND = Rg::ND, CW = Rg::CW, LCD = Rg::LCD, NB = nb_count(CONN);
   constexpr int ZI = WARP / Rg::YB, YI = WARP % Rg::YB;
   constexpr int CBASE = Rg::V_DBL + WARP * LCD;
+  constexpr int OWN = Rg::slot(ZI, YI) * 64;
   const double* scl = sc + 2 * lane;
   const double* sml = sm1 + 2 * lane;
   const double* spl = sp1 + 2 * lane;
-  const double2 c = *reinterpret_cast<const double2*>(scl + Rg::slot(ZI, YI) * 64);
+  if (first) {
+    win.prev = make_double2(0.0, 0.0);
+    win.cur = *reinterpret_cast<const double2*>(scl + OWN);
+    win.f0 = make_double2(0.0, 0.0);
+  }
+  const double2 c = win.cur;
+  const double2 nxt = *reinterpret_cast<const double2*>(spl + OWN);
   const double d = sc[CBASE + Rg::COEF * CW];
   double lx = 0.0, ly = 0.0, dx = 0.0, dy = 0.0;
+  double2 f0 = make_double2(0.0, 0.0);
 #pragma unroll
   for (int e = 0; e < NB; ++e) {
     const NbC t = nb_entry(CONN, e);
-    const double* vl = t.dx < 0 ? sml : t.dx > 0 ? spl : scl;
+    const bool own_x = t.dy == 0 && t.dz == 0;
+    double2 val;
+    if (own_x) {
+      val = t.dx < 0 ? win.prev : t.dx > 0 ? nxt : c;
+    } else {
+      const double* vl = t.dx < 0 ? sml : t.dx > 0 ? spl : scl;
+      val = *reinterpret_cast<const double2*>(vl + Rg::slot(ZI + t.dz, YI + t.dy) * 64);
+    }
     const double* vs = t.dx < 0 ? sm1 : t.dx > 0 ? sp1 : sc;
-    const double2 val = *reinterpret_cast<const double2*>(vl + Rg::slot(ZI + t.dz, YI + t.dy) * 64);
     const int slot = t.kind == 0 ? ND : t.kind == 1 ? t.dir
                      : (t.dz < 0 ? 2 * ND + 1 + t.dir : t.dy < 0 ? ND + 1 + t.dir : t.dir);
-    const double* cp = (t.kind == 2 ? vs : sc) + CBASE + slot * CW;
     double cn, g = 0.0;
-    if (DELTA) {
-      const double2 pr = *reinterpret_cast<const double2*>(cp);  // (new, new - old) in one 16-B load
-      cn = pr.x;
-      g = pr.y;
+    if (t.kind == 2 && own_x) {          // -x: the previous row's +x forward pair
+      cn = win.f0.x;
+      g = win.f0.y;
     } else {
-      cn = cp[0];
+      const double* cp = (t.kind == 2 ? vs : sc) + CBASE + slot * CW;
+      if (DELTA) {
+        const double2 pr = *reinterpret_cast<const double2*>(cp);  // (new, new - old) in one 16-B load
+        cn = pr.x;
+        g = pr.y;
+      } else {
+        cn = cp[0];
+      }
+      if (t.kind == 1 && t.dir == 0) f0 = make_double2(cn, g);
     }
     // L^' v in the reference CSR order (exact products and sums); dL v with FMAs
     if (t.kind == 0) {
@@ -304,6 +332,9 @@ __device__ __forceinline__ void row_compute(const double* sc, const double* sm1,
       if (DELTA) { dx = fma(-g, val.x, dx); dy = fma(-g, val.y, dy); }
     }
   }
+  win.prev = c;
+  win.cur = nxt;
+  win.f0 = f0;
   if (active) {
     q.x = fma(c.x, lx, q.x);
     q.y = fma(c.y, ly, q.y);
@@ -329,13 +360,15 @@ __device__ __forceinline__ void row_compute(const double* sc, const double* sm1,
 template <int CONN, bool DELTA, int LO, int HI>
 __device__ __forceinline__ void row_dispatch(int warp, const double* sc, const double* sm1, const double* sp1, int lane,
                                              bool active, double2& q, double2& s2, double2& sd, double* wrow,
-                                             const ApplyArgs& ap, const double* zrow) {
+                                             const ApplyArgs& ap, const double* zrow, RowWin& win, bool first) {
   if constexpr (HI - LO == 1) {
-    row_compute<CONN, DELTA, LO>(sc, sm1, sp1, lane, active, q, s2, sd, wrow, ap, zrow);
+    row_compute<CONN, DELTA, LO>(sc, sm1, sp1, lane, active, q, s2, sd, wrow, ap, zrow, win, first);
   } else {
     constexpr int MID = (LO + HI) / 2;
-    if (warp < MID) row_dispatch<CONN, DELTA, LO, MID>(warp, sc, sm1, sp1, lane, active, q, s2, sd, wrow, ap, zrow);
-    else row_dispatch<CONN, DELTA, MID, HI>(warp, sc, sm1, sp1, lane, active, q, s2, sd, wrow, ap, zrow);
+    if (warp < MID)
+      row_dispatch<CONN, DELTA, LO, MID>(warp, sc, sm1, sp1, lane, active, q, s2, sd, wrow, ap, zrow, win, first);
+    else
+      row_dispatch<CONN, DELTA, MID, HI>(warp, sc, sm1, sp1, lane, active, q, s2, sd, wrow, ap, zrow, win, first);
   }
 }
 
@@ -484,6 +517,7 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
     double* wrow = (W && line_live) ? W + (my_r0 - w_row0) * ldw + col0 + 2 * lane : nullptr;
     const double* zrow = (!DELTA && ap.Z && line_live) ? ap.Z + (my_r0 - w_row0) * ap.ldz + col0 + 2 * lane : nullptr;
     const double* sc = ring;
+    RowWin win;
     for (int x = 0; x < nxi; ++x) {
       cp_async_wait<PREF - 2>();   // rows <= x+1 have landed (this thread's copies)
       __syncthreads();             // ... every thread's; compute(x-1) finished everywhere
@@ -494,7 +528,8 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
       if (line_live) {
         // the warp's line position is a compile-time constant in each
         // instantiation, so every shared operand is an immediate offset
-        row_dispatch<CONN, DELTA, 0, ST_WARPS>(warp, sc, sm1, sp1, lane, active, q, s2, sd, wrow, ap, zrow);
+        row_dispatch<CONN, DELTA, 0, ST_WARPS>(warp, sc, sm1, sp1, lane, active, q, s2, sd, wrow, ap, zrow, win,
+                                               x == 0);
         if (wrow) wrow += ldw;
         if (zrow) zrow += ap.ldz;
       }
