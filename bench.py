@@ -317,6 +317,28 @@ def _ncu_traffic(kernel: str, cfg, dims, m):
         return None
 
 
+def fp64_probe(lib):
+    """Live FP64 tensor-core peak: back-to-back DMMA.8x8x4 on every SM
+    (swb_fp64_peak_probe), best of 5 after one warm-up, in TFLOP/s."""
+    import torch
+
+    from paper_1607_04174_b200 import _lib
+    from paper_1607_04174_b200.device import stream_handle
+    sink = torch.zeros(1, dtype=torch.float64, device="cuda")
+    flops = _lib.c_dbl()
+    best = 0.0
+    for it in range(6):
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        _lib.check(lib.swb_fp64_peak_probe(20000, _lib.c_vp(sink.data_ptr()), _lib.C.byref(flops),
+                                           stream_handle()))
+        e1.record()
+        torch.cuda.synchronize()
+        if it:
+            best = max(best, flops.value / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    return best
+
+
 def run_sharded(args):
     """N > 1 ranks (torchrun): the c4 volume split into z-slabs, one per GPU
     (strong scaling).  Step = sharded first-order update (halo exchange +
@@ -360,6 +382,7 @@ def run_sharded(args):
         (labels, _, _, rc), = sharded_solve([sh], comm, be, seeds, labs, p["labels"])
         return labels, rc
 
+    fp64_peak = fp64_probe(lib)
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
@@ -410,6 +433,14 @@ def run_sharded(args):
                 "e2e": {"value": n * m / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(len(seeds) * 12),
                         "d2h_bytes_per_step": int(n * 4 // world), "ms_per_step": ems},
                 "gpu_launches": int(launches), "clocks": clk, "phases_ms": phases}
+        rot_ms = phases.get("rotate")
+        if rot_ms:
+            rows = plan.own_end - plan.own_begin
+            ach = 2.0 * rows * m * m / (rot_ms * 1e-3) / 1e12
+            line["roofline"] = {"bound": "tensor", "kernel": "rotation V*C (DMMA NN GEMM), per GPU (rank 0 slab)",
+                                "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak,
+                                "peak_source": "live DMMA.8x8x4 probe (swb_fp64_peak_probe) in this run",
+                                "traffic": None, "algorithmic_bytes": 16.0 * rows * m}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
 
@@ -442,20 +473,7 @@ def run_gpu(args):
         torch.cuda.synchronize()
         return
 
-    # live FP64 tensor-core peak (DMMA probe), best of 5
-    sink = torch.zeros(1, dtype=torch.float64, device="cuda")
-    flops = _lib.c_dbl()
-    best = 0.0
-    for it in range(6):
-        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-        e0.record()
-        _lib.check(lib.swb_fp64_peak_probe(20000, _lib.c_vp(sink.data_ptr()), _lib.C.byref(flops),
-                                           stream_handle()))
-        e1.record()
-        torch.cuda.synchronize()
-        if it:
-            best = max(best, flops.value / (e0.elapsed_time(e1) * 1e-3) / 1e12)
-    fp64_peak = best
+    fp64_peak = fp64_probe(lib)
 
     for i in range(args.warmup):
         gpu_step(state, i)
