@@ -141,6 +141,75 @@ __global__ void __launch_bounds__(SC_THREADS) box_scores_kernel(const double* __
   }
 }
 
+// warp per voxel, the row in registers (K <= 32 * J): min over labels,
+// accumulated per warp in a fixed voxel order, then per block in warp order
+template <int J>
+__global__ void rowmin_reg_kernel(const double* __restrict__ scores, int64_t N, int64_t K, int64_t ld,
+                                  double* __restrict__ part) {
+  __shared__ double wsum[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gw = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  double acc = 0.0;
+  for (int64_t v = gw; v < N; v += nw) {
+    double mn = __longlong_as_double(0x7ff0000000000000LL);
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int64_t k = lane + 32 * j;
+      if (k < K) mn = fmin(mn, scores[v * ld + k]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    acc += mn;
+  }
+  if (lane == 0) wsum[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) s += wsum[w];
+    part[blockIdx.x] = s;
+  }
+}
+
+// warp per voxel, row in registers: logits = -(s/sigma)^2, max, exp, normalise
+template <int J>
+__global__ void softmax_reg_kernel(const double* __restrict__ scores, int64_t N, int64_t K, int64_t ld,
+                                   const double* __restrict__ sigma_p, double* __restrict__ out, int64_t ldo) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const double sigma = *sigma_p;
+  for (int64_t v = gw; v < N; v += nw) {
+    double lg[J];
+    double mx = -__longlong_as_double(0x7ff0000000000000LL);
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int64_t k = lane + 32 * j;
+      if (k < K) {
+        const double r = scores[v * ld + k] / sigma;
+        lg[j] = -(r * r);
+        mx = fmax(mx, lg[j]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      if (lane + 32 * j < K) {
+        lg[j] = exp(lg[j] - mx);
+        s += lg[j];
+      }
+    }
+    s = warp_sum(s);
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int64_t k = lane + 32 * j;
+      if (k < K) out[v * ldo + k] = lg[j] / s;
+    }
+  }
+}
+
 // per-voxel min over labels, summed in fixed order per block (deterministic)
 __global__ void rowmin_sum_kernel(const double* __restrict__ scores, int64_t N, int64_t K, int64_t ld,
                                   double* __restrict__ part) {
@@ -230,11 +299,14 @@ extern "C" int swb_similarity_priors(const double* fixed, const double* moving, 
     patch_scores_kernel<<<grid, 256, 0, st>>>(fixed, moving, nx, ny, nz, ndim, disp, K, patch_radius, scores, ld);
   }
   SWB_CHECK_LAUNCH();
-  rowmin_sum_kernel<<<512, 256, 0, st>>>(scores, N, K, ld, part);
+  if (K <= 128) rowmin_reg_kernel<4><<<512, 256, 0, st>>>(scores, N, K, ld, part);
+  else rowmin_sum_kernel<<<512, 256, 0, st>>>(scores, N, K, ld, part);
   SWB_CHECK_LAUNCH();
   sigma_kernel<<<1, 32, 0, st>>>(part, 512, N, sigma_out);
   SWB_CHECK_LAUNCH();
-  softmax_kernel<<<grid, 256, 0, st>>>(scores, N, K, ld, sigma_out, priors, ldp);
+  if (K <= 32) softmax_reg_kernel<1><<<grid, 256, 0, st>>>(scores, N, K, ld, sigma_out, priors, ldp);
+  else if (K <= 128) softmax_reg_kernel<4><<<grid, 256, 0, st>>>(scores, N, K, ld, sigma_out, priors, ldp);
+  else softmax_kernel<<<grid, 256, 0, st>>>(scores, N, K, ld, sigma_out, priors, ldp);
   SWB_CHECK_LAUNCH();
   return SWB_OK;
 }

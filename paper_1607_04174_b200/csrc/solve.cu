@@ -337,6 +337,76 @@ reconstruct_kernel(const double* __restrict__ V, int64_t ldv, int64_t row_base, 
 }
 
 // Generic finalize for many labels: U already holds V*coeff (rows r_begin..).
+// Register variant for L <= 32 * J: each lane keeps its J entries of the
+// row in registers, so the row is read once and written once (the loop
+// version reads it twice and writes it twice, with one row in flight per
+// warp).  Same operations and order as finalize_many_kernel.
+template <int J>
+__global__ void finalize_many_reg_kernel(int64_t r_begin, int64_t r_end, int64_t L, const double* __restrict__ extra,
+                                         double dnorm, const double* __restrict__ d_sqrt, double* __restrict__ U,
+                                         int64_t ldu, int32_t* __restrict__ labels, double* __restrict__ top2) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  double ex[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int64_t k = lane + 32 * j;
+    ex[j] = (extra && k < L) ? extra[k] : 0.0;
+  }
+  for (int64_t r = r_begin + gw; r < r_end; r += nw) {
+    double* u = U + (r - r_begin) * ldu;
+    double v[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int64_t k = lane + 32 * j;
+      v[j] = k < L ? u[k] : 0.0;
+    }
+    const double ds = d_sqrt[r];
+    const double g = ds / dnorm;
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      if (lane + 32 * j < L) {
+        double x = (v[j] + (extra ? g * ex[j] : 0.0)) / ds;
+        x = x > 0.0 ? x : (x != x ? x : 0.0);
+        v[j] = x;
+        s += x;
+      }
+    }
+    s = warp_sum(s);
+    const bool dead = s == 0.0;
+    if (dead) s = 1.0;
+    double p1 = -1.0, p2 = -1.0;
+    int best = 0x7fffffff;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int64_t k = lane + 32 * j;
+      if (k < L) {
+        const double x = dead ? (1.0 / double(L)) : v[j] / s;
+        u[k] = x;
+        if (x > p1) { p2 = p1; p1 = x; best = static_cast<int>(k); }
+        else if (x > p2) p2 = x;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double q1 = __shfl_xor_sync(0xffffffffu, p1, o);
+      const double q2 = __shfl_xor_sync(0xffffffffu, p2, o);
+      const int qb = __shfl_xor_sync(0xffffffffu, best, o);
+      double n1, n2;
+      int nb;
+      if (q1 > p1 || (q1 == p1 && qb < best)) { n1 = q1; nb = qb; n2 = fmax(p1, q2); }
+      else { n1 = p1; nb = best; n2 = fmax(p2, q1); }
+      p1 = n1; p2 = n2; best = nb;
+    }
+    if (lane == 0) {
+      labels[r - r_begin] = best;
+      if (top2) top2[r - r_begin] = L > 1 ? p1 - p2 : 1.0;
+    }
+  }
+}
+
 __global__ void finalize_many_kernel(int64_t r_begin, int64_t r_end, int64_t L, const double* __restrict__ extra,
                                      double dnorm, const double* __restrict__ d_sqrt, double* __restrict__ U,
                                      int64_t ldu, int32_t* __restrict__ labels, double* __restrict__ top2) {
@@ -721,8 +791,12 @@ extern "C" int swb_reconstruct_label(const double* V, int64_t ldv, int64_t row_b
   if (!U || (ldu & 1) || (ldv & 1)) return SWB_INVALID_PARAM;  // U doubles as the GEMM output
   int rc = swb_gemm_nn_alpha(V + (r_begin - row_base) * ldv, ldv, coeff, L, r_end - r_begin, mr, L, U, ldu, 0, 1.0, st);
   if (rc) return rc;
-  finalize_many_kernel<<<swb_sm_count() * 8, 256, 0, st>>>(r_begin, r_end, L, extra, dnorm, d_sqrt, U, ldu, labels,
-                                                           top2);
+  const int fg = swb_sm_count() * 8;
+  if (L <= 32) finalize_many_reg_kernel<1><<<fg, 256, 0, st>>>(r_begin, r_end, L, extra, dnorm, d_sqrt, U, ldu, labels, top2);
+  else if (L <= 64) finalize_many_reg_kernel<2><<<fg, 256, 0, st>>>(r_begin, r_end, L, extra, dnorm, d_sqrt, U, ldu, labels, top2);
+  else if (L <= 128) finalize_many_reg_kernel<4><<<fg, 256, 0, st>>>(r_begin, r_end, L, extra, dnorm, d_sqrt, U, ldu, labels, top2);
+  else if (L <= 256) finalize_many_reg_kernel<8><<<fg, 256, 0, st>>>(r_begin, r_end, L, extra, dnorm, d_sqrt, U, ldu, labels, top2);
+  else finalize_many_kernel<<<fg, 256, 0, st>>>(r_begin, r_end, L, extra, dnorm, d_sqrt, U, ldu, labels, top2);
   SWB_CHECK_LAUNCH();
   return SWB_OK;
 }
