@@ -99,38 +99,62 @@ panel_kernel(double* __restrict__ A, int64_t n, int64_t lda, int64_t k, int w, i
     sp[i * PANEL_LD + c] = A[(k + i) * lda + k + c];
   }
   __syncthreads();
+  // Thread t owns rows i = t (mod blockDim): its pivot-search candidates and
+  // its row updates are the same rows, so a column step needs only two
+  // barriers (after the warp-level pivot partials, after the swap).
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   for (int jj = 0; jj < w; ++jj) {
     ArgMax a{-1.0, 0x7fffffff};
-    for (int64_t i = jj + threadIdx.x; i < rows; i += blockDim.x) {
+    for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+      if (i < jj) continue;
       const double v = fabs(row(i)[jj]);
       a = argmax_merge(a, ArgMax{v != v ? __longlong_as_double(0x7ff0000000000000LL) : v, static_cast<int>(i)});
     }
-    const ArgMax best = block_argmax(a, sh);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ArgMax b;
+      b.v = __shfl_xor_sync(0xffffffffu, a.v, o);
+      b.i = __shfl_xor_sync(0xffffffffu, a.i, o);
+      a = argmax_merge(a, b);
+    }
+    if (lane == 0) sh[warp] = a;
+    __syncthreads();
+    // every warp reduces the per-warp partials itself (shuffles, no extra barrier)
+    ArgMax best = lane < nwarp ? sh[lane] : ArgMax{-1.0, 0x7fffffff};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ArgMax b;
+      b.v = __shfl_xor_sync(0xffffffffu, best.v, o);
+      b.i = __shfl_xor_sync(0xffffffffu, best.i, o);
+      best = argmax_merge(best, b);
+    }
     const int p = best.i;
     if (threadIdx.x == 0) piv[k + jj] = static_cast<int32_t>(k + p);
-    if (p != jj) {
-      for (int c = threadIdx.x; c < w; c += blockDim.x) {
-        double* rj = row(jj);
-        double* rp = row(p);
-        const double t = rj[c]; rj[c] = rp[c]; rp[c] = t;
-      }
+    for (int c = threadIdx.x; c < w; c += blockDim.x) {
+      double* rj = row(jj);
+      double* rp = row(p);
+      const double t = rj[c];
+      if (p != jj) { rj[c] = rp[c]; rp[c] = t; }
+      prow[c] = p != jj ? rj[c] : t;
     }
-    __syncthreads();
-    if (threadIdx.x < w) prow[threadIdx.x] = row(jj)[threadIdx.x];
     __syncthreads();
     const double pv = prow[jj];
     if (pv == 0.0) {
       if (threadIdx.x == 0) atomicExch(zero_pivot, 1);
       continue;  // LAPACK: column left unscaled, info > 0
     }
-    for (int64_t i = jj + 1 + threadIdx.x; i < rows; i += blockDim.x) {
+    // LAPACK dgetf2 / dgetrf2: scale by the reciprocal when |pivot| >= sfmin
+    const bool recip = fabs(pv) >= 2.2250738585072014e-308;
+    const double rinv = 1.0 / pv;
+    for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+      if (i <= jj) continue;
       double* ri = row(i);
-      const double l = ri[jj] / pv;
+      const double l = recip ? ri[jj] * rinv : ri[jj] / pv;
       ri[jj] = l;
       for (int c = jj + 1; c < w; ++c) ri[c] -= l * prow[c];
     }
-    __syncthreads();
   }
+  __syncthreads();
   for (int64_t e = threadIdx.x; e < srows * w; e += blockDim.x) {
     const int64_t i = e / w, c = e % w;
     A[(k + i) * lda + k + c] = sp[i * PANEL_LD + c];
@@ -219,18 +243,33 @@ __device__ void tri_solve(const double* __restrict__ LU, int64_t n, int64_t lda,
   }
 }
 
+constexpr int64_t GETRS_SMEM_N = 12288;   // 2 * 4 * n bytes of shared memory
+
 __global__ void __launch_bounds__(1024)
 getrs_kernel(const double* __restrict__ LU, int64_t n, int64_t lda, const int32_t* __restrict__ piv,
              double* B, int64_t nrhs, int64_t ldb, int32_t* __restrict__ perm, double* __restrict__ tmp) {
   // B <- P^T B (LAPACK dlaswp forward): compose the interchanges into one
-  // permutation (thread 0, O(n)), then gather the rows in parallel
+  // permutation (thread 0, O(n) dependent swaps -- in shared memory when it
+  // fits, which keeps the serial chain at shared-memory latency), then
+  // gather the rows in parallel
+  extern __shared__ int32_t sperm[];
+  const bool in_smem = n <= GETRS_SMEM_N;
+  int32_t* pm = in_smem ? sperm : perm;
+  int32_t* pv = in_smem ? sperm + n : nullptr;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    pm[j] = static_cast<int32_t>(j);
+    if (in_smem) pv[j] = piv[j];
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    for (int64_t j = 0; j < n; ++j) perm[j] = static_cast<int32_t>(j);
     for (int64_t j = 0; j < n; ++j) {
-      const int64_t p = piv[j];
-      if (p != j) { const int32_t t = perm[j]; perm[j] = perm[p]; perm[p] = t; }
+      const int64_t p = in_smem ? pv[j] : piv[j];
+      if (p != j) { const int32_t t = pm[j]; pm[j] = pm[p]; pm[p] = t; }
     }
   }
+  __syncthreads();
+  if (in_smem)
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) perm[j] = pm[j];
   __syncthreads();
   for (int64_t e = threadIdx.x; e < n * nrhs; e += blockDim.x) {
     const int64_t i = e / nrhs, c = e % nrhs;
@@ -439,7 +478,13 @@ extern "C" int swb_lu_solve(const double* LU, int64_t n, int64_t lda, const int3
   int32_t* perm = static_cast<int32_t*>(workspace);
   double* tmp = reinterpret_cast<double*>(static_cast<char*>(workspace) +
                                           swb_align_up(sizeof(int32_t) * size_t(n + 1), 256));
-  getrs_kernel<<<1, 1024, 0, swb_stream(stream)>>>(LU, n, lda, piv, B, nrhs, ldb, perm, tmp);
+  const size_t smem = n <= GETRS_SMEM_N ? sizeof(int32_t) * 2 * size_t(n) : 0;
+  static size_t attr = 48 * 1024;
+  if (smem > attr) {
+    SWB_CUDA_TRY(cudaFuncSetAttribute(getrs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = smem;
+  }
+  getrs_kernel<<<1, 1024, smem, swb_stream(stream)>>>(LU, n, lda, piv, B, nrhs, ldb, perm, tmp);
   SWB_CHECK_LAUNCH();
   return SWB_OK;
 }
