@@ -97,6 +97,13 @@ class LocalComm:
         for t in tensors:
             t.copy_(total)
 
+    def halo_start(self, shards: list):
+        self.halo_exchange(shards)   # in-process copies: nothing to overlap
+        return None
+
+    def halo_finish(self, handle) -> None:
+        return None
+
     def halo_exchange(self, shards: list) -> None:
         for a, b in zip(shards, shards[1:]):  # a below b
             u = a.plan.unit
@@ -137,6 +144,27 @@ class DistComm:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
 
+    def halo_start(self, shards: list):
+        """Post the halo Send/Recv and return without waiting (the transfer
+        overlaps the graph build and the interior stencil)."""
+        (s,) = shards
+        p = s.plan
+        u = p.unit
+        dist = self.dist
+        ops = []
+        own = s.V[p.own_slice()]
+        if p.halo_lo:
+            ops.append(dist.P2POp(dist.isend, own[:u], p.rank - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, s.V[:u], p.rank - 1, self.group))
+        if p.halo_hi:
+            ops.append(dist.P2POp(dist.isend, own[-u:], p.rank + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, s.V[-u:], p.rank + 1, self.group))
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    def halo_finish(self, handle) -> None:
+        for req in handle or []:
+            req.wait()
+
 
 # ---------------------------------------------------------------------------
 # local numerics on the GPU
@@ -160,17 +188,20 @@ class CudaBackend:
     def zeros(self, shape):
         return self.torch.zeros(shape, dtype=self.torch.float64, device="cuda")
 
-    def stencil_delta(self, lattice, V, plan, m, g_old, g_new, W):
+    def stencil_delta(self, lattice, V, plan, m, g_old, g_new, W, rows=None):
+        """Difference pass over owned rows [r0, r1) (default: all owned rows);
+        W holds the owned rows (row own_begin at W[0])."""
         t = self.torch
+        r0, r1 = rows if rows is not None else (plan.own_begin, plan.own_end)
         quad = t.empty(m, dtype=t.float64, device="cuda")
         norm2 = t.empty_like(quad)
         vtd = t.empty_like(quad)
         lat = lattice.c_struct()
         ws = WORKSPACE.get("stencil", _lib.size("swb_stencil_workspace_bytes", C.byref(lat), m))
-        _lib.call("swb_stencil_delta", C.byref(lat), ptr(V), V.shape[1], plan.row_base, plan.own_begin,
-                  plan.own_end, m, ptr(g_old.what), ptr(g_old.diag), ptr(g_new.what), ptr(g_new.diag),
-                  ptr(g_new.d_sqrt_dev), ptr(W), W.shape[1], ptr(quad), ptr(norm2), ptr(vtd), ptr(ws),
-                  ws.numel(), stream_handle())
+        Wr = W[r0 - plan.own_begin:]
+        _lib.call("swb_stencil_delta", C.byref(lat), ptr(V), V.shape[1], plan.row_base, r0, r1, m,
+                  ptr(g_old.what), ptr(g_old.diag), ptr(g_new.what), ptr(g_new.diag), ptr(g_new.d_sqrt_dev),
+                  ptr(Wr), W.shape[1], ptr(quad), ptr(norm2), ptr(vtd), ptr(ws), ws.numel(), stream_handle())
         return quad, norm2, vtd
 
     def gram_sym(self, X, Y, rows, m):
@@ -311,11 +342,21 @@ def _mark(name):
         api.TIMER.mark(name)
 
 
+def sum_in_order(xs):
+    """x0 + x1 + ... left to right (a fixed summation order)."""
+    total = xs[0]
+    for x in xs[1:]:
+        total = total + x
+    return total
+
+
 def sharded_update(shards: list, comm, backend, new_beta: float, gap_guard: float = 0.5, cut_mask=None):
     """First-order basis update of every local shard (one all-reduce)."""
+    # the halo transfer overlaps the graph build and the interior stencil;
+    # only the first / last owned unit needs the received planes
     _mark("halo")
-    comm.halo_exchange(shards)
-    parts = []
+    handle = comm.halo_start(shards)
+    staged = []
     for sh in shards:
         _mark("graph")
         g_new = backend.graph(sh.image, sh.lattice, new_beta, cut_mask)
@@ -325,8 +366,25 @@ def sharded_update(shards: list, comm, backend, new_beta: float, gap_guard: floa
         if buf is None or tuple(buf.shape) != tuple(sh.V.shape):
             buf = backend.empty(tuple(sh.V.shape))
         W = buf[sh.plan.own_slice()]
+        p_ = sh.plan
+        lo = p_.own_begin + (p_.unit if p_.halo_lo else 0)
+        hi = p_.own_end - (p_.unit if p_.halo_hi else 0)
         _mark("stencil")
-        quad, norm2, vtd = backend.stencil_delta(sh.lattice, sh.V, sh.plan, sh.m, sh.graph, g_new, W)
+        inner = backend.stencil_delta(sh.lattice, sh.V, p_, sh.m, sh.graph, g_new, W, rows=(lo, hi)) \
+            if hi > lo else None
+        staged.append((sh, g_new, buf, W, lo, hi, inner))
+    comm.halo_finish(handle)
+    parts = []
+    for sh, g_new, buf, W, lo, hi, inner in staged:
+        p_ = sh.plan
+        pieces = [inner] if inner is not None else []
+        if lo > p_.own_begin:
+            pieces.append(backend.stencil_delta(sh.lattice, sh.V, p_, sh.m, sh.graph, g_new, W,
+                                                rows=(p_.own_begin, lo)))
+        if p_.own_end > max(hi, lo):
+            pieces.append(backend.stencil_delta(sh.lattice, sh.V, p_, sh.m, sh.graph, g_new, W,
+                                                rows=(max(hi, lo), p_.own_end)))
+        quad, norm2, vtd = (sum_in_order([pc[i] for pc in pieces]) for i in range(3))
         _mark("project")
         P = backend.gram_sym(sh.own(), W, sh.plan.own_end - sh.plan.own_begin, sh.m)
         _mark("pack")

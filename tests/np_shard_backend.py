@@ -38,14 +38,15 @@ class NumpyBackend:
     def _cols(self, plan, V):
         return slice(plan.row_base, plan.row_base + V.shape[0])
 
-    def stencil_delta(self, lattice, V, plan, m, g_old, g_new, W):
-        rows = slice(plan.own_begin, plan.own_end)
+    def stencil_delta(self, lattice, V, plan, m, g_old, g_new, W, rows=None):
+        r0, r1 = rows if rows is not None else (plan.own_begin, plan.own_end)
+        rows = slice(r0, r1)
         cols = self._cols(plan, V)
         Vl = V[:, :m].numpy()
         dL = (g_new.lap.matrix - g_old.lap.matrix).tocsr()[rows][:, cols]
         Ln = g_new.lap.matrix[rows][:, cols]
-        W[:, :m] = _t(dL @ Vl)
-        Vo = Vl[plan.own_slice()]
+        W[r0 - plan.own_begin: r1 - plan.own_begin, :m] = _t(dL @ Vl)
+        Vo = Vl[r0 - plan.row_base: r1 - plan.row_base]
         quad = np.einsum("ij,ij->j", Vo, Ln @ Vl)
         norm2 = np.einsum("ij,ij->j", Vo, Vo)
         vtd = Vo.T @ g_new.lap.d_sqrt[rows]
