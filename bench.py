@@ -372,7 +372,7 @@ def run_sharded(args):
     V = W.orthonormal_basis_slab(plan, m, W.CFG_INDEX[cfg] * 1000 + 17, comm)
     lam = torch.from_numpy(W.synthetic_lambda(cfg, m)).cuda()
     img = torch.from_numpy(np.array(w.intensities)).cuda()
-    sh = Shard(plan, V, m, lam, lattice, img, be.graph(img, lattice, p["beta0"]), p["beta0"])
+    sh = Shard(plan, V, m, lam, lattice, img, be.graph(img, lattice, p["beta0"], plan=plan), p["beta0"])
     sharded_init_vtg([sh], comm, be)
     seeds, labs = W.seeds_for(w)
 

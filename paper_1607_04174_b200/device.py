@@ -190,6 +190,36 @@ class DeviceGraph:
             raise DegenerateGraph("graph has an isolated vertex (zero degree)")
         return cls(lattice, beta, what, diag, d_sqrt, float(np.sqrt(host[0])), cut_mask_dev)
 
+    @classmethod
+    def build_region(cls, intensities_dev, lattice: LatticeSpec, beta: float, u_lo: int, u_hi: int,
+                     cut_mask_dev=None) -> "DeviceGraph":
+        """Coefficients for the units (planes / lines) [u_lo, u_hi) only, in
+        full-size (globally indexed) arrays, zero elsewhere: the slab graph of
+        a z-slab shard.  Degrees of the region's outermost units miss their
+        outside neighbours, so callers build one unit beyond what they read.
+        ``dnorm`` is left NaN (a global reduction; set by the caller)."""
+        torch = require_cuda()
+        if beta < 0:
+            raise InvalidParam(f"beta must be >= 0, got {beta}")
+        dims = lattice.dims
+        unit = dims[0] * dims[1] if len(dims) == 3 else dims[0]
+        sub_dims = tuple(dims[:-1]) + (u_hi - u_lo,)
+        sub = LatticeSpec(sub_dims, lattice.connectivity, lattice.weight_mode)
+        n, nd = lattice.n, lattice.ndir
+        what = torch.zeros(n * nd, dtype=torch.float64, device="cuda")
+        diag = torch.zeros(n, dtype=torch.float64, device="cuda")
+        d_sqrt = torch.zeros(n, dtype=torch.float64, device="cuda")
+        flag = torch.zeros(2, dtype=torch.int32, device="cuda")
+        r0 = u_lo * unit
+        lat = sub.c_struct()
+        cut = C.c_void_p(cut_mask_dev.data_ptr() + r0 * nd) if cut_mask_dev is not None else None
+        _lib.call("swb_graph_build", C.byref(lat), C.c_void_p(intensities_dev.data_ptr() + 8 * r0), float(beta), cut,
+                  C.c_void_p(what.data_ptr() + 8 * r0 * nd), C.c_void_p(diag.data_ptr() + 8 * r0),
+                  C.c_void_p(d_sqrt.data_ptr() + 8 * r0), ptr(flag), stream_handle())
+        if int(flag[0].item()) != 0:
+            raise DegenerateGraph("graph has an isolated vertex (zero degree)")
+        return cls(lattice, beta, what, diag, d_sqrt, float("nan"), cut_mask_dev)
+
     # --- reference Laplacian surface (host, lazy) --------------------------
     @property
     def mode(self):

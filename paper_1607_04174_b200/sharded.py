@@ -2,7 +2,8 @@
 
 The eigenbasis V is split by rows along the slowest grid axis (z in 3-D, y in
 2-D): rank r owns planes [z0, z1) and keeps one halo plane on each interior
-side.  The graph (image, stencil coefficients) is replicated.
+side.  The image is replicated; each rank builds the graph (stencil
+coefficients) of its slab only (owned units, halos and one unit beyond).
 
   update   halo exchange of V (one plane per neighbour) -> local difference
            stencil + local symmetric projection P_r = V_r^T W_r -> ONE
@@ -177,9 +178,23 @@ class CudaBackend:
         import torch
         self.torch = torch
 
-    # graph (replicated)
-    def graph(self, image_dev, lattice: LatticeSpec, beta: float, cut_mask=None) -> DeviceGraph:
-        return DeviceGraph.build(image_dev, lattice, beta, cut_mask)
+    # graph: the whole lattice, or (plan given) the shard's slab -- its owned
+    # units, the halo units and one more unit each side for their degrees
+    def graph(self, image_dev, lattice: LatticeSpec, beta: float, cut_mask=None, plan=None) -> DeviceGraph:
+        if plan is None:
+            return DeviceGraph.build(image_dev, lattice, beta, cut_mask)
+        n_units = lattice.dims[-1]
+        return DeviceGraph.build_region(image_dev, lattice, beta, max(0, plan.u0 - 2), min(n_units, plan.u1 + 2),
+                                        cut_mask)
+
+    def dnorm_partial(self, graph, plan):
+        """sum of d_sqrt^2 over the owned rows (its all-reduce is ||d_sqrt||^2)."""
+        t = self.torch
+        out = t.empty(1, dtype=t.float64, device="cuda")
+        d = graph.d_sqrt_dev[plan.own_begin: plan.own_end]
+        ws = WORKSPACE.get("sumsq", 256 * 8)
+        _lib.call("swb_sumsq", ptr(d), d.numel(), ptr(out), ptr(ws), ws.numel(), stream_handle())
+        return out
 
     def empty(self, shape, dtype="f64"):
         t = self.torch
@@ -359,7 +374,7 @@ def sharded_update(shards: list, comm, backend, new_beta: float, gap_guard: floa
     staged = []
     for sh in shards:
         _mark("graph")
-        g_new = backend.graph(sh.image, sh.lattice, new_beta, cut_mask)
+        g_new = backend.graph(sh.image, sh.lattice, new_beta, cut_mask, plan=sh.plan)
         # ping-pong: the spare local buffer holds W = dL V in its owned rows,
         # then V' (W is dead after P); the old V becomes the next spare
         buf = sh.extra.pop("spare", None)
@@ -389,11 +404,12 @@ def sharded_update(shards: list, comm, backend, new_beta: float, gap_guard: floa
         P = backend.gram_sym(sh.own(), W, sh.plan.own_end - sh.plan.own_begin, sh.m)
         _mark("pack")
         m = sh.m
-        flat = backend.zeros((m * m + 3 * m,))
+        flat = backend.zeros((m * m + 3 * m + 1,))
         flat[: m * m] = P.reshape(-1)
         flat[m * m: m * m + m] = quad
         flat[m * m + m: m * m + 2 * m] = norm2
-        flat[m * m + 2 * m:] = vtd
+        flat[m * m + 2 * m: m * m + 3 * m] = vtd
+        flat[m * m + 3 * m:] = backend.dnorm_partial(g_new, p_)
         parts.append((sh, g_new, buf, flat))
     _mark("allreduce")
     comm.allreduce_sum([p[3] for p in parts])
@@ -401,7 +417,8 @@ def sharded_update(shards: list, comm, backend, new_beta: float, gap_guard: floa
         _mark("coeffs")
         m = sh.m
         P = flat[: m * m].reshape(m, m)
-        quad, norm2, vtd = flat[m * m: m * m + m], flat[m * m + m: m * m + 2 * m], flat[m * m + 2 * m:]
+        quad, norm2, vtd = flat[m * m: m * m + m], flat[m * m + m: m * m + 2 * m], flat[m * m + 2 * m: m * m + 3 * m]
+        g_new.dnorm = float(flat[m * m + 3 * m:].sum().item() ** 0.5)   # global ||d_sqrt||
         Cm, lam, order = backend.update_coeffs(P, sh.values, quad, norm2, m, gap_guard)
         V_new = buf
         _mark("rotate")
@@ -423,6 +440,10 @@ def sharded_update(shards: list, comm, backend, new_beta: float, gap_guard: floa
 def sharded_init_vtg(shards: list, comm, backend):
     """V^T g (g = d_sqrt / ||d_sqrt||) of the current basis: local partial
     over the owned rows + one all-reduce."""
+    dn = [backend.dnorm_partial(sh.graph, sh.plan) for sh in shards]
+    comm.allreduce_sum(dn)
+    for sh, d in zip(shards, dn):
+        sh.graph.dnorm = float(d.sum().item() ** 0.5)   # global ||d_sqrt|| (slab graphs hold their part)
     parts = [backend.column_dot(sh.own(), sh.graph.d_sqrt_dev[sh.plan.own_begin: sh.plan.own_end], sh.m)
              for sh in shards]
     comm.allreduce_sum(parts)

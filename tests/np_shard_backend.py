@@ -22,12 +22,16 @@ def _t(a):
 
 
 class NumpyBackend:
-    def graph(self, image, lattice, beta, cut_mask=None):
+    def graph(self, image, lattice, beta, cut_mask=None, plan=None):
         img = image.numpy() if hasattr(image, "numpy") else np.asarray(image)
         lap = O.build_laplacian(img, lattice.dims, beta, lattice.weight_mode, lattice.connectivity,
                                 cut_edges=cut_mask)
         return SimpleNamespace(lap=lap, d_sqrt_dev=_t(lap.d_sqrt), dnorm=float(np.linalg.norm(lap.d_sqrt)),
                                lattice=lattice)
+
+    def dnorm_partial(self, graph, plan):
+        d = graph.lap.d_sqrt[plan.own_begin: plan.own_end]
+        return _t(np.array([np.dot(d, d)]))
 
     def empty(self, shape, dtype="f64"):
         return torch.zeros(shape, dtype=torch.float64)

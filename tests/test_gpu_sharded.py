@@ -11,7 +11,7 @@ from oracle import rw_oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("world", [1, 2, 4])
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
 @pytest.mark.parametrize("dims,conn,mode", [((12, 10, 16), 6, "sq"), ((24, 32), 8, "sq"), ((20, 24), 4, "abs")])
 def test_sharded_matches_single_gpu(cuda_ok, world, dims, conn, mode):
     import torch
