@@ -161,6 +161,90 @@ panel_kernel(double* __restrict__ A, int64_t n, int64_t lda, int64_t k, int w, i
   }
 }
 
+// Register-resident panel (rows <= 1024, width <= RW): thread t owns panel
+// row t in registers for the whole factorisation, so a column step is a
+// warp-shuffle pivot search, one barrier for the per-warp partials, a row
+// swap + pivot-row broadcast through shared memory (second barrier) and a
+// rank-1 update in registers -- no shared-memory traffic for the update.
+constexpr int RW = 16;
+
+__global__ void __launch_bounds__(1024)
+panel_reg_kernel(double* __restrict__ A, int64_t n, int64_t lda, int64_t k, int w, int32_t* __restrict__ piv,
+                 int32_t* __restrict__ zero_pivot) {
+  __shared__ ArgMax sh[32];
+  __shared__ double prow[RW];
+  __shared__ double swp[RW];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nwarp = blockDim.x >> 5;
+  const int64_t rows = n - k;
+  const bool mine = t < rows;
+  double a[RW];
+#pragma unroll
+  for (int c = 0; c < RW; ++c) a[c] = (mine && c < w) ? A[(k + t) * lda + k + c] : 0.0;
+#pragma unroll
+  for (int jj = 0; jj < RW; ++jj) {
+    if (jj >= w) break;
+    ArgMax best{-1.0, 0x7fffffff};
+    if (mine && t >= jj) {
+      const double v = fabs(a[jj]);
+      best = ArgMax{v != v ? __longlong_as_double(0x7ff0000000000000LL) : v, t};
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ArgMax b;
+      b.v = __shfl_xor_sync(0xffffffffu, best.v, o);
+      b.i = __shfl_xor_sync(0xffffffffu, best.i, o);
+      best = argmax_merge(best, b);
+    }
+    if (lane == 0) sh[warp] = best;
+    __syncthreads();
+    best = lane < nwarp ? sh[lane] : ArgMax{-1.0, 0x7fffffff};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ArgMax b;
+      b.v = __shfl_xor_sync(0xffffffffu, best.v, o);
+      b.i = __shfl_xor_sync(0xffffffffu, best.i, o);
+      best = argmax_merge(best, b);
+    }
+    const int p = best.i;
+    if (t == 0) piv[k + jj] = static_cast<int32_t>(k + p);
+    if (t == p) {
+#pragma unroll
+      for (int c = 0; c < RW; ++c) prow[c] = a[c];       // the new row jj
+    }
+    if (t == jj && p != jj) {
+#pragma unroll
+      for (int c = 0; c < RW; ++c) swp[c] = a[c];        // old row jj goes to row p
+    }
+    __syncthreads();
+    if (p != jj) {
+      if (t == jj) {
+#pragma unroll
+        for (int c = 0; c < RW; ++c) a[c] = prow[c];
+      } else if (t == p) {
+#pragma unroll
+        for (int c = 0; c < RW; ++c) a[c] = swp[c];
+      }
+    }
+    const double pv = prow[jj];
+    if (pv == 0.0) {
+      if (t == 0) atomicExch(zero_pivot, 1);
+      continue;  // LAPACK: column left unscaled, info > 0
+    }
+    if (mine && t > jj) {
+      // LAPACK dgetf2 / dgetrf2: scale by the reciprocal when |pivot| >= sfmin
+      const double l = fabs(pv) >= 2.2250738585072014e-308 ? a[jj] * (1.0 / pv) : a[jj] / pv;
+      a[jj] = l;
+#pragma unroll
+      for (int c = jj + 1; c < RW; ++c) a[c] -= l * prow[c];
+    }
+  }
+  if (mine) {
+#pragma unroll
+    for (int c = 0; c < RW; ++c)
+      if (c < w) A[(k + t) * lda + k + c] = a[c];
+  }
+}
+
 // apply the panel's interchanges to columns outside [k, k+w)
 __global__ void swap_kernel(double* __restrict__ A, int64_t n, int64_t lda, int64_t k, int w,
                             const int32_t* __restrict__ piv) {
@@ -431,9 +515,17 @@ extern "C" int swb_lu_factor(double* A, int64_t n, int64_t lda, int32_t* piv, do
     SWB_CUDA_TRY(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  for (int64_t k = 0; k < n; k += NB) {
-    const int w = static_cast<int>(std::min<int64_t>(NB, n - k));
-    panel_kernel<<<1, PANEL_THREADS, smem, st>>>(A, n, lda, k, w, piv, zp);
+  // systems up to 1024 rows: 16-wide panels held in registers (one row per
+  // thread); larger ones: 32-wide panels in shared memory
+  const bool reg_panel = n <= 1024;
+  const int nb = reg_panel ? RW : NB;
+  const unsigned reg_threads = static_cast<unsigned>((n + 31) / 32 * 32);
+  for (int64_t k = 0; k < n; k += nb) {
+    const int w = static_cast<int>(std::min<int64_t>(nb, n - k));
+    if (reg_panel)
+      panel_reg_kernel<<<1, reg_threads, 0, st>>>(A, n, lda, k, w, piv, zp);
+    else
+      panel_kernel<<<1, PANEL_THREADS, smem, st>>>(A, n, lda, k, w, piv, zp);
     SWB_CHECK_LAUNCH();
     const int64_t others = n - w;
     if (others > 0) {
