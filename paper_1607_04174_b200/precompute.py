@@ -228,13 +228,16 @@ def smallest_eigs_device(graph: DeviceGraph, m: int, eig_tol: float = EIG_TOL, s
         it += 1
     info = {"iterations": it, "k": k, "degree": degree, "applies": op.applies, "history": history}
     take = m if converged >= m else converged
-    V = torch.zeros((n, round_up(max(take, 1), 8)), dtype=torch.float64, device="cuda")
+    values = theta.cpu().numpy()[:take].copy()
+    # the Ritz block becomes the pack's basis in place (its leading dimension
+    # stays round_up(k, 8); columns >= take are zeroed): at BASELINE scale the
+    # three N x k blocks already fill most of HBM
+    del Y, W
+    V = X
+    V[:, take:].zero_()
     if take:
-        V[:, :take].copy_(X[:, :take])
         ws = WORKSPACE.get("columns", _lib.size("swb_column_workspace_bytes", take))
         _lib.call("swb_canonical_signs", ptr(V), V.shape[1], n, take, ptr(ws), ws.numel(), stream_handle())
-    values = theta.cpu().numpy()[:take].copy()
-    del X, Y, W
     if converged < m:
         raise NotConverged(f"only {converged}/{m} eigenpairs converged (iteration cap {max_iter})",
                            partial=(V, values), converged=converged)
