@@ -88,3 +88,45 @@ def test_select_m_then_solve_refreshed(cuda_ok):
     assert m == m_o
     np.testing.assert_allclose(np.array([s["f"] for s in info["steps"]]),
                                np.array([s["f"] for s in info_o["steps"]]), rtol=1e-9, atol=1e-12)
+
+
+def _seed_fit_gpu(V, seeds, labs, d_sqrt, k, steps, bound):
+    """swb_seed_fit_schedule straight through the C ABI (row-major V)."""
+    import torch
+
+    from paper_1607_04174_b200 import _lib
+    from paper_1607_04174_b200.device import WORKSPACE, ptr, round_up, stream_handle
+    n, m = V.shape
+    ldv = round_up(m, 2)
+    Vd = torch.zeros((n, ldv), dtype=torch.float64, device="cuda")
+    Vd[:, :m] = torch.from_numpy(np.asarray(V, dtype=np.float64))
+    s = len(seeds)
+    sidx = torch.tensor(seeds, dtype=torch.int64, device="cuda")
+    slab = torch.tensor(labs, dtype=torch.int32, device="cuda")
+    d = torch.tensor(d_sqrt, dtype=torch.float64, device="cuda")
+    st = torch.tensor(steps, dtype=torch.int32, device="cuda")
+    f = torch.empty((len(steps), k), dtype=torch.float64, device="cuda")
+    ws = WORKSPACE.get("seed_fit_t", _lib.size("swb_seed_fit_workspace_bytes", s, m, k, len(steps)))
+    _lib.call("swb_seed_fit_schedule", ptr(Vd), ldv, None, ptr(sidx), ptr(slab), s, ptr(d), m, k, ptr(st), len(steps),
+              int(max(steps)), float(bound), ptr(f), ptr(ws), ws.numel(), stream_handle())
+    return f.cpu().numpy()
+
+
+def test_seed_fit_known_answers(cuda_ok):
+    """The reference's seed_fit closed forms (tests/test_adaptive.py): exact
+    span, 0.6/0.8 projection (0.64), zero bound, active bound (ridge path)."""
+    # exact span: q_s = I_3, u = e_0
+    f = _seed_fit_gpu(np.eye(3), [0, 1, 2], [0, 1, 1], [1.0, 1.0, 1.0], 2, [3], 100.0)
+    assert f[0, 0] < 1e-12
+    # closed form: q_s = [0.6, 0.8]^T, u = [1, 0] -> 0.64
+    f = _seed_fit_gpu(np.array([[0.6], [0.8]]), [0, 1], [0, 1], [1.0, 1.0], 2, [1], 100.0)
+    assert abs(f[0, 0] - 0.64) < 1e-10
+    # zero bound: alpha = 0, f = |u|^2 = 3
+    f = _seed_fit_gpu(np.ones((4, 2)), [0, 1, 2, 3], [0, 1, 0, 0], [1.0] * 4, 2, [2], 0.0)
+    assert abs(f[0, 0] - 3.0) < 1e-12
+    # active bound: the minimum-norm coefficient (1e3) exceeds the bound
+    q = np.array([[1e-3], [0.0]])
+    f_free = _seed_fit_gpu(q, [0, 1], [0, 1], [1.0, 1.0], 2, [1], 1e9)
+    assert f_free[0, 0] < 1e-12
+    f_tight = _seed_fit_gpu(q, [0, 1], [0, 1], [1.0, 1.0], 2, [1], 1.0)
+    assert abs(f_tight[0, 0] - (1 - 1e-3) ** 2) < 1e-3 * (1 - 1e-3) ** 2
