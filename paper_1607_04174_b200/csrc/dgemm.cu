@@ -517,10 +517,12 @@ int swb_gemm_nn_alpha(const double* A, int64_t lda, const double* B, int64_t ldb
   // pick the column tile that wastes the least of M2
   auto padded = [&](int64_t b) { return (M2 + b - 1) / b * b; };
   const int64_t p80 = padded(80), p64 = padded(64), p128 = padded(128), p32 = padded(32);
+  // (ties prefer the 4-warp configurations: the 8-warp 128-column tile is
+  // register-capped at two CTAs per SM)
   int64_t best = p80;
   int which = 80;
-  if (p128 < best) { best = p128; which = 128; }
   if (p64 < best) { best = p64; which = 64; }
+  if (p128 < best) { best = p128; which = 128; }
   if (p32 < best) { best = p32; which = 32; }
   switch (which) {
     case 128: return launch_nn<4, 2, 4, 8, 3>(A, lda, B, ldb, rows, K, M2, out, ldo, accumulate, alpha, st);
