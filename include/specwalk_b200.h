@@ -316,6 +316,37 @@ int swb_csr_spmm(const int64_t* indptr, const int64_t* indices, const double* da
 int swb_edge_weights(const swb_lattice* lat, const double* intensities, double beta, const uint8_t* cut_mask,
                      double* w, void* stream);
 
+/* ---- composite entry points (whole update / whole solve per call) ---- */
+/* First-order update of SURVEY §7 for beta_old -> beta_new (and/or cut
+ * masks): builds both graphs (graphs.py:127-159), the difference stencil,
+ * the symmetric DMMA projection P, refresh eigenvalues + coefficients C and
+ * the rotation V_out = V C (V_out distinct from V, same ldv; pad columns
+ * zeroed).  Outputs: lambda_out / order_out (M), d_sqrt_out (N, new graph),
+ * vtg_out (M, optional: V_out^T d_sqrt / ||d_sqrt||), dnorm_out (device
+ * double, optional), degenerate_out (2 device ints, optional: nonzero ->
+ * DegenerateGraph for the old / new graph, read after synchronising). */
+size_t swb_update_workspace_bytes(const swb_lattice* lat, int64_t M);
+int swb_update_first_order(const swb_lattice* lat, const double* image, double beta_old, double beta_new,
+                           const uint8_t* cut_old, const uint8_t* cut_new, const double* V, int64_t ldv,
+                           const double* lambda_old, int64_t M, double gap_guard, double* V_out,
+                           double* lambda_out, int64_t* order_out, double* d_sqrt_out, double* vtg_out,
+                           double* dnorm_out, int32_t* degenerate_out, void* workspace, size_t workspace_bytes,
+                           void* stream);
+/* Reduced-basis RW solve (fastrw.py:352-467 + solver.py:55-66 +
+ * images.py:128-130) on a row-major basis V (ldv) with eigenvalues values
+ * (M, ascending) and the graph's stencil coefficients (what, diag, d_sqrt):
+ * gamma == 0 needs seeds and vtg (V^T d_sqrt / ||d_sqrt||, M); gamma > 0
+ * needs priors (N x K, ld ldp).  Writes labels_out (N int32), top2_out and
+ * U_out (optional for K <= 8, required with ldu even beyond).  Synchronous:
+ * returns SWB_SINGULAR_SMALL_SYSTEM when rcond < 1e-14 (rcond_host gets it). */
+size_t swb_rw_solve_workspace_bytes(const swb_lattice* lat, int64_t M, int64_t m_use, int64_t S, int64_t K,
+                                    int with_priors);
+int swb_rw_solve(const swb_lattice* lat, const double* what, const double* diag, const double* d_sqrt,
+                 const double* V, int64_t ldv, const double* values, const double* vtg, int64_t M, int64_t m_use,
+                 const int64_t* seed_idx, const int32_t* seed_lab, int64_t S, int64_t K, double gamma,
+                 const double* priors, int64_t ldp, int32_t* labels_out, double* top2_out, double* U_out,
+                 int64_t ldu, double* rcond_host, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- small helpers used by the host layer --------------------------- */
 /* out = sum_x v[x]^2 over n entries (deterministic). */
 int swb_sumsq(const double* v, int64_t n, double* out, void* workspace,

@@ -56,6 +56,13 @@ SIGNATURES = {
     "swb_csr_spmm": (C.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp]),
     "swb_edge_weights": (C.c_int, [C.POINTER(Lattice), c_vp, c_dbl, c_vp, c_vp, c_vp]),
     "swb_canonical_signs": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_sz, c_vp]),
+    "swb_update_workspace_bytes": (c_sz, [C.POINTER(Lattice), c_i64]),
+    "swb_update_first_order": (C.c_int, [C.POINTER(Lattice), c_vp, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64,
+                                         c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "swb_rw_solve_workspace_bytes": (c_sz, [C.POINTER(Lattice), c_i64, c_i64, c_i64, c_i64, C.c_int]),
+    "swb_rw_solve": (C.c_int, [C.POINTER(Lattice), c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp,
+                               c_vp, c_i64, c_i64, c_dbl, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_sz,
+                               c_vp]),
     "swb_gemm_tn_workspace_bytes": (c_sz, [c_i64, c_i64, c_i64]),
     "swb_gemm_tn": (C.c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, C.c_int, c_vp, c_i64,
                               c_vp, c_sz, c_vp]),
