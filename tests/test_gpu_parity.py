@@ -391,3 +391,26 @@ def test_cut_update_matches_oracle(cuda_ok):
     lam_r, order_r = O.refresh(V, lap1)
     assert_lam(r.lambda_hat, lam_r)
     np.testing.assert_array_equal(r.order, order_r)
+
+
+def test_solve_large_seed_system(cuda_ok):
+    """S = 2000 seeds: a 2001^2 bordered system (panels beyond the
+    register-resident size and beyond the shared-memory panel rows)."""
+    rng = np.random.default_rng(21)
+    dims = (60, 50)
+    n = 3000
+    img = np.clip(0.5 + 0.3 * (np.add.outer(np.arange(60), np.arange(50)).ravel(order="F") > 55) +
+                  rng.normal(0, 0.05, n), 0, 1)
+    lap = O.build_laplacian(img, dims, 20.0)
+    vals, vecs = np.linalg.eigh(lap.matrix.toarray())
+    m = 120
+    image = swb.Image(dims, img)
+    pack = swb.SpectralPack(dims=dims, spacing=(), beta=20.0, eigen=swb.EigenBasis(np.asfortranarray(vecs[:, :m]),
+                                                                                    vals[:m]),
+                            d_sqrt=lap.d_sqrt, provenance=swb.PackProvenance(image.content_hash()))
+    seeds = np.sort(rng.choice(n, 2000, replace=False))
+    labs = (np.add.outer(np.arange(60), np.arange(50)).ravel(order="F")[seeds] > 55).astype(int)
+    f = swb.solve_fast(pack, lap.matrix, _prob(seeds, labs, n=n), m_use=m, want_field=True)
+    u = O.solve_fast(vecs[:, :m], vals[:m], lap.d_sqrt, lap.matrix, seeds, labs, 2, m_use=m)
+    np.testing.assert_allclose(f.values, u, atol=1e-9)
+    assert_labels_match(swb.hard_labels(f).labels, u)
