@@ -414,3 +414,36 @@ def test_solve_large_seed_system(cuda_ok):
     u = O.solve_fast(vecs[:, :m], vals[:m], lap.d_sqrt, lap.matrix, seeds, labs, 2, m_use=m)
     np.testing.assert_allclose(f.values, u, atol=1e-9)
     assert_labels_match(swb.hard_labels(f).labels, u)
+
+
+@pytest.mark.parametrize("dims", [(1, 23), (23, 1), (2, 2), (3, 1, 5), (1, 1, 9)])
+def test_degenerate_shapes_update_and_solve(cuda_ok, dims):
+    """Lines of length one, single-line volumes and tiny lattices through the
+    stencil ring, the projection / rotation and the solve."""
+    rng = np.random.default_rng(sum(dims))
+    n = int(np.prod(dims))
+    img = np.clip(0.5 + 0.2 * rng.standard_normal(n), 0, 1)
+    lap0 = O.build_laplacian(img, dims, 5.0)
+    vals, vecs = np.linalg.eigh(lap0.matrix.toarray())
+    m = min(n, 4)
+    image = swb.Image(dims, img)
+    pack = swb.SpectralPack(dims=dims, spacing=(), beta=5.0, eigen=swb.EigenBasis(np.asfortranarray(vecs[:, :m]),
+                                                                                   vals[:m]),
+                            d_sqrt=lap0.d_sqrt, provenance=swb.PackProvenance(image.content_hash()))
+    dp = swb.to_device(pack, image=image)
+    up = swb.update_basis(dp, image, 7.0, method="first_order", keep_P=True)
+    lap1 = O.build_laplacian(img, dims, 7.0)
+    Vo, lamo, order, P, _ = O.first_order_update(vecs[:, :m], vals[:m], lap0, lap1)
+    np.testing.assert_allclose(up.P.cpu().numpy()[:, :m], P, rtol=0, atol=1e-12)
+    assert_lam(up.lambda_hat, lamo)
+    seeds = np.array([0, n - 1])
+    f = swb.solve_fast(up, up.laplacian, _prob(seeds, [0, 1], n=n), want_field=True)
+    u = O.solve_fast(Vo, lamo, lap1.d_sqrt, lap1.matrix, seeds, [0, 1], 2)
+    np.testing.assert_allclose(f.values, u, atol=1e-9)
+
+
+def test_single_voxel_graph_is_degenerate(cuda_ok):
+    import torch
+    lat = swb.LatticeSpec.make((1, 1))
+    with pytest.raises(swb.DegenerateGraph):
+        swb.DeviceGraph.build(torch.tensor([0.5], dtype=torch.float64, device="cuda"), lat, 1.0)
