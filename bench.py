@@ -549,7 +549,7 @@ def run_gpu(args):
     mp = ROOT / "MEASURED_PEAKS.json"
     if mp.exists():
         peaks = json.loads(mp.read_text())
-    hbm = float(peaks.get("hbm_gbs", 6544.3))
+    hbm = float(peaks.get("hbm_gbs", 6650.0))   # fallback: B200_PROFILING.md
     proj_ms = phases.get("project")
     st_ms = phases.get("stencil")
     rc_ms = phases.get("solve_reconstruct")
@@ -601,6 +601,9 @@ def run_gpu(args):
                      "traffic": _ncu_traffic("rotation_nn", cfg, dims, m),
                      "algorithmic_bytes": 16.0 * n * m},
         "kernels": kernels,
+        "peaks": {"fp64_tflops": fp64_peak, "fp64_source": "of measured: live DMMA probe in this run",
+                  "hbm_gbs": hbm, "hbm_source": "of measured: MEASURED_PEAKS.json hbm_gbs" if mp.exists()
+                  else "of fallback: B200_PROFILING.md"},
         "update": {"ms": upd_ms, "value": n * m / (upd_ms * 1e-3) if upd_ms else None, "unit": UNIT},
         "solve": {"ms": solve_ms, "value": n / (solve_ms * 1e-3) if solve_ms else None, "unit": "voxels/s"},
         "phases_ms": phases,
