@@ -54,6 +54,9 @@ def parse_args():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=0, help="ncu helper: run N steps, no timing")
     ap.add_argument("--sharded", action="store_true", help="use the z-slab sharded path even at N=1")
+    ap.add_argument("--method", choices=["first_order", "rayleigh"], default="first_order",
+                    help="basis update of each step: the north-star first-order update (default) or the "
+                         "reference's eigenvalue-only refresh (refresh.py:63-82)")
     return ap.parse_args()
 
 
@@ -247,6 +250,13 @@ def _next_pack(state, beta):
     """Chained update in ping-pong mode: V' goes into the previous step's
     (retired) basis buffer, so no 54 GB allocation happens per step."""
     import paper_1607_04174_b200 as swb
+    if state.get("method") == "rayleigh":
+        # the reference's refresh: new eigenvalues + column order on the
+        # resident basis (no rotation, nothing to ping-pong)
+        base = state.setdefault("base", state["pack"])
+        pack = swb.refresh(base, state["image"], beta)
+        state["pack"] = pack
+        return pack
     spare = state.pop("spare", None)
     old = state["pack"]
     pack = swb.update_basis(old, state["image"], beta, method="first_order", out=spare)
@@ -466,6 +476,7 @@ def run_gpu(args):
     lib = _lib.load()
 
     state = setup_gpu(cfg, dims, m, rank)
+    state["method"] = args.method
     n = state["n"]
     if args.profile_steps:
         for i in range(args.profile_steps):
@@ -542,6 +553,7 @@ def run_gpu(args):
         return
 
     # ---- roofline of the dominant kernel (rotation GEMM, DMMA) ------------
+    rayleigh = args.method == "rayleigh"
     rot_ms = phases.get("rotate")
     rot_flops = 2.0 * n * m * m
     achieved = rot_flops / (rot_ms * 1e-3) / 1e12 if rot_ms else None
@@ -571,6 +583,13 @@ def run_gpu(args):
     for k in ("stencil_delta", "reconstruct_argmax"):
         if kernels[k].get("gbs"):
             kernels[k]["frac_hbm"] = kernels[k]["gbs"] / hbm
+    if rayleigh:   # the reference's refresh: one read-only stencil pass over V (HBM)
+        sr_ms = phases.get("stencil_rayleigh")
+        kernels = {k: v for k, v in kernels.items() if k not in ("rotation_dmma", "projection_dmma", "stencil_delta")}
+        kernels["stencil_rayleigh"] = {"ms": sr_ms, "gbs": (8.0 * n * m + 48.0 * n) / (sr_ms * 1e-3) / 1e9
+                                       if sr_ms else None}
+        if sr_ms:
+            kernels["stencil_rayleigh"]["frac_hbm"] = kernels["stencil_rayleigh"]["gbs"] / hbm
 
     cpu = None
     if not args.no_cpu:
@@ -585,7 +604,8 @@ def run_gpu(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg}: {'x'.join(map(str, dims_full))} volume, K={m}, first-order beta update "
+        "config": {"workload": f"{cfg}: {'x'.join(map(str, dims_full))} volume, K={m}, "
+                               f"{'refresh (reference, eigenvalue-only)' if rayleigh else 'first-order'} beta update "
                                f"{state['params']['beta0']}<->{state['params']['beta1']} + " + (
                                    f"{state['params']['labels']}-label RW solve, S={s}" if cfg != "c5" else
                                    f"similarity priors (grid {state['params']['grid']}, patch radius "
@@ -594,7 +614,11 @@ def run_gpu(args):
                    "N": n, "K": m, "labels": state["params"]["labels"], "seeds": int(s),
                    "parallelism": "replicas" if world > 1 else "single",
                    "l2": "inputs larger than L2 (V = %.1f GB)" % (n * m * 8 / 1e9)},
-        "roofline": {"bound": "tensor", "kernel": "rotation V*C (DMMA NN GEMM)", "achieved": achieved,
+        "roofline": ({"bound": "hbm", "kernel": "refresh Rayleigh stencil pass (read V once)",
+                      "achieved": kernels["stencil_rayleigh"]["gbs"], "peak": hbm, "unit": "GB/s",
+                      "frac": kernels["stencil_rayleigh"].get("frac_hbm"), "traffic": None,
+                      "algorithmic_bytes": 8.0 * n * m + 48.0 * n} if rayleigh else None) or
+                    {"bound": "tensor", "kernel": "rotation V*C (DMMA NN GEMM)", "achieved": achieved,
                      "peak": fp64_peak, "unit": "TFLOP/s", "frac": (achieved / fp64_peak) if achieved else None,
                      "peak_source": "live DMMA.8x8x4 probe (swb_fp64_peak_probe) in this run; MEASURED_PEAKS.json "
                                     "has no FP64 entry",

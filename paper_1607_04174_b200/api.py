@@ -189,6 +189,7 @@ def refresh(pack, image, new_beta: float, *, connectivity=None, weight_mode=None
     dp = _as_device(pack, image, connectivity, weight_mode)
     if dp.col_map is not None:
         raise InvalidParam("refresh a base pack, not a refreshed one (reference semantics)")
+    _mark("graph")
     graph = DeviceGraph.build(dp.image_dev, dp.lattice, new_beta)
     m = dp.m
     quad = torch.empty(m, dtype=torch.float64, device="cuda")
@@ -198,14 +199,17 @@ def refresh(pack, image, new_beta: float, *, connectivity=None, weight_mode=None
     lat = dp.lattice.c_struct()
     st = stream_handle()
     n = dp.n_vertices
+    _mark("stencil_rayleigh")
     _lib.call("swb_stencil_rayleigh", C.byref(lat), ptr(dp.V), dp.ldv, 0, 0, n, m, ptr(graph.what),
               ptr(graph.diag), ptr(graph.d_sqrt_dev), ptr(quad), ptr(norm2), ptr(vtd), ptr(ws), ws.numel(), st)
     lam = torch.empty(m, dtype=torch.float64, device="cuda")
     order = torch.empty(m, dtype=torch.int64, device="cuda")
+    _mark("coeffs")
     _lib.call("swb_update_coeffs", 0, None, 0, None, ptr(quad), ptr(norm2), m, 0.0, None, 0, ptr(lam),
               ptr(order), st)
     col_map = order.to(torch.int32)
     vtg = gather_vector(vtd, col_map) / graph.dnorm
+    _mark("update_end")
     out = RefreshedPack(dp.V, m, lam, graph.d_sqrt_dev, graph.dnorm, dp.dims, dp.spacing, float(new_beta),
                         dp.provenance, dp.lattice, image_dev=dp.image_dev, graph=graph, vtg=vtg,
                         col_map=col_map, mr=dp.mr)
