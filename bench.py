@@ -349,6 +349,32 @@ def fp64_probe(lib):
     return best
 
 
+def int8_probe(lib):
+    """Live INT8 tensor-core peak: back-to-back tcgen05.mma.kind::i8
+    (M 128, N 256, K 32) on every SM (swb_int8_peak_probe), best of 5 after
+    one warm-up, in TOP/s."""
+    import torch
+
+    from paper_1607_04174_b200 import _lib
+    from paper_1607_04174_b200.device import stream_handle
+    ops = _lib.C.c_double()
+    best = 0.0
+    for it in range(6):
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        _lib.check(lib.swb_int8_peak_probe(4000, _lib.C.byref(ops), stream_handle()))
+        e1.record()
+        torch.cuda.synchronize()
+        if it:
+            best = max(best, ops.value / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    return best
+
+
+# the rotation's digit scheme (csrc/ozaki.cu): 7 digits per operand, the 28
+# digit products with i + j <= 6, each an INT8 GEMM of the rotation's shape
+OZ_PAIRS = 28
+
+
 def run_sharded(args):
     """N > 1 ranks (torchrun): the c4 volume split into z-slabs, one per GPU
     (strong scaling).  Step = sharded first-order update (halo exchange +
@@ -393,6 +419,7 @@ def run_sharded(args):
         return labels, rc
 
     fp64_peak = fp64_probe(lib)
+    int8_peak = int8_probe(lib)
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
@@ -446,11 +473,19 @@ def run_sharded(args):
         rot_ms = phases.get("rotate")
         if rot_ms:
             rows = plan.own_end - plan.own_begin
-            ach = 2.0 * rows * m * m / (rot_ms * 1e-3) / 1e12
-            line["roofline"] = {"bound": "tensor", "kernel": "rotation V*C (DMMA NN GEMM), per GPU (rank 0 slab)",
-                                "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak,
-                                "peak_source": "live DMMA.8x8x4 probe (swb_fp64_peak_probe) in this run",
-                                "traffic": None, "algorithmic_bytes": 16.0 * rows * m}
+            if m <= 512 and not os.environ.get("SWB_ROTATION", "").startswith("d"):
+                ach = OZ_PAIRS * 2.0 * rows * m * m / (rot_ms * 1e-3) / 1e12
+                line["roofline"] = {"bound": "tensor", "kernel": "rotation V*C on INT8 tcgen05 (digit split + "
+                                    "GEMM), per GPU (rank 0 slab)", "achieved": ach, "peak": int8_peak,
+                                    "unit": "TOP/s (int8)", "frac": ach / int8_peak,
+                                    "peak_source": "live tcgen05 kind::i8 probe (swb_int8_peak_probe) in this run",
+                                    "traffic": None, "algorithmic_bytes": 16.0 * rows * m}
+            else:
+                ach = 2.0 * rows * m * m / (rot_ms * 1e-3) / 1e12
+                line["roofline"] = {"bound": "tensor", "kernel": "rotation V*C (DMMA NN GEMM), per GPU (rank 0 slab)",
+                                    "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak,
+                                    "peak_source": "live DMMA.8x8x4 probe (swb_fp64_peak_probe) in this run",
+                                    "traffic": None, "algorithmic_bytes": 16.0 * rows * m}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
 
@@ -485,6 +520,7 @@ def run_gpu(args):
         return
 
     fp64_peak = fp64_probe(lib)
+    int8_peak = int8_probe(lib)
 
     for i in range(args.warmup):
         gpu_step(state, i)
@@ -511,7 +547,8 @@ def run_gpu(args):
     launches = lib.swb_launch_count() - launches0
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
-    phases = {k: float(np.mean(v)) for k, v in api.TIMER.durations().items()}
+    # per-step totals (a phase may repeat within a step: the rotation's row chunks)
+    phases = {k: float(np.sum(v)) / args.steps for k, v in api.TIMER.durations().items()}
     api.TIMER = None
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -552,9 +589,11 @@ def run_gpu(args):
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (rotation GEMM, DMMA) ------------
+    # ---- roofline of the dominant kernel ------------------------------------
     rayleigh = args.method == "rayleigh"
-    rot_ms = phases.get("rotate")
+    rot_split_ms = phases.get("rotate_split")
+    rot_gemm_ms = phases.get("rotate_gemm")
+    rot_ms = sum(phases.get(k, 0.0) for k in ("rotate", "rotate_split", "rotate_gemm")) or None
     rot_flops = 2.0 * n * m * m
     achieved = rot_flops / (rot_ms * 1e-3) / 1e12 if rot_ms else None
     peaks = {}
@@ -567,12 +606,25 @@ def run_gpu(args):
     rc_ms = phases.get("solve_reconstruct")
     upd_ms = sum(v for k, v in phases.items() if not k.startswith("solve") and k not in ("priors", "displacement"))
     solve_ms = sum(v for k, v in phases.items() if k.startswith("solve") or k in ("priors", "displacement"))
+    oz_tops = OZ_PAIRS * rot_flops / (rot_gemm_ms * 1e-3) / 1e12 if rot_gemm_ms else None
+    kp = (m + 31) // 32 * 32
+    split_bytes = 8.0 * n * m + 7.0 * n * kp + 8.0 * n
     kernels = {
-        "rotation_dmma": {"ms": rot_ms, "tflops": achieved, "frac_fp64": achieved / fp64_peak if achieved else None},
+        "rotation": {"ms": rot_ms, "fp64_equiv_tflops": achieved,
+                     "note": "V*C: FP64 via INT8 tcgen05 digit products (split + GEMM); "
+                             "SWB_ROTATION=dmma runs the DMMA GEMM instead"},
+        "rotation_int8_gemm": {"ms": rot_gemm_ms, "int8_tops": oz_tops,
+                               "frac_int8": oz_tops / int8_peak if oz_tops else None},
+        "rotation_digit_split": {"ms": rot_split_ms,
+                                 "gbs": split_bytes / (rot_split_ms * 1e-3) / 1e9 if rot_split_ms else None},
         "projection_dmma": {"ms": proj_ms, "tflops": (n * m * (m + 1)) / (proj_ms * 1e-3) / 1e12 if proj_ms else None},
         "stencil_delta": {"ms": st_ms, "gbs": (16.0 * n * m + 72.0 * n) / (st_ms * 1e-3) / 1e9 if st_ms else None},
         "reconstruct_argmax": {"ms": rc_ms, "gbs": (8.0 * n * m + 20.0 * n) / (rc_ms * 1e-3) / 1e9 if rc_ms else None},
     }
+    if not rot_gemm_ms and rot_ms:   # DMMA rotation (m > 512 or SWB_ROTATION=dmma)
+        kernels["rotation"]["frac_fp64"] = achieved / fp64_peak
+    if rot_split_ms:
+        kernels["rotation_digit_split"]["frac_hbm"] = kernels["rotation_digit_split"]["gbs"] / hbm
     L = state["params"]["labels"]
     if L > 8 and rc_ms:   # many labels: V (coeff) on the DMMA GEMM, then the finalize / argmax pass
         kernels["reconstruct_argmax"] = {"ms": rc_ms, "tflops": 2.0 * n * m * L / (rc_ms * 1e-3) / 1e12,
@@ -585,11 +637,36 @@ def run_gpu(args):
             kernels[k]["frac_hbm"] = kernels[k]["gbs"] / hbm
     if rayleigh:   # the reference's refresh: one read-only stencil pass over V (HBM)
         sr_ms = phases.get("stencil_rayleigh")
-        kernels = {k: v for k, v in kernels.items() if k not in ("rotation_dmma", "projection_dmma", "stencil_delta")}
+        kernels = {k: v for k, v in kernels.items()
+                   if not k.startswith("rotation") and k not in ("projection_dmma", "stencil_delta")}
         kernels["stencil_rayleigh"] = {"ms": sr_ms, "gbs": (8.0 * n * m + 48.0 * n) / (sr_ms * 1e-3) / 1e9
                                        if sr_ms else None}
         if sr_ms:
             kernels["stencil_rayleigh"]["frac_hbm"] = kernels["stencil_rayleigh"]["gbs"] / hbm
+
+    # the dominant kernel by time: the INT8 rotation GEMM or the DMMA projection
+    if rot_gemm_ms and (not proj_ms or rot_gemm_ms >= proj_ms):
+        roofline = {"bound": "tensor", "kernel": "rotation V*C: INT8 tcgen05 digit-product GEMM (oz_gemm_kernel)",
+                    "achieved": oz_tops, "peak": int8_peak, "unit": "TOP/s (int8)",
+                    "frac": oz_tops / int8_peak if oz_tops else None,
+                    "peak_source": "live tcgen05.mma.kind::i8 M128xN256 probe (swb_int8_peak_probe) in this run",
+                    "algorithmic": f"{OZ_PAIRS} digit products x 2*N*K*K ops",
+                    "traffic": _ncu_traffic("rotation_int8_gemm", cfg, dims, m),
+                    "algorithmic_bytes": 16.0 * n * m}
+    else:
+        pj = kernels["projection_dmma"]["tflops"] if proj_ms else None
+        roofline = {"bound": "tensor", "kernel": "projection V^T(dL V) (DMMA TN GEMM, symmetric)",
+                    "achieved": pj, "peak": fp64_peak, "unit": "TFLOP/s",
+                    "frac": pj / fp64_peak if pj else None,
+                    "peak_source": "live DMMA.8x8x4 probe (swb_fp64_peak_probe) in this run; MEASURED_PEAKS.json "
+                                   "has no FP64 entry",
+                    "traffic": _ncu_traffic("projection_tn_sym", cfg, dims, m),
+                    "algorithmic_bytes": 16.0 * n * m}
+        if not rot_gemm_ms and rot_ms and (not proj_ms or rot_ms >= proj_ms):
+            roofline = {"bound": "tensor", "kernel": "rotation V*C (DMMA NN GEMM)", "achieved": achieved,
+                        "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak if achieved else None,
+                        "peak_source": "live DMMA.8x8x4 probe (swb_fp64_peak_probe) in this run",
+                        "traffic": _ncu_traffic("rotation_nn", cfg, dims, m), "algorithmic_bytes": 16.0 * n * m}
 
     cpu = None
     if not args.no_cpu:
@@ -618,14 +695,10 @@ def run_gpu(args):
                       "achieved": kernels["stencil_rayleigh"]["gbs"], "peak": hbm, "unit": "GB/s",
                       "frac": kernels["stencil_rayleigh"].get("frac_hbm"), "traffic": None,
                       "algorithmic_bytes": 8.0 * n * m + 48.0 * n} if rayleigh else None) or
-                    {"bound": "tensor", "kernel": "rotation V*C (DMMA NN GEMM)", "achieved": achieved,
-                     "peak": fp64_peak, "unit": "TFLOP/s", "frac": (achieved / fp64_peak) if achieved else None,
-                     "peak_source": "live DMMA.8x8x4 probe (swb_fp64_peak_probe) in this run; MEASURED_PEAKS.json "
-                                    "has no FP64 entry",
-                     "traffic": _ncu_traffic("rotation_nn", cfg, dims, m),
-                     "algorithmic_bytes": 16.0 * n * m},
+                    roofline,
         "kernels": kernels,
         "peaks": {"fp64_tflops": fp64_peak, "fp64_source": "of measured: live DMMA probe in this run",
+                  "int8_tops": int8_peak, "int8_source": "of measured: live tcgen05 kind::i8 probe in this run",
                   "hbm_gbs": hbm, "hbm_source": "of measured: MEASURED_PEAKS.json hbm_gbs" if mp.exists()
                   else "of fallback: B200_PROFILING.md"},
         "update": {"ms": upd_ms, "value": n * m / (upd_ms * 1e-3) if upd_ms else None, "unit": UNIT},

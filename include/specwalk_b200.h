@@ -126,6 +126,33 @@ int swb_gemm_nn_ex(const double* A, int64_t lda, const double* B, int64_t ldb, i
                    int64_t K, int64_t M2, double* out, int64_t ldo, int accumulate, double alpha,
                    void* stream);
 
+/* out[rows x M2] = A[rows x K] B[K x M2] in FP64 on the INT8 tcgen05 tensor
+ * cores (Ozaki split-integer scheme: 7 digits per operand, 28 digit products,
+ * row / column power-of-two scaling; error ~2^-53 K max|A[r,:]| max|B[:,c]|).
+ * K <= 512 (larger K: INVALID_PARAM; use swb_gemm_nn); the workspace holds the
+ * digit planes of a row chunk. */
+size_t swb_oz_gemm_nn_workspace_bytes(int64_t rows, int64_t K, int64_t M2);
+int swb_oz_gemm_nn(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows, int64_t K,
+                   int64_t M2, double* out, int64_t ldo, void* workspace, size_t workspace_bytes, void* stream);
+/* The same in parts (the host loop of swb_oz_gemm_nn, exposed so callers can
+ * time the digit split and the GEMM separately): B's planes once, then per
+ * row chunk of at most swb_oz_chunk_rows(rows, K, M2) rows the chunk's A
+ * planes and the GEMM.  `rows` (total) sizes the workspace layout. */
+int64_t swb_oz_chunk_rows(int64_t rows, int64_t K, int64_t M2);
+int swb_oz_split_cols(const double* B, int64_t ldb, int64_t rows, int64_t K, int64_t M2, void* workspace,
+                      size_t workspace_bytes, void* stream);
+int swb_oz_split_rows(const double* A_chunk, int64_t lda, int64_t chunk_rows, int64_t rows, int64_t K, int64_t M2,
+                      void* workspace, size_t workspace_bytes, void* stream);
+int swb_oz_gemm_planes(int64_t chunk_rows, int64_t rows, int64_t K, int64_t M2, double* out_chunk, int64_t ldo,
+                       void* workspace, size_t workspace_bytes, void* stream);
+/* measurement: back-to-back INT8 tcgen05 MMAs (M 128, N 256, K 32) on every
+ * SM; *ops_out = 2 x MACs issued (bench.py's live INT8 roofline) */
+int swb_int8_peak_probe(int iters, double* ops_out, void* stream);
+/* diagnostics: the seven int32 digit-product group sums of the first row
+ * chunk, raw[(g * rows_p + r) * np + c], rows_p / np padded to 128 / 64 */
+int swb_oz_gemm_nn_raw(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows, int64_t K,
+                       int64_t M2, int32_t* raw, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- eigen update coefficients (refresh.py:78-79 + first-order) ------ */
 /* method 0 (rayleigh, reference refresh): lam_new = sort(max(quad/norm2,0)),
  *   order = stable argsort; C untouched.

@@ -24,7 +24,7 @@ import weakref
 import numpy as np
 
 from . import _lib
-from .device import (WORKSPACE, DeviceGraph, DevicePack, LatticeSpec, gather_vector, ptr,
+from .device import (WORKSPACE, DeviceGraph, DevicePack, LatticeSpec, gather_vector, ptr, rotate_rows,
                      require_cuda, round_up, stream_handle, to_device, torch_mod)
 from .errors import (ImageMismatch, InsufficientBasis, InvalidParam, SingularSmallSystem)
 from .types import MAX_SEEDS, LabelMap, LaplacianMode, ProbabilityField, content_hash
@@ -310,7 +310,7 @@ def update_basis(pack, image, new_beta: float | None = None, cut_edges=None, met
         if ldv > m:
             Vn[:, m:].zero_()
         _mark("rotate")
-        _lib.call("swb_gemm_nn", ptr(dp.V), ldv, ptr(Cm), ldp, n, m, m, ptr(Vn), ldv, 0, st)
+        rotate_rows(dp.V, ldv, Cm, ldp, n, m, Vn, ldv, st, mark=_mark)
         _mark("update_tail")
         # V'^T d = C^T (V^T d): a 1-row NN product
         vtd_row = torch.zeros((1, ldp), dtype=torch.float64, device="cuda")

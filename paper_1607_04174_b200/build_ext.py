@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT = PKG / "libspecwalk_b200.so"
-SOURCES = ["abi.cu", "dgemm.cu", "graph_stencil.cu", "coeffs.cu", "lu.cu", "solve.cu", "select.cu", "pack_io.cu", "priors.cu", "precompute.cu", "aggregation.cu", "pipeline.cu"]
+SOURCES = ["abi.cu", "dgemm.cu", "graph_stencil.cu", "coeffs.cu", "lu.cu", "solve.cu", "select.cu", "pack_io.cu", "priors.cu", "precompute.cu", "aggregation.cu", "pipeline.cu", "ozaki.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

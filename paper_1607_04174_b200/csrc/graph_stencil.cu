@@ -153,6 +153,13 @@ __device__ __forceinline__ void cp_async8_s(uint32_t s, const void* gmem, bool p
 
 constexpr int ST_WARPS = 8;
 constexpr int ST_CTAS_PER_SM = 2;
+// rows per barrier step: two independent rows per step halve the barriers and
+// give each warp two dependency chains to interleave
+#ifndef SWB_ST_ROWS
+#define SWB_ST_ROWS 2
+#endif
+constexpr int ST_ROWS = SWB_ST_ROWS;
+static_assert(ST_ROWS == 1 || ST_ROWS == 2, "one or two rows per step");
 
 // Compile-time neighbour tables, sorted by flat offset (the reference CSR
 // column order): kind 0 = diagonal, 1 = forward edge `dir` of this voxel,
@@ -239,7 +246,7 @@ struct Ring5 {
   static constexpr int C_DBL = (NL * LCD + 1) / 2 * 2;
   static constexpr int STAGE_DBL = V_DBL + C_DBL;
   static constexpr int PREF = 5;
-  static constexpr int RING = PREF + 2;
+  static constexpr int RING = PREF + ST_ROWS + 1;   // rows x-1 .. x+PREF+ST_ROWS-1 live at once
   // slot of extended line (zi, yi), zi in [-1, ZB], yi in [-1, YB]; -1 = unused corner
   __host__ __device__ static constexpr int slot(int zi, int yi) {
     return !D3 ? (yi + 1)
@@ -369,6 +376,30 @@ __device__ __forceinline__ void row_dispatch(int warp, const double* sc, const d
       row_dispatch<CONN, DELTA, LO, MID>(warp, sc, sm1, sp1, lane, active, q, s2, sd, wrow, ap, zrow, win, first);
     else
       row_dispatch<CONN, DELTA, MID, HI>(warp, sc, sm1, sp1, lane, active, q, s2, sd, wrow, ap, zrow, win, first);
+  }
+}
+
+// two consecutive rows (x over stages s0 | s1 | s2, x+1 over s1 | s2 | s3) in
+// one straight-line leaf; the second row is inert (active2 false, zero
+// stages) past the end of an odd line
+template <int CONN, bool DELTA, int LO, int HI>
+__device__ __forceinline__ void row_dispatch2(int warp, const double* s0, const double* s1, const double* s2p,
+                                              const double* s3, int lane, bool active, bool active2, double2& q,
+                                              double2& s2, double2& sd, double* wrow, int64_t ldw,
+                                              const ApplyArgs& ap, const double* zrow, RowWin& win, bool first) {
+  if constexpr (HI - LO == 1) {
+    row_compute<CONN, DELTA, LO>(s1, s0, s2p, lane, active, q, s2, sd, wrow, ap, zrow, win, first);
+    row_compute<CONN, DELTA, LO>(s2p, s1, s3, lane, active2, q, s2, sd, wrow ? wrow + ldw : wrow, ap,
+                                 zrow ? zrow + ap.ldz : zrow,
+                                 win, false);
+  } else {
+    constexpr int MID = (LO + HI) / 2;
+    if (warp < MID)
+      row_dispatch2<CONN, DELTA, LO, MID>(warp, s0, s1, s2p, s3, lane, active, active2, q, s2, sd, wrow, ldw, ap,
+                                          zrow, win, first);
+    else
+      row_dispatch2<CONN, DELTA, MID, HI>(warp, s0, s1, s2p, s3, lane, active, active2, q, s2, sd, wrow, ldw, ap,
+                                          zrow, win, first);
   }
 }
 
@@ -518,6 +549,28 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
     const double* zrow = (!DELTA && ap.Z && line_live) ? ap.Z + (my_r0 - w_row0) * ap.ldz + col0 + 2 * lane : nullptr;
     const double* sc = ring;
     RowWin win;
+    if constexpr (ST_ROWS == 2) {
+      auto nxt = [&](const double* p) { return p + SD == ring + RING * SD ? ring : p + SD; };
+      const double* sm1 = zst;
+      for (int x = 0; x < nxi; x += 2) {
+        cp_async_wait<PREF - 3>();   // rows <= x+2 have landed (this thread's copies)
+        __syncthreads();             // ... every thread's; rows x-2, x-1 finished everywhere
+        prefetch();                  // rows x+PREF, x+PREF+1 -> stages of rows x-3, x-2
+        prefetch();
+        const double* sp = nxt(sc);
+        const double* sp2 = nxt(sp);
+        const double* s2s = x + 1 < nxi ? sp : zst;
+        const double* s3s = x + 2 < nxi ? sp2 : zst;
+        if (line_live) {
+          row_dispatch2<CONN, DELTA, 0, ST_WARPS>(warp, sm1, sc, s2s, s3s, lane, active, active && x + 1 < nxi, q, s2,
+                                                  sd, wrow, ldw, ap, zrow, win, x == 0);
+          if (wrow) wrow += 2 * ldw;
+          if (zrow) zrow += 2 * ap.ldz;
+        }
+        sm1 = sp;
+        sc = sp2;
+      }
+    } else
     for (int x = 0; x < nxi; ++x) {
       cp_async_wait<PREF - 2>();   // rows <= x+1 have landed (this thread's copies)
       __syncthreads();             // ... every thread's; compute(x-1) finished everywhere

@@ -1,0 +1,678 @@
+// FP64 GEMM on the INT8 tcgen05 tensor cores (Ozaki scheme, split-integer
+// form) for the rotation V' = V * C of the first-order update.
+//
+// sm_100a has no FP64 kind for tcgen05.mma; its FP64 tensor path is the
+// warp-level DMMA (dgemm.cu, ~37 TFLOP/s measured).  The INT8 kind runs at
+// 4.5 POPS dense, and an FP64 product can be assembled exactly from INT8
+// products:
+//
+//   row r of A is scaled by 2^-e_r (e_r = frexp exponent of max_k |A[r,k]|),
+//   so x = A[r,k] 2^-e_r is in (-1, 1); X = rint(x 2^54) (|X| <= 2^54) is
+//   split into S = 7 balanced base-256 digits
+//       X = d_0 2^48 + d_1 2^40 + ... + d_6 2^0,  d_1..d_6 in [-128, 127],
+//   d_0 in [-65, 65] (all signed int8); the columns of B the same way with
+//   exponents f_c.  Then
+//       sum_k A[r,k] B[k,c] ~= 2^(e_r + f_c - 12) sum_g acc_g 2^(-8 g),
+//       acc_g = sum_{i+j=g} sum_k d_i[r,k] d'_j[k,c]   (g = 0..6, 28 pairs)
+//   with every acc_g an exact int32 (|acc_g| <= 7 * 128^2 * K < 2^31 for
+//   K <= 512 here).  The dropped pairs (i + j > 6, zero-mean balanced digits)
+//   and the rounding of X bound the error by ~2^-53 * K * max|A[r,:]| *
+//   max|B[:,c]| in the worst case -- the FP64 GEMM error model with row /
+//   column maxima in place of element magnitudes -- and by ~2^-53 *
+//   sqrt(K) * ... for unbiased data.
+//
+// Layout: the slice kernels write the digits pre-tiled in the tcgen05
+// no-swizzle K-major core-matrix layout, one contiguous block per
+// (row block, K chunk) stage, so the GEMM's producer is two 1-D bulk copies
+// (cp.async.bulk + mbarrier transaction count) per stage.  The GEMM is a
+// persistent warp-specialised kernel: warp 0 copies, warp 1 allocates TMEM
+// and one lane issues the 28 MMAs per K chunk (M = 128, N = 64, K = 32) into
+// seven int32 TMEM accumulators (7 x 64 of the 512 columns), warps 2..5
+// drain TMEM, combine the groups in FP64 (Horner in 2^-8) and store.
+#include "swb_common.cuh"
+
+namespace {
+
+constexpr int OZ_S = 7;                 // digits per operand
+constexpr int OZ_G = 7;                 // product groups g = i + j <= 6
+constexpr int OZ_BM = 128;              // rows per tile (MMA M)
+constexpr int OZ_BN = 64;               // columns per tile (MMA N)
+constexpr int OZ_KC = 32;               // bytes (= int8 K) per stage / per MMA
+constexpr int OZ_STAGES = 4;
+constexpr int OZ_A_SLICE = OZ_BM * OZ_KC;            // 4096 B: [kq 2][row 128][16 B]
+constexpr int OZ_B_SLICE = OZ_BN * OZ_KC;            // 2048 B: [kq 2][col 64][16 B]
+constexpr int OZ_A_STAGE = OZ_S * OZ_A_SLICE;        // 28 KB
+constexpr int OZ_B_STAGE = OZ_S * OZ_B_SLICE;        // 14 KB
+constexpr int OZ_STAGE = OZ_A_STAGE + OZ_B_STAGE;
+constexpr int OZ_EPI_WARPS = 8;
+constexpr int OZ_EPI_COLS = OZ_BN / 2;              // columns per epilogue thread (two rounds of 16)
+constexpr int OZ_THREADS = (2 + OZ_EPI_WARPS) * 32;
+constexpr size_t OZ_SMEM = size_t(OZ_STAGES) * OZ_STAGE + 1024;
+constexpr int OZ_TMEM_COLS = 512;
+constexpr int OZ_MAX_K = 512;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "OZ_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra OZ_DONE;\n\t"
+      "bra OZ_WAIT;\n\t"
+      "OZ_DONE:\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// 32 lanes x 16 consecutive 32-bit columns -> 16 registers per thread
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// shared-memory matrix descriptor, no swizzle, K-major core matrices
+// (8 rows x 16 B): lbo = byte stride between the K-adjacent core matrices,
+// sbo = byte stride between 8-row groups
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFFu);
+  d |= uint64_t((lbo >> 4) & 0x3FFFu) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFFu) << 32;
+  d |= uint64_t(1) << 46;  // descriptor version (sm_100)
+  return d;
+}
+
+// instruction descriptor: kind::i8, s32 accumulate, K-major A and B, M x N
+__host__ __device__ constexpr uint32_t idesc_i8(int a_signed, int b_signed) {
+  return (2u << 4) | (uint32_t(a_signed) << 7) | (uint32_t(b_signed) << 10) | (uint32_t(OZ_BN >> 3) << 17) |
+         (uint32_t(OZ_BM >> 4) << 24);
+}
+
+__device__ __forceinline__ int oz_exponent(double amax) {
+  if (!(amax > 0.0)) return 0;
+  int e;
+  frexp(amax, &e);          // amax = m 2^e, m in [0.5, 1)
+  return e < -960 ? -960 : e;
+}
+
+// 16 consecutive values -> 7 balanced digit vectors of 16 bytes.
+// With Y = X + 0x808080808080, the balanced digits are the bytes of Y:
+// d_s = byte (6 - s) of Y minus 128 (= byte ^ 0x80) for s = 1..6, and
+// d_0 = byte 6 of Y (the signed top, |d_0| <= 65).  Byte gathers are PRMTs.
+__device__ __forceinline__ void oz_digits16(const double (&v)[16], double scale, uint4 (&out)[OZ_S]) {
+  uint32_t lo[16], hi[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+    const unsigned long long Y =
+        static_cast<unsigned long long>(__double2ll_rn(v[t] * scale)) + 0x808080808080ull;
+    lo[t] = static_cast<uint32_t>(Y);
+    hi[t] = static_cast<uint32_t>(Y >> 32);
+  }
+#pragma unroll
+  for (int s = 0; s < OZ_S; ++s) {
+    const int p = 6 - s;                     // byte of Y
+    const uint32_t sel = (p & 3) | (((p & 3) + 4) << 4);
+    const uint32_t flip = s == 0 ? 0u : 0x80808080u;
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t* src = p < 4 ? lo : hi;
+      const uint32_t a = __byte_perm(src[4 * q], src[4 * q + 1], sel);
+      const uint32_t b = __byte_perm(src[4 * q + 2], src[4 * q + 3], sel);
+      w[q] = __byte_perm(a, b, 0x5410) ^ flip;
+    }
+    out[s] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// A (rows x K, row-major, lda) -> row-scaled digits, tiled
+// [row block][K chunk][slice][kq 2][row 128][16 B]; sa[r] = 2^(e_r - 28)
+// (the 2^-12 of the digit scales and the 2^-16 of the epilogue's split sum).
+// A block takes 32 consecutive rows (K <= 512): each warp reads 4 rows
+// (lane = 16-element chunk, coalesced), reduces the row maximum, and writes
+// its digit vectors into a shared staging tile laid out like the global
+// planes; the block then writes every (chunk, slice) plane segment of its 32
+// rows as one contiguous 512-byte run.  Rows >= rows and k >= K are zero.
+constexpr int OZ_SLICE_WARPS = 8;
+constexpr int OZ_SLICE_ROWS = 32;
+constexpr int OZ_SLICE_MAXCH = 32;   // K <= 512
+constexpr size_t OZ_SLICE_SMEM = size_t(OZ_SLICE_MAXCH) * OZ_S * OZ_SLICE_ROWS * 16;
+__global__ void __launch_bounds__(OZ_SLICE_WARPS * 32) oz_slice_rows_kernel(const double* __restrict__ A,
+                                                                            int64_t lda, int64_t rows, int64_t K,
+                                                                            int64_t nkc, uint8_t* __restrict__ sl,
+                                                                            double* __restrict__ sa) {
+  extern __shared__ __align__(16) uint4 stg[];   // [chunk][slice][row 32] x 16 B
+  uint32_t* stg32 = reinterpret_cast<uint32_t*>(stg);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t row0 = int64_t(blockIdx.x) * OZ_SLICE_ROWS;
+  const int nch = static_cast<int>(nkc * 2);
+  const int nseg = (nch + 3) / 4;                // 64-element segments
+  constexpr int RPW = OZ_SLICE_ROWS / OZ_SLICE_WARPS;   // rows per warp
+  constexpr int NSEGMAX = OZ_SLICE_MAXCH / 4;
+  // coalesced: lane holds elements 64 g + 2 lane, +1 of every segment g;
+  // the next row's loads are issued before this row's digits
+  auto load_row = [&](int jj, double2 (&x)[NSEGMAX]) {
+    const int64_t r = row0 + warp * RPW + jj;
+    const bool live = r < rows;
+    const double* row = A + (live ? r : 0) * lda;
+    const bool vec = !(reinterpret_cast<uintptr_t>(row) & 15);
+#pragma unroll
+    for (int g = 0; g < NSEGMAX; ++g) {
+      const int64_t k = int64_t(g) * 64 + 2 * lane;
+      if (g < nseg && live && vec && k + 2 <= K) {
+        x[g] = *reinterpret_cast<const double2*>(row + k);
+      } else {
+        x[g].x = (g < nseg && live && k < K) ? row[k] : 0.0;
+        x[g].y = (g < nseg && live && k + 1 < K) ? row[k + 1] : 0.0;
+      }
+    }
+  };
+  double2 xn[NSEGMAX];
+  load_row(0, xn);
+  for (int j = 0; j < RPW; ++j) {
+    const int lr = warp * RPW + j;
+    const int64_t r = row0 + lr;
+    double2 x[NSEGMAX];
+#pragma unroll
+    for (int g = 0; g < NSEGMAX; ++g) x[g] = xn[g];
+    if (j + 1 < RPW) load_row(j + 1, xn);
+    double amax = 0.0;
+#pragma unroll
+    for (int g = 0; g < NSEGMAX; ++g) amax = fmax(amax, fmax(fabs(x[g].x), fabs(x[g].y)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    const int e = oz_exponent(amax);
+    if (lane == 0) sa[r] = ldexp(1.0, e - 28);
+    const double scale = ldexp(1.0, 54 - e);
+#pragma unroll
+    for (int g = 0; g < OZ_SLICE_MAXCH / 4; ++g) {
+      if (g >= nseg) break;
+      // Y = X + 0x808080808080: balanced digit s = byte (6 - s) of Y (^ 0x80 for s >= 1)
+      const unsigned long long Y0 = static_cast<unsigned long long>(__double2ll_rn(x[g].x * scale)) + 0x808080808080ull;
+      const unsigned long long Y1 = static_cast<unsigned long long>(__double2ll_rn(x[g].y * scale)) + 0x808080808080ull;
+      const uint32_t lo0 = uint32_t(Y0), hi0 = uint32_t(Y0 >> 32), lo1 = uint32_t(Y1), hi1 = uint32_t(Y1 >> 32);
+      const int ch = g * 4 + (lane >> 3);
+#pragma unroll
+      for (int s2 = 0; s2 < OZ_S; ++s2) {
+        const int p = 6 - s2;
+        const uint32_t sel = (p & 3) | (((p & 3) + 4) << 4);
+        uint32_t h = p < 4 ? __byte_perm(lo0, lo1, sel) : __byte_perm(hi0, hi1, sel);
+        h = (h & 0xFFFFu) ^ (s2 == 0 ? 0u : 0x8080u);
+        const uint32_t nb = __shfl_down_sync(0xffffffffu, h, 1);
+        if (!(lane & 1) && ch < nch)
+          stg32[((ch * OZ_S + s2) * OZ_SLICE_ROWS + lr) * 4 + ((lane & 7) >> 1)] = h | (nb << 16);
+      }
+    }
+  }
+  __syncthreads();
+  // plane segment (chunk ch, slice s2): rows row0..row0+31 -> 512 contiguous bytes
+  const int64_t rb = row0 / OZ_BM, rr0 = row0 % OZ_BM;
+  for (int seg = warp; seg < nch * OZ_S; seg += OZ_SLICE_WARPS) {
+    const int ch = seg / OZ_S, s2 = seg % OZ_S;
+    const int64_t kc = ch >> 1, kq = ch & 1;
+    uint4* dst = reinterpret_cast<uint4*>(sl + (rb * nkc + kc) * OZ_A_STAGE + s2 * OZ_A_SLICE + kq * (OZ_BM * 16) +
+                                          rr0 * 16);
+    dst[lane] = stg[seg * OZ_SLICE_ROWS + lane];
+  }
+}
+
+// B (K x M2, row-major, ldb) -> column-scaled digits, tiled
+// [col block][K chunk][slice][kq 2][col 64][16 B]; sb[c] = 2^f_c.
+__global__ void __launch_bounds__(OZ_BN) oz_slice_cols_kernel(const double* __restrict__ B, int64_t ldb,
+                                                              int64_t K, int64_t M2, int64_t nkc,
+                                                              uint8_t* __restrict__ sl, double* __restrict__ sb) {
+  const int64_t cb = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int64_t c = cb * OZ_BN + tid;
+  const bool live = c < M2;
+  double amax = 0.0;
+  if (live)
+    for (int64_t k = 0; k < K; ++k) amax = fmax(amax, fabs(B[k * ldb + c]));
+  const int f = oz_exponent(amax);
+  const double scale = ldexp(1.0, 54 - f);
+  sb[c] = ldexp(1.0, f);
+  const int64_t nch = nkc * 2;
+  for (int64_t ch = 0; ch < nch; ++ch) {
+    double v[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int64_t k = ch * 16 + t;
+      v[t] = (live && k < K) ? B[k * ldb + c] : 0.0;
+    }
+    uint4 d[OZ_S];
+    oz_digits16(v, scale, d);
+    const int64_t kc = ch >> 1, kq = ch & 1;
+    uint8_t* base = sl + (cb * nkc + kc) * OZ_B_STAGE + kq * (OZ_BN * 16) + tid * 16;
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s) *reinterpret_cast<uint4*>(base + s * OZ_B_SLICE) = d[s];
+  }
+}
+
+// out[rows x M2] = sum_g ... (see header).  raw != nullptr: write the seven
+// int32 group accumulators instead, raw[(g * rows_p + r) * np + c].
+//
+// TMEM columns [0, 7 BN): the seven group accumulators (the remaining 64
+// columns cannot hold a second set, so TMEM is single-buffered).  The
+// epilogue (8 warps, two per TMEM lane quarter, 32 columns each) pulls its
+// accumulators into registers in two rounds and releases TMEM right after
+// the last load, so the next tile's MMAs overlap the last round's combine
+// and stores.  Operands come from shared memory (SS): at N = 64 the MMA
+// rate is set by shared-memory bandwidth (6 KB of operands per 128x64x32
+// MMA), measured 48 cycles per MMA in isolation (tools/tc_probe.cu).
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, const uint8_t* __restrict__ bsl,
+               const double* __restrict__ sb, int64_t rows, int64_t M2, int64_t nkc, int64_t n_rb, int64_t n_cb,
+               double* __restrict__ out, int64_t ldo, int32_t* __restrict__ raw) {
+  extern __shared__ __align__(1024) uint8_t oz_smem[];
+  uint8_t* stages = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem) + 127) & ~uintptr_t(127));
+  __shared__ __align__(8) uint64_t full_bar[OZ_STAGES], empty_bar[OZ_STAGES], tfull_bar, tempty_bar;
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n_tiles = n_rb * n_cb;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < OZ_STAGES; ++s) {
+      mbar_init(smem_u32(&full_bar[s]), 1);
+      mbar_init(smem_u32(&empty_bar[s]), 1);
+    }
+    mbar_init(smem_u32(&tfull_bar), 1);
+    mbar_init(smem_u32(&tempty_bar), OZ_EPI_WARPS * 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
+                 "r"(OZ_TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- producer: two bulk copies per stage ----------------
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int64_t rb = t / n_cb, cb = t % n_cb;
+        for (int64_t kc = 0; kc < nkc; ++kc) {
+          mbar_wait(smem_u32(&empty_bar[s]), ph ^ 1);
+          const uint32_t fb = smem_u32(&full_bar[s]);
+          mbar_expect_tx(fb, OZ_STAGE);
+          const uint32_t dst = smem_u32(stages + size_t(s) * OZ_STAGE);
+          bulk_g2s(dst, asl + (rb * nkc + kc) * OZ_A_STAGE, OZ_A_STAGE, fb);
+          bulk_g2s(dst + OZ_A_STAGE, bsl + (cb * nkc + kc) * OZ_B_STAGE, OZ_B_STAGE, fb);
+          if (++s == OZ_STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    int s = 0;
+    uint32_t ph = 0, tph = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      mbar_wait(smem_u32(&tempty_bar), tph ^ 1);
+      tc_fence_after();
+      for (int64_t kc = 0; kc < nkc; ++kc) {
+        mbar_wait(smem_u32(&full_bar[s]), ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a0 = smem_u32(stages + size_t(s) * OZ_STAGE);
+          const uint32_t b0 = a0 + OZ_A_STAGE;
+#pragma unroll
+          for (int g = 0; g < OZ_G; ++g) {
+#pragma unroll
+            for (int i = 0; i <= g; ++i) {
+              const int j = g - i;
+              const uint64_t ad = smem_desc(a0 + i * OZ_A_SLICE, OZ_BM * 16, 128);
+              const uint64_t bd = smem_desc(b0 + j * OZ_B_SLICE, OZ_BN * 16, 128);
+              tc_mma_i8(tmem + uint32_t(g * OZ_BN), ad, bd, idesc_i8(1, 1), (kc > 0 || i > 0) ? 1u : 0u);
+            }
+          }
+          tc_commit(smem_u32(&empty_bar[s]));          // frees the stage when these finish
+          if (kc + 1 == nkc) tc_commit(smem_u32(&tfull_bar));
+        }
+        __syncwarp();
+        if (++s == OZ_STAGES) { s = 0; ph ^= 1; }
+      }
+      tph ^= 1;
+    }
+  } else {
+    // ---------------- epilogue: warps 2..9, two per TMEM lane quarter ----------------
+    const int ew = warp - 2;                        // 0..7
+    const int quarter = warp & 3;                   // TMEM lane quarter this warp may access
+    const int c0 = (ew >> 2) * OZ_EPI_COLS;         // 32-column half
+    const uint32_t tsrc = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(c0);
+    uint32_t tph = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const int64_t rb = t / n_cb, cb = t % n_cb;
+      const int64_t r = rb * OZ_BM + quarter * 32 + lane;
+      const int64_t gc0 = cb * OZ_BN + c0;
+      const double srow = r < rows ? sa[r] : 0.0;
+      mbar_wait(smem_u32(&tfull_bar), tph);
+      tc_fence_after();
+      tph ^= 1;
+      if (raw) {
+        const int64_t rows_p = n_rb * OZ_BM, np = n_cb * OZ_BN;
+        for (int h = 0; h < OZ_EPI_COLS; h += 16)
+          for (int g = 0; g < OZ_G; ++g) {
+            int32_t v[16];
+            tmem_ld16(tsrc + uint32_t(g * OZ_BN + h), v);
+            tmem_wait_ld();
+            for (int q = 0; q < 16; ++q) raw[(g * rows_p + r) * np + gc0 + h + q] = v[q];
+          }
+        tc_fence_before();
+        mbar_arrive(smem_u32(&tempty_bar));
+        continue;
+      }
+#pragma unroll 1
+      for (int h = 0; h < OZ_EPI_COLS; h += 16) {
+        // sum_g acc_g 2^-8g = 2^-16 (H + 2^-32 L), H and L exact in int64
+        long long H[16];
+        {
+          int32_t v[3][16];
+#pragma unroll
+          for (int g = 0; g < 3; ++g) tmem_ld16(tsrc + uint32_t(g * OZ_BN + h), v[g]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            H[q] = (static_cast<long long>(v[0][q]) << 16) + (static_cast<long long>(v[1][q]) << 8) +
+                   static_cast<long long>(v[2][q]);
+        }
+        int32_t v[4][16];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) tmem_ld16(tsrc + uint32_t((g + 3) * OZ_BN + h), v[g]);
+        tmem_wait_ld();
+        if (h + 16 == OZ_EPI_COLS) {               // all of this thread's TMEM is in registers
+          tc_fence_before();
+          mbar_arrive(smem_u32(&tempty_bar));      // the next tile's MMAs may start
+        }
+        if (r >= rows) continue;
+        double* orow = out + r * ldo + gc0 + h;
+        const bool full = gc0 + h + 16 <= M2;
+#pragma unroll
+        for (int q = 0; q < 16; q += 2) {
+          double o2[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const long long L = (static_cast<long long>(v[0][q + u]) << 24) +
+                                (static_cast<long long>(v[1][q + u]) << 16) +
+                                (static_cast<long long>(v[2][q + u]) << 8) + static_cast<long long>(v[3][q + u]);
+            const int64_t gc = gc0 + h + q + u;
+            const double sc = gc < M2 ? sb[gc] : 0.0;
+            o2[u] = fma(static_cast<double>(L), 0x1p-32, static_cast<double>(H[q + u])) * srow * sc;
+          }
+          if (full) {
+            *reinterpret_cast<double2*>(orow + q) = make_double2(o2[0], o2[1]);
+          } else {
+            if (gc0 + h + q < M2) orow[q] = o2[0];
+            if (gc0 + h + q + 1 < M2) orow[q + 1] = o2[1];
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(OZ_TMEM_COLS) : "memory");
+  }
+}
+
+struct OzLayout {
+  int64_t chunk_rows, nkc, n_cb;
+  size_t a_sl, sa, b_sl, sb, total;
+};
+
+OzLayout oz_layout(int64_t rows, int64_t K, int64_t M2) {
+  OzLayout o{};
+  o.nkc = (K + OZ_KC - 1) / OZ_KC;
+  o.n_cb = (M2 + OZ_BN - 1) / OZ_BN;
+  const int64_t rows_p = (rows + OZ_BM - 1) / OZ_BM * OZ_BM;
+  o.chunk_rows = rows_p < (int64_t(1) << 20) ? rows_p : (int64_t(1) << 20);
+  if (o.chunk_rows < OZ_BM) o.chunk_rows = OZ_BM;
+  const int64_t crb = o.chunk_rows / OZ_BM;
+  o.a_sl = swb_align_up(size_t(crb * o.nkc) * OZ_A_STAGE, 256);
+  o.sa = swb_align_up(sizeof(double) * size_t(o.chunk_rows), 256);
+  o.b_sl = swb_align_up(size_t(o.n_cb * o.nkc) * OZ_B_STAGE, 256);
+  o.sb = swb_align_up(sizeof(double) * size_t(o.n_cb * OZ_BN), 256);
+  o.total = o.a_sl + o.sa + o.b_sl + o.sb;
+  return o;
+}
+
+struct OzPtrs {
+  uint8_t* a_sl;
+  double* sa;
+  uint8_t* b_sl;
+  double* sb;
+};
+
+OzPtrs oz_ptrs(const OzLayout& o, void* ws) {
+  char* p = static_cast<char*>(ws);
+  return {reinterpret_cast<uint8_t*>(p), reinterpret_cast<double*>(p + o.a_sl),
+          reinterpret_cast<uint8_t*>(p + o.a_sl + o.sa), reinterpret_cast<double*>(p + o.a_sl + o.sa + o.b_sl)};
+}
+
+int oz_set_attrs() {
+  static bool attr = false;
+  if (!attr) {
+    SWB_CUDA_TRY(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(OZ_SMEM)));
+    SWB_CUDA_TRY(cudaFuncSetAttribute(oz_slice_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(OZ_SLICE_SMEM)));
+    attr = true;
+  }
+  return SWB_OK;
+}
+
+int oz_check(int64_t rows, int64_t K, int64_t M2, void* ws, size_t ws_bytes, OzLayout* o) {
+  if (rows < 0 || K <= 0 || M2 <= 0 || K > OZ_MAX_K || !ws) return SWB_INVALID_PARAM;
+  *o = oz_layout(rows > 0 ? rows : 1, K, M2);
+  if (ws_bytes < o->total) return SWB_WORKSPACE_TOO_SMALL;
+  return oz_set_attrs();
+}
+
+}  // namespace
+
+// Split B (K x M2) into its column-scaled digit planes (workspace B region).
+extern "C" int swb_oz_split_cols(const double* B, int64_t ldb, int64_t rows, int64_t K, int64_t M2, void* workspace,
+                                 size_t workspace_bytes, void* stream) {
+  OzLayout o;
+  int rc = oz_check(rows, K, M2, workspace, workspace_bytes, &o);
+  if (rc) return rc;
+  if (!B || ldb < M2) return SWB_INVALID_PARAM;
+  const OzPtrs q = oz_ptrs(o, workspace);
+  oz_slice_cols_kernel<<<static_cast<unsigned>(o.n_cb), OZ_BN, 0, swb_stream(stream)>>>(B, ldb, K, M2, o.nkc,
+                                                                                          q.b_sl, q.sb);
+  SWB_CHECK_LAUNCH();
+  return SWB_OK;
+}
+
+// Split nr <= swb_oz_chunk_rows() rows of A into their row-scaled digit
+// planes (workspace A region).
+extern "C" int swb_oz_split_rows(const double* A, int64_t lda, int64_t nr, int64_t rows, int64_t K, int64_t M2,
+                                 void* workspace, size_t workspace_bytes, void* stream) {
+  OzLayout o;
+  int rc = oz_check(rows, K, M2, workspace, workspace_bytes, &o);
+  if (rc) return rc;
+  if (!A || lda < K || nr < 0 || nr > o.chunk_rows) return SWB_INVALID_PARAM;
+  if (nr == 0) return SWB_OK;
+  const OzPtrs q = oz_ptrs(o, workspace);
+  const int64_t nrp = (nr + OZ_BM - 1) / OZ_BM * OZ_BM;
+  oz_slice_rows_kernel<<<static_cast<unsigned>(nrp / OZ_SLICE_ROWS), OZ_SLICE_WARPS * 32, OZ_SLICE_SMEM,
+                         swb_stream(stream)>>>(A, lda, nr, K, o.nkc, q.a_sl, q.sa);
+  SWB_CHECK_LAUNCH();
+  return SWB_OK;
+}
+
+// out[nr x M2] from the digit planes in the workspace (raw: diagnostics).
+int swb_oz_planes_gemm(int64_t nr, int64_t rows, int64_t K, int64_t M2, double* out, int64_t ldo, int32_t* raw,
+                       void* workspace, size_t workspace_bytes, cudaStream_t st) {
+  OzLayout o;
+  int rc = oz_check(rows, K, M2, workspace, workspace_bytes, &o);
+  if (rc) return rc;
+  if ((!out && !raw) || nr < 0 || nr > o.chunk_rows) return SWB_INVALID_PARAM;
+  if (out && (ldo < M2 || (ldo & 1) || (reinterpret_cast<uintptr_t>(out) & 15))) return SWB_INVALID_PARAM;
+  if (nr == 0) return SWB_OK;
+  const OzPtrs q = oz_ptrs(o, workspace);
+  const int64_t n_rb = (nr + OZ_BM - 1) / OZ_BM;
+  const int64_t tiles = n_rb * o.n_cb;
+  const int64_t grid_cap = swb_sm_count();
+  const int64_t grid = tiles < grid_cap ? tiles : grid_cap;
+  oz_gemm_kernel<<<static_cast<unsigned>(grid), OZ_THREADS, OZ_SMEM, st>>>(q.a_sl, q.sa, q.b_sl, q.sb, nr, M2, o.nkc,
+                                                                           n_rb, o.n_cb, out, ldo, raw);
+  SWB_CHECK_LAUNCH();
+  return SWB_OK;
+}
+
+extern "C" int swb_oz_gemm_planes(int64_t nr, int64_t rows, int64_t K, int64_t M2, double* out, int64_t ldo,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
+  return swb_oz_planes_gemm(nr, rows, K, M2, out, ldo, nullptr, workspace, workspace_bytes, swb_stream(stream));
+}
+
+extern "C" size_t swb_oz_gemm_nn_workspace_bytes(int64_t rows, int64_t K, int64_t M2) {
+  if (rows <= 0 || K <= 0 || M2 <= 0) return 0;
+  return oz_layout(rows, K, M2).total;
+}
+
+extern "C" int64_t swb_oz_chunk_rows(int64_t rows, int64_t K, int64_t M2) {
+  if (rows <= 0 || K <= 0 || M2 <= 0) return 0;
+  return oz_layout(rows, K, M2).chunk_rows;
+}
+
+// out[rows x M2] = A[rows x K] * B[K x M2] in FP64 via INT8 tensor cores:
+// B's planes once, then per row chunk: A's planes, GEMM.
+extern "C" int swb_oz_gemm_nn(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows, int64_t K,
+                              int64_t M2, double* out, int64_t ldo, void* workspace, size_t workspace_bytes,
+                              void* stream) {
+  if (rows == 0) return SWB_OK;
+  if (!A || !out) return SWB_INVALID_PARAM;
+  int rc;
+  if ((rc = swb_oz_split_cols(B, ldb, rows, K, M2, workspace, workspace_bytes, stream))) return rc;
+  const int64_t chunk = swb_oz_chunk_rows(rows, K, M2);
+  for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
+    const int64_t nr = rows - r0 < chunk ? rows - r0 : chunk;
+    if ((rc = swb_oz_split_rows(A + r0 * lda, lda, nr, rows, K, M2, workspace, workspace_bytes, stream))) return rc;
+    if ((rc = swb_oz_gemm_planes(nr, rows, K, M2, out + r0 * ldo, ldo, workspace, workspace_bytes, stream)))
+      return rc;
+  }
+  return SWB_OK;
+}
+
+// diagnostics: the seven int32 group accumulators of rows [0, min(rows,
+// chunk)) as raw[(g * rows_p + r) * np + c] (rows_p, np padded to 128 / 64)
+extern "C" int swb_oz_gemm_nn_raw(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows,
+                                  int64_t K, int64_t M2, int32_t* raw, void* workspace, size_t workspace_bytes,
+                                  void* stream) {
+  if (rows <= 0 || !raw) return SWB_INVALID_PARAM;
+  int rc;
+  if ((rc = swb_oz_split_cols(B, ldb, rows, K, M2, workspace, workspace_bytes, stream))) return rc;
+  const int64_t nr = rows < swb_oz_chunk_rows(rows, K, M2) ? rows : swb_oz_chunk_rows(rows, K, M2);
+  if ((rc = swb_oz_split_rows(A, lda, nr, rows, K, M2, workspace, workspace_bytes, stream))) return rc;
+  return swb_oz_planes_gemm(nr, rows, K, M2, nullptr, 0, raw, workspace, workspace_bytes, swb_stream(stream));
+}
+
+// ---------------------------------------------------------------------------
+// INT8 tensor-core peak probe (measurement only): back-to-back
+// tcgen05.mma.kind::i8 M = 128, N = 256, K = 32 from shared memory on every
+// SM (the shape that reaches the full rate); bench.py times it for the live
+// INT8 roofline.  ops_out = 2 * MACs issued.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void __launch_bounds__(128, 1) int8_probe_kernel(int iters) {
+  extern __shared__ __align__(1024) uint8_t pr_smem[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 48 * 1024 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(pr_smem)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t a0 = smem_u32(pr_smem), b0 = a0 + 16384;
+    constexpr uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(256 >> 3) << 17) | (8u << 24);
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        tc_mma_i8(tm, smem_desc(a0 + (k & 3) * 4096, OZ_BM * 16, 128), smem_desc(b0 + (k & 1) * 8192, 256 * 16, 128),
+                  idesc, 1u);
+    tc_commit(smem_u32(&bar));
+    mbar_wait(smem_u32(&bar), 0);
+  }
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tm) : "memory");
+}
+}  // namespace
+
+extern "C" int swb_int8_peak_probe(int iters, double* ops_out, void* stream) {
+  if (iters <= 0 || !ops_out) return SWB_INVALID_PARAM;
+  static bool attr = false;
+  if (!attr) {
+    SWB_CUDA_TRY(cudaFuncSetAttribute(int8_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024));
+    attr = true;
+  }
+  const int sms = swb_sm_count();
+  int8_probe_kernel<<<sms, 128, 48 * 1024, swb_stream(stream)>>>(iters);
+  SWB_CHECK_LAUNCH();
+  *ops_out = 2.0 * double(sms) * iters * 8 * 128.0 * 256.0 * 32.0;
+  return SWB_OK;
+}

@@ -12,6 +12,12 @@
 //                            images.py:128-130 (labels), with the reference's
 //                            SingularSmallSystem check (fastrw.py:340)
 #include "swb_common.cuh"
+#include <cstdlib>
+
+extern "C" size_t swb_oz_gemm_nn_workspace_bytes(int64_t rows, int64_t K, int64_t M2);
+extern "C" int swb_oz_gemm_nn(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows, int64_t K,
+                              int64_t M2, double* out, int64_t ldo, void* workspace, size_t workspace_bytes,
+                              void* stream);
 
 namespace {
 
@@ -53,8 +59,21 @@ struct UpdateLayout {
   void* tn_ws;
   size_t tn_bytes;
   void* ss_ws;
+  void* oz_ws;
+  size_t oz_bytes;
   size_t total;
 };
+
+// The rotation V' = V C runs on the INT8 tensor cores (ozaki.cu) when the
+// basis has at most 512 columns; SWB_ROTATION=dmma selects the FP64 DMMA
+// GEMM instead (measurement knob).
+bool rotation_on_int8(int64_t M) {
+  static const bool dmma = [] {
+    const char* e = getenv("SWB_ROTATION");
+    return e && e[0] == 'd';
+  }();
+  return !dmma && M <= 512;
+}
 
 UpdateLayout update_layout(const swb_lattice* lat, int64_t M, void* ws) {
   LatticeDev L{};
@@ -80,6 +99,8 @@ UpdateLayout update_layout(const swb_lattice* lat, int64_t M, void* ws) {
   u.tn_bytes = swb_gemm_tn_workspace_bytes(N, M, M);
   u.tn_ws = c.take<char>(u.tn_bytes);
   u.ss_ws = c.take<char>(256 * 8);
+  u.oz_bytes = rotation_on_int8(M) ? swb_oz_gemm_nn_workspace_bytes(N, M, M) : 0;
+  u.oz_ws = c.take<char>(u.oz_bytes);
   u.total = c.off + 256;
   return u;
 }
@@ -129,7 +150,11 @@ extern "C" int swb_update_first_order(const swb_lattice* lat, const double* imag
     vtg_kernel<<<static_cast<unsigned>((M + 255) / 256), 256, 0, st>>>(u.vtd, u.C, ldp, M, u.dsum, vtg_tmp, dnorm_out);
     SWB_CHECK_LAUNCH();
   }
-  if ((rc = swb_gemm_nn(V, ldv, u.C, ldp, N, M, M, V_out, ldv, 0, stream))) return rc;
+  if (u.oz_bytes) {
+    if ((rc = swb_oz_gemm_nn(V, ldv, u.C, ldp, N, M, M, V_out, ldv, u.oz_ws, u.oz_bytes, stream))) return rc;
+  } else {
+    if ((rc = swb_gemm_nn(V, ldv, u.C, ldp, N, M, M, V_out, ldv, 0, stream))) return rc;
+  }
   if (ldv > M) {
     zero_cols_kernel<<<swb_sm_count() * 4, 256, 0, st>>>(V_out, ldv, N, M);
     SWB_CHECK_LAUNCH();

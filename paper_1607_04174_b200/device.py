@@ -71,6 +71,37 @@ class Workspace:
 WORKSPACE = Workspace()
 
 
+def rotate_rows(V, ldv: int, Cm, ldc: int, rows: int, m: int, out, ldo: int, stream=None, mark=None) -> None:
+    """out[rows x m] = V[rows x m] Cm[m x m] (the first-order rotation,
+    reference update.py V' = V C): on the INT8 tensor cores (csrc/ozaki.cu,
+    FP64-accurate digit scheme) for m <= 512, else the FP64 DMMA GEMM.
+    ``mark(name)`` (the phase timer) brackets the digit split and the GEMM
+    of every row chunk.  SWB_ROTATION=dmma forces the DMMA GEMM
+    (measurement knob)."""
+    import os
+    from . import _lib
+    st = stream if stream is not None else stream_handle()
+    if rows <= 0:
+        return
+    if m > 512 or os.environ.get("SWB_ROTATION", "").startswith("d"):
+        _lib.call("swb_gemm_nn", ptr(V), ldv, ptr(Cm), ldc, rows, m, m, ptr(out), ldo, 0, st)
+        return
+    mark = mark or (lambda name: None)
+    nb = _lib.size("swb_oz_gemm_nn_workspace_bytes", rows, m, m)
+    ws = WORKSPACE.get("oz_gemm", nb)
+    chunk = _lib.size("swb_oz_chunk_rows", rows, m, m)
+    mark("rotate_split")
+    _lib.call("swb_oz_split_cols", ptr(Cm), ldc, rows, m, m, ptr(ws), ws.numel(), st)
+    for r0 in range(0, rows, chunk):
+        nr = min(chunk, rows - r0)
+        mark("rotate_split")
+        _lib.call("swb_oz_split_rows", C.c_void_p(V.data_ptr() + 8 * r0 * ldv), ldv, nr, rows, m, m, ptr(ws),
+                  ws.numel(), st)
+        mark("rotate_gemm")
+        _lib.call("swb_oz_gemm_planes", nr, rows, m, m, C.c_void_p(out.data_ptr() + 8 * r0 * ldo), ldo, ptr(ws),
+                  ws.numel(), st)
+
+
 # ---------------------------------------------------------------------------
 # lattice
 # ---------------------------------------------------------------------------

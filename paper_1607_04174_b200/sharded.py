@@ -30,7 +30,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .device import WORKSPACE, DeviceGraph, LatticeSpec, ptr, round_up, stream_handle
+from .device import WORKSPACE, DeviceGraph, LatticeSpec, ptr, rotate_rows, round_up, stream_handle
 
 
 # ---------------------------------------------------------------------------
@@ -241,8 +241,7 @@ class CudaBackend:
         return Cm, lam, order
 
     def rotate(self, V_own, Cm, m, out_own):
-        _lib.call("swb_gemm_nn", ptr(V_own), V_own.shape[1], ptr(Cm), Cm.shape[1], V_own.shape[0], m, m,
-                  ptr(out_own), out_own.shape[1], 0, stream_handle())
+        rotate_rows(V_own, V_own.shape[1], Cm, Cm.shape[1], V_own.shape[0], m, out_own, out_own.shape[1])
 
     def rotate_vector(self, vtd, Cm, m):
         t = self.torch
