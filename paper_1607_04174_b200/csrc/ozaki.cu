@@ -364,12 +364,15 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
         if (lane == 0) {
           const uint32_t a0 = smem_u32(stages + size_t(s) * OZ_STAGE);
           const uint32_t b0 = a0 + OZ_A_STAGE;
+          // A digit i outer, group g inner: consecutive MMAs accumulate into
+          // different TMEM groups (back-to-back MMAs into one accumulator
+          // serialise on it); group g's first MMA of a tile is (i = 0, j = g)
 #pragma unroll
-          for (int g = 0; g < OZ_G; ++g) {
+          for (int i = 0; i < OZ_S; ++i) {
+            const uint64_t ad = smem_desc(a0 + i * OZ_A_SLICE, OZ_BM * 16, 128);
 #pragma unroll
-            for (int i = 0; i <= g; ++i) {
+            for (int g = i; g < OZ_G; ++g) {
               const int j = g - i;
-              const uint64_t ad = smem_desc(a0 + i * OZ_A_SLICE, OZ_BM * 16, 128);
               const uint64_t bd = smem_desc(b0 + j * OZ_B_SLICE, OZ_BN * 16, 128);
               tc_mma_i8(tmem + uint32_t(g * OZ_BN), ad, bd, idesc_i8(1, 1), (kc > 0 || i > 0) ? 1u : 0u);
             }
@@ -410,8 +413,12 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
         mbar_arrive(smem_u32(&tempty_bar));
         continue;
       }
-#pragma unroll 1
-      for (int h = 0; h < OZ_EPI_COLS; h += 16) {
+      // both 16-column rounds are combined in registers before any store, so
+      // TMEM is released right after the second round's loads
+      double o[2][16];
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int h = hh * 16;
         // sum_g acc_g 2^-8g = 2^-16 (H + 2^-32 L), H and L exact in int64
         long long H[16];
         {
@@ -428,32 +435,29 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
 #pragma unroll
         for (int g = 0; g < 4; ++g) tmem_ld16(tsrc + uint32_t((g + 3) * OZ_BN + h), v[g]);
         tmem_wait_ld();
-        if (h + 16 == OZ_EPI_COLS) {               // all of this thread's TMEM is in registers
+        if (hh == 1) {                              // all of this thread's TMEM is in registers
           tc_fence_before();
-          mbar_arrive(smem_u32(&tempty_bar));      // the next tile's MMAs may start
+          mbar_arrive(smem_u32(&tempty_bar));       // the next tile's MMAs may start
         }
-        if (r >= rows) continue;
-        double* orow = out + r * ldo + gc0 + h;
-        const bool full = gc0 + h + 16 <= M2;
 #pragma unroll
-        for (int q = 0; q < 16; q += 2) {
-          double o2[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const long long L = (static_cast<long long>(v[0][q + u]) << 24) +
-                                (static_cast<long long>(v[1][q + u]) << 16) +
-                                (static_cast<long long>(v[2][q + u]) << 8) + static_cast<long long>(v[3][q + u]);
-            const int64_t gc = gc0 + h + q + u;
-            const double sc = gc < M2 ? sb[gc] : 0.0;
-            o2[u] = fma(static_cast<double>(L), 0x1p-32, static_cast<double>(H[q + u])) * srow * sc;
-          }
-          if (full) {
-            *reinterpret_cast<double2*>(orow + q) = make_double2(o2[0], o2[1]);
-          } else {
-            if (gc0 + h + q < M2) orow[q] = o2[0];
-            if (gc0 + h + q + 1 < M2) orow[q + 1] = o2[1];
-          }
+        for (int q = 0; q < 16; ++q) {
+          const long long L = (static_cast<long long>(v[0][q]) << 24) + (static_cast<long long>(v[1][q]) << 16) +
+                              (static_cast<long long>(v[2][q]) << 8) + static_cast<long long>(v[3][q]);
+          o[hh][q] = fma(static_cast<double>(L), 0x1p-32, static_cast<double>(H[q])) * srow;
         }
+      }
+      if (r >= rows) continue;
+      double* orow = out + r * ldo + gc0;
+      if (gc0 + OZ_EPI_COLS <= M2) {
+#pragma unroll
+        for (int q = 0; q < OZ_EPI_COLS; q += 2) {
+          const double2 sc = *reinterpret_cast<const double2*>(sb + gc0 + q);
+          *reinterpret_cast<double2*>(orow + q) = make_double2(o[q >> 4][q & 15] * sc.x, o[q >> 4][(q & 15) + 1] * sc.y);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < OZ_EPI_COLS; ++q)
+          if (gc0 + q < M2) orow[q] = o[q >> 4][q & 15] * sb[gc0 + q];
       }
     }
   }
