@@ -137,14 +137,17 @@ int swb_oz_gemm_nn(const double* A, int64_t lda, const double* B, int64_t ldb, i
 /* The same in parts (the host loop of swb_oz_gemm_nn, exposed so callers can
  * time the digit split and the GEMM separately): B's planes once, then per
  * row chunk of at most swb_oz_chunk_rows(rows, K, M2) rows the chunk's A
- * planes and the GEMM.  `rows` (total) sizes the workspace layout. */
+ * planes and the GEMM.  `rows` (total) sizes the workspace layout; when rows
+ * exceed one chunk the workspace holds two A-plane buffers (buf 0 / 1) so the
+ * split of chunk i+1 can run on another stream during the GEMM of chunk i
+ * (what swb_oz_gemm_nn does). */
 int64_t swb_oz_chunk_rows(int64_t rows, int64_t K, int64_t M2);
 int swb_oz_split_cols(const double* B, int64_t ldb, int64_t rows, int64_t K, int64_t M2, void* workspace,
                       size_t workspace_bytes, void* stream);
 int swb_oz_split_rows(const double* A_chunk, int64_t lda, int64_t chunk_rows, int64_t rows, int64_t K, int64_t M2,
-                      void* workspace, size_t workspace_bytes, void* stream);
-int swb_oz_gemm_planes(int64_t chunk_rows, int64_t rows, int64_t K, int64_t M2, double* out_chunk, int64_t ldo,
-                       void* workspace, size_t workspace_bytes, void* stream);
+                      int buf, void* workspace, size_t workspace_bytes, void* stream);
+int swb_oz_gemm_planes(int64_t chunk_rows, int64_t rows, int64_t K, int64_t M2, int buf, double* out_chunk,
+                       int64_t ldo, void* workspace, size_t workspace_bytes, void* stream);
 /* measurement: back-to-back INT8 tcgen05 MMAs (M 128, N 256, K 32) on every
  * SM; *ops_out = 2 x MACs issued (bench.py's live INT8 roofline) */
 int swb_int8_peak_probe(int iters, double* ops_out, void* stream);

@@ -182,7 +182,7 @@ __device__ __forceinline__ void oz_digits16(const double (&v)[16], double scale,
 #ifndef OZ_SLICE_WARPS_CFG
 #define OZ_SLICE_WARPS_CFG 4
 #define OZ_SLICE_ROWS_CFG 16
-#define OZ_SLICE_MINB 4
+#define OZ_SLICE_MINB 5   // <= 96 registers: one split block co-resides with a GEMM CTA
 #endif
 constexpr int OZ_SLICE_WARPS = OZ_SLICE_WARPS_CFG;
 constexpr int OZ_SLICE_ROWS = OZ_SLICE_ROWS_CFG;
@@ -480,7 +480,7 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
 }
 
 struct OzLayout {
-  int64_t chunk_rows, nkc, n_cb;
+  int64_t chunk_rows, nkc, n_cb, nbuf;
   size_t a_sl, sa, b_sl, sb, total;
 };
 
@@ -496,7 +496,8 @@ OzLayout oz_layout(int64_t rows, int64_t K, int64_t M2) {
   o.sa = swb_align_up(sizeof(double) * size_t(o.chunk_rows), 256);
   o.b_sl = swb_align_up(size_t(o.n_cb * o.nkc) * OZ_B_STAGE, 256);
   o.sb = swb_align_up(sizeof(double) * size_t(o.n_cb * OZ_BN), 256);
-  o.total = o.a_sl + o.sa + o.b_sl + o.sb;
+  o.nbuf = rows_p > o.chunk_rows ? 2 : 1;   // two chunks' A planes: split i+1 overlaps GEMM i
+  o.total = o.nbuf * (o.a_sl + o.sa) + o.b_sl + o.sb;
   return o;
 }
 
@@ -507,10 +508,12 @@ struct OzPtrs {
   double* sb;
 };
 
-OzPtrs oz_ptrs(const OzLayout& o, void* ws) {
+// layout: B planes | C scales | A planes / row scales of buffer 0 [| buffer 1]
+OzPtrs oz_ptrs(const OzLayout& o, void* ws, int buf) {
   char* p = static_cast<char*>(ws);
-  return {reinterpret_cast<uint8_t*>(p), reinterpret_cast<double*>(p + o.a_sl),
-          reinterpret_cast<uint8_t*>(p + o.a_sl + o.sa), reinterpret_cast<double*>(p + o.a_sl + o.sa + o.b_sl)};
+  char* a = p + o.b_sl + o.sb + size_t(buf) * (o.a_sl + o.sa);
+  return {reinterpret_cast<uint8_t*>(a), reinterpret_cast<double*>(a + o.a_sl), reinterpret_cast<uint8_t*>(p),
+          reinterpret_cast<double*>(p + o.b_sl)};
 }
 
 int oz_set_attrs() {
@@ -541,7 +544,7 @@ extern "C" int swb_oz_split_cols(const double* B, int64_t ldb, int64_t rows, int
   int rc = oz_check(rows, K, M2, workspace, workspace_bytes, &o);
   if (rc) return rc;
   if (!B || ldb < M2) return SWB_INVALID_PARAM;
-  const OzPtrs q = oz_ptrs(o, workspace);
+  const OzPtrs q = oz_ptrs(o, workspace, 0);
   oz_slice_cols_kernel<<<static_cast<unsigned>(o.n_cb), OZ_BN, 0, swb_stream(stream)>>>(B, ldb, K, M2, o.nkc,
                                                                                           q.b_sl, q.sb);
   SWB_CHECK_LAUNCH();
@@ -549,15 +552,15 @@ extern "C" int swb_oz_split_cols(const double* B, int64_t ldb, int64_t rows, int
 }
 
 // Split nr <= swb_oz_chunk_rows() rows of A into their row-scaled digit
-// planes (workspace A region).
+// planes (workspace A buffer `buf`, 0 or 1; 1 exists when rows > one chunk).
 extern "C" int swb_oz_split_rows(const double* A, int64_t lda, int64_t nr, int64_t rows, int64_t K, int64_t M2,
-                                 void* workspace, size_t workspace_bytes, void* stream) {
+                                 int buf, void* workspace, size_t workspace_bytes, void* stream) {
   OzLayout o;
   int rc = oz_check(rows, K, M2, workspace, workspace_bytes, &o);
   if (rc) return rc;
-  if (!A || lda < K || nr < 0 || nr > o.chunk_rows) return SWB_INVALID_PARAM;
+  if (!A || lda < K || nr < 0 || nr > o.chunk_rows || buf < 0 || buf >= o.nbuf) return SWB_INVALID_PARAM;
   if (nr == 0) return SWB_OK;
-  const OzPtrs q = oz_ptrs(o, workspace);
+  const OzPtrs q = oz_ptrs(o, workspace, buf);
   const int64_t nrp = (nr + OZ_BM - 1) / OZ_BM * OZ_BM;
   oz_slice_rows_kernel<<<static_cast<unsigned>(nrp / OZ_SLICE_ROWS), OZ_SLICE_WARPS * 32, OZ_SLICE_SMEM,
                          swb_stream(stream)>>>(A, lda, nr, K, o.nkc, q.a_sl, q.sa);
@@ -566,15 +569,15 @@ extern "C" int swb_oz_split_rows(const double* A, int64_t lda, int64_t nr, int64
 }
 
 // out[nr x M2] from the digit planes in the workspace (raw: diagnostics).
-int swb_oz_planes_gemm(int64_t nr, int64_t rows, int64_t K, int64_t M2, double* out, int64_t ldo, int32_t* raw,
-                       void* workspace, size_t workspace_bytes, cudaStream_t st) {
+int swb_oz_planes_gemm(int64_t nr, int64_t rows, int64_t K, int64_t M2, int buf, double* out, int64_t ldo,
+                       int32_t* raw, void* workspace, size_t workspace_bytes, cudaStream_t st) {
   OzLayout o;
   int rc = oz_check(rows, K, M2, workspace, workspace_bytes, &o);
   if (rc) return rc;
-  if ((!out && !raw) || nr < 0 || nr > o.chunk_rows) return SWB_INVALID_PARAM;
+  if ((!out && !raw) || nr < 0 || nr > o.chunk_rows || buf < 0 || buf >= o.nbuf) return SWB_INVALID_PARAM;
   if (out && (ldo < M2 || (ldo & 1) || (reinterpret_cast<uintptr_t>(out) & 15))) return SWB_INVALID_PARAM;
   if (nr == 0) return SWB_OK;
-  const OzPtrs q = oz_ptrs(o, workspace);
+  const OzPtrs q = oz_ptrs(o, workspace, buf);
   const int64_t n_rb = (nr + OZ_BM - 1) / OZ_BM;
   const int64_t tiles = n_rb * o.n_cb;
   const int64_t grid_cap = swb_sm_count();
@@ -585,9 +588,10 @@ int swb_oz_planes_gemm(int64_t nr, int64_t rows, int64_t K, int64_t M2, double* 
   return SWB_OK;
 }
 
-extern "C" int swb_oz_gemm_planes(int64_t nr, int64_t rows, int64_t K, int64_t M2, double* out, int64_t ldo,
-                                  void* workspace, size_t workspace_bytes, void* stream) {
-  return swb_oz_planes_gemm(nr, rows, K, M2, out, ldo, nullptr, workspace, workspace_bytes, swb_stream(stream));
+extern "C" int swb_oz_gemm_planes(int64_t nr, int64_t rows, int64_t K, int64_t M2, int buf, double* out,
+                                  int64_t ldo, void* workspace, size_t workspace_bytes, void* stream) {
+  return swb_oz_planes_gemm(nr, rows, K, M2, buf, out, ldo, nullptr, workspace, workspace_bytes,
+                            swb_stream(stream));
 }
 
 extern "C" size_t swb_oz_gemm_nn_workspace_bytes(int64_t rows, int64_t K, int64_t M2) {
@@ -601,7 +605,11 @@ extern "C" int64_t swb_oz_chunk_rows(int64_t rows, int64_t K, int64_t M2) {
 }
 
 // out[rows x M2] = A[rows x K] * B[K x M2] in FP64 via INT8 tensor cores:
-// B's planes once, then per row chunk: A's planes, GEMM.
+// B's planes once, then per row chunk the chunk's A planes and the GEMM.
+// The split of chunk i+1 runs on a side stream into the other A buffer while
+// the GEMM of chunk i runs (one split block fits beside a GEMM CTA on every
+// SM: 96 + 160 registers x threads, 47 + 173 KB shared memory), so only the
+// first chunk's split is exposed.
 extern "C" int swb_oz_gemm_nn(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows, int64_t K,
                               int64_t M2, double* out, int64_t ldo, void* workspace, size_t workspace_bytes,
                               void* stream) {
@@ -610,11 +618,41 @@ extern "C" int swb_oz_gemm_nn(const double* A, int64_t lda, const double* B, int
   int rc;
   if ((rc = swb_oz_split_cols(B, ldb, rows, K, M2, workspace, workspace_bytes, stream))) return rc;
   const int64_t chunk = swb_oz_chunk_rows(rows, K, M2);
-  for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
-    const int64_t nr = rows - r0 < chunk ? rows - r0 : chunk;
-    if ((rc = swb_oz_split_rows(A + r0 * lda, lda, nr, rows, K, M2, workspace, workspace_bytes, stream))) return rc;
-    if ((rc = swb_oz_gemm_planes(nr, rows, K, M2, out + r0 * ldo, ldo, workspace, workspace_bytes, stream)))
+  const int64_t nch = (rows + chunk - 1) / chunk;
+  if (nch == 1) {
+    if ((rc = swb_oz_split_rows(A, lda, rows, rows, K, M2, 0, workspace, workspace_bytes, stream))) return rc;
+    return swb_oz_gemm_planes(rows, rows, K, M2, 0, out, ldo, workspace, workspace_bytes, stream);
+  }
+  static cudaStream_t aux = nullptr;
+  static cudaEvent_t ev_in, ev_split[2], ev_gemm[2];
+  if (!aux) {
+    SWB_CUDA_TRY(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+    SWB_CUDA_TRY(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+    for (int b = 0; b < 2; ++b) {
+      SWB_CUDA_TRY(cudaEventCreateWithFlags(&ev_split[b], cudaEventDisableTiming));
+      SWB_CUDA_TRY(cudaEventCreateWithFlags(&ev_gemm[b], cudaEventDisableTiming));
+    }
+  }
+  cudaStream_t st = swb_stream(stream);
+  SWB_CUDA_TRY(cudaEventRecord(ev_in, st));            // A, B's planes ready
+  SWB_CUDA_TRY(cudaStreamWaitEvent(aux, ev_in, 0));
+  auto split = [&](int64_t i) -> int {
+    const int64_t r0 = i * chunk, nr = rows - r0 < chunk ? rows - r0 : chunk;
+    if (i >= 2) SWB_CUDA_TRY(cudaStreamWaitEvent(aux, ev_gemm[i & 1], 0));   // buffer free
+    int e = swb_oz_split_rows(A + r0 * lda, lda, nr, rows, K, M2, int(i & 1), workspace, workspace_bytes, aux);
+    if (e) return e;
+    SWB_CUDA_TRY(cudaEventRecord(ev_split[i & 1], aux));
+    return SWB_OK;
+  };
+  if ((rc = split(0))) return rc;
+  for (int64_t i = 0; i < nch; ++i) {
+    if (i + 1 < nch && (rc = split(i + 1))) return rc;
+    const int64_t r0 = i * chunk, nr = rows - r0 < chunk ? rows - r0 : chunk;
+    SWB_CUDA_TRY(cudaStreamWaitEvent(st, ev_split[i & 1], 0));
+    if ((rc = swb_oz_gemm_planes(nr, rows, K, M2, int(i & 1), out + r0 * ldo, ldo, workspace, workspace_bytes,
+                                 stream)))
       return rc;
+    SWB_CUDA_TRY(cudaEventRecord(ev_gemm[i & 1], st));
   }
   return SWB_OK;
 }
@@ -628,8 +666,8 @@ extern "C" int swb_oz_gemm_nn_raw(const double* A, int64_t lda, const double* B,
   int rc;
   if ((rc = swb_oz_split_cols(B, ldb, rows, K, M2, workspace, workspace_bytes, stream))) return rc;
   const int64_t nr = rows < swb_oz_chunk_rows(rows, K, M2) ? rows : swb_oz_chunk_rows(rows, K, M2);
-  if ((rc = swb_oz_split_rows(A, lda, nr, rows, K, M2, workspace, workspace_bytes, stream))) return rc;
-  return swb_oz_planes_gemm(nr, rows, K, M2, nullptr, 0, raw, workspace, workspace_bytes, swb_stream(stream));
+  if ((rc = swb_oz_split_rows(A, lda, nr, rows, K, M2, 0, workspace, workspace_bytes, stream))) return rc;
+  return swb_oz_planes_gemm(nr, rows, K, M2, 0, nullptr, 0, raw, workspace, workspace_bytes, swb_stream(stream));
 }
 
 // ---------------------------------------------------------------------------

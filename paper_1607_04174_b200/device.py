@@ -87,19 +87,53 @@ def rotate_rows(V, ldv: int, Cm, ldc: int, rows: int, m: int, out, ldo: int, str
         _lib.call("swb_gemm_nn", ptr(V), ldv, ptr(Cm), ldc, rows, m, m, ptr(out), ldo, 0, st)
         return
     mark = mark or (lambda name: None)
+    torch = torch_mod()
     nb = _lib.size("swb_oz_gemm_nn_workspace_bytes", rows, m, m)
     ws = WORKSPACE.get("oz_gemm", nb)
     chunk = _lib.size("swb_oz_chunk_rows", rows, m, m)
+    nch = (rows + chunk - 1) // chunk
     mark("rotate_split")
     _lib.call("swb_oz_split_cols", ptr(Cm), ldc, rows, m, m, ptr(ws), ws.numel(), st)
-    for r0 in range(0, rows, chunk):
-        nr = min(chunk, rows - r0)
-        mark("rotate_split")
-        _lib.call("swb_oz_split_rows", C.c_void_p(V.data_ptr() + 8 * r0 * ldv), ldv, nr, rows, m, m, ptr(ws),
-                  ws.numel(), st)
+    main = torch.cuda.current_stream()
+    aux = _aux_stream() if nch > 1 else main
+    ev_split = [torch.cuda.Event(), torch.cuda.Event()]
+    ev_gemm = [torch.cuda.Event(), torch.cuda.Event()]
+    if nch > 1:
+        aux.wait_stream(main)                     # V and C's planes ready
+
+    def split(i):
+        # chunk i's A planes into buffer i % 2 on the side stream; the split
+        # of chunk i+1 runs beside the GEMM of chunk i (csrc/ozaki.cu)
+        r0 = i * chunk
+        if i >= 2:
+            aux.wait_event(ev_gemm[i & 1])        # the buffer's previous GEMM is done
+        _lib.call("swb_oz_split_rows", C.c_void_p(V.data_ptr() + 8 * r0 * ldv), ldv, min(chunk, rows - r0), rows,
+                  m, m, i & 1, ptr(ws), ws.numel(), C.c_void_p(aux.cuda_stream))
+        ev_split[i & 1].record(aux)
+
+    split(0)
+    for i in range(nch):
+        if i + 1 < nch:
+            split(i + 1)
+        r0 = i * chunk
+        main.wait_event(ev_split[i & 1])
         mark("rotate_gemm")
-        _lib.call("swb_oz_gemm_planes", nr, rows, m, m, C.c_void_p(out.data_ptr() + 8 * r0 * ldo), ldo, ptr(ws),
-                  ws.numel(), st)
+        _lib.call("swb_oz_gemm_planes", min(chunk, rows - r0), rows, m, m, i & 1,
+                  C.c_void_p(out.data_ptr() + 8 * r0 * ldo), ldo, ptr(ws), ws.numel(), st)
+        ev_gemm[i & 1].record(main)
+        mark("rotate_join")
+
+
+_AUX = {}
+
+
+def _aux_stream():
+    """The side stream of the rotation's digit split (one per device)."""
+    torch = torch_mod()
+    dev = torch.cuda.current_device()
+    if dev not in _AUX:
+        _AUX[dev] = torch.cuda.Stream(device=dev)
+    return _AUX[dev]
 
 
 # ---------------------------------------------------------------------------
