@@ -349,10 +349,11 @@ def fp64_probe(lib):
     return best
 
 
-def int8_probe(lib):
+def int8_probe(lib, fn="swb_int8_peak_probe", iters=4000):
     """Live INT8 tensor-core peak: back-to-back tcgen05.mma.kind::i8
     (M 128, N 256, K 32) on every SM (swb_int8_peak_probe), best of 5 after
-    one warm-up, in TOP/s."""
+    one warm-up, in TOP/s.  fn="swb_int8_scheme_probe": the rotation GEMM's
+    own MMA pattern (N 64 into seven accumulators) -- the scheme's ceiling."""
     import torch
 
     from paper_1607_04174_b200 import _lib
@@ -362,7 +363,7 @@ def int8_probe(lib):
     for it in range(6):
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         e0.record()
-        _lib.check(lib.swb_int8_peak_probe(4000, _lib.C.byref(ops), stream_handle()))
+        _lib.check(getattr(lib, fn)(iters, _lib.C.byref(ops), stream_handle()))
         e1.record()
         torch.cuda.synchronize()
         if it:
@@ -521,6 +522,7 @@ def run_gpu(args):
 
     fp64_peak = fp64_probe(lib)
     int8_peak = int8_probe(lib)
+    scheme_peak = int8_probe(lib, "swb_int8_scheme_probe", 600)
 
     for i in range(args.warmup):
         gpu_step(state, i)
@@ -652,7 +654,14 @@ def run_gpu(args):
                     "peak_source": "live tcgen05.mma.kind::i8 M128xN256 probe (swb_int8_peak_probe) in this run",
                     "algorithmic": f"{OZ_PAIRS} digit products x 2*N*K*K ops",
                     "traffic": _ncu_traffic("rotation_int8_gemm", cfg, dims, m),
-                    "algorithmic_bytes": 16.0 * n * m}
+                    "algorithmic_bytes": 16.0 * n * m,
+                    # the scheme's own ceiling: its seven resident int32 group
+                    # accumulators (7 x 64 of 512 TMEM columns) cap the MMA at
+                    # N = 64, measured alone by swb_int8_scheme_probe
+                    "scheme_peak": scheme_peak,
+                    "frac_of_scheme_peak": oz_tops / scheme_peak if oz_tops and scheme_peak else None,
+                    "scheme_peak_source": "live probe of the GEMM's MMA pattern alone (M128 N64 K32 SS, 28 MMAs "
+                                          "into 7 TMEM accumulators; swb_int8_scheme_probe) in this run"}
     else:
         pj = kernels["projection_dmma"]["tflops"] if proj_ms else None
         roofline = {"bound": "tensor", "kernel": "projection V^T(dL V) (DMMA TN GEMM, symmetric)",

@@ -151,6 +151,10 @@ int swb_oz_gemm_planes(int64_t chunk_rows, int64_t rows, int64_t K, int64_t M2, 
 /* measurement: back-to-back INT8 tcgen05 MMAs (M 128, N 256, K 32) on every
  * SM; *ops_out = 2 x MACs issued (bench.py's live INT8 roofline) */
 int swb_int8_peak_probe(int iters, double* ops_out, void* stream);
+/* measurement: the rotation GEMM's MMA pattern alone (M 128, N 64, K 32, SS,
+ * 28 MMAs per K chunk into seven TMEM accumulators) on every SM -- the
+ * ceiling of the digit-product scheme; *ops_out = 2 x MACs issued */
+int swb_int8_scheme_probe(int iters, double* ops_out, void* stream);
 /* diagnostics: the seven int32 digit-product group sums of the first row
  * chunk, raw[(g * rows_p + r) * np + c], rows_p / np padded to 128 / 64 */
 int swb_oz_gemm_nn_raw(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows, int64_t K,

@@ -716,6 +716,65 @@ __global__ void __launch_bounds__(128, 1) int8_probe_kernel(int iters) {
 }
 }  // namespace
 
+// The rotation GEMM's own MMA pattern in isolation: M 128, N 64, K 32 from
+// shared memory into seven rotating TMEM accumulators (7 x 64 columns), i.e.
+// the ceiling of the 28-digit-product scheme, whose seven resident group
+// accumulators cap N at 64 (bench.py reports the GEMM against it too).
+namespace {
+__global__ void __launch_bounds__(128, 1) int8_probe_n64_kernel(int iters) {
+  extern __shared__ __align__(1024) uint8_t pr_smem[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 48 * 1024 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(pr_smem)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t a0 = smem_u32(pr_smem), b0 = a0 + 28672;
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+      for (int i = 0; i < OZ_S; ++i)
+#pragma unroll
+        for (int g = i; g < OZ_G; ++g)
+          tc_mma_i8(tm + uint32_t(g * OZ_BN), smem_desc(a0 + i * OZ_A_SLICE, OZ_BM * 16, 128),
+                    smem_desc(b0 + (g - i) * OZ_B_SLICE, OZ_BN * 16, 128), idesc_i8(1, 1), 1u);
+    tc_commit(smem_u32(&bar));
+    mbar_wait(smem_u32(&bar), 0);
+  }
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
+}
+}  // namespace
+
+extern "C" int swb_int8_scheme_probe(int iters, double* ops_out, void* stream) {
+  if (iters <= 0 || !ops_out) return SWB_INVALID_PARAM;
+  static bool attr = false;
+  if (!attr) {
+    SWB_CUDA_TRY(cudaFuncSetAttribute(int8_probe_n64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024));
+    attr = true;
+  }
+  const int sms = swb_sm_count();
+  int8_probe_n64_kernel<<<sms, 128, 48 * 1024, swb_stream(stream)>>>(iters);
+  SWB_CHECK_LAUNCH();
+  *ops_out = 2.0 * double(sms) * iters * (OZ_S * (OZ_S + 1) / 2) * double(OZ_BM) * OZ_BN * OZ_KC;
+  return SWB_OK;
+}
+
 extern "C" int swb_int8_peak_probe(int iters, double* ops_out, void* stream) {
   if (iters <= 0 || !ops_out) return SWB_INVALID_PARAM;
   static bool attr = false;

@@ -160,3 +160,11 @@ def test_int8_probe_runs(cuda_ok):
     _lib.check(_lib.load().swb_int8_peak_probe(10, C.byref(ops), None))
     torch.cuda.synchronize()
     assert ops.value > 0
+
+
+def test_int8_scheme_probe_runs(cuda_ok):
+    import ctypes as C
+    ops = C.c_double()
+    _lib.check(_lib.load().swb_int8_scheme_probe(10, C.byref(ops), None))
+    torch.cuda.synchronize()
+    assert ops.value == 2.0 * torch.cuda.get_device_properties(0).multi_processor_count * 10 * 28 * 128 * 64 * 32
