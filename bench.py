@@ -69,8 +69,9 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, interval_ms: int = int(os.environ.get("SWB_SMI_MS", "200"))):
         self.index = index
+        self.interval_ms = interval_ms
         self.proc = None
         self.lines = []
 
@@ -78,7 +79,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", str(self.interval_ms)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except OSError:
             self.proc = None
@@ -86,6 +87,14 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+
+    def wait_first(self, timeout: float = 5.0):
+        """Block until nvidia-smi has produced its first sample, so its
+        start-up (NVML init, driver queries) happens before the timed region
+        rather than inside its first step."""
+        t0 = time.time()
+        while self.proc is not None and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.05)
 
     def stop(self) -> dict:
         if self.proc is None:
@@ -425,9 +434,9 @@ def run_sharded(args):
         step(i)
     torch.cuda.synchronize()
     from paper_1607_04174_b200 import api
-    api.TIMER = api.PhaseTimer()
     clocks = ClockSampler(local)
     clocks.start()
+    clocks.wait_first()
     l0 = lib.swb_launch_count()
     dist.barrier()
     torch.cuda.synchronize()
@@ -440,6 +449,11 @@ def run_sharded(args):
     torch.cuda.synchronize()
     launches = lib.swb_launch_count() - l0
     clk = clocks.stop()
+    # phase breakdown from a second, untimed pass with events at the phase boundaries
+    api.TIMER = api.PhaseTimer()
+    for i in range(args.steps):
+        labels, rc = step(args.warmup + i)
+    torch.cuda.synchronize()
     phases = {k: float(np.mean(v)) for k, v in api.TIMER.durations().items()}
     api.TIMER = None
     ms_t = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device="cuda")
@@ -533,9 +547,11 @@ def run_gpu(args):
             dist.barrier()
 
     # ---- device-resident timed region -------------------------------------
-    api.TIMER = api.PhaseTimer()
+    # (no phase events inside it: the per-phase breakdown comes from a second,
+    # untimed pass of the same K steps below)
     clocks = ClockSampler(local)
     clocks.start()
+    clocks.wait_first()
     launches0 = lib.swb_launch_count()
     barrier()
     torch.cuda.synchronize()
@@ -549,7 +565,13 @@ def run_gpu(args):
     launches = lib.swb_launch_count() - launches0
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
-    # per-step totals (a phase may repeat within a step: the rotation's row chunks)
+    # phase breakdown: the same steps again with CUDA events at every phase
+    # boundary; per-step totals (a phase may repeat within a step: the
+    # rotation's row chunks)
+    api.TIMER = api.PhaseTimer()
+    for i in range(args.steps):
+        gpu_step(state, args.warmup + i)
+    torch.cuda.synchronize()
     phases = {k: float(np.sum(v)) / args.steps for k, v in api.TIMER.durations().items()}
     api.TIMER = None
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
