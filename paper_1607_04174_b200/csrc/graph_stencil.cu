@@ -518,22 +518,28 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
 #pragma unroll
     for (int i = 0; i < VPT; ++i) vdst_s[i] = ring_s + 8u * uint32_t(vdst[i]);
     const uint32_t cdst_s = ring_s + 8u * uint32_t(cdst);
-    const int64_t vstep = ldv;
     uint32_t pst_off = 0;  // byte offset of the stage being filled
     int xp = 0;
+    // per-chunk row steps (0 for masked chunks), fixed for the item
+    int64_t vinc[VPT];
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) vinc[i] = vok[i] ? ldv : 0;
+    const int64_t cinc = cok ? cstride : 0;
+    const bool last_chunk = threadIdx.x + (VPT - 1) * ST_WARPS * 32 < VCH;
+    const bool has_coef = threadIdx.x < CSL;
     auto prefetch = [&]() {
       if (xp < nxi) {
 #pragma unroll
         for (int i = 0; i < VPT; ++i) {
-          if (i + 1 < VPT || threadIdx.x + i * ST_WARPS * 32 < VCH) {
+          if (i + 1 < VPT || last_chunk) {
             cp_async16_s(vdst_s[i] + pst_off, vsrc[i], vok[i]);
-            vsrc[i] += vok[i] ? vstep : 0;  // next row (pointer increments only)
+            vsrc[i] += vinc[i];  // next row (pointer increments only)
           }
         }
-        if (threadIdx.x < CSL) {
+        if (has_coef) {
           if (cbytes == 16) cp_async16_s(cdst_s + pst_off, csrc, cok);
           else cp_async8_s(cdst_s + pst_off, csrc, cok);
-          csrc += cok ? cstride : 0;
+          csrc += cinc;
         }
         ++xp;
         pst_off = pst_off + STAGE_BYTES == RING * STAGE_BYTES ? 0u : pst_off + STAGE_BYTES;

@@ -40,6 +40,45 @@ def report(path: str) -> str:
     return "\n".join(out) + "\n"
 
 
+DETAIL_SECTIONS = ("GPU Speed Of Light Throughput", "Memory Workload Analysis", "Compute Workload Analysis",
+                   "Scheduler Statistics", "Warp State Statistics", "Occupancy")
+DETAIL_KEYS = ("Duration", "SM Frequency", "Memory Throughput", "DRAM Throughput", "L1/TEX Cache Throughput",
+               "L2 Cache Throughput", "Compute (SM) Throughput", "Executed Ipc Active", "Issue Slots Busy",
+               "L2 Hit Rate", "Eligible Warps Per Scheduler", "Warp Cycles Per Issued Instruction",
+               "Achieved Occupancy", "Registers Per Thread")
+
+
+def detail(path: str) -> str:
+    """Speed-of-light / scheduler lines and the warp-stall breakdown
+    (pc sampling) of a --set full report."""
+    raw = subprocess.run(["ncu", "-i", path, "--page", "details", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr = rows[0]
+    out = [f"## {path} (--set full)", "", "| kernel | section | metric | value |", "|---|---|---|---|"]
+    for r in rows[1:]:
+        d = dict(zip(hdr, r))
+        if d.get("Section Name") in DETAIL_SECTIONS and d.get("Metric Name") in DETAIL_KEYS:
+            out.append(f"| {short(d['Kernel Name'])} | {d['Section Name']} | {d['Metric Name']} | "
+                       f"{d['Metric Value']} {d.get('Metric Unit', '')} |")
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr = rows[0]
+    pre = "smsp__pcsamp_warps_issue_stalled_"
+    for r in rows[2:]:
+        st = []
+        for i, h in enumerate(hdr):
+            if h.startswith(pre) and not h.endswith("_not_issued"):
+                try:
+                    st.append((float(r[i].replace(",", "")), h[len(pre):]))
+                except ValueError:
+                    pass
+        tot = sum(v for v, _ in st) or 1.0
+        out += ["", f"warp-stall samples, {short(r[hdr.index('Kernel Name')])}:", "",
+                "| reason | share |", "|---|---|"]
+        out += [f"| {k} | {100 * v / tot:.1f}% |" for v, k in sorted(st, reverse=True)[:10]]
+    return "\n".join(out) + "\n"
+
+
 def launches(path: str, skip_prefix_kernels: int = 0) -> str:
     text = open(path).read()
     start = text.find('"ID"')
@@ -67,6 +106,10 @@ if __name__ == "__main__":
     out = sys.argv[1]
     parts = []
     for a in sys.argv[2:]:
-        parts.append(launches(a) if a.endswith(".csv") else report(a))
+        if a.endswith(".csv"):
+            parts.append(launches(a))
+        else:
+            parts.append(report(a))
+            parts.append(detail(a))
     open(out, "w").write("\n".join(parts))
     print(open(out).read())
