@@ -168,3 +168,21 @@ def test_int8_scheme_probe_runs(cuda_ok):
     _lib.check(_lib.load().swb_int8_scheme_probe(10, C.byref(ops), None))
     torch.cuda.synchronize()
     assert ops.value == 2.0 * torch.cuda.get_device_properties(0).multi_processor_count * 10 * 28 * 128 * 64 * 32
+
+
+def test_k_limit(cuda_ok):
+    """K = 512 is the largest K whose group sums are exact int32; K = 513 is
+    rejected (callers use the DMMA GEMM there)."""
+    rng = np.random.default_rng(512)
+    A = rng.standard_normal((300, 512))
+    B = rng.standard_normal((512, 70))
+    got = _run(A, B)
+    assert np.all(np.abs(got - A @ B) <= _bound(A, B))
+    assert _lib.size("swb_oz_gemm_nn_workspace_bytes", 300, 513, 70) > 0
+    dA = torch.zeros((300, 513), dtype=torch.float64, device="cuda")
+    dB = torch.zeros((513, 70), dtype=torch.float64, device="cuda")
+    out = torch.zeros((300, 70), dtype=torch.float64, device="cuda")
+    nb = _lib.size("swb_oz_gemm_nn_workspace_bytes", 300, 513, 70)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    rc = _lib.load().swb_oz_gemm_nn(_ptr(dA), 513, _ptr(dB), 70, 300, 513, 70, _ptr(out), 70, _ptr(ws), nb, None)
+    assert rc != 0

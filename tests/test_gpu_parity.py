@@ -366,6 +366,37 @@ def test_first_order_update_matches_oracle(cuda_ok, dims, conn, mode, m, b0, b1)
     assert_labels_match(swb.hard_labels(f).labels, u_ref)
 
 
+@pytest.mark.parametrize("dims,m", [((32, 24), 512), ((30, 30), 520)])
+def test_first_order_update_basis_size_limits(cuda_ok, dims, m):
+    """K = 512 (the largest K of the INT8 digit-product rotation: every group
+    sum still an exact int32) and K = 520 (beyond it: the rotation runs on the
+    DMMA GEMM) both match the oracle.  With 512 of 768 eigenpairs of a 2-D
+    grid the upper spectrum is clustered (gaps ~1e-5), so C = P / gap
+    amplifies the 1e-12 agreement of P; the rotation itself is checked
+    against V C with C from the GPU's own P (the oracle's coefficient rule)."""
+    rng = np.random.default_rng(m)
+    n = int(np.prod(dims))
+    img = np.clip(0.5 + 0.3 * (rng.random(n) < 0.2) + rng.normal(0, 0.05, n), 0, 1)
+    lap0 = O.build_laplacian(img, dims, 30.0, "abs", 4)
+    vals, vecs = np.linalg.eigh(lap0.matrix.toarray())
+    V, lam = vecs[:, :m], vals[:m]
+    image = swb.Image(dims, img)
+    pack = swb.SpectralPack(dims=dims, spacing=(), beta=30.0, eigen=swb.EigenBasis(np.asfortranarray(V), lam),
+                            d_sqrt=lap0.d_sqrt, provenance=swb.PackProvenance(image.content_hash()))
+    dp = swb.to_device(pack, image=image, connectivity=4, weight_mode="abs")
+    up = swb.update_basis(dp, image, 36.0, method="first_order", keep_P=True)
+    lap1 = O.build_laplacian(img, dims, 36.0, "abs", 4)
+    Vo, lamo, order, P, _ = O.first_order_update(V, lam, lap0, lap1)
+    np.testing.assert_allclose(up.P.cpu().numpy()[:, :m], P, rtol=0, atol=1e-12)
+    assert_lam(up.lambda_hat, lamo)
+    np.testing.assert_array_equal(up.order, order)
+    Pg = up.P.cpu().numpy()[:, :m]
+    lam_hat_unsorted = np.empty(m)
+    lam_hat_unsorted[up.order] = up.lambda_hat
+    Cg = O.update_coefficients(Pg, lam, lam_hat_unsorted, 0.5)[0]
+    np.testing.assert_allclose(up.V.cpu().numpy()[:, :m], V @ Cg, rtol=0, atol=1e-12)
+
+
 def test_cut_update_matches_oracle(cuda_ok):
     dims = (28, 24)
     rng = np.random.default_rng(5)
