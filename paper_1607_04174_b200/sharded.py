@@ -297,10 +297,20 @@ class CudaBackend:
         ws = WORKSPACE.get("small_solve", _lib.size("swb_small_solve_workspace_bytes", s, m, k))
         ldq = q_s.shape[1] if s else round_up(m, 2)
         ldt = t_p.shape[1] if t_p is not None else round_up(k, 2)
-        _lib.call("swb_small_solve", float(gamma), s, m, k, ptr(q_s), ptr(b_qn), ldq, ptr(bg), ptr(lsu), ptr(dsq),
+        # as api.solve_fast: the condition estimate runs on the side stream,
+        # overlapping the reconstruction; join_side() joins it
+        from .api import _side_stream
+        side, ev = _side_stream()
+        t.cuda.current_stream().wait_stream(side)   # a previous shard's estimate still reads the workspace
+        ev.record()
+        _lib.call("swb_small_solve_ex", float(gamma), s, m, k, ptr(q_s), ptr(b_qn), ldq, ptr(bg), ptr(lsu), ptr(dsq),
                   float(dnorm), ptr(slab), ptr(values), ptr(vtg), ptr(t_p), ldt, ptr(coeff), ptr(extra), ptr(rcond),
-                  ptr(ws), ws.numel(), stream_handle())
+                  ptr(ws), ws.numel(), stream_handle(), C.c_void_p(side.cuda_stream), C.c_void_p(ev.cuda_event))
         return coeff, extra, rcond
+
+    def join_side(self):
+        from .api import _side_stream
+        self.torch.cuda.current_stream().wait_stream(_side_stream()[0])
 
     def reconstruct(self, V, plan, m, coeff, extra, dnorm, d_sqrt, k, sidx, slab, s, want_u=False):
         t = self.torch
@@ -495,6 +505,8 @@ def sharded_solve(shards: list, comm, backend, seed_idx, seed_lab, k: int, gamma
         labels, top2, U = backend.reconstruct(sh.V, sh.plan, m, coeff, extra, sh.graph.dnorm, sh.graph.d_sqrt_dev,
                                               k, sidx, slab, s, want_u)
         out.append((labels, top2, U, rcond))
+    if hasattr(backend, "join_side"):
+        backend.join_side()
     _mark("solve_end")
     return out
 
