@@ -403,6 +403,12 @@ def run_sharded(args):
     rank = int(os.environ["RANK"])
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    # stdout carries only rank 0's JSON line: NCCL writes its banner / logs
+    # to file descriptor 1, so fd 1 points at stderr from here on and the
+    # line goes to a duplicate of the original stdout
+    json_out = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = args.config
     dims = tuple(int(x) for x in args.dims.split(",")) if args.dims else None
@@ -501,7 +507,7 @@ def run_sharded(args):
                                     "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak,
                                     "peak_source": "live DMMA.8x8x4 probe (swb_fp64_peak_probe) in this run",
                                     "traffic": None, "algorithmic_bytes": 16.0 * rows * m}
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=json_out, flush=True)
     dist.destroy_process_group()
 
 
