@@ -153,15 +153,20 @@ def cpu_sample(cfg: str, dims, m: int, planes: int = CPU_SLAB_PLANES):
         G = np.linalg.solve(R.T, G.T).T
     lam = W.synthetic_lambda(cfg, m)
     seeds, labs = W.sample_region_seeds(truth, w.params["labels"], w.params["seeds_per_label"], rng)
+    cut = W.cut_for(w) if not d3 else None
     return dict(dims=sdims, img=img, V=np.asfortranarray(G), lam=lam, seeds=seeds, labs=labs, n=n,
-                params=w.params, moving=moving)
+                params=w.params, moving=moving, cut=cut[1:] if cut is not None else None)
 
 
 def cpu_step(s, beta0, beta1, labels):
     from oracle import rw_oracle as O
     p = s["params"]
     lap0 = O.build_laplacian(s["img"], s["dims"], beta0, p["weight_mode"], p["connectivity"])
-    lap1 = O.build_laplacian(s["img"], s["dims"], beta1, p["weight_mode"], p["connectivity"])
+    cut = None
+    if s.get("cut") is not None:   # c2: the block-boundary edge cut (the GPU arm's topology update)
+        x0, y0 = s["cut"]
+        cut = O.block_cut_mask(s["dims"], x0, y0, size=p["cut_block"], connectivity=p["connectivity"])
+    lap1 = O.build_laplacian(s["img"], s["dims"], beta1, p["weight_mode"], p["connectivity"], cut_edges=cut)
     V1, lam1, _, _, _ = O.first_order_update(s["V"], s["lam"], lap0, lap1)
     if s["moving"] is not None:  # c5: registration data term + gamma > 0 solve + expected displacement
         vec = O.grid_vectors(p["grid"])
@@ -252,12 +257,17 @@ def setup_gpu(cfg, dims, m, rank):
                     m=m, params=p, seeds_n=0)
     seeds, labs = W.seeds_for(w)
     prob = swb.LabelProblem(num_labels=p["labels"], seeds=swb.SeedPartition(n, seeds, labs))
-    return dict(w=w, image=image, pack=pack, prob=prob, n=n, m=m, params=p, seeds_n=len(seeds))
+    cut = W.cut_for(w)
+    return dict(w=w, image=image, pack=pack, prob=prob, n=n, m=m, params=p, seeds_n=len(seeds),
+                cut=torch.from_numpy(cut[0]).cuda() if cut is not None else None)
 
 
-def _next_pack(state, beta):
+def _next_pack(state, beta, i=0):
     """Chained update in ping-pong mode: V' goes into the previous step's
-    (retired) basis buffer, so no 54 GB allocation happens per step."""
+    (retired) basis buffer, so no 54 GB allocation happens per step.  A
+    cut-edge config (c2) removes the block-boundary edges on even steps and
+    restores them on odd steps (beta unchanged), so every step is a real
+    topology update of the previous pack."""
     import paper_1607_04174_b200 as swb
     if state.get("method") == "rayleigh":
         # the reference's refresh: new eigenvalues + column order on the
@@ -268,7 +278,8 @@ def _next_pack(state, beta):
         return pack
     spare = state.pop("spare", None)
     old = state["pack"]
-    pack = swb.update_basis(old, state["image"], beta, method="first_order", out=spare)
+    cut = state.get("cut") if i % 2 == 0 else None
+    pack = swb.update_basis(old, state["image"], beta, cut_edges=cut, method="first_order", out=spare)
     state["spare"] = old.V
     state["pack"] = pack
     return pack
@@ -292,7 +303,7 @@ def gpu_step(state, i):
     import paper_1607_04174_b200 as swb
     p = state["params"]
     beta = p["beta1"] if i % 2 == 0 else p["beta0"]
-    pack = _next_pack(state, beta)
+    pack = _next_pack(state, beta, i)
     if state["prob"] is None:
         return registration_solve(state, pack, state["image"], state["moving"])
     field = swb.solve_fast(pack, pack.laplacian, state["prob"])
@@ -310,7 +321,7 @@ def e2e_step(state, i, host_labels):
         # step), host label map + displacement field out
         fixed = swb.Image(state["w"].dims, state["w"].intensities)
         moving = swb.Image(state["w"].dims, p["moving"])
-        pack = _next_pack(state, beta)
+        pack = _next_pack(state, beta, i)
         field = registration_solve(state, pack, fixed, moving)
         host_labels.copy_(field.labels_dev, non_blocking=True)
         state["host_disp"].copy_(field.displacement_dev, non_blocking=True)
@@ -318,7 +329,7 @@ def e2e_step(state, i, host_labels):
     seeds = state["prob"].seeds
     prob = swb.LabelProblem(num_labels=p["labels"],
                             seeds=swb.SeedPartition(state["n"], seeds.seed_indices.copy(), seeds.seed_labels.copy()))
-    pack = _next_pack(state, beta)
+    pack = _next_pack(state, beta, i)
     field = swb.solve_fast(pack, pack.laplacian, prob)
     host_labels.copy_(field.labels_dev, non_blocking=True)
     return field
@@ -719,8 +730,11 @@ def run_gpu(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{cfg}: {'x'.join(map(str, dims_full))} volume, K={m}, "
-                               f"{'refresh (reference, eigenvalue-only)' if rayleigh else 'first-order'} beta update "
-                               f"{state['params']['beta0']}<->{state['params']['beta1']} + " + (
+                               f"{'refresh (reference, eigenvalue-only)' if rayleigh else 'first-order'} " + (
+                                   f"topology update (cut <-> restore the edges crossing a "
+                                   f"{state['params']['cut_block']}x{state['params']['cut_block']} block boundary, "
+                                   f"beta {state['params']['beta0']}) + " if state.get("cut") is not None else
+                                   f"beta update {state['params']['beta0']}<->{state['params']['beta1']} + ") + (
                                    f"{state['params']['labels']}-label RW solve, S={s}" if cfg != "c5" else
                                    f"similarity priors (grid {state['params']['grid']}, patch radius "
                                    f"{state['params']['patch_radius']}) + {state['params']['labels']}-label "

@@ -187,6 +187,36 @@ def sample_region_seeds(labels: np.ndarray, num_labels: int, per_region: int, rn
     return idx[order], lab[order]
 
 
+def block_cut_voxel_mask(dims, connectivity: int, x0: int, y0: int, size: int = 32) -> np.ndarray:
+    """c2's topology change as the API's voxel mask (N x ndir, uint8): the
+    forward edge (v, v + d) is cut when exactly one endpoint lies inside the
+    block [x0, x0+size) x [y0, y0+size) (2-D; voxels x-fastest, the
+    direction order of LatticeSpec.forward_offsets)."""
+    nx, ny = dims
+    x, y = np.meshgrid(np.arange(nx), np.arange(ny), indexing="ij")
+    x, y = x.ravel(order="F"), y.ravel(order="F")
+    inside = lambda a, b: (a >= x0) & (a < x0 + size) & (b >= y0) & (b < y0 + size)  # noqa: E731
+    offs = [(1, 0), (0, 1)] if connectivity == 4 else [(1, 0), (0, 1), (1, 1), (-1, 1)]
+    out = np.zeros((nx * ny, len(offs)), dtype=np.uint8)
+    for d, (dx, dy) in enumerate(offs):
+        xn, yn = x + dx, y + dy
+        ok = (xn >= 0) & (xn < nx) & (yn >= 0) & (yn < ny)
+        out[:, d] = ok & (inside(x, y) != inside(xn, yn))
+    return out
+
+
+def cut_for(w: Workload):
+    """(mask, x0, y0): the seeded block position of a cut-edge config (c2),
+    or None."""
+    size = w.params.get("cut_block")
+    if not size:
+        return None
+    rng = np.random.default_rng([CFG_INDEX[w.name], 7])
+    nx, ny = w.dims
+    x0, y0 = int(rng.integers(0, nx - size)), int(rng.integers(0, ny - size))
+    return block_cut_voxel_mask(w.dims, w.params["connectivity"], x0, y0, size), x0, y0
+
+
 def seeds_for(w: Workload, round_index: int = 0):
     rng = np.random.default_rng([CFG_INDEX[w.name], 1, round_index])
     return sample_region_seeds(w.truth, w.params["labels"], w.params["seeds_per_label"], rng)

@@ -73,3 +73,18 @@ def test_workspace_queries():
     assert lib.swb_gemm_tn_workspace_bytes(16_777_216, 400, 400) > 0
     assert lib.swb_small_solve_workspace_bytes(800, 400, 4) > 801 * 801 * 8
     assert lib.swb_lu_workspace_bytes(801) >= 801 * 8
+
+
+def test_c2_cut_mask_matches_oracle_block_cut():
+    """The bench's c2 topology change (workloads.block_cut_voxel_mask) is the
+    oracle's block cut (edges with exactly one endpoint inside the block)."""
+    import numpy as np
+    from oracle import rw_oracle as O
+    from paper_1607_04174_b200 import workloads as W
+    from paper_1607_04174_b200.device import LatticeSpec
+    for conn in (4, 8):
+        dims = (23, 19)
+        lat = LatticeSpec.make(dims, conn, "sq")
+        want = lat.edge_mask_to_voxel_mask(O.block_cut_mask(dims, 5, 3, size=8, connectivity=conn))
+        got = W.block_cut_voxel_mask(dims, conn, 5, 3, size=8)
+        assert np.array_equal(got, want)
