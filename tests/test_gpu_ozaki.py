@@ -186,3 +186,24 @@ def test_k_limit(cuda_ok):
     ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
     rc = _lib.load().swb_oz_gemm_nn(_ptr(dA), 513, _ptr(dB), 70, 300, 513, 70, _ptr(out), 70, _ptr(ws), nb, None)
     assert rc != 0
+
+
+def test_rotation_at_scale_matches_dmma(cuda_ok):
+    """The c4 rotation shape at 2M+37 rows x K = 400 (three row chunks, the
+    last ragged; V with unit-scale orthonormal-like columns, C near the
+    identity): the INT8 digit-product GEMM agrees with the FP64 DMMA GEMM to
+    the FP64 level everywhere."""
+    from paper_1607_04174_b200.device import rotate_rows
+    rows, K = (2 << 20) + 37, 400
+    g = torch.Generator(device="cuda").manual_seed(4)
+    V = torch.randn((rows, K), dtype=torch.float64, device="cuda", generator=g) / rows ** 0.5
+    C = torch.eye(K, dtype=torch.float64, device="cuda") + 0.05 * torch.randn((K, K), dtype=torch.float64,
+                                                                              device="cuda", generator=g)
+    o1 = torch.empty_like(V)
+    rotate_rows(V, K, C, K, rows, K, o1, K)
+    o2 = torch.empty_like(V)
+    _lib.call("swb_gemm_nn", _ptr(V), K, _ptr(C), K, rows, K, K, _ptr(o2), K, 0, None)
+    torch.cuda.synchronize()
+    scale = V.abs().max().item() * C.abs().max().item() * K
+    assert (o1 - o2).abs().max().item() <= 2.0 ** -50 * scale
+    assert torch.isfinite(o1).all()
