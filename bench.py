@@ -173,7 +173,10 @@ def cpu_step(s, beta0, beta1, labels):
         pri, _ = O.similarity_priors(s["img"], s["moving"], s["dims"], vec, p["patch_radius"])
         u = O.solve_fast(V1, lam1, lap1.d_sqrt, lap1.matrix, [], [], labels, gamma=p["gamma"], priors=pri)
         return O.hard_labels(u), u @ vec
-    u = O.solve_fast(V1, lam1, lap1.d_sqrt, lap1.matrix, s["seeds"], s["labs"], labels)
+    m_use = None
+    if p.get("epsilon") is not None:   # c3: K from the accuracy target (adaptive.py:133-185)
+        m_use, _ = O.select_m(V1, lap1.d_sqrt, s["seeds"], s["labs"], labels, epsilon=p["epsilon"])
+    u = O.solve_fast(V1, lam1, lap1.d_sqrt, lap1.matrix, s["seeds"], s["labs"], labels, m_use=m_use)
     return O.hard_labels(u)
 
 
@@ -258,8 +261,16 @@ def setup_gpu(cfg, dims, m, rank):
     seeds, labs = W.seeds_for(w)
     prob = swb.LabelProblem(num_labels=p["labels"], seeds=swb.SeedPartition(n, seeds, labs))
     cut = W.cut_for(w)
+    round_probs = None
+    if p.get("rounds"):   # c3: cumulative seeds of rounds 0..r (union, first label wins)
+        round_probs, acc_i, acc_l = [], np.empty(0, np.int64), np.empty(0, np.int64)
+        for r in range(p["rounds"]):
+            si, sl = W.seeds_for(w, r)
+            acc_i, first = np.unique(np.concatenate([acc_i, si]), return_index=True)
+            acc_l = np.concatenate([acc_l, sl])[first]
+            round_probs.append(swb.LabelProblem(num_labels=p["labels"], seeds=swb.SeedPartition(n, acc_i, acc_l)))
     return dict(w=w, image=image, pack=pack, prob=prob, n=n, m=m, params=p, seeds_n=len(seeds),
-                cut=torch.from_numpy(cut[0]).cuda() if cut is not None else None)
+                cut=torch.from_numpy(cut[0]).cuda() if cut is not None else None, round_probs=round_probs)
 
 
 def _next_pack(state, beta, i=0):
@@ -299,15 +310,31 @@ def registration_solve(state, pack, fixed, moving):
     return field
 
 
-def gpu_step(state, i):
+def _adaptive_solve(state, pack, prob):
+    """solve_fast with m_use from select_m when the config chooses K from an
+    accuracy target (c3: AdaptivePolicy(epsilon=1e-3), adaptive.py:133-185)."""
     import paper_1607_04174_b200 as swb
+    eps = state["params"].get("epsilon")
+    if eps is None:
+        return swb.solve_fast(pack, pack.laplacian, prob)
+    m_use, _ = swb.select_m(pack, prob, swb.AdaptivePolicy(epsilon=eps))
+    return swb.solve_fast(pack, pack.laplacian, prob, m_use=m_use)
+
+
+def _round_prob(state, i):
+    """c3's interaction rounds: step i solves with the seeds of rounds
+    0..(i mod rounds) (100 more per label each round); else the fixed problem."""
+    probs = state.get("round_probs")
+    return probs[i % len(probs)] if probs else state["prob"]
+
+
+def gpu_step(state, i):
     p = state["params"]
     beta = p["beta1"] if i % 2 == 0 else p["beta0"]
     pack = _next_pack(state, beta, i)
     if state["prob"] is None:
         return registration_solve(state, pack, state["image"], state["moving"])
-    field = swb.solve_fast(pack, pack.laplacian, state["prob"])
-    return field
+    return _adaptive_solve(state, pack, _round_prob(state, i))
 
 
 def e2e_step(state, i, host_labels):
@@ -326,11 +353,11 @@ def e2e_step(state, i, host_labels):
         host_labels.copy_(field.labels_dev, non_blocking=True)
         state["host_disp"].copy_(field.displacement_dev, non_blocking=True)
         return field
-    seeds = state["prob"].seeds
+    seeds = _round_prob(state, i).seeds
     prob = swb.LabelProblem(num_labels=p["labels"],
                             seeds=swb.SeedPartition(state["n"], seeds.seed_indices.copy(), seeds.seed_labels.copy()))
     pack = _next_pack(state, beta, i)
-    field = swb.solve_fast(pack, pack.laplacian, prob)
+    field = _adaptive_solve(state, pack, prob)
     host_labels.copy_(field.labels_dev, non_blocking=True)
     return field
 
@@ -618,6 +645,8 @@ def run_gpu(args):
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         ems = float(et.item())
         s = state["seeds_n"]
+        if state.get("round_probs"):   # mean seed count over the interaction rounds
+            s = float(np.mean([pr.seeds.n_seeds for pr in state["round_probs"]]))
         if state["prob"] is None:
             h2d, d2h = 2 * n * 8, n * 4 + n * 4 * 8
         else:
@@ -725,6 +754,11 @@ def run_gpu(args):
 
     dims_full = tuple(state["w"].dims)
     s = state["seeds_n"]
+    rp = state.get("round_probs")
+    solve_desc = (f"{state['params']['labels']}-label RW solve, S={s}" if not rp else
+                  f"{state['params']['labels']}-label RW solve with K from select_m(epsilon="
+                  f"{state['params']['epsilon']}), {len(rp)} interaction rounds cycled (S = "
+                  f"{rp[0].seeds.n_seeds}..{rp[-1].seeds.n_seeds})")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -735,7 +769,7 @@ def run_gpu(args):
                                    f"{state['params']['cut_block']}x{state['params']['cut_block']} block boundary, "
                                    f"beta {state['params']['beta0']}) + " if state.get("cut") is not None else
                                    f"beta update {state['params']['beta0']}<->{state['params']['beta1']} + ") + (
-                                   f"{state['params']['labels']}-label RW solve, S={s}" if cfg != "c5" else
+                                   solve_desc if cfg != "c5" else
                                    f"similarity priors (grid {state['params']['grid']}, patch radius "
                                    f"{state['params']['patch_radius']}) + {state['params']['labels']}-label "
                                    f"gamma={state['params']['gamma']} RW solve + expected displacement"),

@@ -163,7 +163,80 @@ __global__ void __launch_bounds__(512) jacobi_fit_kernel(const double* __restric
   double smax = 0.0;
   for (int64_t j = 0; j < m; ++j) smax = fmax(smax, nrm[j]);
   const double cutoff = fmax(1e-13 * smax, 1e-300);
-  // per label: b_j = w_j . c_k / sigma_j (top r columns), then the fit
+  // per label: b_j = w_j . c_k / sigma_j (top r columns), then the fit.
+  // m <= 32 * FIT_REG: the b_j and sigma_j of the label live in the warp's
+  // registers (lane l holds j = l, l + 32, ...), computed once, so each of
+  // the up to 200 bisection steps is a register sum over the kept columns
+  // instead of m dot products of length r.
+  constexpr int FIT_REG = 16;
+  if (m <= 32 * FIT_REG) {
+    for (int64_t k = warp; k < K; k += nw) {
+      const double* ck = Ut + k * S;
+      const double u2 = uu[k];
+      double f;
+      if (bound <= 0.0) {
+        f = u2;
+      } else {
+        double bj[FIT_REG], sg[FIT_REG];   // sg = 0: column not kept (below cutoff or outside the top r)
+        double bb = 0.0, a20 = 0.0, bk2 = 0.0, sg0 = 0.0;
+        int nkeep = 0;
+#pragma unroll
+        for (int q = 0; q < FIT_REG; ++q) { bj[q] = 0.0; sg[q] = 0.0; }
+        for (int64_t j = 0; j < m; ++j) {
+          if (rank[j] >= r) continue;
+          const double sgj = nrm[j];
+          double d = 0.0;
+          for (int64_t i = lane; i < r; i += 32) d += W[j * r + i] * ck[i];
+          d = warp_sum(d);
+          const double b = sgj > 0.0 ? d / sgj : 0.0;
+          bb += b * b;
+          if (rank[j] == 0) sg0 = sgj;
+          if (sgj > cutoff) {
+            ++nkeep;
+            bk2 += b * b;
+            const double z = sgj * b / (sgj * sgj);
+            a20 += z * z;
+#pragma unroll
+            for (int q = 0; q < FIT_REG; ++q)
+              if (j == lane + 32 * q) { bj[q] = b; sg[q] = sgj; }
+          }
+        }
+        const double perp = u2 - bb;
+        if (nkeep == 0) {
+          f = u2;
+        } else if (a20 <= bound * bound) {
+          f = fmax(perp, 0.0);
+        } else {
+          auto a2 = [&](double mu) {
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < FIT_REG; ++q) {
+              const double z = sg[q] * bj[q] / (sg[q] * sg[q] + mu);
+              acc += sg[q] > 0.0 ? z * z : 0.0;
+            }
+            return warp_sum(acc);
+          };
+          double lo = 0.0, hi = sg0 * sqrt(bk2) / bound;
+          while (a2(hi) > bound * bound) hi *= 2.0;
+          for (int it = 0; it < 200; ++it) {
+            const double mid = 0.5 * (lo + hi);
+            if (a2(mid) > bound * bound) lo = mid; else hi = mid;
+            if (fabs(sqrt(a2(hi)) - bound) <= 1e-6 * bound) break;
+          }
+          double res = 0.0;
+#pragma unroll
+          for (int q = 0; q < FIT_REG; ++q) {
+            const double z = sg[q] * bj[q] / (sg[q] * sg[q] + hi);
+            const double rr = bj[q] - sg[q] * z;
+            res += sg[q] > 0.0 ? rr * rr : 0.0;
+          }
+          f = fmax(perp + warp_sum(res), 0.0);
+        }
+      }
+      if (lane == 0) f_out[int64_t(st) * K + k] = f;
+    }
+    return;
+  }
   for (int64_t k = warp; k < K; k += nw) {
     const double* ck = Ut + k * S;
     const double u2 = uu[k];
