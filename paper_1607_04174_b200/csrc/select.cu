@@ -93,7 +93,6 @@ __global__ void __launch_bounds__(512) jacobi_fit_kernel(const double* __restric
                                                          double* __restrict__ scratch, int64_t scratch_stride,
                                                          double* __restrict__ f_out) {
   extern __shared__ double sm[];
-  __shared__ double red[32];
   __shared__ int rotated;
   const int st = blockIdx.x;
   const int64_t m = steps[st];
