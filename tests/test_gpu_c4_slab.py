@@ -42,3 +42,38 @@ def test_c4_slab_update_and_solve_match_oracle(cuda_ok):
     gap = O.top2_gap(u_ref)
     lab = swb.hard_labels(f).labels
     assert not ((lab != O.hard_labels(u_ref)) & (gap >= 1e-9)).any()
+
+
+def test_c2_cut_update_and_solve_match_oracle(cuda_ok):
+    """The c2 workload at full size (512^2, 8-connected, K = 200, 3 labels,
+    150 seeds): the bench's block-boundary edge cut as a topology update,
+    then the solve, vs the oracle on the reference's block cut."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    import paper_1607_04174_b200 as swb
+    from oracle import rw_oracle as O
+    from paper_1607_04174_b200 import workloads as W
+    s = bench.cpu_sample("c2", None, 200)
+    p = s["params"]
+    dims, img, V, lam = s["dims"], s["img"], s["V"], s["lam"]
+    x0, y0 = s["cut"]
+    cut_edges = O.block_cut_mask(dims, x0, y0, size=p["cut_block"], connectivity=p["connectivity"])
+    lap0 = O.build_laplacian(img, dims, p["beta0"], p["weight_mode"], p["connectivity"])
+    lap1 = O.build_laplacian(img, dims, p["beta0"], p["weight_mode"], p["connectivity"], cut_edges=cut_edges)
+    Vo, lamo, order, P, _ = O.first_order_update(V, lam, lap0, lap1)
+    u_ref = O.solve_fast(Vo, lamo, lap1.d_sqrt, lap1.matrix, s["seeds"], s["labs"], p["labels"])
+
+    image = swb.Image(dims, img)
+    pack = swb.SpectralPack(dims=dims, spacing=(), beta=p["beta0"], eigen=swb.EigenBasis(V, lam),
+                            d_sqrt=lap0.d_sqrt, provenance=swb.PackProvenance(image.content_hash()))
+    dp = swb.to_device(pack, image=image, connectivity=p["connectivity"], weight_mode=p["weight_mode"])
+    mask = W.block_cut_voxel_mask(dims, p["connectivity"], x0, y0, size=p["cut_block"])
+    up = swb.update_basis(dp, image, p["beta0"], cut_edges=mask, method="first_order", keep_P=True)
+    np.testing.assert_allclose(up.P.cpu().numpy()[:, :200], P, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(up.lambda_hat, lamo, rtol=1e-9, atol=1e-13)
+    np.testing.assert_array_equal(up.order, order)
+    prob = swb.LabelProblem(num_labels=p["labels"], seeds=swb.SeedPartition(s["n"], s["seeds"], s["labs"]))
+    f = swb.solve_fast(up, up.laplacian, prob, want_field=True)
+    np.testing.assert_allclose(f.values, u_ref, rtol=0, atol=1e-9)
+    gap = O.top2_gap(u_ref)
+    assert not ((swb.hard_labels(f).labels != O.hard_labels(u_ref)) & (gap >= 1e-9)).any()
