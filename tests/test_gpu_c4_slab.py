@@ -77,3 +77,34 @@ def test_c2_cut_update_and_solve_match_oracle(cuda_ok):
     np.testing.assert_allclose(f.values, u_ref, rtol=0, atol=1e-9)
     gap = O.top2_gap(u_ref)
     assert not ((swb.hard_labels(f).labels != O.hard_labels(u_ref)) & (gap >= 1e-9)).any()
+
+
+def test_c3_slab_adaptive_solve_matches_oracle(cuda_ok):
+    """c3's adaptive path on a 128 x 128 x 4 slab (K = 150, 2 labels, the
+    bench's cumulative seeds of rounds 0-2): update, select_m(epsilon=1e-3)
+    decision and per-step fits, and the solve at the chosen K vs the oracle."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    import paper_1607_04174_b200 as swb
+    from oracle import rw_oracle as O
+    s = bench.cpu_sample("c3", None, 150)
+    p = s["params"]
+    dims, img, V, lam = s["dims"], s["img"], s["V"], s["lam"]
+    lap0 = O.build_laplacian(img, dims, p["beta0"], p["weight_mode"], p["connectivity"])
+    lap1 = O.build_laplacian(img, dims, p["beta1"], p["weight_mode"], p["connectivity"])
+    Vo, lamo, order, P, _ = O.first_order_update(V, lam, lap0, lap1)
+    m_o, info_o = O.select_m(Vo, lap1.d_sqrt, s["seeds"], s["labs"], p["labels"], epsilon=p["epsilon"])
+    u_ref = O.solve_fast(Vo, lamo, lap1.d_sqrt, lap1.matrix, s["seeds"], s["labs"], p["labels"], m_use=m_o)
+
+    image = swb.Image(dims, img)
+    pack = swb.SpectralPack(dims=dims, spacing=(), beta=p["beta0"], eigen=swb.EigenBasis(V, lam),
+                            d_sqrt=lap0.d_sqrt, provenance=swb.PackProvenance(image.content_hash()))
+    dp = swb.to_device(pack, image=image, connectivity=p["connectivity"], weight_mode=p["weight_mode"])
+    up = swb.update_basis(dp, image, p["beta1"], method="first_order")
+    prob = swb.LabelProblem(num_labels=p["labels"], seeds=swb.SeedPartition(s["n"], s["seeds"], s["labs"]))
+    m_g, info_g = swb.select_m(up, prob, swb.AdaptivePolicy(epsilon=p["epsilon"]))
+    assert m_g == m_o and info_g["saturated"] == info_o["saturated"]
+    np.testing.assert_allclose([st["f"] for st in info_g["steps"]], [st["f"] for st in info_o["steps"]],
+                               rtol=1e-8, atol=1e-12)
+    f = swb.solve_fast(up, up.laplacian, prob, m_use=m_g, want_field=True)
+    np.testing.assert_allclose(f.values, u_ref, rtol=0, atol=1e-9)
