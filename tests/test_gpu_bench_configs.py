@@ -1,4 +1,4 @@
-"""The bench workload's own shape end to end: a 256 x 256 x 4 z-slab of the c4
+"""Every bench configuration's own sample end to end (c1, c2, c3, c4 slab).  c4: a 256 x 256 x 4 z-slab of the c4
 volume with K = 400 (the CPU baseline's sample: synthetic orthonormal basis,
 4 labels, 200 seeds per label), first-order beta update 80 -> 110 and the
 gamma = 0 solve on the GPU vs the oracle restatement."""
@@ -107,4 +107,30 @@ def test_c3_slab_adaptive_solve_matches_oracle(cuda_ok):
     np.testing.assert_allclose([st["f"] for st in info_g["steps"]], [st["f"] for st in info_o["steps"]],
                                rtol=1e-8, atol=1e-12)
     f = swb.solve_fast(up, up.laplacian, prob, m_use=m_g, want_field=True)
+    np.testing.assert_allclose(f.values, u_ref, rtol=0, atol=1e-9)
+
+
+def test_c1_update_and_solve_match_oracle(cuda_ok):
+    """c1 at full size (128^2, 4-connected, (dI)^2 weights, K = 50, 2 labels,
+    40 seeds): beta 90 -> 120 update and solve vs the oracle."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    import paper_1607_04174_b200 as swb
+    from oracle import rw_oracle as O
+    s = bench.cpu_sample("c1", None, 50)
+    p = s["params"]
+    dims, img, V, lam = s["dims"], s["img"], s["V"], s["lam"]
+    lap0 = O.build_laplacian(img, dims, p["beta0"], p["weight_mode"], p["connectivity"])
+    lap1 = O.build_laplacian(img, dims, p["beta1"], p["weight_mode"], p["connectivity"])
+    Vo, lamo, order, P, _ = O.first_order_update(V, lam, lap0, lap1)
+    u_ref = O.solve_fast(Vo, lamo, lap1.d_sqrt, lap1.matrix, s["seeds"], s["labs"], p["labels"])
+    image = swb.Image(dims, img)
+    pack = swb.SpectralPack(dims=dims, spacing=(), beta=p["beta0"], eigen=swb.EigenBasis(V, lam),
+                            d_sqrt=lap0.d_sqrt, provenance=swb.PackProvenance(image.content_hash()))
+    dp = swb.to_device(pack, image=image, connectivity=p["connectivity"], weight_mode=p["weight_mode"])
+    up = swb.update_basis(dp, image, p["beta1"], method="first_order", keep_P=True)
+    np.testing.assert_allclose(up.P.cpu().numpy()[:, :50], P, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(up.lambda_hat, lamo, rtol=1e-9, atol=1e-13)
+    prob = swb.LabelProblem(num_labels=p["labels"], seeds=swb.SeedPartition(s["n"], s["seeds"], s["labs"]))
+    f = swb.solve_fast(up, up.laplacian, prob, want_field=True)
     np.testing.assert_allclose(f.values, u_ref, rtol=0, atol=1e-9)
