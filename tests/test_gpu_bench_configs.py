@@ -1,4 +1,4 @@
-"""Every bench configuration's own sample end to end (c1, c2, c3, c4 slab).  c4: a 256 x 256 x 4 z-slab of the c4
+"""Every bench configuration's own sample end to end (c1, c2, c3, c4 slab, c5 slab).  c4: a 256 x 256 x 4 z-slab of the c4
 volume with K = 400 (the CPU baseline's sample: synthetic orthonormal basis,
 4 labels, 200 seeds per label), first-order beta update 80 -> 110 and the
 gamma = 0 solve on the GPU vs the oracle restatement."""
@@ -134,3 +134,36 @@ def test_c1_update_and_solve_match_oracle(cuda_ok):
     prob = swb.LabelProblem(num_labels=p["labels"], seeds=swb.SeedPartition(s["n"], s["seeds"], s["labs"]))
     f = swb.solve_fast(up, up.laplacian, prob, want_field=True)
     np.testing.assert_allclose(f.values, u_ref, rtol=0, atol=1e-9)
+
+
+def test_c5_slab_registration_matches_oracle(cuda_ok):
+    """c5's bench sample (a 96 x 96 x 4 slab, K = 300, 125 displacement
+    labels, patch radius 2, gamma = 1): update, similarity priors, the
+    125-label solve, argmax and expected displacement vs the oracle."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    import paper_1607_04174_b200 as swb
+    from oracle import rw_oracle as O
+    from paper_1607_04174_b200 import registration as R
+    s = bench.cpu_sample("c5", None, 300)
+    p = s["params"]
+    dims, img, V, lam = s["dims"], s["img"], s["V"], s["lam"]
+    lap0 = O.build_laplacian(img, dims, p["beta0"], p["weight_mode"], p["connectivity"])
+    lap1 = O.build_laplacian(img, dims, p["beta1"], p["weight_mode"], p["connectivity"])
+    Vo, lamo, _, _, _ = O.first_order_update(V, lam, lap0, lap1)
+    vec = O.grid_vectors(p["grid"])
+    pri, _ = O.similarity_priors(img, s["moving"], dims, vec, p["patch_radius"])
+    u_ref = O.solve_fast(Vo, lamo, lap1.d_sqrt, lap1.matrix, [], [], p["labels"], gamma=p["gamma"], priors=pri)
+
+    image = swb.Image(dims, img)
+    pack = swb.SpectralPack(dims=dims, spacing=(), beta=p["beta0"], eigen=swb.EigenBasis(V, lam),
+                            d_sqrt=lap0.d_sqrt, provenance=swb.PackProvenance(image.content_hash()))
+    dp = swb.to_device(pack, image=image, connectivity=p["connectivity"], weight_mode=p["weight_mode"])
+    up = swb.update_basis(dp, image, p["beta1"], method="first_order")
+    grid = R.DisplacementGrid(p["grid"])
+    field, disp, _ = R.register(image, swb.Image(dims, s["moving"]), up, grid=grid, gamma=p["gamma"],
+                                patch_radius=p["patch_radius"])
+    np.testing.assert_allclose(field.values, u_ref, rtol=1e-9, atol=1e-12)
+    gap = O.top2_gap(u_ref)
+    assert not ((swb.hard_labels(field).labels != O.hard_labels(u_ref)) & (gap >= 1e-9)).any()
+    np.testing.assert_allclose(disp, u_ref @ grid.vectors(), rtol=1e-9, atol=1e-12)
