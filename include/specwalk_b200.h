@@ -184,7 +184,11 @@ int swb_seed_rows(const swb_lattice* lat, const double* what, const double* diag
  *   lsu[i,k]   = sum_{t seed in row s_i} L^_{s_i,s_t} [lab_t == k] d_sqrt_{s_t}
  *   dsq_s[i]   = d_sqrt[s_i]
  * col(j) = col_map ? col_map[j] : j; g = d_sqrt / dnorm (dnorm = ||d_sqrt||).
- * Rows not in [own_begin, own_end) contribute zero (z-slab shards). */
+ * Rows not in [own_begin, own_end) contribute zero (z-slab shards).
+ * PRECONDITION: seed_idx strictly ascending (sorted, unique), as
+ * SeedPartition guarantees (graphs.py:51-98) -- seed membership is a binary
+ * search; unsorted input gives wrong results.  swb_check_seeds validates it
+ * on the device; swb_rw_solve calls it and returns SWB_INVALID_PARAM. */
 int swb_seed_project(const double* V, int64_t ldv, int64_t row_base, int64_t own_begin,
                      int64_t own_end, int64_t m, const int32_t* col_map,
                      const int64_t* seed_idx, const int32_t* seed_lab, int64_t S,
@@ -192,6 +196,10 @@ int swb_seed_project(const double* V, int64_t ldv, int64_t row_base, int64_t own
                      const double* d_sqrt, double dnorm, int64_t L, double* q_s,
                      int64_t ldq, double* b_qn, double* bg, double* lsu, double* dsq_s,
                      void* stream);
+/* *flag_out (device double) = 1.0 when seed_idx is not strictly ascending
+ * or not in [0, n), or a label is not in [0, L); else 0.0 (stream-ordered). */
+int swb_check_seeds(const int64_t* seed_idx, const int32_t* seed_lab, int64_t S, int64_t n, int64_t L,
+                    double* flag_out, void* stream);
 /* Dense seed system of fastrw.py:399-454 + LU/rcond/solve of :332-344.
  * Computes the spectral weights w from values (m; 1/(lam+gamma), or the
  * deflated 1/lam for lam > 1e-10 at gamma == 0), g_s = dsq_s/dnorm,
@@ -372,7 +380,8 @@ int swb_update_first_order(const swb_lattice* lat, const double* image, double b
  * gamma == 0 needs seeds and vtg (V^T d_sqrt / ||d_sqrt||, M); gamma > 0
  * needs priors (N x K, ld ldp).  Writes labels_out (N int32), top2_out and
  * U_out (optional for K <= 8, required with ldu even beyond).  Synchronous:
- * returns SWB_SINGULAR_SMALL_SYSTEM when rcond < 1e-14 (rcond_host gets it). */
+ * returns SWB_SINGULAR_SMALL_SYSTEM when rcond < 1e-14 (rcond_host gets it),
+ * SWB_INVALID_PARAM when the seeds are not strictly ascending / in range. */
 size_t swb_rw_solve_workspace_bytes(const swb_lattice* lat, int64_t M, int64_t m_use, int64_t S, int64_t K,
                                     int with_priors);
 int swb_rw_solve(const swb_lattice* lat, const double* what, const double* diag, const double* d_sqrt,

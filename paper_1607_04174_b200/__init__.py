@@ -15,8 +15,9 @@ from .errors import (BackendUnavailable, ChecksumMismatch, DegenerateGraph, Devi
 from .types import (AdaptivePolicy, EigenBasis, Image, LabelMap, LabelProblem, LaplacianMode, PackProvenance,
                     PackSet, ProbabilityField, SeedPartition, SpectralPack, SENTINEL_UNLABELED)
 from .device import DeviceGraph, DevicePack, LatticeSpec, to_device
-from .api import (DeviceField, RefreshedPack, UpdatedPack, hard_labels, nearest_pack, refresh,
+from .api import (DeviceField, RefreshedPack, UpdatedPack, evict_device_pack, hard_labels, nearest_pack, refresh,
                   refresh_from_set, segment, select_m, solve_fast, update_basis)
+from .dropin import install
 from .packs import load_pack, save_pack, xxh64
 from .registration import DevicePriors, DisplacementGrid, expected_displacement, register, similarity_priors
 from .precompute import precompute, smallest_eigs_device

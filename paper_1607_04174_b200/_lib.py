@@ -86,6 +86,7 @@ SIGNATURES = {
     "swb_seed_project": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_i64,
                                    c_vp, c_vp, c_i64, c_vp, c_dbl, c_i64, c_vp, c_i64, c_vp, c_vp,
                                    c_vp, c_vp, c_vp]),
+    "swb_check_seeds": (C.c_int, [c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),
     "swb_small_solve_workspace_bytes": (c_sz, [c_i64, c_i64, c_i64]),
     "swb_small_solve": (C.c_int, [c_dbl, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,
                                   c_dbl, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_sz,

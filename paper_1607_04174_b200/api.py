@@ -103,13 +103,43 @@ def _check_image(pack, image):
         raise ImageMismatch("pack was precomputed from a different image")
 
 
+# host pack -> its device copy, one upload per host pack object.  The
+# reference treats packs as immutable and shared, so a host
+# SpectralPack passed to repeated solve_fast / select_m / refresh calls (the
+# CLI and the service session do exactly that, cli.py:143-156,
+# service/sessions.py:123-157) is uploaded once and its device copy (and its
+# stencil graph) lives as long as the host object.  evict_device_pack() drops
+# it early.
+_pack_cache: dict = {}
+UPLOADS = [0]      # host -> device pack uploads (tests assert one per host pack)
+
+
+def evict_device_pack(pack=None) -> None:
+    """Drop the cached device copy of ``pack`` (every cached pack if None)."""
+    if pack is None:
+        _pack_cache.clear()
+    else:
+        _pack_cache.pop(id(pack), None)
+
+
 def _as_device(pack, image=None, connectivity=None, weight_mode=None) -> DevicePack:
     if isinstance(pack, DevicePack):
         if image is not None and pack.image_dev is None:
             pack.image_dev = image_device(image)
         return pack
-    dp = to_device(pack, image=None, connectivity=connectivity, weight_mode=weight_mode or "abs")
-    if image is not None:
+    key = (connectivity, weight_mode or "abs")
+    ent = _pack_cache.get(id(pack))
+    if ent is not None and ent[0]() is pack and ent[1] == key:
+        dp = ent[2]
+    else:
+        dp = to_device(pack, image=None, connectivity=connectivity, weight_mode=weight_mode or "abs")
+        UPLOADS[0] += 1
+        try:
+            ref = weakref.ref(pack, lambda _r, k=id(pack): _pack_cache.pop(k, None))
+            _pack_cache[id(pack)] = (ref, key, dp)
+        except TypeError:
+            pass   # not weak-referenceable: no safe identity key, upload per call
+    if image is not None and dp.image_dev is None:
         dp.image_dev = image_device(image)
     return dp
 

@@ -321,11 +321,10 @@ int launch_nn(const double* A, int64_t lda, const double* B, int64_t ldb, int64_
               int64_t M2, double* out, int64_t ldo, int accumulate, double alpha, cudaStream_t st) {
   using Cf = Cfg<WARPS_M, WARPS_N, WTM, WTN, STAGES, false>;
   auto kern = gemm_nn_kernel<WARPS_M, WARPS_N, WTM, WTN, STAGES>;
-  static bool attr_done = false;
-  if (!attr_done) {
+  static unsigned long long attr_done = 0;
+  if (swb_first_on_device(&attr_done)) {
     SWB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(Cf::SMEM)));
-    attr_done = true;
   }
   const int64_t tm = (rows + Cf::BM - 1) / Cf::BM;
   const int tn = static_cast<int>((M2 + Cf::BN - 1) / Cf::BN);
@@ -390,7 +389,8 @@ int run_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t r
            cudaStream_t st, bool size_only, size_t* need) {
   using Cf = Cfg<WARPS_M, WARPS_N, WTM, WTN, TN_STAGES, true>;
   auto kern = gemm_tn_kernel<WARPS_M, WARPS_N, WTM, WTN, TN_STAGES>;
-  static int occ = 0;
+  static int occ_dev[64] = {};
+  int& occ = occ_dev[swb_device()];
   if (occ == 0 && !size_only) {
     SWB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(Cf::SMEM)));
@@ -423,7 +423,8 @@ int run_tn_sym(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64
   using Cf = Cfg<2, 2, W, W, TN_STAGES, true>;
   constexpr int G = 2 * W;
   auto kern = gemm_tn_sym_kernel<W, TN_STAGES>;
-  static int occ = 0;
+  static int occ_dev[64] = {};
+  int& occ = occ_dev[swb_device()];
   if (occ == 0 && !size_only) {
     SWB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cf::SMEM)));
     SWB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cf::THREADS, Cf::SMEM));

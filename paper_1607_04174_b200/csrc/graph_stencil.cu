@@ -634,10 +634,9 @@ int launch_stencil5(const StencilGeom& g, const double* V, int64_t ldv, int64_t 
   using Rg = Ring5<CONN, DELTA>;
   const size_t smem = sizeof(double) * size_t(Rg::RING + 1) * Rg::STAGE_DBL;
   auto kern = stencil5_kernel<CONN, DELTA>;
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;
+  if (swb_first_on_device(&attr)) {
     SWB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    attr = true;
   }
   kern<<<static_cast<unsigned>(grid), ST_WARPS * 32, smem, st>>>(g, V, ldv, row_base, blk_begin, blk_end, M, n_cb, cw,
                                                                  cd, d_sqrt, W, ldw, w_row0, slots, slot_ld, ap);

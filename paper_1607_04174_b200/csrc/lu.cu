@@ -509,11 +509,10 @@ extern "C" int swb_lu_factor(double* A, int64_t n, int64_t lda, int32_t* piv, do
     max_kernel<<<1, 1024, 0, st>>>(cs, n, anorm_out);
     SWB_CHECK_LAUNCH();
   }
-  static bool attr = false;
+  static unsigned long long attr = 0;
   const int smem = PANEL_SMEM_ROWS * PANEL_LD * sizeof(double);
-  if (!attr) {
+  if (swb_first_on_device(&attr)) {
     SWB_CUDA_TRY(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
   }
   // systems up to 1024 rows: 16-wide panels held in registers (one row per
   // thread); larger ones: 32-wide panels in shared memory
@@ -571,10 +570,10 @@ extern "C" int swb_lu_solve(const double* LU, int64_t n, int64_t lda, const int3
   double* tmp = reinterpret_cast<double*>(static_cast<char*>(workspace) +
                                           swb_align_up(sizeof(int32_t) * size_t(n + 1), 256));
   const size_t smem = n <= GETRS_SMEM_N ? sizeof(int32_t) * 2 * size_t(n) : 0;
-  static size_t attr = 48 * 1024;
-  if (smem > attr) {
-    SWB_CUDA_TRY(cudaFuncSetAttribute(getrs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr = smem;
+  static unsigned long long attr = 0;   // set once per device to the largest size getrs can ask for
+  if (smem > 48 * 1024 && swb_first_on_device(&attr)) {
+    SWB_CUDA_TRY(cudaFuncSetAttribute(getrs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(sizeof(int32_t) * 2 * size_t(GETRS_SMEM_N))));
   }
   getrs_kernel<<<1, 1024, smem, swb_stream(stream)>>>(LU, n, lda, piv, B, nrhs, ldb, perm, tmp);
   SWB_CHECK_LAUNCH();

@@ -29,6 +29,8 @@
 // and one lane issues the 28 MMAs per K chunk (M = 128, N = 64, K = 32) into
 // seven int32 TMEM accumulators (7 x 64 of the 512 columns), warps 2..5
 // drain TMEM, combine the groups in FP64 (Horner in 2^-8) and store.
+#include <mutex>
+
 #include "swb_common.cuh"
 
 namespace {
@@ -517,13 +519,12 @@ OzPtrs oz_ptrs(const OzLayout& o, void* ws, int buf) {
 }
 
 int oz_set_attrs() {
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;
+  if (swb_first_on_device(&attr)) {
     SWB_CUDA_TRY(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(OZ_SMEM)));
     SWB_CUDA_TRY(cudaFuncSetAttribute(oz_slice_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(OZ_SLICE_SMEM)));
-    attr = true;
   }
   return SWB_OK;
 }
@@ -623,16 +624,29 @@ extern "C" int swb_oz_gemm_nn(const double* A, int64_t lda, const double* B, int
     if ((rc = swb_oz_split_rows(A, lda, rows, rows, K, M2, 0, workspace, workspace_bytes, stream))) return rc;
     return swb_oz_gemm_planes(rows, rows, K, M2, 0, out, ldo, workspace, workspace_bytes, stream);
   }
-  static cudaStream_t aux = nullptr;
-  static cudaEvent_t ev_in, ev_split[2], ev_gemm[2];
-  if (!aux) {
-    SWB_CUDA_TRY(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
-    SWB_CUDA_TRY(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+  // side stream + events per device; the mutex makes the enqueue of one
+  // call's chunk loop atomic, so concurrent callers (different streams) share
+  // the side stream in order and never see each other's event records
+  struct Aux {
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_in, ev_split[2], ev_gemm[2];
+  };
+  static Aux tab[64];
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  Aux& X = tab[swb_device()];
+  if (!X.aux) {
+    SWB_CUDA_TRY(cudaStreamCreateWithFlags(&X.aux, cudaStreamNonBlocking));
+    SWB_CUDA_TRY(cudaEventCreateWithFlags(&X.ev_in, cudaEventDisableTiming));
     for (int b = 0; b < 2; ++b) {
-      SWB_CUDA_TRY(cudaEventCreateWithFlags(&ev_split[b], cudaEventDisableTiming));
-      SWB_CUDA_TRY(cudaEventCreateWithFlags(&ev_gemm[b], cudaEventDisableTiming));
+      SWB_CUDA_TRY(cudaEventCreateWithFlags(&X.ev_split[b], cudaEventDisableTiming));
+      SWB_CUDA_TRY(cudaEventCreateWithFlags(&X.ev_gemm[b], cudaEventDisableTiming));
     }
   }
+  cudaStream_t aux = X.aux;
+  cudaEvent_t& ev_in = X.ev_in;
+  cudaEvent_t* ev_split = X.ev_split;
+  cudaEvent_t* ev_gemm = X.ev_gemm;
   cudaStream_t st = swb_stream(stream);
   SWB_CUDA_TRY(cudaEventRecord(ev_in, st));            // A, B's planes ready
   SWB_CUDA_TRY(cudaStreamWaitEvent(aux, ev_in, 0));
@@ -763,10 +777,9 @@ __global__ void __launch_bounds__(128, 1) int8_probe_n64_kernel(int iters) {
 
 extern "C" int swb_int8_scheme_probe(int iters, double* ops_out, void* stream) {
   if (iters <= 0 || !ops_out) return SWB_INVALID_PARAM;
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;
+  if (swb_first_on_device(&attr)) {
     SWB_CUDA_TRY(cudaFuncSetAttribute(int8_probe_n64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024));
-    attr = true;
   }
   const int sms = swb_sm_count();
   int8_probe_n64_kernel<<<sms, 128, 48 * 1024, swb_stream(stream)>>>(iters);
@@ -777,10 +790,9 @@ extern "C" int swb_int8_scheme_probe(int iters, double* ops_out, void* stream) {
 
 extern "C" int swb_int8_peak_probe(int iters, double* ops_out, void* stream) {
   if (iters <= 0 || !ops_out) return SWB_INVALID_PARAM;
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;
+  if (swb_first_on_device(&attr)) {
     SWB_CUDA_TRY(cudaFuncSetAttribute(int8_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024));
-    attr = true;
   }
   const int sms = swb_sm_count();
   int8_probe_kernel<<<sms, 128, 48 * 1024, swb_stream(stream)>>>(iters);

@@ -193,7 +193,7 @@ SolveLayout solve_layout(const LatticeDev& L, int64_t M, int64_t m_use, int64_t 
   s.t_p = c.take<double>(size_t(m_use) * ldt);
   s.coeff = c.take<double>(size_t(m_use) * K);
   s.extra = c.take<double>(K);
-  s.dsum = c.take<double>(2);
+  s.dsum = c.take<double>(3);   // ||d_sqrt||^2, rcond, seed-check flag
   s.tn_bytes = priors ? swb_gemm_tn_workspace_bytes(N, m_use, K) : 0;
   s.tn_ws = c.take<char>(s.tn_bytes);
   s.ss_bytes = swb_small_solve_workspace_bytes(S, m_use, K);
@@ -237,10 +237,13 @@ extern "C" int swb_rw_solve(const swb_lattice* lat, const double* what, const do
   int rc;
   // ||d_sqrt|| (a host scalar of the kernels below): one synchronous read
   if ((rc = swb_sumsq(d_sqrt, N, w.dsum, w.sum_ws, 256 * 8, stream))) return rc;
-  double dsum = 0.0;
-  SWB_CUDA_TRY(cudaMemcpyAsync(&dsum, w.dsum, sizeof(double), cudaMemcpyDeviceToHost, st));
+  // the seed kernels binary-search seed_idx: validate sorted / unique / in range
+  if ((rc = swb_check_seeds(seed_idx, seed_lab, S, N, K, w.dsum + 2, stream))) return rc;
+  double hs[3] = {0.0, 0.0, 0.0};
+  SWB_CUDA_TRY(cudaMemcpyAsync(hs, w.dsum, sizeof(hs), cudaMemcpyDeviceToHost, st));
   SWB_CUDA_TRY(cudaStreamSynchronize(st));
-  const double dnorm = sqrt(dsum);
+  if (hs[2] != 0.0) return SWB_INVALID_PARAM;
+  const double dnorm = sqrt(hs[0]);
   if (S > 0) {
     if ((rc = swb_seed_rows(lat, what, diag, seed_idx, S, w.ell_idx, w.ell_val, stream))) return rc;
     if ((rc = swb_seed_project(V, ldv, 0, 0, N, m_use, nullptr, seed_idx, seed_lab, S, w.ell_idx, w.ell_val, R,

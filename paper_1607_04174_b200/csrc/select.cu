@@ -374,10 +374,9 @@ extern "C" int swb_seed_fit_schedule(const double* V, int64_t ldv, const int32_t
   if (smem > 200 * 1024) smem = sizeof(double) * 2 * size_t(max_step) + 64;  // W lives in global scratch
   (void)smem;
   const size_t dyn = 200 * 1024 + 1024;
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;
+  if (swb_first_on_device(&attr)) {
     SWB_CUDA_TRY(cudaFuncSetAttribute(jacobi_fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
-    attr = true;
   }
   jacobi_fit_kernel<<<static_cast<unsigned>(n_steps), 512, dyn, st>>>(At, S, M, Ut, K, steps, uu, bound, scratch,
                                                                        sstride, f_out);

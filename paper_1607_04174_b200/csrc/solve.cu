@@ -614,6 +614,30 @@ extern "C" int swb_seed_project(const double* V, int64_t ldv, int64_t row_base, 
   return SWB_OK;
 }
 
+// flag = 1 when the seeds break the kernels' precondition: seed_idx strictly
+// ascending (sorted, unique) and in [0, n), labels in [0, L)
+__global__ void check_seeds_kernel(const int64_t* __restrict__ seed_idx, const int32_t* __restrict__ seed_lab,
+                                   int64_t S, int64_t n, int64_t L, double* __restrict__ flag) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < S; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t s = seed_idx[i];
+    const int32_t l = seed_lab[i];
+    const bool bad = s < 0 || s >= n || l < 0 || l >= L || (i + 1 < S && seed_idx[i + 1] <= s);
+    if (bad) *flag = 1.0;
+  }
+}
+
+extern "C" int swb_check_seeds(const int64_t* seed_idx, const int32_t* seed_lab, int64_t S, int64_t n, int64_t L,
+                               double* flag_out, void* stream) {
+  if (S < 0 || n <= 0 || L <= 0 || !flag_out || (S > 0 && (!seed_idx || !seed_lab))) return SWB_INVALID_PARAM;
+  cudaStream_t st = swb_stream(stream);
+  SWB_CUDA_TRY(cudaMemsetAsync(flag_out, 0, sizeof(double), st));
+  if (S == 0) return SWB_OK;
+  const int blocks = static_cast<int>(std::min<int64_t>((S + 255) / 256, 4 * swb_sm_count()));
+  check_seeds_kernel<<<blocks, 256, 0, st>>>(seed_idx, seed_lab, S, n, L, flag_out);
+  SWB_CHECK_LAUNCH();
+  return SWB_OK;
+}
+
 namespace {
 struct SmallLayout {
   int64_t n, lda, ldr, ldm, lds;
@@ -766,11 +790,10 @@ extern "C" int swb_reconstruct_label(const double* V, int64_t ldv, int64_t row_b
   cudaStream_t st = swb_stream(stream);
   const size_t smem = sizeof(double) * size_t(mr) * L;
   if (L <= 8 && (ldv % 2) == 0 && (reinterpret_cast<uintptr_t>(V) & 15) == 0) {
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;
+    if (swb_first_on_device(&attr)) {
       SWB_CUDA_TRY(cudaFuncSetAttribute(reconstruct_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(RdCfg::SMEM)));
-      attr = true;
     }
     const int64_t rows = r_end - r_begin;
     const int64_t grid = (rows + RdCfg::BM - 1) / RdCfg::BM;

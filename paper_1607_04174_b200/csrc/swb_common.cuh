@@ -27,6 +27,21 @@ int swb_sm_count();
 
 static inline cudaStream_t swb_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Current device ordinal (0 when no device is current).
+static inline int swb_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  return dev & 63;
+}
+
+// True the first time it is called for the current device: per-device
+// one-time setup (cudaFuncSetAttribute is a per-device property, so a
+// process driving several GPUs needs it once on each).
+static inline bool swb_first_on_device(unsigned long long* mask) {
+  const unsigned long long bit = 1ull << swb_device();
+  return (__atomic_fetch_or(mask, bit, __ATOMIC_ACQ_REL) & bit) == 0;
+}
+
 static inline size_t swb_align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Forward-neighbour offsets of the lattice (see swb_lattice docs in the header).

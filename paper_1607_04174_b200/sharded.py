@@ -31,6 +31,7 @@ import numpy as np
 
 from . import _lib
 from .device import WORKSPACE, DeviceGraph, LatticeSpec, ptr, rotate_rows, round_up, stream_handle
+from .errors import InvalidParam
 
 
 # ---------------------------------------------------------------------------
@@ -461,12 +462,30 @@ def sharded_init_vtg(shards: list, comm, backend):
     return shards
 
 
+def _sorted_seeds(seed_idx, seed_lab):
+    """Seeds sorted ascending (labels permuted alike); duplicates are an error
+    (SeedPartition's contract, graphs.py:51-98)."""
+    idx = seed_idx.cpu().numpy() if hasattr(seed_idx, "cpu") else np.asarray(seed_idx)
+    lab = seed_lab.cpu().numpy() if hasattr(seed_lab, "cpu") else np.asarray(seed_lab)
+    idx = idx.astype(np.int64, copy=False).ravel()
+    lab = lab.astype(np.int64, copy=False).ravel()
+    if idx.size > 1 and np.any(np.diff(idx) <= 0):
+        o = np.argsort(idx, kind="stable")
+        idx, lab = idx[o], lab[o]
+        if np.any(np.diff(idx) == 0):
+            raise InvalidParam("duplicate seed index")
+    return idx, lab
+
+
 def sharded_solve(shards: list, comm, backend, seed_idx, seed_lab, k: int, gamma: float = 0.0, priors=None,
                   want_u: bool = False):
     """Reduced-basis RW solve of every local shard (one all-reduce).
 
     ``priors`` (gamma > 0): per shard, the owned rows (backend array).
-    Returns per shard (labels_own, top2_own, U_own or None, rcond)."""
+    Returns per shard (labels_own, top2_own, U_own or None, rcond).
+    Seeds may come in any order (the seed kernels need them sorted and
+    unique: they are sorted here, duplicates raise InvalidParam)."""
+    seed_idx, seed_lab = _sorted_seeds(seed_idx, seed_lab)
     s = int(len(seed_idx))
     staged = []
     _mark("solve_seeds")

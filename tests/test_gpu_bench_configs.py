@@ -14,6 +14,8 @@ torch = pytest.importorskip("torch")
 
 ROOT = Path(__file__).resolve().parent.parent
 
+from vprime_check import compare_vprime
+
 
 def test_c4_slab_update_and_solve_match_oracle(cuda_ok):
     sys.path.insert(0, str(ROOT))
@@ -36,6 +38,7 @@ def test_c4_slab_update_and_solve_match_oracle(cuda_ok):
     np.testing.assert_allclose(up.P.cpu().numpy()[:, :400], P, rtol=0, atol=1e-12)
     np.testing.assert_allclose(up.lambda_hat, lamo, rtol=1e-9, atol=1e-13)
     np.testing.assert_array_equal(up.order, order)
+    compare_vprime(up.V.cpu().numpy()[:, :400], Vo, lam, order, label="c4 slab 256x256x4 K=400 beta 80->110")
     prob = swb.LabelProblem(num_labels=p["labels"], seeds=swb.SeedPartition(s["n"], s["seeds"], s["labs"]))
     f = swb.solve_fast(up, up.laplacian, prob, want_field=True)
     np.testing.assert_allclose(f.values, u_ref, rtol=0, atol=1e-9)
@@ -72,6 +75,7 @@ def test_c2_cut_update_and_solve_match_oracle(cuda_ok):
     np.testing.assert_allclose(up.P.cpu().numpy()[:, :200], P, rtol=0, atol=1e-12)
     np.testing.assert_allclose(up.lambda_hat, lamo, rtol=1e-9, atol=1e-13)
     np.testing.assert_array_equal(up.order, order)
+    compare_vprime(up.V.cpu().numpy()[:, :200], Vo, lam, order, label="c2 512^2 8-conn K=200 block cut")
     prob = swb.LabelProblem(num_labels=p["labels"], seeds=swb.SeedPartition(s["n"], s["seeds"], s["labs"]))
     f = swb.solve_fast(up, up.laplacian, prob, want_field=True)
     np.testing.assert_allclose(f.values, u_ref, rtol=0, atol=1e-9)
@@ -101,6 +105,8 @@ def test_c3_slab_adaptive_solve_matches_oracle(cuda_ok):
                             d_sqrt=lap0.d_sqrt, provenance=swb.PackProvenance(image.content_hash()))
     dp = swb.to_device(pack, image=image, connectivity=p["connectivity"], weight_mode=p["weight_mode"])
     up = swb.update_basis(dp, image, p["beta1"], method="first_order")
+    np.testing.assert_array_equal(up.order, order)
+    compare_vprime(up.V.cpu().numpy()[:, :150], Vo, lam, order, label="c3 slab 128x128x4 K=150 beta 100->140")
     prob = swb.LabelProblem(num_labels=p["labels"], seeds=swb.SeedPartition(s["n"], s["seeds"], s["labs"]))
     m_g, info_g = swb.select_m(up, prob, swb.AdaptivePolicy(epsilon=p["epsilon"]))
     assert m_g == m_o and info_g["saturated"] == info_o["saturated"]
@@ -131,6 +137,8 @@ def test_c1_update_and_solve_match_oracle(cuda_ok):
     up = swb.update_basis(dp, image, p["beta1"], method="first_order", keep_P=True)
     np.testing.assert_allclose(up.P.cpu().numpy()[:, :50], P, rtol=0, atol=1e-12)
     np.testing.assert_allclose(up.lambda_hat, lamo, rtol=1e-9, atol=1e-13)
+    np.testing.assert_array_equal(up.order, order)
+    compare_vprime(up.V.cpu().numpy()[:, :50], Vo, lam, order, label="c1 128^2 K=50 beta 90->120")
     prob = swb.LabelProblem(num_labels=p["labels"], seeds=swb.SeedPartition(s["n"], s["seeds"], s["labs"]))
     f = swb.solve_fast(up, up.laplacian, prob, want_field=True)
     np.testing.assert_allclose(f.values, u_ref, rtol=0, atol=1e-9)
@@ -150,7 +158,7 @@ def test_c5_slab_registration_matches_oracle(cuda_ok):
     dims, img, V, lam = s["dims"], s["img"], s["V"], s["lam"]
     lap0 = O.build_laplacian(img, dims, p["beta0"], p["weight_mode"], p["connectivity"])
     lap1 = O.build_laplacian(img, dims, p["beta1"], p["weight_mode"], p["connectivity"])
-    Vo, lamo, _, _, _ = O.first_order_update(V, lam, lap0, lap1)
+    Vo, lamo, order, _, _ = O.first_order_update(V, lam, lap0, lap1)
     vec = O.grid_vectors(p["grid"])
     pri, _ = O.similarity_priors(img, s["moving"], dims, vec, p["patch_radius"])
     u_ref = O.solve_fast(Vo, lamo, lap1.d_sqrt, lap1.matrix, [], [], p["labels"], gamma=p["gamma"], priors=pri)
@@ -160,6 +168,8 @@ def test_c5_slab_registration_matches_oracle(cuda_ok):
                             d_sqrt=lap0.d_sqrt, provenance=swb.PackProvenance(image.content_hash()))
     dp = swb.to_device(pack, image=image, connectivity=p["connectivity"], weight_mode=p["weight_mode"])
     up = swb.update_basis(dp, image, p["beta1"], method="first_order")
+    np.testing.assert_array_equal(up.order, order)
+    compare_vprime(up.V.cpu().numpy()[:, :300], Vo, lam, order, label="c5 slab 96x96x4 K=300 beta 50->70")
     grid = R.DisplacementGrid(p["grid"])
     field, disp, _ = R.register(image, swb.Image(dims, s["moving"]), up, grid=grid, gamma=p["gamma"],
                                 patch_radius=p["patch_radius"])
@@ -167,3 +177,54 @@ def test_c5_slab_registration_matches_oracle(cuda_ok):
     gap = O.top2_gap(u_ref)
     assert not ((swb.hard_labels(field).labels != O.hard_labels(u_ref)) & (gap >= 1e-9)).any()
     np.testing.assert_allclose(disp, u_ref @ grid.vectors(), rtol=1e-9, atol=1e-12)
+
+
+def test_c4_full_size_rotation_and_projection_properties(cuda_ok):
+    """c4 at its full bench size (256^3, K = 400, the bench's own synthetic
+    basis and beta 80 -> 110 step), where the CPU oracle cannot hold V
+    (54 GB): size-independent checks of the update.
+
+    * rotation: V' rows are V rows times C, so 16,384 randomly sampled rows of
+      the GPU V' (INT8 digit-product rotation) are compared with the FP64
+      product V[rows] @ C in numpy at 1e-9 relative per row (normwise);
+    * projection: for unit columns diag(P) = v^T L'(110) v - v^T L(80) v, i.e.
+      the difference of two independent refresh passes (the Rayleigh
+      stencil kernel, refresh.py:75-77) -- a full-size identity between the
+      difference-stencil + DMMA projection and the reference refresh;
+    * eigenvalues / order equal the refresh at 110 (same Rayleigh quotients).
+    """
+    sys.path.insert(0, str(ROOT))
+    import bench
+    import paper_1607_04174_b200 as swb
+    free, _ = torch.cuda.mem_get_info()
+    if free < 125e9:
+        pytest.skip("needs ~125 GB of free HBM")
+    st = bench.setup_gpu("c4", None, 400, 0)
+    p = st["params"]
+    pack, image = st["pack"], st["image"]
+    m = 400
+    r0 = swb.refresh(pack, image, p["beta0"])
+    r1 = swb.refresh(pack, image, p["beta1"])
+    q0 = np.empty(m)
+    q0[r0.order] = r0.lambda_hat
+    q1 = np.empty(m)
+    q1[r1.order] = r1.lambda_hat
+    up = swb.update_basis(pack, image, p["beta1"], method="first_order", keep_P=True)
+    np.testing.assert_array_equal(up.order, r1.order)
+    np.testing.assert_allclose(up.lambda_hat, r1.lambda_hat, rtol=1e-12, atol=1e-15)
+    P = up.P.cpu().numpy()[:, :m]
+    np.testing.assert_allclose(P, P.T, rtol=0, atol=1e-15)
+    np.testing.assert_allclose(np.diag(P), q1 - q0, rtol=0, atol=1e-12)
+    rng = np.random.default_rng(4)
+    rows = torch.from_numpy(np.sort(rng.choice(st["n"], 16384, replace=False))).cuda()
+    Vr = pack.V[rows, :m].cpu().numpy()
+    Vpr = up.V[rows, :m].cpu().numpy()
+    Cm = up.C.cpu().numpy()[:, :m]
+    want = Vr @ Cm
+    err = np.linalg.norm(Vpr - want, axis=1) / np.linalg.norm(want, axis=1)
+    big = np.abs(want) > 1e-3 * np.abs(want).max(axis=1, keepdims=True)
+    elem = np.abs(Vpr - want)[big] / np.abs(want)[big]
+    print(f"c4 full-size V' rows: max row rel err {err.max():.3e}, max elem rel err (|x| > 1e-3 row max) "
+          f"{elem.max():.3e}")
+    assert err.max() <= 1e-9
+    assert elem.max() <= 1e-9

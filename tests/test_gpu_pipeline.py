@@ -108,3 +108,27 @@ def test_composite_solve_priors_many_labels(cuda_ok):
                              priors=pri)
     np.testing.assert_allclose(U, f.values, atol=1e-12)
     np.testing.assert_array_equal(labels, swb.hard_labels(f).labels)
+
+
+def test_composite_solve_rejects_unsorted_or_duplicate_seeds(cuda_ok):
+    """The seed kernels binary-search seed_idx, so swb_rw_solve validates the
+    SeedPartition contract (sorted, unique, in range; graphs.py:51-98) and
+    returns InvalidParam instead of silently wrong labels."""
+    import torch
+    rng, n, image, dp = _case((20, 18), 24, 12.0, conn=4)
+    g = DeviceGraph.build(dp.image_dev, dp.lattice, 12.0)
+    seeds = np.sort(rng.choice(n, 10, replace=False))
+    labs = np.arange(10) % 2
+    _solve_c(dp.lattice, g, dp.V, dp.values_dev, dp.ensure_vtg(), dp.m, seeds, labs, 2)   # valid: passes
+    for bad_s, bad_l in [(seeds[::-1].copy(), labs), (np.concatenate([seeds[:9], seeds[8:9]]), labs),
+                         (np.concatenate([seeds[:9], [n]]), labs), (seeds, np.where(labs == 1, 2, 0))]:
+        with pytest.raises(swb.InvalidParam):
+            _solve_c(dp.lattice, g, dp.V, dp.values_dev, dp.ensure_vtg(), dp.m, bad_s, bad_l, 2)
+    flag = torch.empty(1, dtype=torch.float64, device="cuda")
+    sidx = torch.tensor(seeds, device="cuda")
+    slab = torch.tensor(labs.astype(np.int32), device="cuda")
+    _lib.call("swb_check_seeds", ptr(sidx), ptr(slab), 10, n, 2, ptr(flag), stream_handle())
+    assert float(flag.item()) == 0.0
+    sidx_bad = torch.tensor(seeds[::-1].copy(), device="cuda")
+    _lib.call("swb_check_seeds", ptr(sidx_bad), ptr(slab), 10, n, 2, ptr(flag), stream_handle())
+    assert float(flag.item()) == 1.0

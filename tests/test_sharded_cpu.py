@@ -108,3 +108,16 @@ def test_slab_plan_partition():
         for p in plans:
             assert p.row_base + p.local_rows >= p.own_end
             assert p.own_slice().stop - p.own_slice().start == p.own_end - p.own_begin
+
+
+def test_sharded_solve_sorts_seeds_and_rejects_duplicates():
+    """sharded_solve takes raw seed arrays: they are sorted (labels permuted
+    alike) before the binary-searching seed kernels; duplicates raise."""
+    from paper_1607_04174_b200 import errors
+    from paper_1607_04174_b200.sharded import _sorted_seeds
+    idx, lab = _sorted_seeds(np.array([9, 3, 7, 1]), np.array([0, 1, 2, 3]))
+    assert idx.tolist() == [1, 3, 7, 9] and lab.tolist() == [3, 1, 2, 0]
+    idx, lab = _sorted_seeds(torch.tensor([2, 5]), torch.tensor([1, 0]))
+    assert idx.tolist() == [2, 5] and lab.tolist() == [1, 0]
+    with pytest.raises(errors.InvalidParam):
+        _sorted_seeds(np.array([4, 2, 4]), np.array([0, 1, 0]))
