@@ -38,7 +38,8 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "basis-update N·K/s and RW-solve voxels/s; % HBM / FP64-tensor roofline"
 UNIT = "N·K/s"
-CPU_SLAB_PLANES = 4
+CPU_SLAB_PLANES = 4          # the --impl reference arm's per-step sample (K steps must end in minutes)
+CPU_SLAB_PLANES_ALL = 32     # the all-cores cpu_baseline sample (a 256x256x32 z-slab)
 
 
 def parse_args():
@@ -180,21 +181,83 @@ def cpu_step(s, beta0, beta1, labels):
     return O.hard_labels(u)
 
 
-def cpu_baseline(cfg, dims, m, steps=2):
-    s = cpu_sample(cfg, dims, m)
+def cpu_model() -> str:
+    """The host CPU's model name (lscpu, else /proc/cpuinfo)."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def blas_threads() -> int:
+    from threadpoolctl import threadpool_info
+    info = threadpool_info()
+    return max([int(x.get("num_threads", 1)) for x in info] or [1])
+
+
+def _time_cpu(s, threads, steps):
+    """Best of ``steps`` oracle steps under a BLAS thread limit (None = all)."""
+    from threadpoolctl import threadpool_limits
     p = s["params"]
-    cpu_step(s, p["beta0"], p["beta1"], p["labels"])  # warm
     t = []
-    for i in range(steps):
-        t0 = time.perf_counter()
-        b0, b1 = (p["beta0"], p["beta1"]) if i % 2 == 0 else (p["beta1"], p["beta0"])
-        cpu_step(s, b0, b1, p["labels"])
-        t.append(time.perf_counter() - t0)
-    sec = min(t)
-    return {"value": s["n"] * m / sec, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-            "sample": f"{cfg} z-slab {'x'.join(map(str, s['dims']))} ({s['n']} voxels) x K={m}: oracle "
-                      f"first-order update + " + ("priors + gamma=1 solve + labels + displacement" if cfg == "c5" else
-                                                  "gamma=0 solve + labels") + f", best of {steps}, {sec:.2f} s/step"}
+    with threadpool_limits(limits=threads):
+        used = blas_threads()
+        for i in range(steps):
+            b0, b1 = (p["beta0"], p["beta1"]) if i % 2 == 0 else (p["beta1"], p["beta0"])
+            t0 = time.perf_counter()
+            cpu_step(s, b0, b1, p["labels"])
+            t.append(time.perf_counter() - t0)
+    return min(t), used
+
+
+def _describe(cfg, s, m):
+    what = ("priors + gamma=1 solve + labels + displacement" if cfg == "c5" else
+            "select_m + gamma=0 solve + labels" if s["params"].get("epsilon") is not None else
+            "gamma=0 solve + labels")
+    where = f"z-slab {'x'.join(map(str, s['dims']))}" if len(s["dims"]) == 3 else f"{'x'.join(map(str, s['dims']))}"
+    return f"{cfg} {where} ({s['n']} voxels) x K={m}: oracle first-order update + {what}"
+
+
+def cpu_baseline(cfg, dims, m):
+    """The oracle restatement (oracle/rw_oracle.py on numpy/scipy/OpenBLAS) on
+    the box's host cores: all cores on a 32-plane z-slab of a
+    3-D volume (the whole image in 2-D) and 1 thread on the 4-plane slab,
+    both reported as N·K/s; the per-N·K rate is extrapolated linearly in N to
+    the full volume (the oracle's work is linear in N: measured 22.6 vs 22.9
+    M N·K/s at 4 vs 8 planes).  The scipy-sparse parts are single-threaded
+    whatever the limit."""
+    d3 = len(W_dims(cfg, dims)) == 3
+    small = cpu_sample(cfg, dims, m, planes=CPU_SLAB_PLANES)
+    big = cpu_sample(cfg, dims, m, planes=CPU_SLAB_PLANES_ALL) if d3 else small
+    _time_cpu(small, None, 1)                            # warm-up: imports, BLAS thread pool
+    steps = 1 if d3 else 2
+    t_all, th_all = _time_cpu(big, None, steps)
+    t_one, _ = _time_cpu(small, 1, steps)
+    v_all = big["n"] * m / t_all
+    v_one = small["n"] * m / t_one
+    return {"value": v_all, "unit": UNIT, "cores": th_all, "kind": "port",
+            "sample": f"{_describe(cfg, big, m)}; all {th_all} BLAS threads, best of {steps}, {t_all:.2f} s/step",
+            "extrapolated": d3, "extrapolation": "per-N·K rate of the slab, linear in N" if d3 else None,
+            "cpu_model": cpu_model(), "host_cpus": os.cpu_count(),
+            "all_cores": {"value": v_all, "threads": th_all, "s_per_step": t_all, "voxels": big["n"]},
+            "single_thread": {"value": v_one, "threads": 1, "s_per_step": t_one, "voxels": small["n"],
+                              "sample": f"{_describe(cfg, small, m)}; 1 BLAS thread (threadpoolctl), best of "
+                                        f"{steps}"}}
+
+
+def W_dims(cfg, dims):
+    from paper_1607_04174_b200 import workloads as W
+    return tuple(dims) if dims else tuple(W.CONFIGS[cfg]["dims"])
 
 
 def run_reference(args):
@@ -207,6 +270,7 @@ def run_reference(args):
     m = args.m or W.CONFIGS[cfg]["m"]
     s = cpu_sample(cfg, dims, m)
     p = s["params"]
+    threads = blas_threads()
     for i in range(args.warmup):
         cpu_step(s, p["beta0"], p["beta1"], p["labels"])
     t0 = time.perf_counter()
@@ -221,9 +285,12 @@ def run_reference(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{cfg} {'x'.join(map(str, dims_full))} K={m}", "K": m,
                        "sample_voxels": s["n"]},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                             "sample": f"z-slab {'x'.join(map(str, s['dims']))} of {cfg} ({s['n']} voxels)"
-                                       f" x K={m}, oracle/rw_oracle.py on numpy/scipy"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"{_describe(cfg, s, m)}; oracle/rw_oracle.py on numpy/scipy/OpenBLAS, all "
+                                       f"{threads} BLAS threads, mean of {args.steps} steps after {args.warmup}",
+                             "extrapolated": len(s["dims"]) == 3,
+                             "extrapolation": "per-N·K rate of the slab, linear in N" if len(s["dims"]) == 3
+                             else None, "cpu_model": cpu_model(), "host_cpus": os.cpu_count()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -418,6 +485,48 @@ def int8_probe(lib, fn="swb_int8_peak_probe", iters=4000):
     return best
 
 
+def int8_sustained_probe(lib, seconds=1.5, pattern=0):
+    """INT8 tensor-core rate with pseudo-random operands, held for ~seconds
+    so the board reaches its power cap (the regime of the rotation GEMM inside
+    the step): mean over the second half of back-to-back launches, TOP/s."""
+    import torch
+
+    from paper_1607_04174_b200 import _lib
+    from paper_1607_04174_b200.device import stream_handle
+    ops = _lib.C.c_double()
+    iters = 40000 if pattern == 0 else 6000
+    rates = []
+    t_end = time.perf_counter() + seconds
+    seed = 1
+    while time.perf_counter() < t_end or len(rates) < 8:
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        _lib.check(lib.swb_int8_probe_ex(pattern, iters, seed, _lib.C.byref(ops), stream_handle()))
+        e1.record()
+        torch.cuda.synchronize()
+        rates.append(ops.value / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+        seed += 1
+    tail = rates[len(rates) // 2:]
+    return float(np.mean(tail))
+
+
+def measured_peaks() -> dict:
+    mp = ROOT / "MEASURED_PEAKS.json"
+    return json.loads(mp.read_text()) if mp.exists() else {}
+
+
+def int8_denominator(peaks: dict, live_sustained: float | None):
+    """INT8 roofline denominator: dense INT8 = 2 x dense bf16 on B200, and the
+    rotation runs inside a long power-capped step, so 2 x the measured
+    sustained cuBLAS bf16 rate (MEASURED_PEAKS.json); without that file, the
+    live random-operand sustained probe."""
+    if peaks.get("bf16_tflops_sustained"):
+        return (2.0 * float(peaks["bf16_tflops_sustained"]),
+                "of measured: 2 x MEASURED_PEAKS.json bf16_tflops_sustained (dense INT8 = 2 x dense bf16 on B200; "
+                "sustained: the GEMM runs inside a long power-capped step)")
+    return live_sustained, "live random-operand INT8 probe held ~1.5 s in this run (MEASURED_PEAKS.json absent)"
+
+
 # the rotation's digit scheme (csrc/ozaki.cu): 7 digits per operand, the 28
 # digit products with i + j <= 6, each an INT8 GEMM of the rotation's shape
 OZ_PAIRS = 28
@@ -473,7 +582,9 @@ def run_sharded(args):
         return labels, rc
 
     fp64_peak = fp64_probe(lib)
-    int8_peak = int8_probe(lib)
+    int8_den, int8_den_src = int8_denominator(measured_peaks(), None)
+    if int8_den is None:
+        int8_den, int8_den_src = int8_denominator({}, int8_sustained_probe(lib))
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
@@ -535,9 +646,9 @@ def run_sharded(args):
             if m <= 512 and not os.environ.get("SWB_ROTATION", "").startswith("d"):
                 ach = OZ_PAIRS * 2.0 * rows * m * m / (rot_ms * 1e-3) / 1e12
                 line["roofline"] = {"bound": "tensor", "kernel": "rotation V*C on INT8 tcgen05 (digit split + "
-                                    "GEMM), per GPU (rank 0 slab)", "achieved": ach, "peak": int8_peak,
-                                    "unit": "TOP/s (int8)", "frac": ach / int8_peak,
-                                    "peak_source": "live tcgen05 kind::i8 probe (swb_int8_peak_probe) in this run",
+                                    "GEMM), per GPU (rank 0 slab)", "achieved": ach, "peak": int8_den,
+                                    "unit": "TOP/s (int8)", "frac": ach / int8_den,
+                                    "peak_source": int8_den_src,
                                     "traffic": None, "algorithmic_bytes": 16.0 * rows * m}
             else:
                 ach = 2.0 * rows * m * m / (rot_ms * 1e-3) / 1e12
@@ -579,8 +690,9 @@ def run_gpu(args):
         return
 
     fp64_peak = fp64_probe(lib)
-    int8_peak = int8_probe(lib)
+    int8_peak = int8_probe(lib)                   # zero operands, short: the burst figure
     scheme_peak = int8_probe(lib, "swb_int8_scheme_probe", 600)
+    int8_sust = int8_sustained_probe(lib)         # random operands, held ~1.5 s: power-capped
 
     for i in range(args.warmup):
         gpu_step(state, i)
@@ -668,10 +780,8 @@ def run_gpu(args):
     rot_ms = sum(phases.get(k, 0.0) for k in ("rotate", "rotate_split", "rotate_gemm", "rotate_join")) or None
     rot_flops = 2.0 * n * m * m
     achieved = rot_flops / (rot_ms * 1e-3) / 1e12 if rot_ms else None
-    peaks = {}
+    peaks = measured_peaks()
     mp = ROOT / "MEASURED_PEAKS.json"
-    if mp.exists():
-        peaks = json.loads(mp.read_text())
     hbm = float(peaks.get("hbm_gbs", 6650.0))   # fallback: B200_PROFILING.md
     proj_ms = phases.get("project")
     st_ms = phases.get("stencil")
@@ -685,8 +795,7 @@ def run_gpu(args):
         "rotation": {"ms": rot_ms, "fp64_equiv_tflops": achieved,
                      "note": "V*C: FP64 via INT8 tcgen05 digit products (split + GEMM); "
                              "SWB_ROTATION=dmma runs the DMMA GEMM instead"},
-        "rotation_int8_gemm": {"ms": rot_gemm_ms, "int8_tops": oz_tops,
-                               "frac_int8": oz_tops / int8_peak if oz_tops else None},
+        "rotation_int8_gemm": {"ms": rot_gemm_ms, "int8_tops": oz_tops},
         "rotation_digit_split": {"ms_exposed": rot_split_ms, "bytes": split_bytes,
                                  "note": "chunk i+1 split on a side stream during GEMM i; ms = exposed part"},
         "projection_dmma": {"ms": proj_ms, "tflops": (n * m * (m + 1)) / (proj_ms * 1e-3) / 1e12 if proj_ms else None},
@@ -714,12 +823,22 @@ def run_gpu(args):
         if sr_ms:
             kernels["stencil_rayleigh"]["frac_hbm"] = kernels["stencil_rayleigh"]["gbs"] / hbm
 
+    # INT8 denominator (int8_denominator); the zero-operand burst probe and
+    # the live random-operand sustained probe are reported beside it
+    int8_den, int8_den_src = int8_denominator(peaks, int8_sust)
     # the dominant kernel by time: the INT8 rotation GEMM or the DMMA projection
     if rot_gemm_ms and (not proj_ms or rot_gemm_ms >= proj_ms):
         roofline = {"bound": "tensor", "kernel": "rotation V*C: INT8 tcgen05 digit-product GEMM (oz_gemm_kernel)",
-                    "achieved": oz_tops, "peak": int8_peak, "unit": "TOP/s (int8)",
-                    "frac": oz_tops / int8_peak if oz_tops else None,
-                    "peak_source": "live tcgen05.mma.kind::i8 M128xN256 probe (swb_int8_peak_probe) in this run",
+                    "achieved": oz_tops, "peak": int8_den, "unit": "TOP/s (int8)",
+                    "frac": oz_tops / int8_den if oz_tops else None,
+                    "peak_source": int8_den_src,
+                    "peak_burst_zero_operands": int8_peak,
+                    "peak_burst_source": "live tcgen05.mma.kind::i8 M128xN256 probe on zero-filled shared memory, "
+                                         "2 ms launches (swb_int8_peak_probe): burst clock, no operand switching",
+                    "peak_live_random_sustained": int8_sust,
+                    "frac_of_live_random_sustained": oz_tops / int8_sust if oz_tops and int8_sust else None,
+                    "peak_live_random_sustained_source": "the same MMA stream on pseudo-random operand bytes, "
+                                                         "back-to-back for ~1.5 s (swb_int8_probe_ex)",
                     "algorithmic": f"{OZ_PAIRS} digit products x 2*N*K*K ops",
                     "traffic": _ncu_traffic("rotation_int8_gemm", cfg, dims, m),
                     "algorithmic_bytes": 16.0 * n * m,
@@ -783,7 +902,8 @@ def run_gpu(args):
                     roofline,
         "kernels": kernels,
         "peaks": {"fp64_tflops": fp64_peak, "fp64_source": "of measured: live DMMA probe in this run",
-                  "int8_tops": int8_peak, "int8_source": "of measured: live tcgen05 kind::i8 probe in this run",
+                  "int8_tops": int8_den, "int8_source": int8_den_src,
+                  "int8_tops_burst_zero_operands": int8_peak, "int8_tops_live_random_sustained": int8_sust,
                   "hbm_gbs": hbm, "hbm_source": "of measured: MEASURED_PEAKS.json hbm_gbs" if mp.exists()
                   else "of fallback: B200_PROFILING.md"},
         "update": {"ms": upd_ms, "value": n * m / (upd_ms * 1e-3) if upd_ms else None, "unit": UNIT},

@@ -155,6 +155,11 @@ int swb_int8_peak_probe(int iters, double* ops_out, void* stream);
  * 28 MMAs per K chunk into seven TMEM accumulators) on every SM -- the
  * ceiling of the digit-product scheme; *ops_out = 2 x MACs issued */
 int swb_int8_scheme_probe(int iters, double* ops_out, void* stream);
+/* the two probes with a choice of operands: pattern 0 = the dense M128 N256
+ * probe, 1 = the scheme probe; seed 0 = zero operands (burst figure), else
+ * pseudo-random operand bytes (the data-dependent power of real operands:
+ * run long enough, this is the sustained, power-capped figure) */
+int swb_int8_probe_ex(int pattern, int iters, unsigned int seed, double* ops_out, void* stream);
 /* diagnostics: the seven int32 digit-product group sums of the first row
  * chunk, raw[(g * rows_p + r) * np + c], rows_p / np padded to 128 / 64 */
 int swb_oz_gemm_nn_raw(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows, int64_t K,

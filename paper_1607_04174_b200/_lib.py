@@ -78,6 +78,7 @@ SIGNATURES = {
     "swb_oz_chunk_rows": (c_i64, [c_i64, c_i64, c_i64]),
     "swb_int8_peak_probe": (C.c_int, [C.c_int, C.POINTER(C.c_double), c_vp]),
     "swb_int8_scheme_probe": (C.c_int, [C.c_int, C.POINTER(C.c_double), c_vp]),
+    "swb_int8_probe_ex": (C.c_int, [C.c_int, C.c_int, C.c_uint, C.POINTER(C.c_double), c_vp]),
     "swb_oz_gemm_nn_raw": (C.c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, C.c_size_t,
                                      c_vp]),
     "swb_update_coeffs": (C.c_int, [C.c_int, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_dbl, c_vp, c_i64,

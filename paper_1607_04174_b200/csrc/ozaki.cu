@@ -691,13 +691,24 @@ extern "C" int swb_oz_gemm_nn_raw(const double* A, int64_t lda, const double* B,
 // INT8 roofline.  ops_out = 2 * MACs issued.
 // ---------------------------------------------------------------------------
 namespace {
-__global__ void __launch_bounds__(128, 1) int8_probe_kernel(int iters) {
+__device__ __forceinline__ uint32_t probe_hash(uint32_t seed, uint32_t i) {
+  uint32_t x = seed * 0x9E3779B9u ^ (i + blockIdx.x * 0x85EBCA6Bu);
+  x ^= x >> 16; x *= 0x7FEB352Du; x ^= x >> 15; x *= 0x846CA68Bu; x ^= x >> 16;
+  return x;
+}
+
+__global__ void __launch_bounds__(128, 1) int8_probe_kernel(int iters, uint32_t seed) {
   extern __shared__ __align__(1024) uint8_t pr_smem[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ uint32_t slot;
   const int warp = threadIdx.x >> 5;
+  // operands: zeros (seed 0: the burst figure) or pseudo-random bytes (the
+  // data-dependent switching power of real operands)
   for (int i = threadIdx.x; i < 48 * 1024 / 16; i += blockDim.x)
-    reinterpret_cast<uint4*>(pr_smem)[i] = make_uint4(0, 0, 0, 0);
+    reinterpret_cast<uint4*>(pr_smem)[i] =
+        seed ? make_uint4(probe_hash(seed, 4 * i), probe_hash(seed, 4 * i + 1), probe_hash(seed, 4 * i + 2),
+                          probe_hash(seed, 4 * i + 3))
+             : make_uint4(0, 0, 0, 0);
   if (threadIdx.x == 0) {
     mbar_init(smem_u32(&bar), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -735,13 +746,18 @@ __global__ void __launch_bounds__(128, 1) int8_probe_kernel(int iters) {
 // the ceiling of the 28-digit-product scheme, whose seven resident group
 // accumulators cap N at 64 (bench.py reports the GEMM against it too).
 namespace {
-__global__ void __launch_bounds__(128, 1) int8_probe_n64_kernel(int iters) {
+__global__ void __launch_bounds__(128, 1) int8_probe_n64_kernel(int iters, uint32_t seed) {
   extern __shared__ __align__(1024) uint8_t pr_smem[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ uint32_t slot;
   const int warp = threadIdx.x >> 5;
+  // operands: zeros (seed 0: the burst figure) or pseudo-random bytes (the
+  // data-dependent switching power of real operands)
   for (int i = threadIdx.x; i < 48 * 1024 / 16; i += blockDim.x)
-    reinterpret_cast<uint4*>(pr_smem)[i] = make_uint4(0, 0, 0, 0);
+    reinterpret_cast<uint4*>(pr_smem)[i] =
+        seed ? make_uint4(probe_hash(seed, 4 * i), probe_hash(seed, 4 * i + 1), probe_hash(seed, 4 * i + 2),
+                          probe_hash(seed, 4 * i + 3))
+             : make_uint4(0, 0, 0, 0);
   if (threadIdx.x == 0) {
     mbar_init(smem_u32(&bar), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -776,27 +792,41 @@ __global__ void __launch_bounds__(128, 1) int8_probe_n64_kernel(int iters) {
 }  // namespace
 
 extern "C" int swb_int8_scheme_probe(int iters, double* ops_out, void* stream) {
+  return swb_int8_probe_ex(1, iters, 0, ops_out, stream);
+}
+
+extern "C" int swb_int8_peak_probe(int iters, double* ops_out, void* stream) {
+  return swb_int8_probe_ex(0, iters, 0, ops_out, stream);
+}
+
+static int int8_scheme_probe_impl(int iters, uint32_t seed, double* ops_out, void* stream) {
   if (iters <= 0 || !ops_out) return SWB_INVALID_PARAM;
   static unsigned long long attr = 0;
   if (swb_first_on_device(&attr)) {
     SWB_CUDA_TRY(cudaFuncSetAttribute(int8_probe_n64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024));
   }
   const int sms = swb_sm_count();
-  int8_probe_n64_kernel<<<sms, 128, 48 * 1024, swb_stream(stream)>>>(iters);
+  int8_probe_n64_kernel<<<sms, 128, 48 * 1024, swb_stream(stream)>>>(iters, seed);
   SWB_CHECK_LAUNCH();
   *ops_out = 2.0 * double(sms) * iters * (OZ_S * (OZ_S + 1) / 2) * double(OZ_BM) * OZ_BN * OZ_KC;
   return SWB_OK;
 }
 
-extern "C" int swb_int8_peak_probe(int iters, double* ops_out, void* stream) {
+static int int8_peak_probe_impl(int iters, uint32_t seed, double* ops_out, void* stream) {
   if (iters <= 0 || !ops_out) return SWB_INVALID_PARAM;
   static unsigned long long attr = 0;
   if (swb_first_on_device(&attr)) {
     SWB_CUDA_TRY(cudaFuncSetAttribute(int8_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024));
   }
   const int sms = swb_sm_count();
-  int8_probe_kernel<<<sms, 128, 48 * 1024, swb_stream(stream)>>>(iters);
+  int8_probe_kernel<<<sms, 128, 48 * 1024, swb_stream(stream)>>>(iters, seed);
   SWB_CHECK_LAUNCH();
   *ops_out = 2.0 * double(sms) * iters * 8 * 128.0 * 256.0 * 32.0;
   return SWB_OK;
+}
+
+extern "C" int swb_int8_probe_ex(int pattern, int iters, unsigned int seed, double* ops_out, void* stream) {
+  if (pattern == 0) return int8_peak_probe_impl(iters, seed, ops_out, stream);
+  if (pattern == 1) return int8_scheme_probe_impl(iters, seed, ops_out, stream);
+  return SWB_INVALID_PARAM;
 }
