@@ -317,6 +317,11 @@ uint64_t swb_xxh64_digest(const void* state);
  * row-major f64 device basis (ld >= m). */
 int swb_f32_colmajor_to_f64_rowmajor(const float* src, int64_t n, int64_t m, double* dst, int64_t ld,
                                      void* stream);
+/* same for an f64 column-major block (in-memory reference packs, Fortran V);
+ * dst may point at a column offset of the basis (dst + c0, ld = ldv) so a
+ * pack streams into the device basis block by block */
+int swb_f64_colmajor_to_f64_rowmajor(const double* src, int64_t n, int64_t m, double* dst, int64_t ld,
+                                     void* stream);
 /* and back (save_pack): first m columns (through col_map if given). */
 int swb_f64_rowmajor_to_f32_colmajor(const double* src, int64_t n, int64_t ld, int64_t m,
                                      const int32_t* col_map, float* dst, void* stream);

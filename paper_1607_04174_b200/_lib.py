@@ -118,6 +118,7 @@ SIGNATURES = {
     "swb_xxh64_update": (None, [c_vp, c_vp, c_sz]),
     "swb_xxh64_digest": (C.c_uint64, [c_vp]),
     "swb_f32_colmajor_to_f64_rowmajor": (C.c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp]),
+    "swb_f64_colmajor_to_f64_rowmajor": (C.c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp]),
     "swb_f64_rowmajor_to_f32_colmajor": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "swb_similarity_priors_workspace_bytes": (c_sz, [c_i64, c_i64]),
     "swb_similarity_priors": (C.c_int, [c_vp, c_vp, c_i64, c_i64, c_i64, c_i32, c_vp, c_i64, c_i32, c_vp, c_i64,

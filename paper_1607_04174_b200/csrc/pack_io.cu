@@ -102,6 +102,35 @@ extern "C" int swb_f32_colmajor_to_f64_rowmajor(const float* src, int64_t n, int
 }
 
 namespace {
+// transpose src (m x n f64 column-major block) -> dst (n x ld f64 row-major)
+__global__ void f64cm_to_f64rm_kernel(const double* __restrict__ src, int64_t n, int64_t m, double* __restrict__ dst,
+                                      int64_t ld) {
+  __shared__ double tile[32][33];
+  const int64_t j0 = int64_t(blockIdx.y) * 32, r0 = int64_t(blockIdx.x) * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t j = j0 + k, r = r0 + threadIdx.x;
+    if (j < m && r < n) tile[k][threadIdx.x] = src[j * n + r];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t r = r0 + k, j = j0 + threadIdx.x;
+    if (r < n && j < m) dst[r * ld + j] = tile[threadIdx.x][k];
+  }
+}
+}  // namespace
+
+extern "C" int swb_f64_colmajor_to_f64_rowmajor(const double* src, int64_t n, int64_t m, double* dst, int64_t ld,
+                                                void* stream) {
+  if (!src || !dst || n < 0 || m < 0 || ld < m) return SWB_INVALID_PARAM;
+  if (n == 0 || m == 0) return SWB_OK;
+  dim3 tb(32, 8), tg(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>((m + 31) / 32));
+  if (tg.y > 65535) return SWB_INVALID_PARAM;
+  f64cm_to_f64rm_kernel<<<tg, tb, 0, swb_stream(stream)>>>(src, n, m, dst, ld);
+  SWB_CHECK_LAUNCH();
+  return SWB_OK;
+}
+
+namespace {
 // inverse: row-major f64 device basis (n x ld, first m columns, optional
 // column map) -> f32 column-major block (m x n rows of n floats)
 __global__ void f64rm_to_f32cm_kernel(const double* __restrict__ src, int64_t n, int64_t ld, int64_t m,

@@ -473,8 +473,18 @@ def upload_basis(vectors, m: int | None = None):
         m = mm
     ldv = round_up(max(m, 1), 8)
     V = torch.zeros((n, ldv), dtype=torch.float64, device="cuda")
-    if vec.flags.f_contiguous:
-        # column-major on the host == row-major (m x N): upload, then transpose on device
+    if vec.flags.f_contiguous and vec.dtype in (np.float32, np.float64):
+        # column-major on the host (the reference layout, f32 memmap or f64):
+        # streamed in column blocks through pinned memory, transposed on the
+        # device (staging.py) -- no second host copy of the basis
+        from .staging import upload_columns
+        cm = vec.T          # (mm, n) C-contiguous view: row j = column j
+
+        def fetch(c0, c1, out):
+            np.copyto(out.reshape(c1 - c0, n), cm[c0:c1])
+
+        upload_columns(V, ldv, n, m, vec.dtype, fetch)
+    elif vec.flags.f_contiguous:
         dev = torch.from_numpy(np.ascontiguousarray(vec[:, :m].T)).to("cuda")
         V[:, :m].copy_(dev.t().to(torch.float64))
     else:

@@ -59,49 +59,74 @@ def _read_exact(fh, count, what):
 
 
 def load_pack(path, connectivity=None, weight_mode="abs", image=None) -> DevicePack:
-    """fastrw.py:264-325 -> a GPU-resident pack (row-major f64 basis)."""
+    """fastrw.py:264-325 -> a GPU-resident pack (row-major f64 basis).
+
+    One pass over the file: the header, eigenvalues and d_sqrt are read and
+    hashed, then the f32 column-major eigenvector block streams through two
+    pinned staging buffers into the device basis (transposed on the GPU,
+    staging.upload_columns) while the same staged bytes feed the XXH64; the
+    checksum is compared at the end (ChecksumMismatch, nothing returned).
+    The host never holds the whole block (the reference streams 64-column
+    blocks from a memmap, fastrw.py:310-314)."""
+    from .staging import upload_columns
     try:
-        fh = open(path, "rb")
+        fh = open(path, "rb", buffering=0)
     except OSError as exc:
         raise IoError(str(exc)) from exc
+    lib = _lib.load()
+    hs = C.create_string_buffer(lib.swb_xxh64_state_bytes())
+    lib.swb_xxh64_init(hs, 0)
+
+    def read(count, what):
+        data = _read_exact(fh, count, what)
+        lib.swb_xxh64_update(hs, data, len(data))
+        return data
+
     with fh:
-        if _read_exact(fh, 4, "magic") != MAGIC:
+        if read(4, "magic") != MAGIC:
             raise FormatError(f"{path}: not a pack file (bad magic)")
-        version = struct.unpack("<I", _read_exact(fh, 4, "version"))[0]
+        version = struct.unpack("<I", read(4, "version"))[0]
         if version != VERSION:
             raise FormatError(f"{path}: unsupported pack version {version}")
-        d = struct.unpack("<B", _read_exact(fh, 1, "rank"))[0]
+        d = struct.unpack("<B", read(1, "rank"))[0]
         if d not in (1, 2, 3):
             raise FormatError(f"{path}: bad dimensionality {d}")
-        dims = np.frombuffer(_read_exact(fh, 8 * d, "dims"), dtype="<u8")
-        spacing = np.frombuffer(_read_exact(fh, 8 * d, "spacing"), dtype="<f8")
-        beta = struct.unpack("<d", _read_exact(fh, 8, "beta"))[0]
-        m = struct.unpack("<I", _read_exact(fh, 4, "m"))[0]
-        n = struct.unpack("<Q", _read_exact(fh, 8, "N"))[0]
+        dims = np.frombuffer(read(8 * d, "dims"), dtype="<u8")
+        spacing = np.frombuffer(read(8 * d, "spacing"), dtype="<f8")
+        beta = struct.unpack("<d", read(8, "beta"))[0]
+        m = struct.unpack("<I", read(4, "m"))[0]
+        n = struct.unpack("<Q", read(8, "N"))[0]
         if int(np.prod(dims)) != n:
             raise FormatError(f"{path}: dims/N mismatch")
-        values = np.frombuffer(_read_exact(fh, 8 * m, "eigenvalues"), dtype="<f8").astype(np.float64)
-        d_sqrt = np.frombuffer(_read_exact(fh, 4 * n, "d_sqrt"), dtype="<f4").astype(np.float64)
-        q_offset = fh.tell()
-        q_bytes = 4 * n * m
-        fh.seek(0, 2)
-        size = fh.tell()
-        expected = q_offset + q_bytes + 8 + 32
+        q_offset = fh.tell() + 8 * m + 4 * n
+        size = os.fstat(fh.fileno()).st_size
+        expected = q_offset + 4 * n * m + 8 + 32
         if size != expected:
             raise FormatError(f"{path}: size {size} != expected {expected} bytes")
-        fh.seek(0)
-        digest = xxh64_file(fh, q_offset + q_bytes)
+        values = np.frombuffer(read(8 * m, "eigenvalues"), dtype="<f8").astype(np.float64)
+        d_sqrt = np.frombuffer(read(4 * n, "d_sqrt"), dtype="<f4").astype(np.float64)
+        torch = require_cuda()
+        ldv = round_up(max(m, 1), 8)
+        V = torch.zeros((int(n), ldv), dtype=torch.float64, device="cuda")
+
+        def fetch(c0, c1, out):
+            mv = memoryview(out).cast("B")
+            got = 0
+            while got < mv.nbytes:
+                k = fh.readinto(mv[got:])
+                if not k:
+                    raise FormatError("pack file truncated while reading eigenvectors")
+                got += k
+
+        def hash_block(out):
+            lib.swb_xxh64_update(hs, out.ctypes.data_as(C.c_void_p), out.nbytes)
+
+        upload_columns(V, ldv, int(n), int(m), np.float32, fetch, on_block=hash_block)
+        digest = int(lib.swb_xxh64_digest(hs))
         stored = struct.unpack("<Q", _read_exact(fh, 8, "checksum"))[0]
         if digest != stored:
             raise ChecksumMismatch(f"{path}: checksum mismatch")
         image_hash = _read_exact(fh, 32, "image hash")
-    torch = require_cuda()
-    vec = np.memmap(path, dtype="<f4", mode="r", offset=q_offset, shape=(int(m), int(n)))  # row j = column j
-    stage = torch.from_numpy(np.array(vec)).to("cuda")
-    ldv = round_up(max(m, 1), 8)
-    V = torch.zeros((int(n), ldv), dtype=torch.float64, device="cuda")
-    _lib.call("swb_f32_colmajor_to_f64_rowmajor", ptr(stage), int(n), int(m), ptr(V), ldv, stream_handle())
-    del stage
     dims_t = tuple(int(x) for x in dims)
     dsq = torch.from_numpy(d_sqrt).to("cuda")
     img_dev = None
@@ -114,8 +139,14 @@ def load_pack(path, connectivity=None, weight_mode="abs", image=None) -> DeviceP
 
 
 def save_pack(pack, path) -> None:
-    """fastrw.py:228-254 from a GPU pack; byte-identical to the reference."""
-    torch = require_cuda()
+    """fastrw.py:228-254 from a GPU pack; byte-identical to the reference.
+
+    The f32 column-major payload streams device -> pinned host blocks
+    (staging.download_columns_f32, the refreshed pack's column order folded
+    into the transpose) straight into the file and the XXH64, so the host
+    holds one staging block, not the payload."""
+    from .staging import download_columns_f32
+    require_cuda()
     dims = tuple(int(x) for x in pack.dims)
     d = len(dims)
     m = int(pack.m)
@@ -125,21 +156,23 @@ def save_pack(pack, path) -> None:
                        np.asarray(pack.spacing if pack.spacing else (1.0,) * d, dtype="<f8").tobytes(),
                        struct.pack("<d", float(pack.beta)), struct.pack("<I", m), struct.pack("<Q", n)])
     values = np.asarray(pack.values, dtype="<f8").tobytes()
-    d_sqrt = np.asarray(pack.d_sqrt).astype("<f4").tobytes()
-    out = torch.empty((m, n), dtype=torch.float32, device="cuda")
-    _lib.call("swb_f64_rowmajor_to_f32_colmajor", ptr(pack.V), n, pack.ldv, m, ptr(pack.col_map), ptr(out),
-              stream_handle())
-    q = out.cpu().numpy().astype("<f4").tobytes()
+    d_sqrt = np.asarray(pack.d_sqrt).astype("<f4", copy=False).tobytes()
     lib = _lib.load()
     st = C.create_string_buffer(lib.swb_xxh64_state_bytes())
     lib.swb_xxh64_init(st, 0)
-    for chunk in (header, values, d_sqrt, q):
-        lib.swb_xxh64_update(st, chunk, len(chunk))
-    checksum = struct.pack("<Q", int(lib.swb_xxh64_digest(st)))
     ihash = pack.provenance.image_hash if pack.provenance is not None else b"\0" * 32
     try:
         with open(path, "wb") as fh:
-            for chunk in (header, values, d_sqrt, q, checksum, ihash):
+            for chunk in (header, values, d_sqrt):
+                lib.swb_xxh64_update(st, chunk, len(chunk))
                 fh.write(chunk)
+
+            def sink(block):
+                lib.swb_xxh64_update(st, block.ctypes.data_as(C.c_void_p), block.nbytes)
+                fh.write(memoryview(block).cast("B"))
+
+            download_columns_f32(pack.V, pack.ldv, n, m, pack.col_map, sink)
+            fh.write(struct.pack("<Q", int(lib.swb_xxh64_digest(st))))
+            fh.write(ihash)
     except OSError as exc:
         raise IoError(str(exc)) from exc
