@@ -566,7 +566,13 @@ def run_sharded(args):
     n = int(np.prod(w.dims))
     lattice = LatticeSpec.make(w.dims, p["connectivity"], p["weight_mode"])
     plan = SlabPlan.make(w.dims, world, rank)
-    comm = DistComm()
+    # SWB_COMM=c: the collectives through the library's own NCCL entry points
+    # (swb_comm_*, the C-host path) instead of torch.distributed
+    if os.environ.get("SWB_COMM", "") == "c":
+        from paper_1607_04174_b200.sharded import CComm
+        comm = CComm(rank, world)
+    else:
+        comm = DistComm()
     be = CudaBackend()
     V = W.orthonormal_basis_slab(plan, m, W.CFG_INDEX[cfg] * 1000 + 17, comm)
     lam = torch.from_numpy(W.synthetic_lambda(cfg, m)).cuda()

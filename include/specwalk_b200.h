@@ -43,6 +43,7 @@ extern "C" {
 #define SWB_DEGENERATE_GRAPH 4       /* errors.DegenerateGraph       */
 #define SWB_CUDA_ERROR 5             /* device / launch failure      */
 #define SWB_WORKSPACE_TOO_SMALL 6    /* caller workspace too small   */
+#define SWB_COMM_ERROR 7             /* NCCL failure / unavailable    */
 
 /* Lattice description.  connectivity: 4 (2-D, reference), 8 (2-D,
  * BASELINE config-2 extension) or 6 (3-D, reference); nz == 1 in 2-D.
@@ -407,6 +408,32 @@ int swb_sumsq(const double* v, int64_t n, double* out, void* workspace,
 /* dst[r, j] = src[r, col_map[j]] for j < m (column gather / permutation). */
 int swb_gather_columns(const double* src, int64_t lds, int64_t rows, const int32_t* col_map,
                        int64_t m, double* dst, int64_t ldd, void* stream);
+
+/* ---- NCCL communicator for the z-slab sharded path ----
+ * One process per GPU.  Rank 0 makes a unique id, the host ships the 128
+ * bytes to every rank (any channel), each rank calls swb_comm_init with its
+ * device current.  NCCL is dlopen'ed on first use (the library links none);
+ * failures return SWB_COMM_ERROR, text in swb_comm_last_error(). */
+#define SWB_COMM_ID_BYTES 128
+typedef struct swb_comm swb_comm;
+const char* swb_comm_last_error(void);
+int swb_comm_nccl_version(int* version);
+int swb_comm_unique_id(uint8_t* id_out);
+int swb_comm_init(const uint8_t* id, int nranks, int rank, swb_comm** out);
+int swb_comm_destroy(swb_comm* comm);
+int swb_comm_rank(const swb_comm* comm, int* rank, int* nranks);
+/* recv = sum over ranks of send (count f64; in place when send == recv):
+ * the update's (P, quad, norm2, V^T d, |d|^2) and the solve's (q_s, b_qn,
+ * ...) partials.  Stream-ordered. */
+int swb_comm_allreduce_f64(swb_comm* comm, const double* send, double* recv, int64_t count, void* stream);
+/* One-plane halo exchange of a z-slab shard of V (row-major, ldv): the
+ * buffer holds [lower halo plane if has_lo] [own_rows owned rows] [upper
+ * halo plane if has_hi], a plane = unit_rows = nx*ny rows.  Sends the first
+ * owned plane to rank-1 and the last to rank+1, receives the neighbours'
+ * planes into the halos (one NCCL group).  Stream-ordered: run the interior
+ * stencil on another stream to overlap it. */
+int swb_comm_halo_exchange(swb_comm* comm, double* V, int64_t ldv, int64_t unit_rows, int64_t own_rows,
+                           int has_lo, int has_hi, void* stream);
 
 #ifdef __cplusplus
 }

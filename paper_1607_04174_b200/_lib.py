@@ -34,6 +34,14 @@ SIGNATURES = {
     "swb_status_string": (C.c_char_p, [C.c_int]),
     "swb_last_cuda_error": (C.c_char_p, []),
     "swb_launch_count": (C.c_ulonglong, []),
+    "swb_comm_last_error": (C.c_char_p, []),
+    "swb_comm_nccl_version": (C.c_int, [C.POINTER(C.c_int)]),
+    "swb_comm_unique_id": (C.c_int, [c_vp]),
+    "swb_comm_init": (C.c_int, [c_vp, C.c_int, C.c_int, C.POINTER(c_vp)]),
+    "swb_comm_destroy": (C.c_int, [c_vp]),
+    "swb_comm_rank": (C.c_int, [c_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "swb_comm_allreduce_f64": (C.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "swb_comm_halo_exchange": (C.c_int, [c_vp, c_vp, c_i64, c_i64, c_i64, C.c_int, C.c_int, c_vp]),
     "swb_num_directions": (C.c_int, [C.POINTER(Lattice)]),
     "swb_graph_build": (C.c_int, [C.POINTER(Lattice), c_vp, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "swb_stencil_workspace_bytes": (c_sz, [C.POINTER(Lattice), c_i64]),
@@ -161,6 +169,8 @@ def check(status: int, what: str = "") -> None:
     msg = f"{what}: {name}" if what else name
     if status == 5:
         msg += f" ({lib.swb_last_cuda_error().decode()})"
+    elif status == 7:
+        msg += f" ({lib.swb_comm_last_error().decode()})"
     raise errors.from_status(status, msg)
 
 

@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT = PKG / "libspecwalk_b200.so"
-SOURCES = ["abi.cu", "dgemm.cu", "graph_stencil.cu", "coeffs.cu", "lu.cu", "solve.cu", "select.cu", "pack_io.cu", "priors.cu", "precompute.cu", "aggregation.cu", "pipeline.cu", "ozaki.cu"]
+SOURCES = ["abi.cu", "dgemm.cu", "graph_stencil.cu", "coeffs.cu", "lu.cu", "solve.cu", "select.cu", "pack_io.cu", "priors.cu", "precompute.cu", "aggregation.cu", "pipeline.cu", "ozaki.cu", "comm.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -60,7 +60,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if failed:
         raise RuntimeError("nvcc compilation failed")
     tmp = OUT.with_suffix(".so.tmp")
-    subprocess.run([nvcc, *ARCH, "-shared", "-cudart=static", "-o", str(tmp), *map(str, objs)], check=True)
+    subprocess.run([nvcc, *ARCH, "-shared", "-cudart=static", "-o", str(tmp), *map(str, objs), "-ldl"], check=True)
     os.replace(tmp, OUT)
     return OUT
 

@@ -34,6 +34,7 @@ extern "C" const char* swb_status_string(int status) {
     case SWB_DEGENERATE_GRAPH: return "DegenerateGraph";
     case SWB_CUDA_ERROR: return "CudaError";
     case SWB_WORKSPACE_TOO_SMALL: return "WorkspaceTooSmall";
+    case SWB_COMM_ERROR: return "CommError";
     default: return "unknown";
   }
 }

@@ -168,6 +168,69 @@ class DistComm:
             req.wait()
 
 
+class CComm:
+    """The same collectives through this library's own NCCL entry points
+    (swb_comm_*, csrc/comm.cu) -- the path a C host takes.  One shard per
+    process; the communicator's unique id is made by rank 0 and shipped to
+    the other ranks over ``bootstrap`` (a torch.distributed group of any
+    backend, e.g. gloo), or passed in as ``unique_id`` (128 bytes)."""
+
+    def __init__(self, rank: int, world: int, unique_id: bytes | None = None, bootstrap=None):
+        import torch
+        self.torch = torch
+        lib = _lib.load()
+        if unique_id is None:
+            buf = (C.c_uint8 * 128)()
+            if rank == 0:
+                _lib.check(lib.swb_comm_unique_id(buf), "swb_comm_unique_id")
+            if world > 1:
+                import torch.distributed as dist
+                obj = [bytes(buf)]
+                dist.broadcast_object_list(obj, src=0, group=bootstrap)
+                buf = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+            unique_id = bytes(buf)
+        self._id = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        self.handle = C.c_void_p()
+        _lib.check(lib.swb_comm_init(self._id, world, rank, C.byref(self.handle)), "swb_comm_init")
+        self.rank, self.world = rank, world
+        self.stream = torch.cuda.Stream()
+
+    def close(self) -> None:
+        if self.handle:
+            _lib.load().swb_comm_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def allreduce_sum(self, tensors: list) -> None:
+        st = stream_handle()
+        for t in tensors:
+            _lib.call("swb_comm_allreduce_f64", self.handle, ptr(t), ptr(t), t.numel(), st)
+
+    def _halo(self, s, st) -> None:
+        p = s.plan
+        own_rows = p.own_end - p.own_begin
+        _lib.call("swb_comm_halo_exchange", self.handle, ptr(s.V), s.V.stride(0), p.unit, own_rows,
+                  int(bool(p.halo_lo)), int(bool(p.halo_hi)), st)
+
+    def halo_exchange(self, shards: list) -> None:
+        (s,) = shards
+        self._halo(s, stream_handle())
+
+    def halo_start(self, shards: list):
+        """Post the Send/Recv on the comm stream (after the current stream's
+        work on V); the interior stencil runs meanwhile."""
+        (s,) = shards
+        cur = self.torch.cuda.current_stream()
+        self.stream.wait_stream(cur)
+        self._halo(s, C.c_void_p(self.stream.cuda_stream))
+        ev = self.torch.cuda.Event()
+        ev.record(self.stream)
+        return ev
+
+    def halo_finish(self, handle) -> None:
+        if handle is not None:
+            self.torch.cuda.current_stream().wait_event(handle)
+
+
 # ---------------------------------------------------------------------------
 # local numerics on the GPU
 # ---------------------------------------------------------------------------

@@ -88,3 +88,24 @@ def test_c2_cut_mask_matches_oracle_block_cut():
         want = lat.edge_mask_to_voxel_mask(O.block_cut_mask(dims, 5, 3, size=8, connectivity=conn))
         got = W.block_cut_voxel_mask(dims, conn, 5, 3, size=8)
         assert np.array_equal(got, want)
+
+
+def test_comm_entry_points_without_device():
+    """swb_comm_* (csrc/comm.cu): NCCL is dlopen'ed on first use; version and
+    unique-id need no GPU; bad arguments are InvalidParam before any NCCL call."""
+    lib = _lib.load()
+    v = ctypes.c_int()
+    rc = lib.swb_comm_nccl_version(ctypes.byref(v))
+    if rc == 7:
+        pytest.skip(f"NCCL not loadable here: {lib.swb_comm_last_error().decode()}")
+    assert rc == 0 and v.value >= 21800
+    buf = (ctypes.c_uint8 * 128)()
+    assert lib.swb_comm_unique_id(buf) == 0 and any(bytes(buf))
+    h = ctypes.c_void_p()
+    assert lib.swb_comm_init(buf, 0, 0, ctypes.byref(h)) == 1
+    assert lib.swb_comm_init(buf, 2, 2, ctypes.byref(h)) == 1
+    assert lib.swb_comm_init(None, 1, 0, ctypes.byref(h)) == 1
+    assert lib.swb_comm_allreduce_f64(None, None, None, 4, None) == 1
+    assert lib.swb_comm_halo_exchange(None, None, 8, 4, 4, 0, 0, None) == 1
+    assert lib.swb_comm_destroy(None) == 0
+    assert lib.swb_status_string(7).decode() == "CommError"

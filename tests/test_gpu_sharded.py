@@ -51,3 +51,44 @@ def test_sharded_matches_single_gpu(cuda_ok, world, dims, conn, mode):
     labels = torch.cat([o[0] for o in out]).cpu().numpy()
     gap = O.top2_gap(ref.values)
     assert not ((labels != swb.hard_labels(ref).labels) & (gap > 1e-9)).any()
+
+
+@pytest.mark.parametrize("dims,conn,mode", [((12, 10, 16), 6, "sq"), ((24, 32), 8, "sq")])
+def test_sharded_through_c_comm_matches_local(cuda_ok, dims, conn, mode):
+    """The sharded update + solve with the collectives through the library's
+    own NCCL entry points (swb_comm_*: unique id, init, all-reduce, halo
+    Send/Recv) -- one rank (one GPU is what the sandbox has) -- equals the
+    in-process LocalComm run bit for bit."""
+    import torch
+    from paper_1607_04174_b200.sharded import (CComm, CudaBackend, LocalComm, make_shards_from_global,
+                                                sharded_solve, sharded_update)
+    rng = np.random.default_rng(7)
+    n = int(np.prod(dims))
+    img = np.clip(0.5 + 0.3 * (rng.random(n) < 0.3) + rng.normal(0, 0.05, n), 0, 1)
+    lap0 = O.build_laplacian(img, dims, 10.0, mode, conn)
+    vals, vecs = np.linalg.eigh(lap0.matrix.toarray())
+    m = 24
+    image = swb.Image(dims, img)
+    pack = swb.SpectralPack(dims=dims, spacing=(), beta=10.0,
+                            eigen=swb.EigenBasis(np.asfortranarray(vecs[:, :m]), vals[:m]),
+                            d_sqrt=lap0.d_sqrt, provenance=swb.PackProvenance(image.content_hash()))
+    dp = swb.to_device(pack, image=image, connectivity=conn, weight_mode=mode)
+    seeds = np.sort(rng.choice(n, 12, replace=False))
+    labs = np.arange(12) % 2
+    outs = []
+    for comm in (LocalComm(), CComm(0, 1)):
+        shards = make_shards_from_global(dp.V, dp.values_dev, None, dp.lattice, dp.image_dev, 10.0, 1)
+        be = CudaBackend()
+        sharded_update(shards, comm, be, 14.0)
+        out = sharded_solve(shards, comm, be, seeds, labs, 2, want_u=True)
+        torch.cuda.synchronize()
+        outs.append((shards[0].own()[:, :m].cpu().numpy(), out[0][2].cpu().numpy(), out[0][0].cpu().numpy()))
+        if isinstance(comm, CComm):
+            buf = torch.arange(10, dtype=torch.float64, device="cuda")
+            comm.allreduce_sum([buf])
+            assert buf.cpu().numpy().tolist() == list(range(10))
+            comm.close()
+    (va, ua, la), (vb, ub, lb) = outs
+    np.testing.assert_array_equal(va, vb)
+    np.testing.assert_array_equal(ua, ub)
+    np.testing.assert_array_equal(la, lb)
