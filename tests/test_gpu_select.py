@@ -130,3 +130,38 @@ def test_seed_fit_known_answers(cuda_ok):
     assert f_free[0, 0] < 1e-12
     f_tight = _seed_fit_gpu(q, [0, 1], [0, 1], [1.0, 1.0], 2, [1], 1.0)
     assert abs(f_tight[0, 0] - (1 - 1e-3) ** 2) < 1e-3 * (1 - 1e-3) ** 2
+
+
+@pytest.mark.parametrize("n,m,s,k,bound_scale,dup", [(5000, 150, 400, 2, 1e-2, False), (4000, 60, 200, 3, 1.0, True),
+                                                     (4000, 60, 200, 2, 1e-2, True), (3000, 64, 64, 2, 1e-2, False)])
+def test_seed_fit_both_paths_match_oracle(cuda_ok, n, m, s, k, bound_scale, dup):
+    """select.cu has two paths per scheduled m: the bidiagonal ridge (square,
+    well-conditioned R_m: sigma_min > 1e-6 sigma_0) and the Jacobi SVD
+    (ill-conditioned or S < m).  A basis column that nearly duplicates its
+    neighbour (difference 1e-9) makes every R_m past it ill-conditioned
+    (sigma_min ~ 1e-9 sigma_0: kept by the reference's 1e-13 cutoff, but
+    below the fast path's gate), so those steps take the Jacobi path while
+    the earlier ones take the bidiagonal one; a small bound makes the ridge
+    (adaptive.py:96-110) bind.  (An exactly duplicated column is not a
+    well-posed comparison: the reference's left singular vector of the zero
+    singular value, and so its perp, is whatever LAPACK's gesdd picks.)"""
+    rng = np.random.default_rng(n + m + s + int(dup))
+    V = np.linalg.qr(rng.standard_normal((n, m)))[0]
+    if dup:
+        V[:, m // 2] = V[:, m // 2 - 1] + 1e-9 * V[:, m // 2]
+    d_sqrt = 1.0 + rng.random(n)
+    seeds = np.sort(rng.choice(n, s, replace=False))
+    labs = rng.integers(0, k, s)
+    pack = _pack(V, np.linspace(0, 0.1, m), d_sqrt * bound_scale, (n, 1))
+    prob = swb.LabelProblem(num_labels=k, seeds=swb.SeedPartition(n, seeds, labs))
+    pol = swb.AdaptivePolicy(epsilon=1e-12)
+    m_use, info = swb.select_m(pack, prob, pol)
+    sched = pol.schedule(m, k)
+    bound = float(np.sqrt(np.sum((d_sqrt * bound_scale) ** 2)))
+    u = np.zeros((s, k))
+    u[np.arange(s), labs] = 1.0
+    u *= (d_sqrt * bound_scale)[seeds, None]
+    want = np.array([[O.seed_fit(V[seeds, :mm], u[:, c], bound) for c in range(k)] for mm in sched])
+    got = np.array([st["f"] for st in info["steps"]])
+    assert got.shape == want.shape
+    np.testing.assert_allclose(got, want, rtol=1e-8, atol=1e-10 * max(1.0, np.abs(want).max()))
