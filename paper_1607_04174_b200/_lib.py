@@ -8,11 +8,14 @@ calls raise instead of computing anything on the CPU.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from . import errors
 
-_LIB_PATH = Path(__file__).resolve().parent / "libspecwalk_b200.so"
+# SWB_LIB: load another build of the library (A/B measurement of compile-time
+# variants, tools/build_variant.py); default the in-tree build
+_LIB_PATH = Path(os.environ.get("SWB_LIB") or Path(__file__).resolve().parent / "libspecwalk_b200.so")
 
 c_i64 = C.c_int64
 c_i32 = C.c_int32

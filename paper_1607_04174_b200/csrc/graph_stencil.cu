@@ -152,7 +152,13 @@ __device__ __forceinline__ void cp_async8_s(uint32_t s, const void* gmem, bool p
 }
 
 constexpr int ST_WARPS = 8;
-constexpr int ST_CTAS_PER_SM = 2;
+#ifndef SWB_ST_CTAS
+#define SWB_ST_CTAS 2
+#endif
+#ifndef SWB_ST_PREF
+#define SWB_ST_PREF 5
+#endif
+constexpr int ST_CTAS_PER_SM = SWB_ST_CTAS;
 // rows per barrier step: two independent rows per step halve the barriers and
 // give each warp two dependency chains to interleave
 #ifndef SWB_ST_ROWS
@@ -245,7 +251,7 @@ struct Ring5 {
   static constexpr int V_DBL = NS * 64;
   static constexpr int C_DBL = (NL * LCD + 1) / 2 * 2;
   static constexpr int STAGE_DBL = V_DBL + C_DBL;
-  static constexpr int PREF = 5;
+  static constexpr int PREF = SWB_ST_PREF;
   static constexpr int RING = PREF + ST_ROWS + 1;   // rows x-1 .. x+PREF+ST_ROWS-1 live at once
   // slot of extended line (zi, yi), zi in [-1, ZB], yi in [-1, YB]; -1 = unused corner
   __host__ __device__ static constexpr int slot(int zi, int yi) {
