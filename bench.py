@@ -45,7 +45,9 @@ CPU_SLAB_PLANES_ALL = 32     # the all-cores cpu_baseline sample (BASELINE.md §
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: 6 at c4; small configs run enough steps for ~1.5 s of timed "
+                         "region, so the clock sampler sees the load)")
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c4")
@@ -703,6 +705,15 @@ def run_gpu(args):
     for i in range(args.warmup):
         gpu_step(state, i)
     torch.cuda.synchronize()
+    if args.steps is None:
+        # default K: 6 at c4 (a ~0.25 s step); smaller configs time enough
+        # steps for ~1.5 s so the nvidia-smi sampler sees the loaded clock
+        t0 = time.perf_counter()
+        for i in range(2):
+            gpu_step(state, args.warmup + i)
+        torch.cuda.synchronize()
+        per = (time.perf_counter() - t0) / 2
+        args.steps = int(min(2000, max(6, round(1.5 / max(per, 1e-6)))))
 
     def barrier():
         if world > 1:
@@ -927,6 +938,9 @@ def run_gpu(args):
 
 def main():
     args = parse_args()
+    if args.steps is None and (args.impl == "reference" or int(os.environ.get("WORLD_SIZE", "1")) > 1
+                               or args.sharded):
+        args.steps = 6
     if args.impl == "reference":
         run_reference(args)
     elif int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.sharded:
