@@ -563,7 +563,9 @@ extern "C" int swb_oz_split_rows(const double* A, int64_t lda, int64_t nr, int64
   if (nr == 0) return SWB_OK;
   const OzPtrs q = oz_ptrs(o, workspace, buf);
   const int64_t nrp = (nr + OZ_BM - 1) / OZ_BM * OZ_BM;
-  oz_slice_rows_kernel<<<static_cast<unsigned>(nrp / OZ_SLICE_ROWS), OZ_SLICE_WARPS * 32, OZ_SLICE_SMEM,
+  // staging for this K only (2 nkc 16-column halves), not the K <= 512 maximum
+  const size_t split_smem = size_t(2 * o.nkc) * OZ_S * OZ_SLICE_ROWS * 16;
+  oz_slice_rows_kernel<<<static_cast<unsigned>(nrp / OZ_SLICE_ROWS), OZ_SLICE_WARPS * 32, split_smem,
                          swb_stream(stream)>>>(A, lda, nr, K, o.nkc, q.a_sl, q.sa);
   SWB_CHECK_LAUNCH();
   return SWB_OK;
