@@ -202,6 +202,16 @@ int swb_seed_project(const double* V, int64_t ldv, int64_t row_base, int64_t own
                      const double* d_sqrt, double dnorm, int64_t L, double* q_s,
                      int64_t ldq, double* b_qn, double* bg, double* lsu, double* dsq_s,
                      void* stream);
+/* dgecon of A = I - Ut Vt^T (n x n; Ut, Vt n x r, ld ldr) from the LU of
+ * K = I_r - Vt^T Ut (swb_lu_factor: K, pivots pk) via the Woodbury identity;
+ * anorm = ||A||_1 (device).  The seed systems use it when r << n. */
+size_t swb_gecon_wb_workspace_bytes(int64_t n, int64_t r);
+int swb_gecon_wb(int64_t n, int64_t r, const double* Ut, const double* Vt, int64_t ldr, const double* K, int64_t ldk,
+                 const int32_t* pk, const double* anorm, double* rcond_out, void* workspace, size_t workspace_bytes,
+                 void* stream);
+/* *out = ||A||_1 (device double; workspace n + 1 doubles) */
+int swb_norm1(const double* A, int64_t n, int64_t lda, double* out, void* workspace, size_t workspace_bytes,
+              void* stream);
 /* *flag_out (device double) = 1.0 when seed_idx is not strictly ascending
  * or not in [0, n), or a label is not in [0, L); else 0.0 (stream-ordered). */
 int swb_check_seeds(const int64_t* seed_idx, const int32_t* seed_lab, int64_t S, int64_t n, int64_t L,

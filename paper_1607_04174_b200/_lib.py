@@ -98,6 +98,9 @@ SIGNATURES = {
     "swb_seed_project": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_i64,
                                    c_vp, c_vp, c_i64, c_vp, c_dbl, c_i64, c_vp, c_i64, c_vp, c_vp,
                                    c_vp, c_vp, c_vp]),
+    "swb_gecon_wb_workspace_bytes": (c_sz, [c_i64, c_i64]),
+    "swb_gecon_wb": (C.c_int, [c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "swb_norm1": (C.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_sz, c_vp]),
     "swb_check_seeds": (C.c_int, [c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),
     "swb_small_solve_workspace_bytes": (c_sz, [c_i64, c_i64, c_i64]),
     "swb_small_solve": (C.c_int, [c_dbl, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,

@@ -391,7 +391,71 @@ __device__ int block_idamax(const double* x, int64_t n, ArgMax* sh) {
   return block_argmax(a, sh).i;
 }
 
-// dgecon (norm '1') with dlacn2; x, xs = 2n doubles + isgn n ints of scratch.
+// LAPACK dlacn2 (Higham's 1-norm estimator of ||A^-1||_1, the heart of
+// dgecon), kase loop unrolled into straight-line code.  inv() / inv_t()
+// overwrite x (n) with A^-1 x / A^-T x; the whole CTA calls them.
+template <class Inv, class InvT>
+__device__ double dlacn2_est(int64_t n, double* __restrict__ x, int32_t* __restrict__ isgn, Inv inv, InvT inv_t,
+                             double* red, ArgMax* sh, int* flag) {
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x[i] = 1.0 / double(n);
+  __syncthreads();
+  inv();
+  double est;
+  if (n == 1) return fabs(x[0]);
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += fabs(x[i]);
+  est = block_sum(s, red);
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const bool pos = x[i] >= 0.0;
+    x[i] = pos ? 1.0 : -1.0;
+    isgn[i] = pos ? 1 : -1;
+  }
+  __syncthreads();
+  inv_t();
+  int j = block_idamax(x, n, sh);
+  int iter = 2;
+  while (true) {
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x[i] = (i == j) ? 1.0 : 0.0;
+    __syncthreads();
+    inv();
+    const double estold = est;
+    s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += fabs(x[i]);
+    est = block_sum(s, red);
+    if (threadIdx.x == 0) *flag = 0;
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+      if ((x[i] >= 0.0 ? 1 : -1) != isgn[i]) *flag = 1;
+    __syncthreads();
+    const bool changed = *flag != 0;
+    __syncthreads();
+    if (!changed || est <= estold) break;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const bool pos = x[i] >= 0.0;
+      x[i] = pos ? 1.0 : -1.0;
+      isgn[i] = pos ? 1 : -1;
+    }
+    __syncthreads();
+    inv_t();
+    const int jlast = j;
+    j = block_idamax(x, n, sh);
+    if (x[jlast] != fabs(x[j]) && iter < 5) { ++iter; continue; }
+    break;
+  }
+  // the alternative estimate (dlacn2's final step)
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double sgn = (i & 1) ? -1.0 : 1.0;
+    x[i] = sgn * (1.0 + double(i) / double(n - 1));
+  }
+  __syncthreads();
+  inv();
+  s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += fabs(x[i]);
+  const double temp = 2.0 * (block_sum(s, red) / double(3 * n));
+  return temp > est ? temp : est;
+}
+
+// dgecon (norm '1'): rcond = 1 / (anorm * est) on the LU factors of A.
 __global__ void __launch_bounds__(1024)
 gecon_kernel(const double* __restrict__ LU, int64_t n, int64_t lda, const double* __restrict__ anorm_p,
              double* __restrict__ x, int32_t* __restrict__ isgn, double* __restrict__ rcond_out) {
@@ -408,73 +472,85 @@ gecon_kernel(const double* __restrict__ LU, int64_t n, int64_t lda, const double
     if (LU[i * lda + i] == 0.0) flag = 1;
   __syncthreads();
   if (flag) { if (threadIdx.x == 0) *rcond_out = 0.0; return; }
+  // ||A^-1||_1 == ||U^-1 L^-1||_1: the row permutation does not change column sums
+  auto inv = [&]() { tri_solve(LU, n, lda, x, 1, 1, 0); tri_solve(LU, n, lda, x, 1, 1, 1); };
+  auto inv_t = [&]() { tri_solve(LU, n, lda, x, 1, 1, 2); tri_solve(LU, n, lda, x, 1, 1, 3); };
+  const double est = dlacn2_est(n, x, isgn, inv, inv_t, red, sh, &flag);
+  if (threadIdx.x == 0) *rcond_out = est != 0.0 ? (1.0 / est) / anorm : 0.0;
+}
 
-  auto apply_inv = [&]() { tri_solve(LU, n, lda, x, 1, 1, 0); tri_solve(LU, n, lda, x, 1, 1, 1); };
-  auto apply_inv_t = [&]() { tri_solve(LU, n, lda, x, 1, 1, 2); tri_solve(LU, n, lda, x, 1, 1, 3); };
-
-  // dlacn2, kase loop unrolled into straight-line code
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x[i] = 1.0 / double(n);
+// dgecon of A = I - Ut Vt^T (n x n, Ut / Vt n x r row-major, ld ldr) through
+// the Woodbury identity, with K = I_r - Vt^T Ut factored (LU, pivots pk):
+//   A^-1 x  = x + Ut K^-1 (Vt^T x),   A^-T x = x + Vt K^-T (Ut^T x).
+// The estimator sees the same A^-1 / A^-T products as dgecon on A itself.
+__global__ void __launch_bounds__(1024)
+gecon_wb_kernel(int64_t n, int64_t r, const double* __restrict__ Ut, const double* __restrict__ Vt, int64_t ldr,
+                const double* __restrict__ K, int64_t ldk, const int32_t* __restrict__ pk,
+                const double* __restrict__ anorm_p, double* __restrict__ x, double* __restrict__ t,
+                int32_t* __restrict__ isgn, double* __restrict__ rcond_out) {
+  __shared__ double red[32];
+  __shared__ ArgMax sh[32];
+  __shared__ int flag;
+  const double anorm = *anorm_p;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (n == 0) { if (threadIdx.x == 0) *rcond_out = 1.0; return; }
+  if (!(anorm > 0.0)) { if (threadIdx.x == 0) *rcond_out = (anorm == 0.0) ? 0.0 : anorm; return; }
+  if (threadIdx.x == 0) flag = 0;
   __syncthreads();
-  apply_inv();
-  double est;
-  if (n == 1) {
-    est = fabs(x[0]);
-  } else {
-    double s = 0.0;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += fabs(x[i]);
-    est = block_sum(s, red);
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-      const bool pos = x[i] >= 0.0;
-      x[i] = pos ? 1.0 : -1.0;
-      isgn[i] = pos ? 1 : -1;
+  for (int64_t i = threadIdx.x; i < r; i += blockDim.x)
+    if (K[i * ldk + i] == 0.0) flag = 1;           // K singular <=> A singular
+  __syncthreads();
+  if (flag) { if (threadIdx.x == 0) *rcond_out = 0.0; return; }
+  // t = X^T x (X n x r), column by thread
+  auto proj = [&](const double* X) {
+    for (int64_t j = threadIdx.x; j < r; j += blockDim.x) {
+      double a = 0.0;
+      for (int64_t i = 0; i < n; ++i) a = fma(X[i * ldr + j], x[i], a);
+      t[j] = a;
     }
     __syncthreads();
-    apply_inv_t();
-    int j = block_idamax(x, n, sh);
-    int iter = 2;
-    bool alt = false;
-    while (true) {
-      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x[i] = (i == j) ? 1.0 : 0.0;
-      __syncthreads();
-      apply_inv();
-      const double estold = est;
-      s = 0.0;
-      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += fabs(x[i]);
-      est = block_sum(s, red);
-      if (threadIdx.x == 0) flag = 0;
-      __syncthreads();
-      for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
-        if ((x[i] >= 0.0 ? 1 : -1) != isgn[i]) flag = 1;
-      __syncthreads();
-      const bool changed = flag != 0;
-      __syncthreads();
-      if (!changed || est <= estold) { alt = true; break; }
-      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const bool pos = x[i] >= 0.0;
-        x[i] = pos ? 1.0 : -1.0;
-        isgn[i] = pos ? 1 : -1;
-      }
-      __syncthreads();
-      apply_inv_t();
-      const int jlast = j;
-      j = block_idamax(x, n, sh);
-      if (x[jlast] != fabs(x[j]) && iter < 5) { ++iter; continue; }
-      alt = true;
-      break;
+  };
+  // x += X t, row by warp
+  auto add = [&](const double* X) {
+    for (int64_t i = warp; i < n; i += nw) {
+      double a = 0.0;
+      for (int64_t j = lane; j < r; j += 32) a = fma(X[i * ldr + j], t[j], a);
+      a = warp_sum(a);
+      if (lane == 0) x[i] += a;
     }
-    if (alt) {
-      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const double sgn = (i & 1) ? -1.0 : 1.0;
-        x[i] = sgn * (1.0 + double(i) / double(n - 1));
+    __syncthreads();
+  };
+  auto perm = [&](bool forward) {          // t <- P t (getrs order) or P^T t
+    if (threadIdx.x == 0) {
+      if (forward) {
+        for (int64_t j = 0; j < r; ++j) {
+          const int64_t p = pk[j];
+          if (p != j) { const double v = t[j]; t[j] = t[p]; t[p] = v; }
+        }
+      } else {
+        for (int64_t j = r - 1; j >= 0; --j) {
+          const int64_t p = pk[j];
+          if (p != j) { const double v = t[j]; t[j] = t[p]; t[p] = v; }
+        }
       }
-      __syncthreads();
-      apply_inv();
-      s = 0.0;
-      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += fabs(x[i]);
-      const double temp = 2.0 * (block_sum(s, red) / double(3 * n));
-      if (temp > est) est = temp;
     }
-  }
+    __syncthreads();
+  };
+  auto inv = [&]() {                        // x <- A^-1 x
+    proj(Vt);
+    perm(true);
+    tri_solve(K, r, ldk, t, 1, 1, 0);
+    tri_solve(K, r, ldk, t, 1, 1, 1);
+    add(Ut);
+  };
+  auto inv_t = [&]() {                      // x <- A^-T x
+    proj(Ut);
+    tri_solve(K, r, ldk, t, 1, 1, 2);
+    tri_solve(K, r, ldk, t, 1, 1, 3);
+    perm(false);
+    add(Vt);
+  };
+  const double est = dlacn2_est(n, x, isgn, inv, inv_t, red, sh, &flag);
   if (threadIdx.x == 0) *rcond_out = est != 0.0 ? (1.0 / est) / anorm : 0.0;
 }
 
@@ -583,5 +659,40 @@ extern "C" int swb_lu_solve(const double* LU, int64_t n, int64_t lda, const int3
 extern "C" int swb_check_rcond(double rcond) {
   // fastrw.py:340: not finite or < 1e-14 -> SingularSmallSystem
   if (!(rcond == rcond) || rcond == __builtin_inf() || rcond < 1e-14) return SWB_SINGULAR_SMALL_SYSTEM;
+  return SWB_OK;
+}
+
+extern "C" size_t swb_gecon_wb_workspace_bytes(int64_t n, int64_t r) {
+  return swb_align_up(sizeof(double) * size_t(n + 1), 256) + swb_align_up(sizeof(double) * size_t(r + 1), 256) +
+         swb_align_up(sizeof(int32_t) * size_t(n + 1), 256);
+}
+
+extern "C" int swb_gecon_wb(int64_t n, int64_t r, const double* Ut, const double* Vt, int64_t ldr, const double* K,
+                            int64_t ldk, const int32_t* pk, const double* anorm, double* rcond_out, void* ws,
+                            size_t ws_bytes, void* stream) {
+  if (n < 0 || r <= 0 || !Ut || !Vt || !K || !pk || !anorm || !rcond_out || ldr < r || ldk < r) return SWB_INVALID_PARAM;
+  if (!ws || ws_bytes < swb_gecon_wb_workspace_bytes(n, r)) return SWB_WORKSPACE_TOO_SMALL;
+  char* base = static_cast<char*>(ws);
+  double* x = reinterpret_cast<double*>(base);
+  double* t = reinterpret_cast<double*>(base + swb_align_up(sizeof(double) * size_t(n + 1), 256));
+  int32_t* isgn = reinterpret_cast<int32_t*>(base + swb_align_up(sizeof(double) * size_t(n + 1), 256) +
+                                             swb_align_up(sizeof(double) * size_t(r + 1), 256));
+  gecon_wb_kernel<<<1, 1024, 0, swb_stream(stream)>>>(n, r, Ut, Vt, ldr, K, ldk, pk, anorm, x, t, isgn, rcond_out);
+  SWB_CHECK_LAUNCH();
+  return SWB_OK;
+}
+
+extern "C" int swb_norm1(const double* A, int64_t n, int64_t lda, double* out, void* ws, size_t ws_bytes,
+                         void* stream) {
+  // ||A||_1 (max column sum of |A|, NaN-propagating like np.linalg.norm)
+  if (n < 0 || !out || (n > 0 && (!A || lda < n))) return SWB_INVALID_PARAM;
+  if (!ws || ws_bytes < sizeof(double) * size_t(n + 1)) return SWB_WORKSPACE_TOO_SMALL;
+  cudaStream_t st = swb_stream(stream);
+  if (n == 0) { SWB_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double), st)); return SWB_OK; }
+  double* cs = static_cast<double*>(ws);
+  colabs_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(A, n, lda, cs);
+  SWB_CHECK_LAUNCH();
+  max_kernel<<<1, 1024, 0, st>>>(cs, n, out);
+  SWB_CHECK_LAUNCH();
   return SWB_OK;
 }

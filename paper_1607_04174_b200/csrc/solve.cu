@@ -4,6 +4,8 @@
 //            LU + rcond + solve, coefficients coeff (m x L)
 //   pass 2   reconstruction V*coeff (+ g c), finalize (solver.py:55-66) and
 //            hard labels (images.py:128-130) fused in one HBM-bound kernel
+#include <cstdlib>
+
 #include "swb_common.cuh"
 #include "dmma_core.cuh"
 
@@ -642,6 +644,10 @@ namespace {
 struct SmallLayout {
   int64_t n, lda, ldr, ldm, lds;
   size_t off_A, off_rhs, off_bw, off_qt, off_piv, off_anorm, off_lu, off_tn, off_proj, off_w, off_rs, total;
+  // Woodbury path (A = I - Ut Vt^T of rank r << n): Ut, Vt (n x ldw), K (r x ldk), its pivots / LU / solve
+  // scratch, t (r x ldr), the TN GEMM scratch, gecon scratch
+  int64_t r, ldw, ldk;
+  size_t off_ut, off_vt, off_k, off_pk, off_luk, off_t, off_rsk, off_tnw, off_gw, off_nrm;
 };
 
 SmallLayout small_layout(int64_t S, int64_t m, int64_t L, int gamma_zero) {
@@ -664,8 +670,57 @@ SmallLayout small_layout(int64_t S, int64_t m, int64_t L, int gamma_zero) {
   Ly.off_w = take(sizeof(double) * size_t(2 * m + S + 1));
   Ly.off_rs = take(swb_lu_solve_workspace_bytes(Ly.n, L));
   Ly.off_tn = take(S > 0 ? swb_gemm_tn_workspace_bytes(S, m, L) : 0);
+  Ly.r = gamma_zero ? m + 2 : m;
+  Ly.ldw = (Ly.r + 1) / 2 * 2;
+  Ly.ldk = (Ly.r + 7) / 8 * 8;
+  Ly.off_ut = take(sizeof(double) * size_t(Ly.n) * Ly.ldw);
+  Ly.off_vt = take(sizeof(double) * size_t(Ly.n) * Ly.ldw);
+  Ly.off_k = take(sizeof(double) * size_t(Ly.r) * Ly.ldk);
+  Ly.off_pk = take(sizeof(int32_t) * size_t(Ly.r + 1));
+  Ly.off_luk = take(swb_lu_workspace_bytes(Ly.r));
+  Ly.off_t = take(sizeof(double) * size_t(Ly.r) * Ly.ldr);
+  Ly.off_rsk = take(swb_lu_solve_workspace_bytes(Ly.r, L));
+  Ly.off_tnw = take(std::max(swb_gemm_tn_workspace_bytes(Ly.n, Ly.r, Ly.r), swb_gemm_tn_workspace_bytes(Ly.n, Ly.r, L)));
+  Ly.off_gw = take(swb_gecon_wb_workspace_bytes(Ly.n, Ly.r));
+  Ly.off_nrm = take(sizeof(double) * size_t(Ly.n + 1));
   Ly.total = o;
   return Ly;
+}
+
+// Woodbury factors of the seed system (fastrw.py:430-450): A = I - Ut Vt^T.
+// gamma > 0: Ut = (b_qn w), Vt = q_s (r = m).  gamma = 0, bordered
+// (S+1) x (S+1) (r = m + 2): the border column -bg and corner alpha = g_s.g_s
+// join the low-rank part as two extra columns,
+//   Ut = [[b_qn w, bg, 0], [(gq w)^T, 0, 1]],  Vt = [[q_s, 0, 0], [0, 1, 1 - alpha]],
+// so I - Ut Vt^T reproduces A[:S,:S] = I - (b_qn w) q_s^T, A[:S,S] = -bg,
+// A[S,:S] = -(gq w)^T q_s^T and A[S,S] = alpha exactly.
+__global__ void wb_factors_kernel(int64_t S, int64_t m, int g0, const double* __restrict__ Bw, int64_t ldm,
+                                  const double* __restrict__ q_s, int64_t ldq, const double* __restrict__ bg,
+                                  const double* __restrict__ w, const double* __restrict__ gq,
+                                  const double* __restrict__ A, int64_t lda, double* __restrict__ Ut,
+                                  double* __restrict__ Vt, int64_t ldw) {
+  const int64_t n = g0 ? S + 1 : S, r = g0 ? m + 2 : m;
+  const double alpha = g0 ? A[S * lda + S] : 0.0;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n * r; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / r, j = e % r;
+    double u, v;
+    if (i < S) {
+      u = j < m ? Bw[i * ldm + j] : (j == m ? bg[i] : 0.0);
+      v = j < m ? q_s[i * ldq + j] : 0.0;
+    } else {
+      u = j < m ? gq[j] * w[j] : (j == m ? 0.0 : 1.0);
+      v = j < m ? 0.0 : (j == m ? 1.0 : 1.0 - alpha);
+    }
+    Ut[i * ldw + j] = u;
+    Vt[i * ldw + j] = v;
+  }
+}
+
+__global__ void eye_minus_kernel(double* __restrict__ K, int64_t ldk, int64_t r) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < r * r; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / r, j = e % r;
+    K[i * ldk + j] = (i == j ? 1.0 : 0.0) - K[i * ldk + j];
+  }
 }
 }  // namespace
 
@@ -754,11 +809,42 @@ extern "C" int swb_small_solve_ex(double gamma, int64_t S, int64_t m, int64_t L,
     rc = swb_gemm_nn_alpha(Bw, Ly.ldm, t_p, ldt, S, m, L, rhs, Ly.ldr, 1, gamma, st);  // + gamma (Bw) t_p
     if (rc) return rc;
   }
-  rc = swb_lu_factor(A, Ly.n, Ly.lda, piv, anorm, luws, swb_lu_workspace_bytes(Ly.n), stream);
-  if (rc) return rc;
-  rc = swb_lu_solve(A, Ly.n, Ly.lda, piv, rhs, L, Ly.ldr, base + Ly.off_rs, swb_lu_solve_workspace_bytes(Ly.n, L),
-                    stream);
-  if (rc) return rc;
+  // A = I - Ut Vt^T has rank-r structure (r = m or m + 2): when r is well
+  // below n, factor the r x r K = I - Vt^T Ut instead of A (Woodbury):
+  // f = rhs + Ut K^-1 (Vt^T rhs), rcond of A from the same identity
+  // (SWB_WOODBURY=0: always the LU of A)
+  static const bool wb_env = [] { const char* e = getenv("SWB_WOODBURY"); return !(e && e[0] == '0'); }();
+  const bool wood = wb_env && Ly.n >= Ly.r + 64;
+  double* Ut = reinterpret_cast<double*>(base + Ly.off_ut);
+  double* Vt = reinterpret_cast<double*>(base + Ly.off_vt);
+  double* Kf = reinterpret_cast<double*>(base + Ly.off_k);
+  int32_t* pk = reinterpret_cast<int32_t*>(base + Ly.off_pk);
+  if (wood) {
+    wb_factors_kernel<<<grid, 256, 0, st>>>(S, m, g0, Bw, Ly.ldm, q_s, ldq, bg, w, gq, A, Ly.lda, Ut, Vt, Ly.ldw);
+    SWB_CHECK_LAUNCH();
+    void* tnw = base + Ly.off_tnw;
+    const size_t tnw_bytes = std::max(swb_gemm_tn_workspace_bytes(Ly.n, Ly.r, Ly.r),
+                                      swb_gemm_tn_workspace_bytes(Ly.n, Ly.r, L));
+    if ((rc = swb_gemm_tn(Vt, Ly.ldw, Ut, Ly.ldw, Ly.n, Ly.r, Ly.r, 0, Kf, Ly.ldk, tnw, tnw_bytes, stream))) return rc;
+    eye_minus_kernel<<<grid, 256, 0, st>>>(Kf, Ly.ldk, Ly.r);
+    SWB_CHECK_LAUNCH();
+    if ((rc = swb_norm1(A, Ly.n, Ly.lda, anorm, base + Ly.off_nrm, sizeof(double) * size_t(Ly.n + 1), stream)))
+      return rc;
+    if ((rc = swb_lu_factor(Kf, Ly.r, Ly.ldk, pk, nullptr, base + Ly.off_luk, swb_lu_workspace_bytes(Ly.r), stream)))
+      return rc;
+    double* tb = reinterpret_cast<double*>(base + Ly.off_t);
+    if ((rc = swb_gemm_tn(Vt, Ly.ldw, rhs, Ly.ldr, Ly.n, Ly.r, L, 0, tb, Ly.ldr, tnw, tnw_bytes, stream))) return rc;
+    if ((rc = swb_lu_solve(Kf, Ly.r, Ly.ldk, pk, tb, L, Ly.ldr, base + Ly.off_rsk,
+                           swb_lu_solve_workspace_bytes(Ly.r, L), stream)))
+      return rc;
+    if ((rc = swb_gemm_nn_alpha(Ut, Ly.ldw, tb, Ly.ldr, Ly.n, Ly.r, L, rhs, Ly.ldr, 1, 1.0, st))) return rc;
+  } else {
+    rc = swb_lu_factor(A, Ly.n, Ly.lda, piv, anorm, luws, swb_lu_workspace_bytes(Ly.n), stream);
+    if (rc) return rc;
+    rc = swb_lu_solve(A, Ly.n, Ly.lda, piv, rhs, L, Ly.ldr, base + Ly.off_rs, swb_lu_solve_workspace_bytes(Ly.n, L),
+                      stream);
+    if (rc) return rc;
+  }
   // proj = q_s^T f_s (m x L), reduction over the S seed rows
   rc = swb_gemm_tn(q_s, ldq, rhs, Ly.ldr, S, m, L, 0, proj, Ly.ldr, tnws, swb_gemm_tn_workspace_bytes(S, m, L), stream);
   if (rc) return rc;
@@ -774,9 +860,12 @@ extern "C" int swb_small_solve_ex(double gamma, int64_t S, int64_t m, int64_t L,
     // workspace or reading rcond_out
     SWB_CUDA_TRY(cudaEventRecord(reinterpret_cast<cudaEvent_t>(rcond_event), st));
     SWB_CUDA_TRY(cudaStreamWaitEvent(swb_stream(rcond_stream), reinterpret_cast<cudaEvent_t>(rcond_event), 0));
-    return swb_lu_rcond(A, Ly.n, Ly.lda, piv, anorm, rcond_out, luws, swb_lu_workspace_bytes(Ly.n), rcond_stream);
   }
-  return swb_lu_rcond(A, Ly.n, Ly.lda, piv, anorm, rcond_out, luws, swb_lu_workspace_bytes(Ly.n), stream);
+  void* rs_stream = (rcond_stream && rcond_event) ? rcond_stream : stream;
+  if (wood)
+    return swb_gecon_wb(Ly.n, Ly.r, Ut, Vt, Ly.ldw, Kf, Ly.ldk, pk, anorm, rcond_out, base + Ly.off_gw,
+                        swb_gecon_wb_workspace_bytes(Ly.n, Ly.r), rs_stream);
+  return swb_lu_rcond(A, Ly.n, Ly.lda, piv, anorm, rcond_out, luws, swb_lu_workspace_bytes(Ly.n), rs_stream);
 }
 
 extern "C" int swb_reconstruct_label(const double* V, int64_t ldv, int64_t row_base, int64_t r_begin, int64_t r_end,

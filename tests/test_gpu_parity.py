@@ -476,3 +476,68 @@ def test_single_voxel_graph_is_degenerate(cuda_ok):
     lat = swb.LatticeSpec.make((1, 1))
     with pytest.raises(swb.DegenerateGraph):
         swb.DeviceGraph.build(torch.tensor([0.5], dtype=torch.float64, device="cuda"), lat, 1.0)
+
+
+@pytest.mark.parametrize("dims,conn,m,S,gamma", [((40, 36), 4, 30, 200, 0.0), ((40, 36), 4, 30, 200, 0.7),
+                                                 ((14, 12, 10), 6, 60, 300, 0.0), ((48, 40), 8, 20, 600, 0.0)])
+def test_woodbury_seed_system_matches_lapack(cuda_ok, dims, conn, m, S, gamma):
+    """With many more seeds than basis columns the seed system A = I - Ut Vt^T
+    (rank m, or m + 2 with the gamma = 0 border) is solved through the r x r
+    K = I - Vt^T Ut (Woodbury) and its rcond estimated from the same identity:
+    fields match the oracle's LU solve, rcond LAPACK dgecon on the full A."""
+    rng = np.random.default_rng(S + m)
+    n = int(np.prod(dims))
+    img = np.clip(0.5 + 0.3 * (rng.random(n) < 0.25) + rng.normal(0, 0.05, n), 0, 1)
+    lap = O.build_laplacian(img, dims, 20.0, "abs", conn)
+    vals, vecs = np.linalg.eigh(lap.matrix.toarray())
+    V, lam = vecs[:, :m], vals[:m]
+    k = 3
+    seeds = np.sort(rng.choice(n, S, replace=False))
+    labs = rng.integers(0, k, S)
+    pri = None
+    if gamma > 0:
+        pri = rng.random((n, k))
+        pri /= pri.sum(axis=1, keepdims=True)
+    pack = swb.SpectralPack(dims=dims, spacing=(), beta=20.0, eigen=swb.EigenBasis(np.asfortranarray(V), lam),
+                            d_sqrt=lap.d_sqrt, provenance=swb.PackProvenance(b""))
+    prob = swb.LabelProblem(num_labels=k, seeds=swb.SeedPartition(n, seeds, labs), priors=pri, gamma=gamma)
+    f = swb.solve_fast(pack, lap, prob, want_field=True)
+    u_ref, parts = O.solve_fast(V, lam, lap.d_sqrt, lap.matrix, seeds, labs, k, gamma=gamma, priors=pri,
+                                return_parts=True)
+    np.testing.assert_allclose(f.values, u_ref, rtol=0, atol=1e-10)
+    assert_labels_match(swb.hard_labels(f).labels, u_ref)
+    np.testing.assert_allclose(f.rcond_dev.item(), parts["rcond"], rtol=1e-6)
+
+
+def test_woodbury_singular_seed_system(cuda_ok):
+    """A rank-deficient basis (duplicated columns) makes the seed system
+    singular; through the Woodbury path it raises SingularSmallSystem exactly
+    when the oracle's LU / dgecon does."""
+    dims = (40, 36)
+    rng = np.random.default_rng(3)
+    n = int(np.prod(dims))
+    img = np.clip(0.5 + 0.3 * (rng.random(n) < 0.25) + rng.normal(0, 0.05, n), 0, 1)
+    lap = O.build_laplacian(img, dims, 20.0, "abs", 4)
+    vals, vecs = np.linalg.eigh(lap.matrix.toarray())
+    m = 12
+    V = vecs[:, :m].copy()
+    V[:, 3] = V[:, 2]
+    V[:, 4] = V[:, 2]
+    lam = np.full(m, 1e-3)
+    seeds = np.sort(rng.choice(n, 150, replace=False))
+    labs = np.arange(150) % 2
+    pack = swb.SpectralPack(dims=dims, spacing=(), beta=20.0, eigen=swb.EigenBasis(np.asfortranarray(V), lam),
+                            d_sqrt=lap.d_sqrt, provenance=swb.PackProvenance(b""))
+    prob = _prob(seeds, labs, n=n)
+    try:
+        O.solve_fast(V, lam, lap.d_sqrt, lap.matrix, seeds, labs, 2)
+        expect = None
+    except O.OracleError as exc:
+        expect = exc.kind
+    if expect == "SingularSmallSystem":
+        with pytest.raises(swb.SingularSmallSystem):
+            swb.solve_fast(pack, lap, prob)
+    else:
+        f = swb.solve_fast(pack, lap, prob, want_field=True)
+        np.testing.assert_allclose(f.values, O.solve_fast(V, lam, lap.d_sqrt, lap.matrix, seeds, labs, 2),
+                                   rtol=0, atol=1e-9)
