@@ -152,6 +152,11 @@ __device__ __forceinline__ void cp_async8_s(uint32_t s, const void* gmem, bool p
 }
 
 constexpr int ST_WARPS = 8;
+// SWB_ST_EXACT=1 (default): L^'v in the reference's CSR order with separate
+// multiply / add (refresh eigenvalues track scipy to ~1e-16); 0: FMAs
+#ifndef SWB_ST_EXACT
+#define SWB_ST_EXACT 1
+#endif
 #ifndef SWB_ST_CTAS
 #define SWB_ST_CTAS 2
 #endif
@@ -166,6 +171,15 @@ constexpr int ST_CTAS_PER_SM = SWB_ST_CTAS;
 #endif
 constexpr int ST_ROWS = SWB_ST_ROWS;
 static_assert(ST_ROWS == 1 || ST_ROWS == 2, "one or two rows per step");
+// x-lines per warp: 1 = a warp covers one line x 64 columns; 2 = each half-warp
+// one line x 32 columns (32-column blocks: K = 400 wastes 16 of 416 columns
+// instead of 48 of 448, and the CTA's 16 lines share a smaller halo)
+#ifndef SWB_ST_LPW
+#define SWB_ST_LPW 2
+#endif
+constexpr int ST_LPW = SWB_ST_LPW;
+static_assert(ST_LPW == 1 || ST_LPW == 2, "one or two lines per warp");
+constexpr int ST_CBW = 64 / ST_LPW;   // columns per line (column block width)
 
 // Compile-time neighbour tables, sorted by flat offset (the reference CSR
 // column order): kind 0 = diagonal, 1 = forward edge `dir` of this voxel,
@@ -224,8 +238,10 @@ __global__ void pair_coeffs_kernel(const double* __restrict__ wn, const double* 
 
 // ---------------------------------------------------------------------------
 // Stencil pass v5: CTA-shared ring.  A CTA's 8 warps own a block of
-// ZB x YB x-lines (3-D: 4 z x 2 y; 2-D: 8 y) of one 64-column block; warp w
-// takes line (zi, yi) = (w / YB, w % YB).  Each ring stage holds, for voxel
+// ZB x YB x-lines (3-D: 4 z x 2*LPW y; 2-D: 8*LPW y) of one CBW-column block;
+// warp w takes the LPW lines (zi, yi) = (w / (YB/LPW), (w % (YB/LPW))*LPW + h),
+// h = lane / (CBW/2) -- a warp's lines are y-adjacent, so with the linear slot
+// grid below half-warp h's operands sit h slots past half-warp 0's.  Each ring stage holds, for voxel
 // row x, every V line the block needs exactly once -- the 8 centre lines plus
 // the one-line halo around the block (no corners) -- together with each
 // centre line's coefficients (forward + diag, and the forward coefficients
@@ -239,16 +255,22 @@ template <int CONN, bool DELTA>
 struct Ring5 {
   static constexpr bool D3 = CONN == 6;
   static constexpr int ND = nb_ndir(CONN);
+  static constexpr int LPW = ST_LPW, CBW = ST_CBW, HL = CBW / 2;     // lines per warp, columns, lanes per line
   static constexpr int ZB = D3 ? 4 : 1;
-  static constexpr int YB = D3 ? 2 : 8;
-  static constexpr int NL = ZB * YB;                                   // centre lines (= warps)
-  // extended grid (ZB+2) x (YB+2) without corners (3-D); 2-D: 1 x (YB+2)
-  static constexpr int NS = D3 ? NL + 2 * ZB + 2 * YB : YB + 2;        // V line slots
+  static constexpr int YB = D3 ? 2 * LPW : 8 * LPW;
+  static constexpr int WY = YB / LPW;                                  // warps along y
+  static constexpr int NL = ZB * YB;                                   // centre lines (= warps x LPW)
+  // extended grid (ZB+2) x (YB+2) without corners (3-D); 2-D: 1 x (YB+2).
+  // LPW = 1: compact slots; LPW = 2: the full linear grid (4 corner slots
+  // never filled) so that slot(z, y + 1) = slot(z, y) + 1 everywhere
+  static constexpr bool LIN = LPW > 1;
+  static constexpr int NSU = D3 ? NL + 2 * ZB + 2 * YB : YB + 2;       // V line slots in use
+  static constexpr int NS = D3 && LIN ? (ZB + 2) * (YB + 2) : NSU;     // V line slots
   static constexpr int CW = DELTA ? 2 : 1;
   static constexpr int NCL = D3 ? 3 : 2;                               // coefficient rows per line
   static constexpr int COEF = (ND + 1) + ND * (NCL - 1);
   static constexpr int LCD = (COEF * CW + 1 + 1) / 2 * 2;              // doubles per line (+ d_sqrt), 16-B aligned
-  static constexpr int V_DBL = NS * 64;
+  static constexpr int V_DBL = NS * CBW;
   static constexpr int C_DBL = (NL * LCD + 1) / 2 * 2;
   static constexpr int STAGE_DBL = V_DBL + C_DBL;
   static constexpr int PREF = SWB_ST_PREF;
@@ -256,12 +278,28 @@ struct Ring5 {
   // slot of extended line (zi, yi), zi in [-1, ZB], yi in [-1, YB]; -1 = unused corner
   __host__ __device__ static constexpr int slot(int zi, int yi) {
     return !D3 ? (yi + 1)
+           : LIN ? (zi + 1) * (YB + 2) + (yi + 1)
                  : (zi >= 0 && zi < ZB && yi >= 0 && yi < YB) ? zi * YB + yi
                  : (zi >= 0 && zi < ZB && yi == -1) ? NL + zi
                  : (zi >= 0 && zi < ZB && yi == YB) ? NL + ZB + zi
                  : (yi >= 0 && yi < YB && zi == -1) ? NL + 2 * ZB + yi
                  : (yi >= 0 && yi < YB && zi == ZB) ? NL + 2 * ZB + YB + yi
                  : -1;
+  }
+  // slot of the u-th line in use (copy order) -> extended (zi, yi)
+  __host__ __device__ static void used_line(int u, int& ez, int& ey) {
+    if (!D3) { ez = 0; ey = u - 1; return; }
+    if (LIN) {
+      const int s = u < YB ? u + 1 : u < YB + ZB * (YB + 2) ? u + 2 : u + 3;   // skip the corners
+      ez = s / (YB + 2) - 1;
+      ey = s % (YB + 2) - 1;
+      return;
+    }
+    if (u < NL) { ez = u / YB; ey = u % YB; }
+    else if (u < NL + ZB) { ez = u - NL; ey = -1; }
+    else if (u < NL + 2 * ZB) { ez = u - NL - ZB; ey = YB; }
+    else if (u < NL + 2 * ZB + YB) { ey = u - NL - 2 * ZB; ez = -1; }
+    else { ey = u - NL - 2 * ZB - YB; ez = ZB; }
   }
 };
 
@@ -283,18 +321,24 @@ struct RowWin {
   double2 prev, cur, f0;
 };
 
+// `lane` here is the thread's V offset inside its half-warp's line slot
+// (h * CBW + 2 * li doubles) and `coff` its coefficient offset (h * LCD).
 template <int CONN, bool DELTA, int WARP>
 __device__ __forceinline__ void row_compute(const double* sc, const double* sm1, const double* sp1, int lane,
-                                            bool active, double2& q, double2& s2, double2& sd, double* wrow,
-                                            const ApplyArgs& ap, const double* zrow, RowWin& win, bool first) {
+                                            int coff, bool active, double2& q, double2& s2, double2& sd,
+                                            double* wrow, const ApplyArgs& ap, const double* zrow, RowWin& win,
+                                            bool first) {
   using Rg = Ring5<CONN, DELTA>;
-  constexpr int ND = Rg::ND, CW = Rg::CW, LCD = Rg::LCD, NB = nb_count(CONN);
-  constexpr int ZI = WARP / Rg::YB, YI = WARP % Rg::YB;
-  constexpr int CBASE = Rg::V_DBL + WARP * LCD;
-  constexpr int OWN = Rg::slot(ZI, YI) * 64;
-  const double* scl = sc + 2 * lane;
-  const double* sml = sm1 + 2 * lane;
-  const double* spl = sp1 + 2 * lane;
+  constexpr int ND = Rg::ND, CW = Rg::CW, LCD = Rg::LCD, NB = nb_count(CONN), CBW = Rg::CBW;
+  constexpr int ZI = WARP / Rg::WY, YI = (WARP % Rg::WY) * Rg::LPW;   // half-warp 0's line
+  constexpr int CBASE = Rg::V_DBL + (ZI * Rg::YB + YI) * LCD;
+  constexpr int OWN = Rg::slot(ZI, YI) * CBW;
+  const double* scl = sc + lane;
+  const double* sml = sm1 + lane;
+  const double* spl = sp1 + lane;
+  sc += coff;
+  sm1 += coff;
+  sp1 += coff;
   if (first) {
     win.prev = make_double2(0.0, 0.0);
     win.cur = *reinterpret_cast<const double2*>(scl + OWN);
@@ -314,7 +358,7 @@ __device__ __forceinline__ void row_compute(const double* sc, const double* sm1,
       val = t.dx < 0 ? win.prev : t.dx > 0 ? nxt : c;
     } else {
       const double* vl = t.dx < 0 ? sml : t.dx > 0 ? spl : scl;
-      val = *reinterpret_cast<const double2*>(vl + Rg::slot(ZI + t.dz, YI + t.dy) * 64);
+      val = *reinterpret_cast<const double2*>(vl + Rg::slot(ZI + t.dz, YI + t.dy) * CBW);
     }
     const double* vs = t.dx < 0 ? sm1 : t.dx > 0 ? sp1 : sc;
     const int slot = t.kind == 0 ? ND : t.kind == 1 ? t.dir
@@ -336,12 +380,22 @@ __device__ __forceinline__ void row_compute(const double* sc, const double* sm1,
     }
     // L^' v in the reference CSR order (exact products and sums); dL v with FMAs
     if (t.kind == 0) {
+#if SWB_ST_EXACT
       lx = __dadd_rn(lx, __dmul_rn(cn, val.x));
       ly = __dadd_rn(ly, __dmul_rn(cn, val.y));
+#else
+      lx = fma(cn, val.x, lx);
+      ly = fma(cn, val.y, ly);
+#endif
       if (DELTA) { dx = fma(g, val.x, dx); dy = fma(g, val.y, dy); }
     } else {
+#if SWB_ST_EXACT
       lx = __dadd_rn(lx, __dmul_rn(-cn, val.x));
       ly = __dadd_rn(ly, __dmul_rn(-cn, val.y));
+#else
+      lx = fma(-cn, val.x, lx);
+      ly = fma(-cn, val.y, ly);
+#endif
       if (DELTA) { dx = fma(-g, val.x, dx); dy = fma(-g, val.y, dy); }
     }
   }
@@ -372,16 +426,18 @@ __device__ __forceinline__ void row_compute(const double* sc, const double* sm1,
 // warp-uniform binary dispatch to the compile-time line position
 template <int CONN, bool DELTA, int LO, int HI>
 __device__ __forceinline__ void row_dispatch(int warp, const double* sc, const double* sm1, const double* sp1, int lane,
-                                             bool active, double2& q, double2& s2, double2& sd, double* wrow,
+                                             int coff, bool active, double2& q, double2& s2, double2& sd, double* wrow,
                                              const ApplyArgs& ap, const double* zrow, RowWin& win, bool first) {
   if constexpr (HI - LO == 1) {
-    row_compute<CONN, DELTA, LO>(sc, sm1, sp1, lane, active, q, s2, sd, wrow, ap, zrow, win, first);
+    row_compute<CONN, DELTA, LO>(sc, sm1, sp1, lane, coff, active, q, s2, sd, wrow, ap, zrow, win, first);
   } else {
     constexpr int MID = (LO + HI) / 2;
     if (warp < MID)
-      row_dispatch<CONN, DELTA, LO, MID>(warp, sc, sm1, sp1, lane, active, q, s2, sd, wrow, ap, zrow, win, first);
+      row_dispatch<CONN, DELTA, LO, MID>(warp, sc, sm1, sp1, lane, coff, active, q, s2, sd, wrow, ap, zrow, win,
+                                         first);
     else
-      row_dispatch<CONN, DELTA, MID, HI>(warp, sc, sm1, sp1, lane, active, q, s2, sd, wrow, ap, zrow, win, first);
+      row_dispatch<CONN, DELTA, MID, HI>(warp, sc, sm1, sp1, lane, coff, active, q, s2, sd, wrow, ap, zrow, win,
+                                         first);
   }
 }
 
@@ -390,22 +446,41 @@ __device__ __forceinline__ void row_dispatch(int warp, const double* sc, const d
 // stages) past the end of an odd line
 template <int CONN, bool DELTA, int LO, int HI>
 __device__ __forceinline__ void row_dispatch2(int warp, const double* s0, const double* s1, const double* s2p,
-                                              const double* s3, int lane, bool active, bool active2, double2& q,
+                                              const double* s3, int lane, int coff, bool active, bool active2,
+                                              double2& q,
                                               double2& s2, double2& sd, double* wrow, int64_t ldw,
                                               const ApplyArgs& ap, const double* zrow, RowWin& win, bool first) {
   if constexpr (HI - LO == 1) {
-    row_compute<CONN, DELTA, LO>(s1, s0, s2p, lane, active, q, s2, sd, wrow, ap, zrow, win, first);
-    row_compute<CONN, DELTA, LO>(s2p, s1, s3, lane, active2, q, s2, sd, wrow ? wrow + ldw : wrow, ap,
+    row_compute<CONN, DELTA, LO>(s1, s0, s2p, lane, coff, active, q, s2, sd, wrow, ap, zrow, win, first);
+    row_compute<CONN, DELTA, LO>(s2p, s1, s3, lane, coff, active2, q, s2, sd, wrow ? wrow + ldw : wrow, ap,
                                  zrow ? zrow + ap.ldz : zrow,
                                  win, false);
   } else {
     constexpr int MID = (LO + HI) / 2;
     if (warp < MID)
-      row_dispatch2<CONN, DELTA, LO, MID>(warp, s0, s1, s2p, s3, lane, active, active2, q, s2, sd, wrow, ldw, ap,
-                                          zrow, win, first);
+      row_dispatch2<CONN, DELTA, LO, MID>(warp, s0, s1, s2p, s3, lane, coff, active, active2, q, s2, sd, wrow, ldw,
+                                          ap, zrow, win, first);
     else
-      row_dispatch2<CONN, DELTA, MID, HI>(warp, s0, s1, s2p, s3, lane, active, active2, q, s2, sd, wrow, ldw, ap,
-                                          zrow, win, first);
+      row_dispatch2<CONN, DELTA, MID, HI>(warp, s0, s1, s2p, s3, lane, coff, active, active2, q, s2, sd, wrow, ldw,
+                                          ap, zrow, win, first);
+  }
+}
+
+// add a warp's per-column partial sums into its slots (the LPW lines of a warp
+// cover the same columns: fold half-warp 1 into half-warp 0 first); warp-uniform
+template <int LPW, int HL>
+__device__ __forceinline__ void flush_slots(double* sl, int h, double2 q, double2 s2, double2 sd) {
+  if constexpr (LPW == 2) {
+    constexpr unsigned FULL = 0xffffffffu;
+    q.x += __shfl_down_sync(FULL, q.x, HL);
+    q.y += __shfl_down_sync(FULL, q.y, HL);
+    s2.x += __shfl_down_sync(FULL, s2.x, HL);
+    s2.y += __shfl_down_sync(FULL, s2.y, HL);
+    sd.x += __shfl_down_sync(FULL, sd.x, HL);
+    sd.y += __shfl_down_sync(FULL, sd.y, HL);
+  }
+  if (h == 0) {
+    sl[0] += q.x; sl[1] += s2.x; sl[2] += sd.x; sl[3] += q.y; sl[4] += s2.y; sl[5] += sd.y;
   }
 }
 
@@ -417,8 +492,8 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
                 double* __restrict__ slots, int64_t slot_ld, const ApplyArgs ap) {
   using Rg = Ring5<CONN, DELTA>;
   constexpr int ND = Rg::ND, CW = Rg::CW, RING = Rg::RING, PREF = Rg::PREF, SD = Rg::STAGE_DBL;
-  constexpr int ZB = Rg::ZB, YB = Rg::YB, NS = Rg::NS, NL = Rg::NL, LCD = Rg::LCD;
-  static_assert(NL == ST_WARPS, "one warp per centre line");
+  constexpr int ZB = Rg::ZB, YB = Rg::YB, NL = Rg::NL, LCD = Rg::LCD, CBW = Rg::CBW, HL = Rg::HL;
+  static_assert(NL == ST_WARPS * Rg::LPW, "LPW centre lines per warp");
   extern __shared__ __align__(16) double ring[];
   double* zst = ring + RING * SD;  // zero stage for x-1 < 0 / x+1 >= nx
   const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
@@ -426,7 +501,9 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
   for (int i = threadIdx.x; i < SD; i += blockDim.x) zst[i] = 0.0;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int zi = warp / YB, yi = warp % YB;
+  const int h = lane / HL, li = lane % HL;          // half-warp (line) and lane within it
+  const int zi = warp / Rg::WY, yi = (warp % Rg::WY) * Rg::LPW + h;
+  const int voff = h * CBW + 2 * li, coff = h * LCD;
   const int64_t gwarp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nx = g.lat.nx, ny = g.lat.ny, nz = g.lat.nz;
   const int64_t plane = nx * ny;
@@ -438,7 +515,7 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
   const int64_t n_items = int64_t(n_cb) * per_cb;
 
   // copy assignment of this thread (fixed per kernel): V chunks j = tid + i*256
-  constexpr int VCH = NS * 32;                       // 16-byte chunks per stage (32 per line)
+  constexpr int VCH = Rg::NSU * HL;                  // 16-byte chunks per stage (HL per line)
   constexpr int VPT = (VCH + ST_WARPS * 32 - 1) / (ST_WARPS * 32);
   constexpr int CSL = NL * (Rg::COEF + 1);           // coefficient / d_sqrt slots per stage
   __syncthreads();
@@ -457,13 +534,12 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
     const bool line_live = (Rg::D3 ? my_z < z_end : true) && my_y < y_end;
     if (cb != cur_cb) {
       if (cur_cb >= 0) {
-        double* sl = slots + gwarp * slot_ld * 3 + (int64_t(cur_cb) * 64 + 2 * lane) * 3;
-        sl[0] += q.x; sl[1] += s2.x; sl[2] += sd.x; sl[3] += q.y; sl[4] += s2.y; sl[5] += sd.y;
+        flush_slots<Rg::LPW, HL>(slots + gwarp * slot_ld * 3 + (int64_t(cur_cb) * CBW + 2 * li) * 3, h, q, s2, sd);
       }
       q = make_double2(0.0, 0.0); s2 = q; sd = q;
       cur_cb = cb;
     }
-    const int64_t col0 = int64_t(cb) * 64;
+    const int64_t col0 = int64_t(cb) * CBW;
     // per-thread copy sources for this item: V chunks
     const double* vsrc[VPT];
     int vdst[VPT];
@@ -473,22 +549,17 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
       const int j = threadIdx.x + i * ST_WARPS * 32;
       vok[i] = false; vsrc[i] = V; vdst[i] = 0;
       if (j < VCH) {
-        const int s = j >> 5, ch = j & 31;
-        // decode slot -> extended (zi, yi)
+        const int u = j / HL, ch = j % HL;
         int ez = 0, ey = 0;
-        if (!Rg::D3) { ey = s - 1; }
-        else if (s < NL) { ez = s / YB; ey = s % YB; }
-        else if (s < NL + ZB) { ez = s - NL; ey = -1; }
-        else if (s < NL + 2 * ZB) { ez = s - NL - ZB; ey = YB; }
-        else if (s < NL + 2 * ZB + YB) { ey = s - NL - 2 * ZB; ez = -1; }
-        else { ey = s - NL - 2 * ZB - YB; ez = ZB; }
+        Rg::used_line(u, ez, ey);
+        const int s = Rg::slot(ez, ey);
         const int64_t lz = z0 + ez, ly = y0 + ey;
         const int64_t col = col0 + 2 * ch;
         const bool ok = lz >= 0 && lz < nz && ly >= 0 && ly < ny && col < M &&
                         (Rg::D3 ? true : ly < ny);
         vok[i] = ok;
         vsrc[i] = ok ? V + ((lz * ny + ly) * nx - row_base) * ldv + col : V;
-        vdst[i] = s * 64 + 2 * ch;
+        vdst[i] = s * CBW + 2 * ch;
       }
     }
     // coefficient slot: line l = cs / (COEF+1), k = cs % (COEF+1) (k == COEF -> d_sqrt)
@@ -555,10 +626,10 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
 #pragma unroll
     for (int i = 0; i < PREF; ++i) prefetch();
 
-    const bool active = line_live && (col0 + 2 * lane < M);
+    const bool active = line_live && (col0 + 2 * li < M);
     const int64_t my_r0 = (my_z * ny + my_y) * nx;
-    double* wrow = (W && line_live) ? W + (my_r0 - w_row0) * ldw + col0 + 2 * lane : nullptr;
-    const double* zrow = (!DELTA && ap.Z && line_live) ? ap.Z + (my_r0 - w_row0) * ap.ldz + col0 + 2 * lane : nullptr;
+    double* wrow = (W && line_live) ? W + (my_r0 - w_row0) * ldw + col0 + 2 * li : nullptr;
+    const double* zrow = (!DELTA && ap.Z && line_live) ? ap.Z + (my_r0 - w_row0) * ap.ldz + col0 + 2 * li : nullptr;
     const double* sc = ring;
     RowWin win;
     if constexpr (ST_ROWS == 2) {
@@ -574,8 +645,8 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
         const double* s2s = x + 1 < nxi ? sp : zst;
         const double* s3s = x + 2 < nxi ? sp2 : zst;
         if (line_live) {
-          row_dispatch2<CONN, DELTA, 0, ST_WARPS>(warp, sm1, sc, s2s, s3s, lane, active, active && x + 1 < nxi, q, s2,
-                                                  sd, wrow, ldw, ap, zrow, win, x == 0);
+          row_dispatch2<CONN, DELTA, 0, ST_WARPS>(warp, sm1, sc, s2s, s3s, voff, coff, active, active && x + 1 < nxi, q,
+                                                  s2, sd, wrow, ldw, ap, zrow, win, x == 0);
           if (wrow) wrow += 2 * ldw;
           if (zrow) zrow += 2 * ap.ldz;
         }
@@ -593,7 +664,7 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
       if (line_live) {
         // the warp's line position is a compile-time constant in each
         // instantiation, so every shared operand is an immediate offset
-        row_dispatch<CONN, DELTA, 0, ST_WARPS>(warp, sc, sm1, sp1, lane, active, q, s2, sd, wrow, ap, zrow, win,
+        row_dispatch<CONN, DELTA, 0, ST_WARPS>(warp, sc, sm1, sp1, voff, coff, active, q, s2, sd, wrow, ap, zrow, win,
                                                x == 0);
         if (wrow) wrow += ldw;
         if (zrow) zrow += ap.ldz;
@@ -603,10 +674,8 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
     cp_async_wait<0>();
     __syncthreads();
   }
-  if (cur_cb >= 0) {
-    double* sl = slots + gwarp * slot_ld * 3 + (int64_t(cur_cb) * 64 + 2 * lane) * 3;
-    sl[0] += q.x; sl[1] += s2.x; sl[2] += sd.x; sl[3] += q.y; sl[4] += s2.y; sl[5] += sd.y;
-  }
+  if (cur_cb >= 0)
+    flush_slots<Rg::LPW, HL>(slots + gwarp * slot_ld * 3 + (int64_t(cur_cb) * CBW + 2 * li) * 3, h, q, s2, sd);
 }
 
 // out[col] = sum over warps (fixed order) of slots[w][col][k]
@@ -657,9 +726,9 @@ struct StencilWs {
 
 StencilWs stencil_ws_layout(const LatticeDev& L, int64_t M) {
   StencilWs w{};
-  const int64_t n_cb = (M + 63) / 64;
+  const int64_t n_cb = (M + ST_CBW - 1) / ST_CBW;
   const int64_t N = L.nx * L.ny * L.nz;
-  w.slots = swb_align_up(sizeof(double) * size_t(stencil_grid() * ST_WARPS) * size_t(n_cb * 64) * 3, 256);
+  w.slots = swb_align_up(sizeof(double) * size_t(stencil_grid() * ST_WARPS) * size_t(n_cb * ST_CBW) * 3, 256);
   w.zeros = swb_align_up(sizeof(double2) * size_t(L.nx * L.ndir + 1), 256);
   w.pairs = swb_align_up(sizeof(double2) * size_t(N * (L.ndir + 1)), 256);
   w.total = w.slots + w.zeros + w.pairs;
@@ -687,8 +756,8 @@ int run_stencil(const swb_lattice* lat, const double* V, int64_t ldv, int64_t ro
   if (W && (ldw & 1)) return SWB_INVALID_PARAM;
   const StencilWs lay = stencil_ws_layout(L, M);
   if (!ws || ws_bytes < lay.total) return SWB_WORKSPACE_TOO_SMALL;
-  const int n_cb = static_cast<int>((M + 63) / 64);
-  const int64_t slot_ld = int64_t(n_cb) * 64;
+  const int n_cb = static_cast<int>((M + ST_CBW - 1) / ST_CBW);
+  const int64_t slot_ld = int64_t(n_cb) * ST_CBW;
   const int64_t grid = stencil_grid();
   const int64_t n_warps = grid * ST_WARPS;
   char* base = static_cast<char*>(ws);
