@@ -522,11 +522,15 @@ stencil5_kernel(const StencilGeom g, const double* __restrict__ V, int64_t ldv, 
 
   double2 q = make_double2(0.0, 0.0), s2 = q, sd = q;
   int cur_cb = -1;
+  // static round-robin, y fastest (a global work counter with z-fastest
+  // bands raised the L2 hit rate 28% -> 53% but ran 11% slower, and made the
+  // per-warp Rayleigh partial sums run-to-run nondeterministic)
   for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
     const int cb = static_cast<int>(it / per_cb);
     const int64_t rem = it % per_cb;
-    const int64_t z0 = Rg::D3 ? blk_begin + (rem / n_yb) * ZB : 0;
-    const int64_t y0 = Rg::D3 ? (rem % n_yb) * YB : blk_begin + (rem % n_yb) * YB;
+    const int64_t zb = rem / n_yb, yb = rem % n_yb;
+    const int64_t z0 = Rg::D3 ? blk_begin + zb * ZB : 0;
+    const int64_t y0 = Rg::D3 ? yb * YB : blk_begin + yb * YB;
     const int64_t z_end = Rg::D3 ? blk_end : 1;
     const int64_t y_end = Rg::D3 ? ny : blk_end;
     // my centre line

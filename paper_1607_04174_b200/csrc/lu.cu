@@ -57,12 +57,25 @@ __device__ ArgMax block_argmax(ArgMax a, ArgMax* sh) {
 }
 
 // column sums of |A| (for the 1-norm)
-__global__ void colabs_kernel(const double* __restrict__ A, int64_t n, int64_t lda, double* __restrict__ cs) {
-  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (j >= n) return;
+// cs[j] = sum_i |A[i, j]|: a (32 x 8) block per 32 columns, the 8 row
+// groups (rows ty, ty + 8, ...) reduced in a fixed order -- coalesced rows
+// and 8 independent load streams instead of one serial column walk
+__global__ void __launch_bounds__(256) colabs_kernel(const double* __restrict__ A, int64_t n, int64_t lda,
+                                                     double* __restrict__ cs) {
+  __shared__ double red[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t j = blockIdx.x * 32 + tx;
   double s = 0.0;
-  for (int64_t i = 0; i < n; ++i) s += fabs(A[i * lda + j]);
-  cs[j] = s;
+  if (j < n)
+    for (int64_t i = ty; i < n; i += 8) s += fabs(A[i * lda + j]);
+  red[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && j < n) {
+    double t = red[0][tx];
+#pragma unroll
+    for (int g = 1; g < 8; ++g) t += red[g][tx];
+    cs[j] = t;
+  }
 }
 
 __global__ void max_kernel(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
@@ -296,20 +309,25 @@ __device__ void tri_solve(const double* __restrict__ LU, int64_t n, int64_t lda,
   // element (i, j) of the triangular operator T
   auto T = [&](int64_t i, int64_t j) -> double { return (op == 2 || op == 3) ? LU[j * lda + i] : LU[i * lda + j]; };
   const int64_t nblk = (n + 31) / 32;
+  // the diagonal block, staged so that the serial chain below waits on
+  // shared-memory loads rather than global ones
+  __shared__ double sblk[32 * 33];
   for (int64_t bb = 0; bb < nblk; ++bb) {
     const int64_t blk = forward ? bb : nblk - 1 - bb;
     const int64_t b0 = blk * 32, b1 = min(n, b0 + 32);
     const int bs = static_cast<int>(b1 - b0);
+    for (int e = threadIdx.x; e < bs * bs; e += blockDim.x) sblk[(e / bs) * 33 + e % bs] = T(b0 + e / bs, b0 + e % bs);
+    __syncthreads();
     // diagonal block: warp per rhs column, lane per row
     for (int64_t c = warp; c < nrhs; c += nw) {
       double x = lane < bs ? B[(b0 + lane) * ldb + c] : 0.0;
       for (int s = 0; s < bs; ++s) {
         const int r = forward ? s : bs - 1 - s;
         double xr = __shfl_sync(0xffffffffu, x, r);
-        if (!unit) xr = xr / T(b0 + r, b0 + r);
+        if (!unit) xr = xr / sblk[r * 33 + r];
         if (lane == r) x = xr;
         const bool below = forward ? (lane > r) : (lane < r);
-        if (below && lane < bs) x -= T(b0 + lane, b0 + r) * xr;
+        if (below && lane < bs) x -= sblk[lane * 33 + r] * xr;
       }
       if (lane < bs) B[(b0 + lane) * ldb + c] = x;
     }
@@ -580,7 +598,7 @@ extern "C" int swb_lu_factor(double* A, int64_t n, int64_t lda, int32_t* piv, do
     return SWB_OK;
   }
   if (anorm_out) {
-    colabs_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(A, n, lda, cs);
+    colabs_kernel<<<static_cast<unsigned>((n + 31) / 32), 256, 0, st>>>(A, n, lda, cs);
     SWB_CHECK_LAUNCH();
     max_kernel<<<1, 1024, 0, st>>>(cs, n, anorm_out);
     SWB_CHECK_LAUNCH();
@@ -690,7 +708,7 @@ extern "C" int swb_norm1(const double* A, int64_t n, int64_t lda, double* out, v
   cudaStream_t st = swb_stream(stream);
   if (n == 0) { SWB_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double), st)); return SWB_OK; }
   double* cs = static_cast<double*>(ws);
-  colabs_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(A, n, lda, cs);
+  colabs_kernel<<<static_cast<unsigned>((n + 31) / 32), 256, 0, st>>>(A, n, lda, cs);
   SWB_CHECK_LAUNCH();
   max_kernel<<<1, 1024, 0, st>>>(cs, n, out);
   SWB_CHECK_LAUNCH();

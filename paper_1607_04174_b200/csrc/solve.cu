@@ -193,8 +193,15 @@ __global__ void border_kernel(int64_t S, int64_t m, int64_t L, const double* __r
       double s = 0.0;
       for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q) s += red[q];
       A[S * lda + S] = s;
-      for (int64_t k = 0; k < L; ++k) rhs[S * ldr + k] = 0.0;
-      for (int64_t t = 0; t < S; ++t) rhs[S * ldr + lab[t]] += g_s[t] * dsq_s[t];
+    }
+    // rhs[S, k]: one warp per label, lanes over the seeds
+    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int64_t k = warp; k < L; k += nw) {
+      double a = 0.0;
+      for (int64_t t = lane; t < S; t += 32)
+        if (lab[t] == k) a += g_s[t] * dsq_s[t];
+      a = warp_sum(a);
+      if (lane == 0) rhs[S * ldr + k] = a;
     }
   }
 }
@@ -226,23 +233,39 @@ __global__ void coeff_kernel(int64_t m, int64_t L, const double* __restrict__ w,
 
 __global__ void set_value_kernel(double* p, double v) { *p = v; }
 
-// fastrw.py:399-403 spectral weights; g_s = d_sqrt[s]/||d_sqrt|| (fastrw.py:412, 442);
-// gq = V^T g_masked = (V^T g) - q_s^T g_s (fastrw.py:426) when vtg is given
+// fastrw.py:399-403 spectral weights; g_s = d_sqrt[s]/||d_sqrt|| (fastrw.py:412, 442)
 __global__ void weights_kernel(int64_t m, int64_t S, double gamma, const double* __restrict__ values,
-                               const double* __restrict__ vtg, const double* __restrict__ q_s, int64_t ldq,
                                const double* __restrict__ dsq_s, double dnorm, double* __restrict__ w,
-                               double* __restrict__ gq, double* __restrict__ g_s) {
+                               double* __restrict__ g_s) {
   const int64_t t0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t t = t0; t < S; t += stride) g_s[t] = dsq_s[t] / dnorm;
   for (int64_t j = t0; j < m; j += stride) {
     const double v = values[j];
     w[j] = gamma == 0.0 ? (v > 1e-10 ? 1.0 / v : 0.0) : 1.0 / (v + gamma);
-    if (vtg) {
-      double s = 0.0;
-      for (int64_t t = 0; t < S; ++t) s += q_s[t * ldq + j] * (dsq_s[t] / dnorm);
-      gq[j] = vtg[j] - s;
-    }
+  }
+}
+
+// gq = V^T g_masked = (V^T g) - q_s^T g_s (fastrw.py:426):
+// gq[j] = vtg[j] - sum_t q_s[t, j] g_s[t], g_s = dsq_s / dnorm: a (32 x 8)
+// block per 32 columns, the 8 seed-row groups reduced in a fixed order
+__global__ void __launch_bounds__(256) gq_kernel(int64_t m, int64_t S, const double* __restrict__ vtg,
+                                                 const double* __restrict__ q_s, int64_t ldq,
+                                                 const double* __restrict__ dsq_s, double dnorm,
+                                                 double* __restrict__ gq) {
+  __shared__ double red[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t j = blockIdx.x * 32 + tx;
+  double s = 0.0;
+  if (j < m)
+    for (int64_t t = ty; t < S; t += 8) s += q_s[t * ldq + j] * (dsq_s[t] / dnorm);
+  red[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && j < m) {
+    double a = red[0][tx];
+#pragma unroll
+    for (int g = 1; g < 8; ++g) a += red[g][tx];
+    gq[j] = vtg[j] - a;
   }
 }
 
@@ -778,8 +801,12 @@ extern "C" int swb_small_solve_ex(double gamma, int64_t S, int64_t m, int64_t L,
   if (!g0 && ldt < L) return SWB_INVALID_PARAM;
 
   weights_kernel<<<std::max<int64_t>(1, std::min<int64_t>((std::max(m, S) + 255) / 256, 1024)), 256, 0, st>>>(
-      m, S, gamma, values, g0 ? vtg : nullptr, q_s, ldq, dsq_s, dnorm, w, gq, g_s);
+      m, S, gamma, values, dsq_s, dnorm, w, g_s);
   SWB_CHECK_LAUNCH();
+  if (g0) {
+    gq_kernel<<<static_cast<unsigned>((m + 31) / 32), 256, 0, st>>>(m, S, vtg, q_s, ldq, dsq_s, dnorm, gq);
+    SWB_CHECK_LAUNCH();
+  }
   if (S == 0) {  // gamma > 0, no seeds: coeff = w * gamma t_p (fastrw.py:437-438)
     coeff_kernel<<<grid, 256, 0, st>>>(m, L, w, nullptr, 0, t_p, ldt, gamma, coeff);
     SWB_CHECK_LAUNCH();
