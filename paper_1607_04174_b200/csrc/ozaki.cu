@@ -53,6 +53,28 @@ constexpr size_t OZ_SMEM = size_t(OZ_STAGES) * OZ_STAGE + 1024;
 constexpr int OZ_TMEM_COLS = 512;
 constexpr int OZ_MAX_K = 512;
 
+// Wide MMAs (OZ_WIDE = 1): the B stage holds the seven digit planes of a
+// column block side by side in N ([kq 2][plane 7][col 64][16 B]), so the
+// digits E_0 .. E_(6-i) that A digit i meets are ONE contiguous 64 (7 - i)-
+// column operand, and the group accumulators sit at TMEM column 64 g in the
+// same order: A digit i times B columns [64 (g0 - i), 64 (g0 - i + n)) lands
+// exactly on groups g0 .. g0 + n - 1.  The 28 digit products of a K chunk
+// become 10 MMAs of N = 64..256 (the same int32 sums, bit for bit), which
+// read the A digit once per MMA instead of once per group: at N = 64 every
+// MMA re-read 4 KB of A for 2 KB of B and the shared-memory port (128 B per
+// cycle) capped the rate; now A is read 10 times per chunk, not 28.
+// OZ_WIDE = 0 keeps the 28 N = 64 MMAs ([plane 7][kq 2][col 64][16 B]).
+#ifndef OZ_WIDE
+#define OZ_WIDE 1
+#endif
+#if OZ_WIDE
+constexpr uint32_t OZ_B_LBO = OZ_S * OZ_BN * 16;    // K-adjacent core matrices: past all 7 planes
+constexpr uint32_t OZ_B_PLANE = OZ_BN * 16;         // plane j's columns follow plane j-1's
+#else
+constexpr uint32_t OZ_B_LBO = OZ_BN * 16;
+constexpr uint32_t OZ_B_PLANE = OZ_B_SLICE;
+#endif
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -128,9 +150,40 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
 }
 
 // instruction descriptor: kind::i8, s32 accumulate, K-major A and B, M x N
-__host__ __device__ constexpr uint32_t idesc_i8(int a_signed, int b_signed) {
-  return (2u << 4) | (uint32_t(a_signed) << 7) | (uint32_t(b_signed) << 10) | (uint32_t(OZ_BN >> 3) << 17) |
+__host__ __device__ constexpr uint32_t idesc_i8(int a_signed, int b_signed, int n = OZ_BN) {
+  return (2u << 4) | (uint32_t(a_signed) << 7) | (uint32_t(b_signed) << 10) | (uint32_t(n >> 3) << 17) |
          (uint32_t(OZ_BM >> 4) << 24);
+}
+
+// The 28 digit products of one K chunk (A digit planes at a0 + i 4 KB, B
+// planes at b0 + j OZ_B_PLANE) into the seven group accumulators at TMEM
+// column 64 g.  acc = 0 only for a tile's first chunk: its digit-0 MMAs
+// come first and cover every group once, so they overwrite and all later
+// MMAs accumulate.
+__device__ __forceinline__ void oz_issue_chunk(uint32_t tmem, uint32_t a0, uint32_t b0, bool first) {
+#if OZ_WIDE
+  // (i, g0, n): A digit i x B digits g0 - i .. g0 - i + n - 1 -> groups g0 .. g0 + n - 1 (N = 64 n <= 256)
+  constexpr int seq[10][3] = {{0, 0, 4}, {0, 4, 3}, {1, 1, 3}, {1, 4, 3}, {2, 2, 2},
+                              {2, 4, 3}, {3, 3, 4}, {4, 4, 3}, {5, 5, 2}, {6, 6, 1}};
+#pragma unroll
+  for (int q = 0; q < 10; ++q) {
+    const int i = seq[q][0], g0 = seq[q][1], n = seq[q][2];
+    tc_mma_i8(tmem + uint32_t(g0 * OZ_BN), smem_desc(a0 + i * OZ_A_SLICE, OZ_BM * 16, 128),
+              smem_desc(b0 + (g0 - i) * OZ_B_PLANE, OZ_B_LBO, 128), idesc_i8(1, 1, n * OZ_BN),
+              (first && i == 0) ? 0u : 1u);
+  }
+#else
+  // A digit i outer, group g inner: consecutive MMAs accumulate into
+  // different TMEM groups; group g's first MMA of a tile is (i = 0, j = g)
+#pragma unroll
+  for (int i = 0; i < OZ_S; ++i) {
+    const uint64_t ad = smem_desc(a0 + i * OZ_A_SLICE, OZ_BM * 16, 128);
+#pragma unroll
+    for (int g = i; g < OZ_G; ++g)
+      tc_mma_i8(tmem + uint32_t(g * OZ_BN), ad, smem_desc(b0 + (g - i) * OZ_B_PLANE, OZ_B_LBO, 128), idesc_i8(1, 1),
+                (first && i == 0) ? 0u : 1u);
+  }
+#endif
 }
 
 __device__ __forceinline__ int oz_exponent(double amax) {
@@ -298,9 +351,9 @@ __global__ void __launch_bounds__(OZ_BN) oz_slice_cols_kernel(const double* __re
     uint4 d[OZ_S];
     oz_digits16(v, scale, d);
     const int64_t kc = ch >> 1, kq = ch & 1;
-    uint8_t* base = sl + (cb * nkc + kc) * OZ_B_STAGE + kq * (OZ_BN * 16) + tid * 16;
+    uint8_t* base = sl + (cb * nkc + kc) * OZ_B_STAGE + kq * OZ_B_LBO + tid * 16;
 #pragma unroll
-    for (int s = 0; s < OZ_S; ++s) *reinterpret_cast<uint4*>(base + s * OZ_B_SLICE) = d[s];
+    for (int s = 0; s < OZ_S; ++s) *reinterpret_cast<uint4*>(base + s * OZ_B_PLANE) = d[s];
   }
 }
 
@@ -376,20 +429,7 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
         tc_fence_after();
         if (lane == 0) {
           const uint32_t a0 = smem_u32(stages + size_t(s) * OZ_STAGE);
-          const uint32_t b0 = a0 + OZ_A_STAGE;
-          // A digit i outer, group g inner: consecutive MMAs accumulate into
-          // different TMEM groups (back-to-back MMAs into one accumulator
-          // serialise on it); group g's first MMA of a tile is (i = 0, j = g)
-#pragma unroll
-          for (int i = 0; i < OZ_S; ++i) {
-            const uint64_t ad = smem_desc(a0 + i * OZ_A_SLICE, OZ_BM * 16, 128);
-#pragma unroll
-            for (int g = i; g < OZ_G; ++g) {
-              const int j = g - i;
-              const uint64_t bd = smem_desc(b0 + j * OZ_B_SLICE, OZ_BN * 16, 128);
-              tc_mma_i8(tmem + uint32_t(g * OZ_BN), ad, bd, idesc_i8(1, 1), (kc > 0 || i > 0) ? 1u : 0u);
-            }
-          }
+          oz_issue_chunk(tmem, a0, a0 + OZ_A_STAGE, kc == 0);
           tc_commit(smem_u32(&empty_bar[s]));          // frees the stage when these finish
           if (kc + 1 == nkc) tc_commit(smem_u32(&tfull_bar));
         }
@@ -776,13 +816,7 @@ __global__ void __launch_bounds__(128, 1) int8_probe_n64_kernel(int iters, uint3
   const uint32_t tm = slot;
   if (threadIdx.x == 0) {
     const uint32_t a0 = smem_u32(pr_smem), b0 = a0 + 28672;
-    for (int it = 0; it < iters; ++it)
-#pragma unroll
-      for (int i = 0; i < OZ_S; ++i)
-#pragma unroll
-        for (int g = i; g < OZ_G; ++g)
-          tc_mma_i8(tm + uint32_t(g * OZ_BN), smem_desc(a0 + i * OZ_A_SLICE, OZ_BM * 16, 128),
-                    smem_desc(b0 + (g - i) * OZ_B_SLICE, OZ_BN * 16, 128), idesc_i8(1, 1), 1u);
+    for (int it = 0; it < iters; ++it) oz_issue_chunk(tm, a0, b0, false);
     tc_commit(smem_u32(&bar));
     mbar_wait(smem_u32(&bar), 0);
   }
