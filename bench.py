@@ -469,7 +469,8 @@ def int8_probe(lib, fn="swb_int8_peak_probe", iters=4000):
     """Live INT8 tensor-core peak: back-to-back tcgen05.mma.kind::i8
     (M 128, N 256, K 32) on every SM (swb_int8_peak_probe), best of 5 after
     one warm-up, in TOP/s.  fn="swb_int8_scheme_probe": the rotation GEMM's
-    own MMA pattern (N 64 into seven accumulators) -- the scheme's ceiling."""
+    own MMA sequence (10 MMAs of N 64..256 per K chunk into seven group
+    accumulators) -- the scheme's ceiling."""
     import torch
 
     from paper_1607_04174_b200 import _lib
@@ -844,8 +845,10 @@ def run_gpu(args):
     # the live random-operand sustained probe are reported beside it
     int8_den, int8_den_src = int8_denominator(peaks, int8_sust)
     # the dominant kernel by time: the INT8 rotation GEMM or the DMMA projection
-    if rot_gemm_ms and (not proj_ms or rot_gemm_ms >= proj_ms):
-        roofline = {"bound": "tensor", "kernel": "rotation V*C: INT8 tcgen05 digit-product GEMM (oz_gemm_kernel)",
+    # (the INT8 rotation's own roofline is kept under kernels either way)
+    rot_roof = None
+    if rot_gemm_ms:
+        rot_roof = {"bound": "tensor", "kernel": "rotation V*C: INT8 tcgen05 digit-product GEMM (oz_gemm_kernel)",
                     "achieved": oz_tops, "peak": int8_den, "unit": "TOP/s (int8)",
                     "frac": oz_tops / int8_den if oz_tops else None,
                     "peak_source": int8_den_src,
@@ -859,13 +862,19 @@ def run_gpu(args):
                     "algorithmic": f"{OZ_PAIRS} digit products x 2*N*K*K ops",
                     "traffic": _ncu_traffic("rotation_int8_gemm", cfg, dims, m),
                     "algorithmic_bytes": 16.0 * n * m,
-                    # the scheme's own ceiling: its seven resident int32 group
-                    # accumulators (7 x 64 of 512 TMEM columns) cap the MMA at
-                    # N = 64, measured alone by swb_int8_scheme_probe
+                    # the scheme's own ceiling: the GEMM's MMA sequence alone
+                    # (10 MMAs of N = 64..256 per K chunk into the seven
+                    # resident int32 group accumulators), swb_int8_scheme_probe
                     "scheme_peak": scheme_peak,
                     "frac_of_scheme_peak": oz_tops / scheme_peak if oz_tops and scheme_peak else None,
-                    "scheme_peak_source": "live probe of the GEMM's MMA pattern alone (M128 N64 K32 SS, 28 MMAs "
-                                          "into 7 TMEM accumulators; swb_int8_scheme_probe) in this run"}
+                    "scheme_peak_source": "live probe of the GEMM's MMA sequence alone (M128 K32 SS, the 28 digit "
+                                          "products of a K chunk as 10 MMAs of N = 64..256 into 7 TMEM group "
+                                          "accumulators; swb_int8_scheme_probe) in this run"}
+        kernels["rotation_int8_gemm"].update(
+            {k: rot_roof[k] for k in ("frac", "peak", "frac_of_live_random_sustained", "scheme_peak",
+                                      "frac_of_scheme_peak", "traffic")})
+    if rot_roof and (not proj_ms or rot_gemm_ms >= proj_ms):
+        roofline = rot_roof
     else:
         pj = kernels["projection_dmma"]["tflops"] if proj_ms else None
         roofline = {"bound": "tensor", "kernel": "projection V^T(dL V) (DMMA TN GEMM, symmetric)",

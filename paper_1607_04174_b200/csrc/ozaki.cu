@@ -242,7 +242,12 @@ __device__ __forceinline__ void oz_digits16(const double (&v)[16], double scale,
 constexpr int OZ_SLICE_WARPS = OZ_SLICE_WARPS_CFG;
 constexpr int OZ_SLICE_ROWS = OZ_SLICE_ROWS_CFG;
 constexpr int OZ_SLICE_MAXCH = 32;   // K <= 512
-constexpr size_t OZ_SLICE_SMEM = size_t(OZ_SLICE_MAXCH) * OZ_S * OZ_SLICE_ROWS * 16;
+// staging: [chunk][slice][row 16] x 16 B plus one 16-B pad per chunk, so the
+// four chunks a warp's digit store touches land in different banks (without
+// the pad the chunk stride is 0 mod 32 words: a 4-way conflict on every
+// store, and the co-running GEMM is bound by the same shared-memory port)
+constexpr int OZ_SLICE_CH_STRIDE = OZ_S * OZ_SLICE_ROWS + 1;   // uint4 per chunk
+constexpr size_t OZ_SLICE_SMEM = size_t(OZ_SLICE_MAXCH) * OZ_SLICE_CH_STRIDE * 16;
 __global__ void __launch_bounds__(OZ_SLICE_WARPS * 32, OZ_SLICE_MINB) oz_slice_rows_kernel(const double* __restrict__ A,
                                                                             int64_t lda, int64_t rows, int64_t K,
                                                                             int64_t nkc, uint8_t* __restrict__ sl,
@@ -306,7 +311,7 @@ __global__ void __launch_bounds__(OZ_SLICE_WARPS * 32, OZ_SLICE_MINB) oz_slice_r
         h = (h & 0xFFFFu) ^ (s2 == 0 ? 0u : 0x8080u);
         const uint32_t nb = __shfl_down_sync(0xffffffffu, h, 1);
         if (!(lane & 1) && ch < nch)
-          stg32[((ch * OZ_S + s2) * OZ_SLICE_ROWS + lr) * 4 + ((lane & 7) >> 1)] = h | (nb << 16);
+          stg32[(ch * OZ_SLICE_CH_STRIDE + s2 * OZ_SLICE_ROWS + lr) * 4 + ((lane & 7) >> 1)] = h | (nb << 16);
       }
     }
   }
@@ -320,7 +325,7 @@ __global__ void __launch_bounds__(OZ_SLICE_WARPS * 32, OZ_SLICE_MINB) oz_slice_r
     for (int seg = threadIdx.x / OZ_SLICE_ROWS; seg < nch * OZ_S; seg += SEG_STEP) {
       const int ch = seg / OZ_S, s2 = seg - ch * OZ_S;
       *reinterpret_cast<uint4*>(base + (ch >> 1) * OZ_A_STAGE + s2 * OZ_A_SLICE + (ch & 1) * (OZ_BM * 16)) =
-          stg[seg * OZ_SLICE_ROWS + lr];
+          stg[ch * OZ_SLICE_CH_STRIDE + s2 * OZ_SLICE_ROWS + lr];
     }
   }
 }
@@ -356,6 +361,23 @@ __global__ void __launch_bounds__(OZ_BN) oz_slice_cols_kernel(const double* __re
     for (int s = 0; s < OZ_S; ++s) *reinterpret_cast<uint4*>(base + s * OZ_B_PLANE) = d[s];
   }
 }
+
+// OZ_PROF (variant builds only, tools/oz_bench.py SWB_OZ_PROF=1): per-role
+// clock64 sums, [role][wait0, wait1, total, count] for role 0 = producer
+// (wait empty), 1 = MMA issuer (wait tile-empty | wait stage-full),
+// 2 = epilogue (wait tile-full | tile-full -> TMEM released)
+#ifndef OZ_PROF
+#define OZ_PROF 0
+#endif
+#ifndef OZ_EPI2
+#define OZ_EPI2 1
+#endif
+#if OZ_PROF
+__device__ unsigned long long oz_prof[12];
+#define OZ_T(x) const long long x = clock64()
+#else
+#define OZ_T(x)
+#endif
 
 // out[rows x M2] = sum_g ... (see header).  raw != nullptr: write the seven
 // int32 group accumulators instead, raw[(g * rows_p + r) * np + c].
@@ -421,11 +443,23 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
     // ---------------- MMA issuer ----------------
     int s = 0;
     uint32_t ph = 0, tph = 0;
+#if OZ_PROF
+    long long w_te = 0, w_full = 0;
+    OZ_T(t_begin);
+#endif
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      OZ_T(t0);
       mbar_wait(smem_u32(&tempty_bar), tph ^ 1);
+#if OZ_PROF
+      w_te += clock64() - t0;
+#endif
       tc_fence_after();
       for (int64_t kc = 0; kc < nkc; ++kc) {
+        OZ_T(t1);
         mbar_wait(smem_u32(&full_bar[s]), ph);
+#if OZ_PROF
+        w_full += clock64() - t1;
+#endif
         tc_fence_after();
         if (lane == 0) {
           const uint32_t a0 = smem_u32(stages + size_t(s) * OZ_STAGE);
@@ -438,6 +472,14 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
       }
       tph ^= 1;
     }
+#if OZ_PROF
+    if (lane == 0) {
+      atomicAdd(&oz_prof[4], (unsigned long long)w_te);
+      atomicAdd(&oz_prof[5], (unsigned long long)w_full);
+      atomicAdd(&oz_prof[6], (unsigned long long)(clock64() - t_begin));
+      atomicAdd(&oz_prof[7], 1ull);
+    }
+#endif
   } else {
     // ---------------- epilogue: warps 2..9, two per TMEM lane quarter ----------------
     const int ew = warp - 2;                        // 0..7
@@ -445,12 +487,21 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
     const int c0 = (ew >> 2) * OZ_EPI_COLS;         // 32-column half
     const uint32_t tsrc = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(c0);
     uint32_t tph = 0;
+#if OZ_PROF
+    long long w_tf = 0, w_drain = 0, t_rel = 0;
+    OZ_T(t_begin);
+#endif
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
       const int64_t rb = t / n_cb, cb = t % n_cb;
       const int64_t r = rb * OZ_BM + quarter * 32 + lane;
       const int64_t gc0 = cb * OZ_BN + c0;
       const double srow = r < rows ? sa[r] : 0.0;
+      OZ_T(t0);
       mbar_wait(smem_u32(&tfull_bar), tph);
+#if OZ_PROF
+      const long long t_got = clock64();
+      w_tf += t_got - t0;
+#endif
       tc_fence_after();
       tph ^= 1;
       if (raw) {
@@ -469,6 +520,52 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
       // both 16-column rounds are combined in registers before any store, so
       // TMEM is released right after the second round's loads
       double o[2][16];
+#if OZ_EPI2
+      // two TMEM waits per tile (not four): round 1's loads are issued in two
+      // batches around round 0's combine, so at most ~144 accumulator /
+      // partial registers are live (10 warps: <= 168 registers per thread)
+      {
+        double o0[16];
+        int32_t w[3][16];
+        {
+          int32_t v[OZ_G][16];
+#pragma unroll
+          for (int g = 0; g < OZ_G; ++g) tmem_ld16(tsrc + uint32_t(g * OZ_BN), v[g]);
+          tmem_wait_ld();
+          long long H0[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            H0[q] = (static_cast<long long>(v[0][q]) << 16) + (static_cast<long long>(v[1][q]) << 8) +
+                    static_cast<long long>(v[2][q]);
+#pragma unroll
+          for (int g = 0; g < 3; ++g) tmem_ld16(tsrc + uint32_t(g * OZ_BN + 16), w[g]);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const long long L = (static_cast<long long>(v[3][q]) << 24) + (static_cast<long long>(v[4][q]) << 16) +
+                                (static_cast<long long>(v[5][q]) << 8) + static_cast<long long>(v[6][q]);
+            o0[q] = fma(static_cast<double>(L), 0x1p-32, static_cast<double>(H0[q])) * srow;
+          }
+        }
+        int32_t x[4][16];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) tmem_ld16(tsrc + uint32_t((g + 3) * OZ_BN + 16), x[g]);
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(smem_u32(&tempty_bar));         // the next tile's MMAs may start
+#if OZ_PROF
+        w_drain += clock64() - t_got;
+#endif
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          o[0][q] = o0[q];
+          const long long H = (static_cast<long long>(w[0][q]) << 16) + (static_cast<long long>(w[1][q]) << 8) +
+                              static_cast<long long>(w[2][q]);
+          const long long L = (static_cast<long long>(x[0][q]) << 24) + (static_cast<long long>(x[1][q]) << 16) +
+                              (static_cast<long long>(x[2][q]) << 8) + static_cast<long long>(x[3][q]);
+          o[1][q] = fma(static_cast<double>(L), 0x1p-32, static_cast<double>(H)) * srow;
+        }
+      }
+#else
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         const int h = hh * 16;
@@ -491,6 +588,9 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
         if (hh == 1) {                              // all of this thread's TMEM is in registers
           tc_fence_before();
           mbar_arrive(smem_u32(&tempty_bar));       // the next tile's MMAs may start
+#if OZ_PROF
+          w_drain += clock64() - t_got;
+#endif
         }
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
@@ -499,6 +599,7 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
           o[hh][q] = fma(static_cast<double>(L), 0x1p-32, static_cast<double>(H[q])) * srow;
         }
       }
+#endif
       if (r >= rows) continue;
       double* orow = out + r * ldo + gc0;
       if (gc0 + OZ_EPI_COLS <= M2) {
@@ -513,6 +614,15 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
           if (gc0 + q < M2) orow[q] = o[q >> 4][q & 15] * sb[gc0 + q];
       }
     }
+#if OZ_PROF
+    (void)t_rel;
+    if (lane == 0) {
+      atomicAdd(&oz_prof[8], (unsigned long long)w_tf);
+      atomicAdd(&oz_prof[9], (unsigned long long)w_drain);
+      atomicAdd(&oz_prof[10], (unsigned long long)(clock64() - t_begin));
+      atomicAdd(&oz_prof[11], 1ull);
+    }
+#endif
   }
   __syncthreads();
   if (warp == 1) {
@@ -604,7 +714,7 @@ extern "C" int swb_oz_split_rows(const double* A, int64_t lda, int64_t nr, int64
   const OzPtrs q = oz_ptrs(o, workspace, buf);
   const int64_t nrp = (nr + OZ_BM - 1) / OZ_BM * OZ_BM;
   // staging for this K only (2 nkc 16-column halves), not the K <= 512 maximum
-  const size_t split_smem = size_t(2 * o.nkc) * OZ_S * OZ_SLICE_ROWS * 16;
+  const size_t split_smem = size_t(2 * o.nkc) * OZ_SLICE_CH_STRIDE * 16;
   oz_slice_rows_kernel<<<static_cast<unsigned>(nrp / OZ_SLICE_ROWS), OZ_SLICE_WARPS * 32, split_smem,
                          swb_stream(stream)>>>(A, lda, nr, K, o.nkc, q.a_sl, q.sa);
   SWB_CHECK_LAUNCH();
@@ -637,6 +747,14 @@ extern "C" int swb_oz_gemm_planes(int64_t nr, int64_t rows, int64_t K, int64_t M
                             swb_stream(stream));
 }
 
+#if OZ_PROF
+extern "C" int swb_oz_prof_read(unsigned long long* out) {
+  SWB_CUDA_TRY(cudaDeviceSynchronize());
+  SWB_CUDA_TRY(cudaMemcpyFromSymbol(out, oz_prof, sizeof(oz_prof)));
+  return SWB_OK;
+}
+#endif
+
 extern "C" size_t swb_oz_gemm_nn_workspace_bytes(int64_t rows, int64_t K, int64_t M2) {
   if (rows <= 0 || K <= 0 || M2 <= 0) return 0;
   return oz_layout(rows, K, M2).total;
@@ -662,9 +780,18 @@ extern "C" int swb_oz_gemm_nn(const double* A, int64_t lda, const double* B, int
   if ((rc = swb_oz_split_cols(B, ldb, rows, K, M2, workspace, workspace_bytes, stream))) return rc;
   const int64_t chunk = swb_oz_chunk_rows(rows, K, M2);
   const int64_t nch = (rows + chunk - 1) / chunk;
-  if (nch == 1) {
-    if ((rc = swb_oz_split_rows(A, lda, rows, rows, K, M2, 0, workspace, workspace_bytes, stream))) return rc;
-    return swb_oz_gemm_planes(rows, rows, K, M2, 0, out, ldo, workspace, workspace_bytes, stream);
+#ifndef OZ_OVERLAP
+#define OZ_OVERLAP 1
+#endif
+  if (nch == 1 || !OZ_OVERLAP) {   // OZ_OVERLAP = 0 (variant builds): split and GEMM in turn
+    for (int64_t i = 0; i < nch; ++i) {
+      const int64_t r0 = i * chunk, nr = rows - r0 < chunk ? rows - r0 : chunk;
+      if ((rc = swb_oz_split_rows(A + r0 * lda, lda, nr, rows, K, M2, 0, workspace, workspace_bytes, stream)))
+        return rc;
+      if ((rc = swb_oz_gemm_planes(nr, rows, K, M2, 0, out + r0 * ldo, ldo, workspace, workspace_bytes, stream)))
+        return rc;
+    }
+    return SWB_OK;
   }
   // side stream + events per device; the mutex makes the enqueue of one
   // call's chunk loop atomic, so concurrent callers (different streams) share

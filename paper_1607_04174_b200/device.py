@@ -95,10 +95,11 @@ def rotate_rows(V, ldv: int, Cm, ldc: int, rows: int, m: int, out, ldo: int, str
     mark("rotate_split")
     _lib.call("swb_oz_split_cols", ptr(Cm), ldc, rows, m, m, ptr(ws), ws.numel(), st)
     main = torch.cuda.current_stream()
-    aux = _aux_stream() if nch > 1 else main
+    # SWB_OZ_SERIAL=1 (measurement knob): split and GEMM in turn on one stream
+    aux = _aux_stream() if nch > 1 and os.environ.get("SWB_OZ_SERIAL") != "1" else main
     ev_split = [torch.cuda.Event(), torch.cuda.Event()]
     ev_gemm = [torch.cuda.Event(), torch.cuda.Event()]
-    if nch > 1:
+    if aux is not main:
         aux.wait_stream(main)                     # V and C's planes ready
 
     def split(i):
