@@ -433,8 +433,8 @@ def e2e_step(state, i, host_labels):
 
 def _ncu_traffic(kernel: str, cfg, dims, m):
     """DRAM bytes per launch of `kernel` from the committed ncu capture of the
-    same workload (profiles/r2_c4_kernel_metrics.json, tools/prof_r2.sh), else None."""
-    f = ROOT / "profiles" / "r2_c4_kernel_metrics.json"
+    same workload (profiles/r2c_c4_kernel_metrics.json, tools/prof_r2c.sh), else None."""
+    f = ROOT / "profiles" / "r2c_c4_kernel_metrics.json"
     if cfg != "c4" or dims is not None or m != 400 or not f.exists():
         return None
     try:
