@@ -397,9 +397,31 @@ def _round_prob(state, i):
     return probs[i % len(probs)] if probs else state["prob"]
 
 
+def _fused(state) -> bool:
+    """update_and_solve (the solve's reconstruction folded into the rotation)
+    for the gamma = 0 configs with a fixed K; SWB_FUSED=0 times the two
+    separate calls (update_basis, solve_fast) instead."""
+    return (os.environ.get("SWB_FUSED", "1") != "0" and state.get("method") != "rayleigh"
+            and state["prob"] is not None and state["params"].get("epsilon") is None)
+
+
+def _next_pack_and_solve(state, beta, i, prob):
+    """_next_pack + solve_fast as one update_and_solve call (ping-pong V')."""
+    import paper_1607_04174_b200 as swb
+    spare = state.pop("spare", None)
+    old = state["pack"]
+    cut = state.get("cut") if i % 2 == 0 else None
+    pack, field = swb.update_and_solve(old, state["image"], prob, beta, cut_edges=cut, out=spare)
+    state["spare"] = old.V
+    state["pack"] = pack
+    return field
+
+
 def gpu_step(state, i):
     p = state["params"]
     beta = p["beta1"] if i % 2 == 0 else p["beta0"]
+    if _fused(state):
+        return _next_pack_and_solve(state, beta, i, _round_prob(state, i))
     pack = _next_pack(state, beta, i)
     if state["prob"] is None:
         return registration_solve(state, pack, state["image"], state["moving"])
@@ -425,8 +447,11 @@ def e2e_step(state, i, host_labels):
     seeds = _round_prob(state, i).seeds
     prob = swb.LabelProblem(num_labels=p["labels"],
                             seeds=swb.SeedPartition(state["n"], seeds.seed_indices.copy(), seeds.seed_labels.copy()))
-    pack = _next_pack(state, beta, i)
-    field = _adaptive_solve(state, pack, prob)
+    if _fused(state):
+        field = _next_pack_and_solve(state, beta, i, prob)
+    else:
+        pack = _next_pack(state, beta, i)
+        field = _adaptive_solve(state, pack, prob)
     host_labels.copy_(field.labels_dev, non_blocking=True)
     return field
 
@@ -823,14 +848,22 @@ def run_gpu(args):
     if not rot_gemm_ms and rot_ms:   # DMMA rotation (m > 512 or SWB_ROTATION=dmma)
         kernels["rotation"]["frac_fp64"] = achieved / fp64_peak
     L = state["params"]["labels"]
+    fz_ms = phases.get("solve_finalize")
+    if fz_ms and not rc_ms:   # update_and_solve: V' coeff came out of the rotation's padding columns
+        del kernels["reconstruct_argmax"]
+        kernels["finalize_argmax"] = {
+            "ms": fz_ms, "gbs": (8.0 * L + 20.0) * n / (fz_ms * 1e-3) / 1e9,
+            "note": "update_and_solve: the reconstruction V' coeff = V (C coeff) rides in the rotation GEMM's "
+                    "padding columns; this pass reads the N x L products + d_sqrt, writes labels / top-2"}
+        kernels["finalize_argmax"]["frac_hbm"] = kernels["finalize_argmax"]["gbs"] / hbm
     if L > 8 and rc_ms:   # many labels: V (coeff) on the DMMA GEMM, then the finalize / argmax pass
         kernels["reconstruct_argmax"] = {"ms": rc_ms, "tflops": 2.0 * n * m * L / (rc_ms * 1e-3) / 1e12,
                                          "note": "NN GEMM N x K x L + finalize/argmax pass"}
     for k in ("projection_dmma", "reconstruct_argmax"):
-        if kernels[k].get("tflops"):
+        if k in kernels and kernels[k].get("tflops"):
             kernels[k]["frac_fp64"] = kernels[k]["tflops"] / fp64_peak
     for k in ("stencil_delta", "reconstruct_argmax"):
-        if kernels[k].get("gbs"):
+        if k in kernels and kernels[k].get("gbs"):
             kernels[k]["frac_hbm"] = kernels[k]["gbs"] / hbm
     if rayleigh:   # the reference's refresh: one read-only stencil pass over V (HBM)
         sr_ms = phases.get("stencil_rayleigh")

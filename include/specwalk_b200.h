@@ -149,6 +149,15 @@ int swb_oz_split_rows(const double* A_chunk, int64_t lda, int64_t chunk_rows, in
                       int buf, void* workspace, size_t workspace_bytes, void* stream);
 int swb_oz_gemm_planes(int64_t chunk_rows, int64_t rows, int64_t K, int64_t M2, int buf, double* out_chunk,
                        int64_t ldo, void* workspace, size_t workspace_bytes, void* stream);
+/* The same GEMM with the product's columns split between two outputs:
+ * [0, ncol_main) -> out_chunk (ldo), [ncol_main, M2) -> out2_chunk (ldo2).
+ * Extra B columns appended after the K rotation columns ride in the last
+ * column tile's padding (64-column tiles), so e.g. V (C coeff) -- the RW
+ * solve's reconstruction V' coeff -- comes out of the rotation at no extra
+ * tensor-core work (update_and_solve). */
+int swb_oz_gemm_planes_split(int64_t chunk_rows, int64_t rows, int64_t K, int64_t M2, int buf, double* out_chunk,
+                             int64_t ldo, int64_t ncol_main, double* out2_chunk, int64_t ldo2, void* workspace,
+                             size_t workspace_bytes, void* stream);
 /* measurement: back-to-back INT8 tcgen05 MMAs (M 128, N 256, K 32) on every
  * SM; *ops_out = 2 x MACs issued (bench.py's live INT8 roofline) */
 int swb_int8_peak_probe(int iters, double* ops_out, void* stream);
@@ -298,6 +307,16 @@ int swb_seed_fit_schedule(const double* V, int64_t ldv, const int32_t* col_map,
 int swb_prior_hat(const double* priors, int64_t ldp, int64_t row_begin, int64_t row_end,
                   int64_t L, const double* d_sqrt, const int64_t* seed_idx, int64_t S,
                   double* out, int64_t ldo, void* stream);
+/* Finalize + hard labels of a reconstruction computed elsewhere: uraw
+ * (rows [r_begin, r_end), ld ldr) holds V'[x, :] coeff; then exactly the
+ * tail of swb_reconstruct_label: u = (uraw + g_x*extra)/d_sqrt_x, clip >= 0,
+ * dead row -> 1/L, normalise, label / top2, U optional (L > 8: in place,
+ * U == uraw).  d_sqrt is globally indexed; uraw / U / labels / top2 by
+ * (r - r_begin).  Used by update_and_solve, whose rotation GEMM emits
+ * V (C coeff) in its padding columns (swb_oz_gemm_planes_split). */
+int swb_finalize_label(int64_t r_begin, int64_t r_end, int64_t L, const double* uraw, int64_t ldr,
+                       const double* extra, double dnorm, const double* d_sqrt, double* U, int64_t ldu,
+                       int32_t* labels, double* top2, void* stream);
 /* hard_labels of an existing field (images.py:128-130). */
 int swb_argmax_rows(const double* U, int64_t ldu, int64_t N, int64_t L, int32_t* labels,
                     double* top2, void* stream);

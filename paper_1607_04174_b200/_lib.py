@@ -86,6 +86,10 @@ SIGNATURES = {
     "swb_oz_split_cols": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, C.c_size_t, c_vp]),
     "swb_oz_split_rows": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, C.c_int, c_vp, C.c_size_t, c_vp]),
     "swb_oz_gemm_planes": (C.c_int, [c_i64, c_i64, c_i64, c_i64, C.c_int, c_vp, c_i64, c_vp, C.c_size_t, c_vp]),
+    "swb_oz_gemm_planes_split": (C.c_int, [c_i64, c_i64, c_i64, c_i64, C.c_int, c_vp, c_i64, c_i64, c_vp, c_i64,
+                                           c_vp, C.c_size_t, c_vp]),
+    "swb_finalize_label": (C.c_int, [c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_dbl, c_vp, c_vp, c_i64, c_vp, c_vp,
+                                     c_vp]),
     "swb_oz_chunk_rows": (c_i64, [c_i64, c_i64, c_i64]),
     "swb_int8_peak_probe": (C.c_int, [C.c_int, C.POINTER(C.c_double), c_vp]),
     "swb_int8_scheme_probe": (C.c_int, [C.c_int, C.POINTER(C.c_double), c_vp]),

@@ -263,7 +263,8 @@ def refresh_from_set(packs, image, new_beta: float, **kw) -> RefreshedPack:
 
 
 def update_basis(pack, image, new_beta: float | None = None, cut_edges=None, method: str = "first_order",
-                 gap_guard: float = 0.5, *, connectivity=None, weight_mode=None, keep_P: bool = False, out=None):
+                 gap_guard: float = 0.5, *, connectivity=None, weight_mode=None, keep_P: bool = False, out=None,
+                 _pre_rotate=None):
     """Update the eigenbasis for a new beta and/or cut edges (north-star (a)).
 
     method="rayleigh": exactly the reference refresh (no rotation).
@@ -339,9 +340,6 @@ def update_basis(pack, image, new_beta: float | None = None, cut_edges=None, met
         Vn = W  # W is dead after the projection: the rotation writes V' into its buffer
         if ldv > m:
             Vn[:, m:].zero_()
-        _mark("rotate")
-        rotate_rows(dp.V, ldv, Cm, ldp, n, m, Vn, ldv, st, mark=_mark)
-        _mark("update_tail")
         # V'^T d = C^T (V^T d): a 1-row NN product
         vtd_row = torch.zeros((1, ldp), dtype=torch.float64, device="cuda")
         vtd_row[0, :m].copy_(vtd)
@@ -352,6 +350,16 @@ def update_basis(pack, image, new_beta: float | None = None, cut_edges=None, met
         out.C = Cm
         if keep_P:
             out.P = P
+        # update_and_solve: the solve's seed system runs here, on V' rows
+        # formed from V and C, and returns extra B columns for the rotation
+        extra = _pre_rotate(out, dp, Cm, ldp) if _pre_rotate is not None else None
+        _mark("rotate")
+        if extra is None:
+            rotate_rows(dp.V, ldv, Cm, ldp, n, m, Vn, ldv, st, mark=_mark)
+        else:
+            m2, c_aug, ldca, out2, ldo2 = extra
+            rotate_rows(dp.V, ldv, c_aug, ldca, n, m, Vn, ldv, st, mark=_mark, m2=m2, out2=out2, ldo2=ldo2)
+        _mark("update_tail")
     out.base = pack if method == "rayleigh" else None   # an updated pack owns new memory: no strong ref
     out.new_beta = beta
     out.order_dev = order
@@ -419,7 +427,7 @@ def _ell_from_lap(lap, seed_idx: np.ndarray):
 
 
 def solve_fast(pack, lap, prob, m_use: int | None = None, streaming_block: int | None = None,
-               *, want_field: bool = False, check: bool = True) -> DeviceField:
+               *, want_field: bool = False, check: bool = True, _defer: bool = False) -> DeviceField:
     """fastrw.py:352-467 on the device.
 
     ``pack``: DevicePack / RefreshedPack / UpdatedPack, or a host pack
@@ -534,6 +542,9 @@ def solve_fast(pack, lap, prob, m_use: int | None = None, streaming_block: int |
                   stream_handle())
         return U
 
+    if _defer:   # update_and_solve: the reconstruction comes out of the rotation
+        return dict(dp=dp, n=n, k=k, s=s, mr=mr, cf=cf, extra=extra, rcond=rcond, side=side, labels=labels,
+                    top2=top2, sidx=sidx, slab=slab, ldu=ldu, reconstruct=reconstruct, check=check)
     _mark("solve_reconstruct")
     U = reconstruct(want_field or k > 8)
     torch.cuda.current_stream().wait_stream(side)
@@ -547,6 +558,94 @@ def solve_fast(pack, lap, prob, m_use: int | None = None, streaming_block: int |
     field = DeviceField(dp.dims, k, labels, top2, U, recompute=lambda: reconstruct(True))
     field.rcond_dev = rcond
     return field
+
+
+def update_and_solve(pack, image, prob, new_beta: float | None = None, cut_edges=None, *, gap_guard: float = 0.5,
+                     m_use: int | None = None, want_field: bool = False, check: bool = True, out=None,
+                     connectivity=None, weight_mode=None):
+    """``update_basis(pack, image, new_beta, cut_edges)`` followed by
+    ``solve_fast(updated, None, prob, m_use)`` with one pass less over the
+    basis: returns ``(updated_pack, field)``, the same objects the two calls
+    return (V' in full; labels / top-2 / U of the solve on V').
+
+    The seed system only needs V' at the seeds and their stencil neighbours,
+    so it is solved BEFORE the rotation on those rows formed as V[rows] C
+    (a small DMMA product scattered into the V' buffer, which the rotation
+    then overwrites); its coefficients enter the rotation as extra columns
+    of C -- V' coeff = V (C coeff) -- which ride in the padding of the INT8
+    GEMM's last 64-column tile (K = 400: 48 free columns), so the
+    reconstruction (fastrw.py:456-466) costs no pass over V' and no tensor
+    work; a row-wise finalize + argmax (solver.py:55-66, images.py:128-130)
+    reads the N x L products.  gamma > 0 (priors) and the all-/no-seed
+    cases take the two separate calls."""
+    torch = require_cuda()
+    seeds = prob.seeds
+    s = int(seeds.n_seeds)
+    dp0 = _as_device(pack, image, connectivity, weight_mode)
+    if float(prob.gamma) != 0 or s == 0 or s >= dp0.n_vertices:
+        up = update_basis(pack, image, new_beta, cut_edges, gap_guard=gap_guard, out=out,
+                          connectivity=connectivity, weight_mode=weight_mode)
+        return up, solve_fast(up, None, prob, m_use, want_field=want_field, check=check)
+    state = {}
+
+    def pre_rotate(up, dp, Cm, ldp):
+        m, ldv, st = up.m, up.ldv, stream_handle()
+        g_new = up.graph
+        # V' rows at the seeds and their stencil neighbours: V[rows] C
+        _mark("solve_prefill")
+        sidx = torch.from_numpy(np.ascontiguousarray(seeds.seed_indices, dtype=np.int64)).to("cuda")
+        R = 2 * g_new.lattice.ndir + 1
+        ell_idx = torch.empty((s, R), dtype=torch.int64, device="cuda")
+        ell_val = torch.empty((s, R), dtype=torch.float64, device="cuda")
+        lat = g_new.lattice.c_struct()
+        _lib.call("swb_seed_rows", C.byref(lat), ptr(g_new.what), ptr(g_new.diag), ptr(sidx), s, ptr(ell_idx),
+                  ptr(ell_val), st)
+        rows = torch.where(ell_idx >= 0, ell_idx, sidx[:, None]).reshape(-1)
+        vg = dp.V.index_select(0, rows)
+        vp = torch.zeros_like(vg)
+        _lib.call("swb_gemm_nn", ptr(vg), ldv, ptr(Cm), ldp, rows.numel(), m, m, ptr(vp), ldv, 0, st)
+        up.V.index_copy_(0, rows, vp)
+        d = solve_fast(up, None, prob, m_use, want_field=want_field, check=check, _defer=True)
+        k, mr, cf = d["k"], d["mr"], d["cf"]
+        # C_aug = [C | C[:, :mr] coeff]; V C_aug[:, m:] = V' coeff
+        m2 = m + k
+        ldca = round_up(m2, 2)
+        c_aug = torch.zeros((m, ldca), dtype=torch.float64, device="cuda")
+        c_aug[:, :m].copy_(Cm[:, :m])
+        ccf = torch.empty((m, round_up(k, 2)), dtype=torch.float64, device="cuda")
+        _lib.call("swb_gemm_nn", ptr(Cm), ldp, ptr(cf), k, m, mr, k, ptr(ccf), ccf.shape[1], 0, st)
+        c_aug[:, m:m2].copy_(ccf[:, :k])
+        uraw = torch.empty((up.n_vertices, k), dtype=torch.float64, device="cuda")
+        state.update(d=d, uraw=uraw)
+        return m2, c_aug, ldca, uraw, k
+
+    up = update_basis(pack, image, new_beta, cut_edges, gap_guard=gap_guard, out=out, connectivity=connectivity,
+                      weight_mode=weight_mode, _pre_rotate=pre_rotate)
+    d, uraw = state["d"], state["uraw"]
+    n, k, dev = d["n"], d["k"], d["dp"]
+    labels, top2, ldu = d["labels"], d["top2"], d["ldu"]
+    _mark("solve_finalize")
+    U = torch.empty((n, ldu), dtype=torch.float64, device="cuda") if (want_field or k > 8) else None
+    if k > 8:   # the many-label finalize works in place
+        U[:, :k].copy_(uraw)
+        _lib.call("swb_finalize_label", 0, n, k, ptr(U), ldu, ptr(d["extra"]), dev.dnorm, ptr(dev.d_sqrt_dev),
+                  ptr(U), ldu, ptr(labels), ptr(top2), stream_handle())
+    else:
+        _lib.call("swb_finalize_label", 0, n, k, ptr(uraw), k, ptr(d["extra"]), dev.dnorm, ptr(dev.d_sqrt_dev),
+                  ptr(U), ldu, ptr(labels), ptr(top2), stream_handle())
+    _lib.call("swb_apply_seeds", ptr(d["sidx"]), ptr(d["slab"]), d["s"], 0, n, k, ptr(U), ldu, ptr(labels),
+              ptr(top2), stream_handle())
+    torch.cuda.current_stream().wait_stream(d["side"])
+    _mark("solve_end")
+    if check:
+        rc = float(d["rcond"].item())
+        if _lib.load().swb_check_rcond(rc) != 0:
+            raise SingularSmallSystem(
+                f"seed system numerically singular (cond ~ {1.0 / max(rc, 1e-300):.3e})",
+                condition=1.0 / max(rc, 1e-300))
+    field = DeviceField(dev.dims, k, labels, top2, U, recompute=lambda: d["reconstruct"](True))
+    field.rcond_dev = d["rcond"]
+    return up, field
 
 
 def hard_labels(field) -> LabelMap:

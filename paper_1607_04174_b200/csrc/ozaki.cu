@@ -393,7 +393,8 @@ __device__ unsigned long long oz_prof[12];
 __global__ void __launch_bounds__(OZ_THREADS, 1)
 oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, const uint8_t* __restrict__ bsl,
                const double* __restrict__ sb, int64_t rows, int64_t M2, int64_t nkc, int64_t n_rb, int64_t n_cb,
-               double* __restrict__ out, int64_t ldo, int32_t* __restrict__ raw) {
+               double* __restrict__ out, int64_t ldo, int32_t* __restrict__ raw, int64_t ncol_main,
+               double* __restrict__ out2, int64_t ldo2) {
   extern __shared__ __align__(1024) uint8_t oz_smem[];
   uint8_t* stages = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem) + 127) & ~uintptr_t(127));
   __shared__ __align__(8) uint64_t full_bar[OZ_STAGES], empty_bar[OZ_STAGES], tfull_bar, tempty_bar;
@@ -602,16 +603,21 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
 #endif
       if (r >= rows) continue;
       double* orow = out + r * ldo + gc0;
-      if (gc0 + OZ_EPI_COLS <= M2) {
+      if (gc0 + OZ_EPI_COLS <= ncol_main) {
 #pragma unroll
         for (int q = 0; q < OZ_EPI_COLS; q += 2) {
           const double2 sc = *reinterpret_cast<const double2*>(sb + gc0 + q);
           *reinterpret_cast<double2*>(orow + q) = make_double2(o[q >> 4][q & 15] * sc.x, o[q >> 4][(q & 15) + 1] * sc.y);
         }
       } else {
+        // the ragged last column tile: columns [ncol_main, M2) (extra B
+        // columns riding in the tile's padding) go to out2
 #pragma unroll
-        for (int q = 0; q < OZ_EPI_COLS; ++q)
-          if (gc0 + q < M2) orow[q] = o[q >> 4][q & 15] * sb[gc0 + q];
+        for (int q = 0; q < OZ_EPI_COLS; ++q) {
+          const int64_t c = gc0 + q;
+          if (c < ncol_main) orow[q] = o[q >> 4][q & 15] * sb[c];
+          else if (c < M2) out2[r * ldo2 + (c - ncol_main)] = o[q >> 4][q & 15] * sb[c];
+        }
       }
     }
 #if OZ_PROF
@@ -721,14 +727,19 @@ extern "C" int swb_oz_split_rows(const double* A, int64_t lda, int64_t nr, int64
   return SWB_OK;
 }
 
-// out[nr x M2] from the digit planes in the workspace (raw: diagnostics).
+// out[nr x M2] from the digit planes in the workspace (raw: diagnostics);
+// with ncol_main < M2 the columns [ncol_main, M2) go to out2 instead.
 int swb_oz_planes_gemm(int64_t nr, int64_t rows, int64_t K, int64_t M2, int buf, double* out, int64_t ldo,
-                       int32_t* raw, void* workspace, size_t workspace_bytes, cudaStream_t st) {
+                       int32_t* raw, void* workspace, size_t workspace_bytes, cudaStream_t st,
+                       int64_t ncol_main = -1, double* out2 = nullptr, int64_t ldo2 = 0) {
   OzLayout o;
   int rc = oz_check(rows, K, M2, workspace, workspace_bytes, &o);
   if (rc) return rc;
+  if (ncol_main < 0) ncol_main = M2;
   if ((!out && !raw) || nr < 0 || nr > o.chunk_rows || buf < 0 || buf >= o.nbuf) return SWB_INVALID_PARAM;
-  if (out && (ldo < M2 || (ldo & 1) || (reinterpret_cast<uintptr_t>(out) & 15))) return SWB_INVALID_PARAM;
+  if (ncol_main > M2 || (ncol_main < M2 && (!out2 || ldo2 < M2 - ncol_main))) return SWB_INVALID_PARAM;
+  // 32-column epilogue segments below ncol_main use 16-B stores
+  if (out && (ldo < ncol_main || (ldo & 1) || (reinterpret_cast<uintptr_t>(out) & 15))) return SWB_INVALID_PARAM;
   if (nr == 0) return SWB_OK;
   const OzPtrs q = oz_ptrs(o, workspace, buf);
   const int64_t n_rb = (nr + OZ_BM - 1) / OZ_BM;
@@ -736,7 +747,8 @@ int swb_oz_planes_gemm(int64_t nr, int64_t rows, int64_t K, int64_t M2, int buf,
   const int64_t grid_cap = swb_sm_count();
   const int64_t grid = tiles < grid_cap ? tiles : grid_cap;
   oz_gemm_kernel<<<static_cast<unsigned>(grid), OZ_THREADS, OZ_SMEM, st>>>(q.a_sl, q.sa, q.b_sl, q.sb, nr, M2, o.nkc,
-                                                                           n_rb, o.n_cb, out, ldo, raw);
+                                                                           n_rb, o.n_cb, out, ldo, raw, ncol_main,
+                                                                           out2, ldo2);
   SWB_CHECK_LAUNCH();
   return SWB_OK;
 }
@@ -745,6 +757,14 @@ extern "C" int swb_oz_gemm_planes(int64_t nr, int64_t rows, int64_t K, int64_t M
                                   int64_t ldo, void* workspace, size_t workspace_bytes, void* stream) {
   return swb_oz_planes_gemm(nr, rows, K, M2, buf, out, ldo, nullptr, workspace, workspace_bytes,
                             swb_stream(stream));
+}
+
+extern "C" int swb_oz_gemm_planes_split(int64_t nr, int64_t rows, int64_t K, int64_t M2, int buf, double* out,
+                                        int64_t ldo, int64_t ncol_main, double* out2, int64_t ldo2, void* workspace,
+                                        size_t workspace_bytes, void* stream) {
+  if (ncol_main < 0) return SWB_INVALID_PARAM;
+  return swb_oz_planes_gemm(nr, rows, K, M2, buf, out, ldo, nullptr, workspace, workspace_bytes,
+                            swb_stream(stream), ncol_main, out2, ldo2);
 }
 
 #if OZ_PROF

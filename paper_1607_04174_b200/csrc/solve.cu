@@ -940,6 +940,82 @@ extern "C" int swb_reconstruct_label(const double* V, int64_t ldv, int64_t row_b
   return SWB_OK;
 }
 
+// finalize + argmax of a reconstruction computed elsewhere (update_and_solve:
+// the rotation GEMM's extra columns hold V (C coeff) = V' coeff): one thread
+// per row, the same operations in the same order as reconstruct_dmma_kernel's
+// epilogue (fastrw.py:462-464, solver.py:55-66, images.py:128-130).
+template <int L>
+__global__ void __launch_bounds__(256) finalize_rows_kernel(int64_t rows, const double* __restrict__ uraw,
+                                                             int64_t ldr, const double* __restrict__ extra,
+                                                             double dnorm, const double* __restrict__ d_sqrt,
+                                                             double* __restrict__ U, int64_t ldu,
+                                                             int32_t* __restrict__ labels, double* __restrict__ top2) {
+  const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (r >= rows) return;
+  double v[L];
+#pragma unroll
+  for (int k = 0; k < L; ++k) v[k] = uraw[r * ldr + k];
+  const double ds = d_sqrt[r];
+  const double g = ds / dnorm;
+  double sum = 0.0;
+#pragma unroll
+  for (int k = 0; k < L; ++k) {
+    double u = (v[k] + g * (extra ? extra[k] : 0.0)) / ds;
+    u = u > 0.0 ? u : (u != u ? u : 0.0);
+    v[k] = u;
+    sum += u;
+  }
+  if (sum == 0.0) {
+#pragma unroll
+    for (int k = 0; k < L; ++k) v[k] = 1.0 / double(L);
+    sum = 1.0;
+  }
+  int best = 0;
+  double p1 = -1.0, p2 = -1.0;
+#pragma unroll
+  for (int k = 0; k < L; ++k) {
+    const double p = v[k] / sum;
+    v[k] = p;
+    if (p > p1) { p2 = p1; p1 = p; best = k; } else if (p > p2) p2 = p;
+  }
+  labels[r] = best;
+  if (top2) top2[r] = L > 1 ? p1 - p2 : 1.0;
+  if (U) {
+#pragma unroll
+    for (int k = 0; k < L; ++k) U[r * ldu + k] = v[k];
+  }
+}
+
+extern "C" int swb_finalize_label(int64_t r_begin, int64_t r_end, int64_t L, const double* uraw, int64_t ldr,
+                                  const double* extra, double dnorm, const double* d_sqrt, double* U, int64_t ldu,
+                                  int32_t* labels, double* top2, void* stream) {
+  if (!uraw || !d_sqrt || !labels || L <= 0 || r_end < r_begin || ldr < L || !(dnorm > 0.0) || (U && ldu < L))
+    return SWB_INVALID_PARAM;
+  const int64_t rows = r_end - r_begin;
+  if (rows == 0) return SWB_OK;
+  cudaStream_t st = swb_stream(stream);
+  const double* ds = d_sqrt + r_begin;
+  if (L <= 8) {
+    const unsigned grid = static_cast<unsigned>((rows + 255) / 256);
+    switch (L) {
+#define SWB_FR(n) case n: finalize_rows_kernel<n><<<grid, 256, 0, st>>>(rows, uraw, ldr, extra, dnorm, ds, U, ldu, labels, top2); break;
+      SWB_FR(1) SWB_FR(2) SWB_FR(3) SWB_FR(4) SWB_FR(5) SWB_FR(6) SWB_FR(7) SWB_FR(8)
+#undef SWB_FR
+      default: break;
+    }
+    SWB_CHECK_LAUNCH();
+    return SWB_OK;
+  }
+  // many labels: in place (U must be the raw buffer), warp per row
+  if (U != uraw || ldu != ldr) return SWB_INVALID_PARAM;
+  const int fg = swb_sm_count() * 8;
+  if (L <= 32) finalize_many_reg_kernel<1><<<fg, 256, 0, st>>>(r_begin, r_end, L, extra, dnorm, d_sqrt, U, ldu, labels, top2);
+  else if (L <= 64) finalize_many_reg_kernel<2><<<fg, 256, 0, st>>>(r_begin, r_end, L, extra, dnorm, d_sqrt, U, ldu, labels, top2);
+  else finalize_many_kernel<<<fg, 256, 0, st>>>(r_begin, r_end, L, extra, dnorm, d_sqrt, U, ldu, labels, top2);
+  SWB_CHECK_LAUNCH();
+  return SWB_OK;
+}
+
 extern "C" int swb_apply_seeds(const int64_t* seed_idx, const int32_t* seed_lab, int64_t S, int64_t r_begin,
                                int64_t r_end, int64_t L, double* U, int64_t ldu, int32_t* labels, double* top2,
                                void* stream) {

@@ -71,29 +71,38 @@ class Workspace:
 WORKSPACE = Workspace()
 
 
-def rotate_rows(V, ldv: int, Cm, ldc: int, rows: int, m: int, out, ldo: int, stream=None, mark=None) -> None:
+def rotate_rows(V, ldv: int, Cm, ldc: int, rows: int, m: int, out, ldo: int, stream=None, mark=None,
+                m2: int | None = None, out2=None, ldo2: int = 0) -> None:
     """out[rows x m] = V[rows x m] Cm[m x m] (the first-order rotation,
     reference update.py V' = V C): on the INT8 tensor cores (csrc/ozaki.cu,
     FP64-accurate digit scheme) for m <= 512, else the FP64 DMMA GEMM.
     ``mark(name)`` (the phase timer) brackets the digit split and the GEMM
     of every row chunk.  SWB_ROTATION=dmma forces the DMMA GEMM
-    (measurement knob)."""
+    (measurement knob).
+
+    ``m2 > m``: Cm is m x m2 and its columns [m, m2) are extra products
+    V Cm[:, m:m2] written to ``out2`` (ld ``ldo2``); on the INT8 path they
+    ride in the last column tile's padding (update_and_solve)."""
     import os
     from . import _lib
     st = stream if stream is not None else stream_handle()
     if rows <= 0:
         return
+    m2 = m if m2 is None else int(m2)
     if m > 512 or os.environ.get("SWB_ROTATION", "").startswith("d"):
         _lib.call("swb_gemm_nn", ptr(V), ldv, ptr(Cm), ldc, rows, m, m, ptr(out), ldo, 0, st)
+        if m2 > m:
+            cx = Cm[:m, m:m2].contiguous()
+            _lib.call("swb_gemm_nn", ptr(V), ldv, ptr(cx), m2 - m, rows, m, m2 - m, ptr(out2), ldo2, 0, st)
         return
     mark = mark or (lambda name: None)
     torch = torch_mod()
-    nb = _lib.size("swb_oz_gemm_nn_workspace_bytes", rows, m, m)
+    nb = _lib.size("swb_oz_gemm_nn_workspace_bytes", rows, m, m2)
     ws = WORKSPACE.get("oz_gemm", nb)
-    chunk = _lib.size("swb_oz_chunk_rows", rows, m, m)
+    chunk = _lib.size("swb_oz_chunk_rows", rows, m, m2)
     nch = (rows + chunk - 1) // chunk
     mark("rotate_split")
-    _lib.call("swb_oz_split_cols", ptr(Cm), ldc, rows, m, m, ptr(ws), ws.numel(), st)
+    _lib.call("swb_oz_split_cols", ptr(Cm), ldc, rows, m, m2, ptr(ws), ws.numel(), st)
     main = torch.cuda.current_stream()
     # SWB_OZ_SERIAL=1 (measurement knob): split and GEMM in turn on one stream
     aux = _aux_stream() if nch > 1 and os.environ.get("SWB_OZ_SERIAL") != "1" else main
@@ -109,7 +118,7 @@ def rotate_rows(V, ldv: int, Cm, ldc: int, rows: int, m: int, out, ldo: int, str
         if i >= 2:
             aux.wait_event(ev_gemm[i & 1])        # the buffer's previous GEMM is done
         _lib.call("swb_oz_split_rows", C.c_void_p(V.data_ptr() + 8 * r0 * ldv), ldv, min(chunk, rows - r0), rows,
-                  m, m, i & 1, ptr(ws), ws.numel(), C.c_void_p(aux.cuda_stream))
+                  m, m2, i & 1, ptr(ws), ws.numel(), C.c_void_p(aux.cuda_stream))
         ev_split[i & 1].record(aux)
 
     split(0)
@@ -119,8 +128,13 @@ def rotate_rows(V, ldv: int, Cm, ldc: int, rows: int, m: int, out, ldo: int, str
         r0 = i * chunk
         main.wait_event(ev_split[i & 1])
         mark("rotate_gemm")
-        _lib.call("swb_oz_gemm_planes", min(chunk, rows - r0), rows, m, m, i & 1,
-                  C.c_void_p(out.data_ptr() + 8 * r0 * ldo), ldo, ptr(ws), ws.numel(), st)
+        if m2 > m:
+            _lib.call("swb_oz_gemm_planes_split", min(chunk, rows - r0), rows, m, m2, i & 1,
+                      C.c_void_p(out.data_ptr() + 8 * r0 * ldo), ldo, m, C.c_void_p(out2.data_ptr() + 8 * r0 * ldo2),
+                      ldo2, ptr(ws), ws.numel(), st)
+        else:
+            _lib.call("swb_oz_gemm_planes", min(chunk, rows - r0), rows, m, m, i & 1,
+                      C.c_void_p(out.data_ptr() + 8 * r0 * ldo), ldo, ptr(ws), ws.numel(), st)
         ev_gemm[i & 1].record(main)
         mark("rotate_join")
 
