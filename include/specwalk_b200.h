@@ -135,6 +135,11 @@ int swb_gemm_nn_ex(const double* A, int64_t lda, const double* B, int64_t ldb, i
 size_t swb_oz_gemm_nn_workspace_bytes(int64_t rows, int64_t K, int64_t M2);
 int swb_oz_gemm_nn(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows, int64_t K,
                    int64_t M2, double* out, int64_t ldo, void* workspace, size_t workspace_bytes, void* stream);
+/* The same with the product's columns [ncol_main, M2) written to out2 (ld
+ * ldo2) instead of out (swb_update_and_solve's extra columns C coeff). */
+int swb_oz_gemm_nn_split(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows, int64_t K,
+                         int64_t M2, int64_t ncol_main, double* out, int64_t ldo, double* out2, int64_t ldo2,
+                         void* workspace, size_t workspace_bytes, void* stream);
 /* The same in parts (the host loop of swb_oz_gemm_nn, exposed so callers can
  * time the digit split and the GEMM separately): B's planes once, then per
  * row chunk of at most swb_oz_chunk_rows(rows, K, M2) rows the chunk's A
@@ -429,6 +434,27 @@ int swb_rw_solve(const swb_lattice* lat, const double* what, const double* diag,
                  const int64_t* seed_idx, const int32_t* seed_lab, int64_t S, int64_t K, double gamma,
                  const double* priors, int64_t ldp, int32_t* labels_out, double* top2_out, double* U_out,
                  int64_t ldu, double* rcond_host, void* workspace, size_t workspace_bytes, void* stream);
+
+/* The first-order update (swb_update_first_order) and the gamma = 0 RW solve
+ * on the updated basis (swb_rw_solve with m_use columns) in one call, with
+ * one pass less over the basis (api.update_and_solve): the seed system is
+ * solved before the rotation on the V' rows of the seeds' stencil
+ * neighbourhoods formed as V[rows] C, and its coefficients ride as K extra
+ * columns of C in the INT8 rotation (swb_oz_gemm_nn_split), whose products
+ * V (C coeff) = V' coeff are finalized (swb_finalize_label) into labels_out /
+ * top2_out / U_out (U_out optional for K <= 8).  V_out, lambda_out,
+ * order_out, d_sqrt_out and vtg_out are swb_update_first_order's outputs.
+ * Synchronous (two host reads): SWB_DEGENERATE_GRAPH, SWB_INVALID_PARAM for
+ * unsorted / out-of-range seeds, SWB_SINGULAR_SMALL_SYSTEM (rcond_host). */
+size_t swb_update_and_solve_workspace_bytes(const swb_lattice* lat, int64_t M, int64_t m_use, int64_t S, int64_t K,
+                                            int64_t ldv);
+int swb_update_and_solve(const swb_lattice* lat, const double* image, double beta_old, double beta_new,
+                         const uint8_t* cut_old, const uint8_t* cut_new, const double* V, int64_t ldv,
+                         const double* lambda_old, int64_t M, double gap_guard, double* V_out, double* lambda_out,
+                         int64_t* order_out, double* d_sqrt_out, double* vtg_out, int64_t m_use,
+                         const int64_t* seed_idx, const int32_t* seed_lab, int64_t S, int64_t K, int32_t* labels_out,
+                         double* top2_out, double* U_out, int64_t ldu, double* rcond_host, void* workspace,
+                         size_t workspace_bytes, void* stream);
 
 /* ---- small helpers used by the host layer --------------------------- */
 /* out = sum_x v[x]^2 over n entries (deterministic). */

@@ -70,6 +70,12 @@ SIGNATURES = {
     "swb_update_workspace_bytes": (c_sz, [C.POINTER(Lattice), c_i64]),
     "swb_update_first_order": (C.c_int, [C.POINTER(Lattice), c_vp, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64,
                                          c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "swb_update_and_solve_workspace_bytes": (c_sz, [C.POINTER(Lattice), c_i64, c_i64, c_i64, c_i64, c_i64]),
+    "swb_update_and_solve": (C.c_int, [C.POINTER(Lattice), c_vp, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64,
+                                       c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp,
+                                       c_vp, c_i64, c_vp, c_vp, c_sz, c_vp]),
+    "swb_oz_gemm_nn_split": (C.c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,
+                                       c_vp, C.c_size_t, c_vp]),
     "swb_rw_solve_workspace_bytes": (c_sz, [C.POINTER(Lattice), c_i64, c_i64, c_i64, c_i64, C.c_int]),
     "swb_rw_solve": (C.c_int, [C.POINTER(Lattice), c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp,
                                c_vp, c_i64, c_i64, c_dbl, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_sz,

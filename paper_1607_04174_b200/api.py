@@ -427,7 +427,7 @@ def _ell_from_lap(lap, seed_idx: np.ndarray):
 
 
 def solve_fast(pack, lap, prob, m_use: int | None = None, streaming_block: int | None = None,
-               *, want_field: bool = False, check: bool = True, _defer: bool = False) -> DeviceField:
+               *, want_field: bool = False, check: bool = True, _defer: bool = False, _sidx=None) -> DeviceField:
     """fastrw.py:352-467 on the device.
 
     ``pack``: DevicePack / RefreshedPack / UpdatedPack, or a host pack
@@ -458,7 +458,8 @@ def solve_fast(pack, lap, prob, m_use: int | None = None, streaming_block: int |
     gamma = float(prob.gamma)
     st = stream_handle()
     _mark("solve_seeds")
-    sidx = torch.from_numpy(np.ascontiguousarray(seeds.seed_indices, dtype=np.int64)).to("cuda")
+    sidx = _sidx if _sidx is not None else \
+        torch.from_numpy(np.ascontiguousarray(seeds.seed_indices, dtype=np.int64)).to("cuda")
     slab = torch.from_numpy(np.ascontiguousarray(seeds.seed_labels, dtype=np.int32)).to("cuda")
     labels = torch.empty(n, dtype=torch.int32, device="cuda")
     top2 = torch.empty(n, dtype=torch.float64, device="cuda")
@@ -605,7 +606,7 @@ def update_and_solve(pack, image, prob, new_beta: float | None = None, cut_edges
         vp = torch.zeros_like(vg)
         _lib.call("swb_gemm_nn", ptr(vg), ldv, ptr(Cm), ldp, rows.numel(), m, m, ptr(vp), ldv, 0, st)
         up.V.index_copy_(0, rows, vp)
-        d = solve_fast(up, None, prob, m_use, want_field=want_field, check=check, _defer=True)
+        d = solve_fast(up, None, prob, m_use, want_field=want_field, check=check, _defer=True, _sidx=sidx)
         k, mr, cf = d["k"], d["mr"], d["cf"]
         # C_aug = [C | C[:, :mr] coeff]; V C_aug[:, m:] = V' coeff
         m2 = m + k

@@ -791,11 +791,28 @@ extern "C" int64_t swb_oz_chunk_rows(int64_t rows, int64_t K, int64_t M2) {
 // the GEMM of chunk i runs (one split block fits beside a GEMM CTA on every
 // SM: 96 + 160 registers x threads, 47 + 173 KB shared memory), so only the
 // first chunk's split is exposed.
+extern "C" int swb_oz_gemm_nn_split(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows,
+                                    int64_t K, int64_t M2, int64_t ncol_main, double* out, int64_t ldo, double* out2,
+                                    int64_t ldo2, void* workspace, size_t workspace_bytes, void* stream);
+
 extern "C" int swb_oz_gemm_nn(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows, int64_t K,
                               int64_t M2, double* out, int64_t ldo, void* workspace, size_t workspace_bytes,
                               void* stream) {
+  return swb_oz_gemm_nn_split(A, lda, B, ldb, rows, K, M2, M2, out, ldo, nullptr, 0, workspace, workspace_bytes,
+                              stream);
+}
+
+// The same with the product's columns [ncol_main, M2) written to out2 (ld
+// ldo2) instead of out: update_and_solve's extra columns C coeff.
+extern "C" int swb_oz_gemm_nn_split(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows,
+                                    int64_t K, int64_t M2, int64_t ncol_main, double* out, int64_t ldo, double* out2,
+                                    int64_t ldo2, void* workspace, size_t workspace_bytes, void* stream) {
   if (rows == 0) return SWB_OK;
-  if (!A || !out) return SWB_INVALID_PARAM;
+  if (!A || !out || ncol_main < 0 || ncol_main > M2) return SWB_INVALID_PARAM;
+  auto gemm = [&](int64_t nr, int buf, int64_t r0) {
+    return swb_oz_planes_gemm(nr, rows, K, M2, buf, out + r0 * ldo, ldo, nullptr, workspace, workspace_bytes,
+                              swb_stream(stream), ncol_main, out2 ? out2 + r0 * ldo2 : nullptr, ldo2);
+  };
   int rc;
   if ((rc = swb_oz_split_cols(B, ldb, rows, K, M2, workspace, workspace_bytes, stream))) return rc;
   const int64_t chunk = swb_oz_chunk_rows(rows, K, M2);
@@ -808,8 +825,7 @@ extern "C" int swb_oz_gemm_nn(const double* A, int64_t lda, const double* B, int
       const int64_t r0 = i * chunk, nr = rows - r0 < chunk ? rows - r0 : chunk;
       if ((rc = swb_oz_split_rows(A + r0 * lda, lda, nr, rows, K, M2, 0, workspace, workspace_bytes, stream)))
         return rc;
-      if ((rc = swb_oz_gemm_planes(nr, rows, K, M2, 0, out + r0 * ldo, ldo, workspace, workspace_bytes, stream)))
-        return rc;
+      if ((rc = gemm(nr, 0, r0))) return rc;
     }
     return SWB_OK;
   }
@@ -852,9 +868,7 @@ extern "C" int swb_oz_gemm_nn(const double* A, int64_t lda, const double* B, int
     if (i + 1 < nch && (rc = split(i + 1))) return rc;
     const int64_t r0 = i * chunk, nr = rows - r0 < chunk ? rows - r0 : chunk;
     SWB_CUDA_TRY(cudaStreamWaitEvent(st, ev_split[i & 1], 0));
-    if ((rc = swb_oz_gemm_planes(nr, rows, K, M2, int(i & 1), out + r0 * ldo, ldo, workspace, workspace_bytes,
-                                 stream)))
-      return rc;
+    if ((rc = gemm(nr, int(i & 1), r0))) return rc;
     SWB_CUDA_TRY(cudaEventRecord(ev_gemm[i & 1], st));
   }
   return SWB_OK;

@@ -11,6 +11,9 @@
 //   swb_rw_solve             fastrw.py:352-467 + solver.py:55-66 +
 //                            images.py:128-130 (labels), with the reference's
 //                            SingularSmallSystem check (fastrw.py:340)
+//   swb_update_and_solve     the two in one call with one pass less over the
+//                            basis (api.update_and_solve): seed system first,
+//                            reconstruction as extra rotation columns
 #include "swb_common.cuh"
 #include <cstdlib>
 
@@ -75,7 +78,7 @@ bool rotation_on_int8(int64_t M) {
   return !dmma && M <= 512;
 }
 
-UpdateLayout update_layout(const swb_lattice* lat, int64_t M, void* ws) {
+UpdateLayout update_layout(const swb_lattice* lat, int64_t M, void* ws, bool rotation_ws = true) {
   LatticeDev L{};
   swb_make_lattice(lat, &L);
   const int64_t N = L.nx * L.ny * L.nz;
@@ -99,7 +102,7 @@ UpdateLayout update_layout(const swb_lattice* lat, int64_t M, void* ws) {
   u.tn_bytes = swb_gemm_tn_workspace_bytes(N, M, M);
   u.tn_ws = c.take<char>(u.tn_bytes);
   u.ss_ws = c.take<char>(256 * 8);
-  u.oz_bytes = rotation_on_int8(M) ? swb_oz_gemm_nn_workspace_bytes(N, M, M) : 0;
+  u.oz_bytes = rotation_ws && rotation_on_int8(M) ? swb_oz_gemm_nn_workspace_bytes(N, M, M) : 0;
   u.oz_ws = c.take<char>(u.oz_bytes);
   u.total = c.off + 256;
   return u;
@@ -264,6 +267,191 @@ extern "C" int swb_rw_solve(const swb_lattice* lat, const double* what, const do
   if ((rc = swb_reconstruct_label(V, ldv, 0, 0, N, m_use, w.coeff, with_priors ? nullptr : w.extra, dnorm, d_sqrt, K,
                                   U_out, ldu, labels_out, top2_out, stream)))
     return rc;
+  if ((rc = swb_apply_seeds(seed_idx, seed_lab, S, 0, N, K, U_out, ldu, labels_out, top2_out, stream))) return rc;
+  double rc_h = 0.0;
+  SWB_CUDA_TRY(cudaMemcpyAsync(&rc_h, rcond_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+  SWB_CUDA_TRY(cudaStreamSynchronize(st));
+  if (rcond_host) *rcond_host = rc_h;
+  return swb_check_rcond(rc_h);
+}
+
+// ---------------------------------------------------------------------------
+// update + solve in one pass over the basis (api.update_and_solve)
+// ---------------------------------------------------------------------------
+extern "C" int swb_oz_gemm_nn_split(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t rows,
+                                    int64_t K, int64_t M2, int64_t ncol_main, double* out, int64_t ldo, double* out2,
+                                    int64_t ldo2, void* workspace, size_t workspace_bytes, void* stream);
+
+namespace {
+
+// row e = s R + t of the seed stencil neighbourhoods: ell_idx[e], or the seed
+// itself for an off-grid (-1) entry
+__device__ __forceinline__ int64_t ell_row(const int64_t* ell_idx, const int64_t* seed_idx, int64_t e, int64_t R) {
+  const int64_t r = ell_idx[e];
+  return r >= 0 ? r : seed_idx[e / R];
+}
+
+__global__ void gather_ell_rows_kernel(const double* __restrict__ V, int64_t ldv, const int64_t* __restrict__ ell_idx,
+                                       const int64_t* __restrict__ seed_idx, int64_t E, int64_t R, int64_t M,
+                                       double* __restrict__ out) {
+  for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+    const double* src = V + ell_row(ell_idx, seed_idx, e, R) * ldv;
+    for (int64_t j = threadIdx.x; j < ldv; j += blockDim.x) out[e * ldv + j] = j < M ? src[j] : 0.0;
+  }
+}
+
+// identical rows may appear several times: every writer stores the same values
+__global__ void scatter_ell_rows_kernel(const double* __restrict__ src, int64_t ldv, const int64_t* __restrict__ ell_idx,
+                                        const int64_t* __restrict__ seed_idx, int64_t E, int64_t R, int64_t M,
+                                        double* __restrict__ V) {
+  for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+    double* dst = V + ell_row(ell_idx, seed_idx, e, R) * ldv;
+    for (int64_t j = threadIdx.x; j < M; j += blockDim.x) dst[j] = src[e * ldv + j];
+  }
+}
+
+// C_aug[i, :] = [C[i, :M] | ccf[i, :K] | 0]
+__global__ void aug_kernel(const double* __restrict__ C, int64_t ldp, const double* __restrict__ ccf, int64_t ldk,
+                           int64_t M, int64_t K, double* __restrict__ caug, int64_t ldca) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < M * ldca; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / ldca, j = e % ldca;
+    caug[e] = j < M ? C[i * ldp + j] : (j < M + K ? ccf[i * ldk + (j - M)] : 0.0);
+  }
+}
+
+struct FusedLayout {
+  UpdateLayout u;
+  SolveLayout s;
+  double *rows_v, *rows_vp, *ccf, *caug, *uraw, *dnorm;
+  void* oz_ws;
+  size_t oz_bytes, total;
+};
+
+FusedLayout fused_layout(const swb_lattice* lat, int64_t M, int64_t m_use, int64_t S, int64_t K, int64_t ldv,
+                         void* ws) {
+  LatticeDev L{};
+  swb_make_lattice(lat, &L);
+  const int64_t N = L.nx * L.ny * L.nz;
+  const int64_t R = 2 * L.ndir + 1;
+  FusedLayout f{};
+  f.u = update_layout(lat, M, ws, false);   // the split-output rotation below has its own workspace
+  char* base = ws ? static_cast<char*>(ws) + f.u.total : nullptr;
+  f.s = solve_layout(L, M, m_use, S, K, false, base);
+  Carver c{base ? base + f.s.total : nullptr};
+  const int64_t ldca = (M + K + 1) / 2 * 2, ldk = (K + 1) / 2 * 2;
+  f.rows_v = c.take<double>(size_t(S) * R * ldv);
+  f.rows_vp = c.take<double>(size_t(S) * R * ldv);
+  f.ccf = c.take<double>(size_t(M) * ldk);
+  f.caug = c.take<double>(size_t(M) * ldca);
+  f.uraw = c.take<double>(size_t(N) * ldk);
+  f.dnorm = c.take<double>(1);
+  f.oz_bytes = rotation_on_int8(M) ? swb_oz_gemm_nn_workspace_bytes(N, M, M + K) : 0;
+  f.oz_ws = c.take<char>(f.oz_bytes);
+  f.total = f.u.total + f.s.total + c.off + 256;
+  return f;
+}
+
+}  // namespace
+
+extern "C" size_t swb_update_and_solve_workspace_bytes(const swb_lattice* lat, int64_t M, int64_t m_use, int64_t S,
+                                                       int64_t K, int64_t ldv) {
+  LatticeDev L;
+  if (swb_make_lattice(lat, &L) || M <= 0 || m_use <= 0 || m_use > M || S <= 0 || K <= 0 || ldv < M) return 0;
+  return fused_layout(lat, M, m_use, S, K, ldv, nullptr).total;
+}
+
+extern "C" int swb_update_and_solve(const swb_lattice* lat, const double* image, double beta_old, double beta_new,
+                                    const uint8_t* cut_old, const uint8_t* cut_new, const double* V, int64_t ldv,
+                                    const double* lambda_old, int64_t M, double gap_guard, double* V_out,
+                                    double* lambda_out, int64_t* order_out, double* d_sqrt_out, double* vtg_out,
+                                    int64_t m_use, const int64_t* seed_idx, const int32_t* seed_lab, int64_t S,
+                                    int64_t K, int32_t* labels_out, double* top2_out, double* U_out, int64_t ldu,
+                                    double* rcond_host, void* workspace, size_t workspace_bytes, void* stream) {
+  LatticeDev L;
+  if (swb_make_lattice(lat, &L) || !image || !V || !V_out || V == V_out || !lambda_old || !lambda_out ||
+      !order_out || !d_sqrt_out || !vtg_out || M <= 0 || ldv < M || (ldv & 1) || m_use <= 0 || m_use > M || S <= 0 ||
+      K <= 0 || !seed_idx || !seed_lab || !labels_out)
+    return SWB_INVALID_PARAM;
+  if (m_use < K) return SWB_INSUFFICIENT_BASIS;
+  if (K > 8 && (!U_out || ldu < K || (ldu & 1))) return SWB_INVALID_PARAM;
+  if (!workspace || workspace_bytes < swb_update_and_solve_workspace_bytes(lat, M, m_use, S, K, ldv))
+    return SWB_WORKSPACE_TOO_SMALL;
+  cudaStream_t st = swb_stream(stream);
+  const int64_t N = L.nx * L.ny * L.nz;
+  const int64_t R = 2 * L.ndir + 1, E = S * R;
+  const int64_t ldp = (M + 1) / 2 * 2, ldq = (m_use + 1) / 2 * 2, ldt = (K + 1) / 2 * 2;
+  const int64_t ldca = (M + K + 1) / 2 * 2, ldk = (K + 1) / 2 * 2;
+  FusedLayout f = fused_layout(lat, M, m_use, S, K, ldv, workspace);
+  const UpdateLayout& u = f.u;
+  const SolveLayout& w = f.s;
+  int rc;
+  // ---- the update up to the rotation (swb_update_first_order's sequence) ----
+  if ((rc = swb_graph_build(lat, image, beta_old, cut_old, u.what_o, u.diag_o, u.dsq_o, u.flag, stream))) return rc;
+  if ((rc = swb_graph_build(lat, image, beta_new, cut_new, u.what_n, u.diag_n, d_sqrt_out, u.flag + 1, stream)))
+    return rc;
+  if ((rc = swb_stencil_delta(lat, V, ldv, 0, 0, N, M, u.what_o, u.diag_o, u.what_n, u.diag_n, d_sqrt_out, V_out,
+                              ldv, u.quad, u.norm2, u.vtd, u.st_ws, u.st_bytes, stream)))
+    return rc;
+  if ((rc = swb_gemm_tn(V, ldv, V_out, ldv, N, M, M, 1, u.P, ldp, u.tn_ws, u.tn_bytes, stream))) return rc;
+  if ((rc = swb_update_coeffs(1, u.P, ldp, lambda_old, u.quad, u.norm2, M, gap_guard, u.C, ldp, lambda_out, order_out,
+                              stream)))
+    return rc;
+  if ((rc = swb_sumsq(d_sqrt_out, N, u.dsum, u.ss_ws, 256 * 8, stream))) return rc;
+  vtg_kernel<<<static_cast<unsigned>((M + 255) / 256), 256, 0, st>>>(u.vtd, u.C, ldp, M, u.dsum, vtg_out, f.dnorm);
+  SWB_CHECK_LAUNCH();
+  if (ldv > M) {   // V' pad columns (the seed-row scatter and the rotation write [0, M) only)
+    zero_cols_kernel<<<swb_sm_count() * 4, 256, 0, st>>>(V_out, ldv, N, M);
+    SWB_CHECK_LAUNCH();
+  }
+  // host scalars: ||d_sqrt||, the degenerate-graph flags, seed validity
+  if ((rc = swb_check_seeds(seed_idx, seed_lab, S, N, K, w.dsum + 2, stream))) return rc;
+  double hs[2] = {0.0, 0.0};
+  int32_t hf[2] = {0, 0};
+  SWB_CUDA_TRY(cudaMemcpyAsync(hs, f.dnorm, sizeof(double), cudaMemcpyDeviceToHost, st));
+  SWB_CUDA_TRY(cudaMemcpyAsync(hs + 1, w.dsum + 2, sizeof(double), cudaMemcpyDeviceToHost, st));
+  SWB_CUDA_TRY(cudaMemcpyAsync(hf, u.flag, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  SWB_CUDA_TRY(cudaStreamSynchronize(st));
+  if (hf[0] || hf[1]) return SWB_DEGENERATE_GRAPH;
+  if (hs[1] != 0.0) return SWB_INVALID_PARAM;
+  const double dnorm = hs[0];
+  // ---- the seed system on V' rows formed as V[rows] C ----
+  if ((rc = swb_seed_rows(lat, u.what_n, u.diag_n, seed_idx, S, w.ell_idx, w.ell_val, stream))) return rc;
+  const unsigned eg = static_cast<unsigned>(E < 65535 ? E : 65535);
+  gather_ell_rows_kernel<<<eg, 128, 0, st>>>(V, ldv, w.ell_idx, seed_idx, E, R, M, f.rows_v);
+  SWB_CHECK_LAUNCH();
+  if ((rc = swb_gemm_nn(f.rows_v, ldv, u.C, ldp, E, M, M, f.rows_vp, ldv, 0, stream))) return rc;
+  scatter_ell_rows_kernel<<<eg, 128, 0, st>>>(f.rows_vp, ldv, w.ell_idx, seed_idx, E, R, M, V_out);
+  SWB_CHECK_LAUNCH();
+  if ((rc = swb_seed_project(V_out, ldv, 0, 0, N, m_use, nullptr, seed_idx, seed_lab, S, w.ell_idx, w.ell_val, R,
+                             d_sqrt_out, dnorm, K, w.q_s, ldq, w.b_qn, w.bg, w.lsu, w.dsq_s, stream)))
+    return rc;
+  double* rcond_dev = w.dsum + 1;
+  if ((rc = swb_small_solve(0.0, S, m_use, K, w.q_s, w.b_qn, ldq, w.bg, w.lsu, w.dsq_s, dnorm, seed_lab, lambda_out,
+                            vtg_out, nullptr, ldt, w.coeff, w.extra, rcond_dev, w.ss_ws, w.ss_bytes, stream)))
+    return rc;
+  // ---- C_aug = [C | C[:, :m_use] coeff]; the rotation emits V' and V' coeff ----
+  if ((rc = swb_gemm_nn(u.C, ldp, w.coeff, K, M, m_use, K, f.ccf, ldk, 0, stream))) return rc;
+  aug_kernel<<<swb_sm_count() * 4, 256, 0, st>>>(u.C, ldp, f.ccf, ldk, M, K, f.caug, ldca);
+  SWB_CHECK_LAUNCH();
+  if (f.oz_bytes) {
+    if ((rc = swb_oz_gemm_nn_split(V, ldv, f.caug, ldca, N, M, M + K, M, V_out, ldv, f.uraw, ldk, f.oz_ws,
+                                   f.oz_bytes, stream)))
+      return rc;
+  } else {
+    if ((rc = swb_gemm_nn(V, ldv, u.C, ldp, N, M, M, V_out, ldv, 0, stream))) return rc;
+    if ((rc = swb_gemm_nn(V, ldv, f.ccf, ldk, N, M, K, f.uraw, ldk, 0, stream))) return rc;
+  }
+  // ---- finalize + argmax + seeds ----
+  if (K > 8) {   // the many-label finalize works in place in U
+    SWB_CUDA_TRY(cudaMemcpy2DAsync(U_out, ldu * sizeof(double), f.uraw, ldk * sizeof(double), K * sizeof(double), N,
+                                   cudaMemcpyDeviceToDevice, st));
+    if ((rc = swb_finalize_label(0, N, K, U_out, ldu, w.extra, dnorm, d_sqrt_out, U_out, ldu, labels_out, top2_out,
+                                 stream)))
+      return rc;
+  } else if ((rc = swb_finalize_label(0, N, K, f.uraw, ldk, w.extra, dnorm, d_sqrt_out, U_out, ldu, labels_out,
+                                      top2_out, stream))) {
+    return rc;
+  }
   if ((rc = swb_apply_seeds(seed_idx, seed_lab, S, 0, N, K, U_out, ldu, labels_out, top2_out, stream))) return rc;
   double rc_h = 0.0;
   SWB_CUDA_TRY(cudaMemcpyAsync(&rc_h, rcond_dev, sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -1,4 +1,5 @@
-"""The composite C entry points (swb_update_first_order, swb_rw_solve) --
+"""The composite C entry points (swb_update_first_order, swb_rw_solve,
+swb_update_and_solve) --
 the whole update / whole solve for hosts that bind the C ABI directly --
 against the Python API path (same kernels; tolerance 1e-12) and, through
 it, the oracle."""
@@ -132,3 +133,56 @@ def test_composite_solve_rejects_unsorted_or_duplicate_seeds(cuda_ok):
     sidx_bad = torch.tensor(seeds[::-1].copy(), device="cuda")
     _lib.call("swb_check_seeds", ptr(sidx_bad), ptr(slab), 10, n, 2, ptr(flag), stream_handle())
     assert float(flag.item()) == 1.0
+
+
+@pytest.mark.parametrize("dims,conn,k,m_use", [((12, 10, 8), 6, 2, 36), ((30, 26), 8, 3, 29), ((16, 14, 6), 6, 11, 36)])
+def test_composite_fused_update_and_solve(cuda_ok, dims, conn, k, m_use):
+    """swb_update_and_solve (one call: update + gamma = 0 solve with the
+    reconstruction riding in the rotation) vs swb_update_first_order +
+    swb_rw_solve on the same inputs: V' bit for bit (same digit products),
+    eigenvalues / order / vtg identical, fields to 1e-12, labels off near-ties."""
+    import torch
+    rng, n, image, dp = _case(dims, 36, 12.0, conn=conn)
+    V_out, lam, order, dsq, vtg, dnorm, deg = _update_c(dp, 12.0, 17.0)
+    seeds = np.sort(rng.choice(n, 4 * k + 6, replace=False))
+    labs = np.arange(seeds.size) % k
+    g = DeviceGraph.build(dp.image_dev, dp.lattice, 17.0)
+    lat = dp.lattice.c_struct()
+    m, ldv = dp.m, dp.ldv
+    s = seeds.size
+    sidx = torch.tensor(seeds, dtype=torch.int64, device="cuda")
+    slab = torch.tensor(labs, dtype=torch.int32, device="cuda")
+    # the reference pair at m_use: swb_rw_solve on the updated basis
+    nbytes = _lib.size("swb_rw_solve_workspace_bytes", C.byref(lat), m, m_use, s, k, 0)
+    ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    ldu = round_up(k, 2)
+    labels1 = torch.empty(n, dtype=torch.int32, device="cuda")
+    top2_1 = torch.empty(n, dtype=torch.float64, device="cuda")
+    U1 = torch.empty((n, ldu), dtype=torch.float64, device="cuda")
+    rc1 = C.c_double(0.0)
+    _lib.call("swb_rw_solve", C.byref(lat), ptr(g.what), ptr(g.diag), ptr(g.d_sqrt_dev), ptr(V_out), ldv, ptr(lam),
+              ptr(vtg), m, m_use, ptr(sidx), ptr(slab), s, k, 0.0, None, 0, ptr(labels1), ptr(top2_1), ptr(U1), ldu,
+              C.byref(rc1), ptr(ws), nbytes, stream_handle())
+    # fused
+    V2 = torch.empty_like(dp.V)
+    lam2 = torch.empty(m, dtype=torch.float64, device="cuda")
+    order2 = torch.empty(m, dtype=torch.int64, device="cuda")
+    dsq2 = torch.empty(n, dtype=torch.float64, device="cuda")
+    vtg2 = torch.empty(m, dtype=torch.float64, device="cuda")
+    labels2 = torch.empty(n, dtype=torch.int32, device="cuda")
+    top2_2 = torch.empty(n, dtype=torch.float64, device="cuda")
+    U2 = torch.empty((n, ldu), dtype=torch.float64, device="cuda")
+    nbytes = _lib.size("swb_update_and_solve_workspace_bytes", C.byref(lat), m, m_use, s, k, ldv)
+    ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    rc2 = C.c_double(0.0)
+    _lib.call("swb_update_and_solve", C.byref(lat), ptr(dp.image_dev), 12.0, 17.0, None, None, ptr(dp.V), ldv,
+              ptr(dp.values_dev), m, 0.5, ptr(V2), ptr(lam2), ptr(order2), ptr(dsq2), ptr(vtg2), m_use, ptr(sidx),
+              ptr(slab), s, k, ptr(labels2), ptr(top2_2), ptr(U2), ldu, C.byref(rc2), ptr(ws), nbytes,
+              stream_handle())
+    assert torch.equal(V2[:, :m], V_out[:, :m])
+    assert torch.equal(lam2, lam) and torch.equal(order2, order) and torch.equal(vtg2, vtg)
+    np.testing.assert_allclose(U2[:, :k].cpu().numpy(), U1[:, :k].cpu().numpy(), rtol=0, atol=1e-12)
+    t = top2_1.cpu().numpy()
+    l1, l2 = labels1.cpu().numpy(), labels2.cpu().numpy()
+    assert not ((l1 != l2) & (t >= 1e-9)).any()
+    np.testing.assert_allclose(rc2.value, rc1.value, rtol=1e-6)
