@@ -55,6 +55,8 @@ def parse_args():
     ap.add_argument("--m", type=int, default=None, help="override K")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="time CUDA-graph replays of the step (two chained steps per graph; fixed seeds)")
     ap.add_argument("--profile-steps", type=int, default=0, help="ncu helper: run N steps, no timing")
     ap.add_argument("--sharded", action="store_true", help="use the z-slab sharded path even at N=1")
     ap.add_argument("--method", choices=["first_order", "rayleigh"], default="first_order",
@@ -745,6 +747,38 @@ def run_gpu(args):
         if world > 1:
             dist.barrier()
 
+    captured = None
+    if args.graph:
+        # two chained steps per graph (beta1 then back to beta0: the V' buffers
+        # ping-pong back to where they started); the last pack's eigenvalues
+        # and V'^T g are copied into the first pack's tensors so that every
+        # replay continues the chain (swb.CapturedStep)
+        if not _fused(state):
+            raise SystemExit("--graph: configs whose step is one update_and_solve (c1, c2, c4)")
+        from paper_1607_04174_b200.capture import CapturedStep
+
+        def two_steps():
+            x = state["pack"]
+            x.ensure_vtg()
+            f0 = gpu_step(state, 0)
+            f1 = gpu_step(state, 1)
+            z = state["pack"]
+            x.values_dev.copy_(z.values_dev)
+            x.vtg.copy_(z.vtg)
+            state["pack"], state["spare"] = x, state["spare"]
+            return f0, f1
+
+        captured = CapturedStep(two_steps)
+        args.steps += args.steps % 2
+
+    def run_steps(i0, k):
+        if captured is None:
+            for i in range(k):
+                gpu_step(state, i0 + i)
+        else:
+            for _ in range(k // 2):
+                captured.replay()
+
     # ---- device-resident timed region -------------------------------------
     # (no phase events inside it: the per-phase breakdown comes from a second,
     # untimed pass of the same K steps below)
@@ -756,12 +790,20 @@ def run_gpu(args):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
-    for i in range(args.steps):
-        gpu_step(state, args.warmup + i)
+    run_steps(args.warmup, args.steps)
     e1.record()
     barrier()
     torch.cuda.synchronize()
     launches = lib.swb_launch_count() - launches0
+    if captured is not None:
+        captured.check()
+        # graph replays launch the captured kernels without passing the host
+        # counter: count the library launches of one eager pair of steps
+        c0 = lib.swb_launch_count()
+        gpu_step(state, 0)
+        gpu_step(state, 1)
+        torch.cuda.synchronize()
+        launches = (lib.swb_launch_count() - c0) * (args.steps // 2)
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
     # phase breakdown: the same steps again with CUDA events at every phase
@@ -953,6 +995,7 @@ def run_gpu(args):
                                    f"gamma={state['params']['gamma']} RW solve + expected displacement"),
                    "N": n, "K": m, "labels": state["params"]["labels"], "seeds": int(s),
                    "parallelism": "replicas" if world > 1 else "single",
+                   "cuda_graph": bool(getattr(args, "graph", False)),
                    "l2": "inputs larger than L2 (V = %.1f GB)" % (n * m * 8 / 1e9)},
         "roofline": ({"bound": "hbm", "kernel": "refresh Rayleigh stencil pass (read V once)",
                       "achieved": kernels["stencil_rayleigh"]["gbs"], "peak": hbm, "unit": "GB/s",

@@ -20,6 +20,7 @@ from .device import DeviceGraph, DevicePack, LatticeSpec, to_device
 from .api import (DeviceField, RefreshedPack, UpdatedPack, evict_device_pack, hard_labels, nearest_pack, refresh,
                   refresh_from_set, segment, select_m, solve_fast, update_and_solve, update_basis)
 from .dropin import install
+from .capture import CapturedStep
 from .packs import load_pack, save_pack, xxh64
 from .registration import DevicePriors, DisplacementGrid, expected_displacement, register, similarity_priors
 from .precompute import precompute, smallest_eigs_device

@@ -141,6 +141,11 @@ def rotate_rows(V, ldv: int, Cm, ldc: int, rows: int, m: int, out, ldo: int, str
 
 _AUX = {}
 
+# CUDA-graph capture state (capture.CapturedStep): "record" while its eager
+# warm-up runs (host scalars of the graphs it builds are kept), "on" while
+# the step is being captured (no host reads; checks deferred to replays).
+CAPTURE = {"on": False, "record": False, "dnorm": {}}
+
 
 def _aux_stream():
     """The side stream of the rotation's digit split (one per device)."""
@@ -249,9 +254,16 @@ class DeviceGraph:
 
     @classmethod
     def build(cls, intensities_dev, lattice: LatticeSpec, beta: float, cut_mask_dev=None) -> "DeviceGraph":
+        """Graph coefficients on the device plus two host scalars (||d_sqrt||
+        and the degenerate flag: one small D2H).  While a CapturedStep records
+        its CUDA graph (CAPTURE["on"]) the kernels are captured as usual but
+        the host scalars come from its eager warm-up runs of the same graph
+        (same image buffer, lattice, beta, cut), which already validated it."""
         torch = require_cuda()
         if beta < 0:
             raise InvalidParam(f"beta must be >= 0, got {beta}")
+        key = (intensities_dev.data_ptr(), lattice.dims, lattice.connectivity, lattice.weight_mode, float(beta),
+               cut_mask_dev.data_ptr() if cut_mask_dev is not None else 0)
         n = lattice.n
         what = torch.empty(n * lattice.ndir, dtype=torch.float64, device="cuda")
         diag = torch.empty(n, dtype=torch.float64, device="cuda")
@@ -264,11 +276,18 @@ class DeviceGraph:
         ss = torch.empty(1, dtype=torch.float64, device="cuda")
         ws = WORKSPACE.get("sumsq", 256 * 8)
         _lib.call("swb_sumsq", ptr(d_sqrt), n, ptr(ss), ptr(ws), ws.numel(), st)
+        if CAPTURE["on"]:
+            if key not in CAPTURE["dnorm"]:
+                raise InvalidParam("graph capture: this graph was not built in the eager warm-up")
+            return cls(lattice, beta, what, diag, d_sqrt, CAPTURE["dnorm"][key], cut_mask_dev)
         # one small D2H for the degenerate flag and ||d_sqrt|| (host scalars)
         host = torch.cat([ss, flag[:1].to(torch.float64)]).cpu().numpy()
         if host[1] != 0:
             raise DegenerateGraph("graph has an isolated vertex (zero degree)")
-        return cls(lattice, beta, what, diag, d_sqrt, float(np.sqrt(host[0])), cut_mask_dev)
+        dnorm = float(np.sqrt(host[0]))
+        if CAPTURE["record"]:
+            CAPTURE["dnorm"][key] = dnorm
+        return cls(lattice, beta, what, diag, d_sqrt, dnorm, cut_mask_dev)
 
     @classmethod
     def build_region(cls, intensities_dev, lattice: LatticeSpec, beta: float, u_lo: int, u_hi: int,
