@@ -425,9 +425,17 @@ int run_tn_sym(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64
   auto kern = gemm_tn_sym_kernel<W, TN_STAGES>;
   static int occ_dev[64] = {};
   int& occ = occ_dev[swb_device()];
+  // SWB_TN_OCC=n (measurement knob): at most n CTAs per SM, by padding the
+  // dynamic shared memory, to leave room for a co-running kernel
+  static const size_t smem_req = [] {
+    const char* e = getenv("SWB_TN_OCC");
+    const int cap = e ? atoi(e) : 0;
+    return cap >= 1 && cap <= 3 ? std::max<size_t>(Cf::SMEM, size_t(228 * 1024) / size_t(cap + 1) + 1024)
+                                : size_t(Cf::SMEM);
+  }();
   if (occ == 0 && !size_only) {
-    SWB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cf::SMEM)));
-    SWB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cf::THREADS, Cf::SMEM));
+    SWB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_req)));
+    SWB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cf::THREADS, smem_req));
     if (occ < 1) occ = 1;
   }
   const int slots = swb_sm_count() * (occ > 0 ? occ : 8) * tn_waves();
@@ -449,7 +457,7 @@ int run_tn_sym(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64
   if (size_only) return SWB_OK;
   if (ws_bytes < *need || ws == nullptr) return SWB_WORKSPACE_TOO_SMALL;
   double* partial = reinterpret_cast<double*>(ws);
-  kern<<<n_ctas, Cf::THREADS, Cf::SMEM, st>>>(X, ldx, Y, ldy, rows, M, T, per_full, chunk_full, per_diag, chunk_diag,
+  kern<<<n_ctas, Cf::THREADS, smem_req, st>>>(X, ldx, Y, ldy, rows, M, T, per_full, chunk_full, per_diag, chunk_diag,
                                               partial);
   SWB_CHECK_LAUNCH();
   const int64_t total = int64_t(T * (T + 1) / 2) * Cf::BM * Cf::BN;
