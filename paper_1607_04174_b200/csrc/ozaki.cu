@@ -232,12 +232,15 @@ __device__ __forceinline__ void oz_digits16(const double (&v)[16], double scale,
 // staging tile laid out like the global planes; the block then writes every
 // (chunk, slice) plane segment of its 16 rows as one contiguous 256-byte run.
 // Rows >= rows and k >= K are zero.
-// 4 warps x 4 rows per block, 4 blocks per SM (measured per 1M x 400 rows:
-// 1.41 ms vs 1.59 ms for 8 warps x 4 rows and 2.01 ms for 4 warps x 2 rows)
+// 8 warps x 4 rows per block (32 rows: 512-B plane segments), 2 blocks per
+// SM.  Per 1M x 400 rows alone: 1.23 ms (5.2 TB/s) vs 1.28 ms for 4 warps x
+// 16 rows (the round-1 shape, sized so that one split block co-resided with
+// a GEMM CTA; the wide-MMA GEMM's 168 registers leave no room for that, and
+// under the step's power cap a co-running split costs its own time anyway).
 #ifndef OZ_SLICE_WARPS_CFG
-#define OZ_SLICE_WARPS_CFG 4
-#define OZ_SLICE_ROWS_CFG 16
-#define OZ_SLICE_MINB 5   // <= 96 registers: one split block co-resides with a GEMM CTA
+#define OZ_SLICE_WARPS_CFG 8
+#define OZ_SLICE_ROWS_CFG 32
+#define OZ_SLICE_MINB 2
 #endif
 constexpr int OZ_SLICE_WARPS = OZ_SLICE_WARPS_CFG;
 constexpr int OZ_SLICE_ROWS = OZ_SLICE_ROWS_CFG;
