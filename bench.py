@@ -23,6 +23,11 @@ from __future__ import annotations
 import argparse
 import json
 import os
+
+# with SWB_EMIT=1 the c4 step keeps two 54 GB bases and the rotation's 46 GB
+# of digit planes resident; expandable segments keep the allocator's freed
+# setup temporaries from fragmenting HBM around them
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 import statistics
 import subprocess
 import sys

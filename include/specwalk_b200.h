@@ -163,6 +163,19 @@ int swb_oz_gemm_planes(int64_t chunk_rows, int64_t rows, int64_t K, int64_t M2, 
 int swb_oz_gemm_planes_split(int64_t chunk_rows, int64_t rows, int64_t K, int64_t M2, int buf, double* out_chunk,
                              int64_t ldo, int64_t ncol_main, double* out2_chunk, int64_t ldo2, void* workspace,
                              size_t workspace_bytes, void* stream);
+/* The split-output GEMM that also records row_amax[r] = bits of
+ * max_{c < ncol_main} |out[r, c]| (atomicMax; row_amax zeroed by the caller,
+ * indexed from out_chunk's first row): the next rotation's row scales. */
+int swb_oz_gemm_planes_ex(int64_t chunk_rows, int64_t rows, int64_t K, int64_t M2, int buf, double* out_chunk,
+                          int64_t ldo, int64_t ncol_main, double* out2_chunk, int64_t ldo2,
+                          unsigned long long* row_amax_chunk, void* workspace, size_t workspace_bytes, void* stream);
+/* A workspace with one A-plane buffer per row chunk (buf 0 .. chunks-1: all
+ * of A's planes resident, e.g. emitted by swb_gemm_tn_sym_emit), and the
+ * plane geometry for such producers: info[5] = {chunk_rows, nkc, byte
+ * offset of buffer 0's planes, bytes of a buffer's planes (its row scales
+ * follow), byte stride between buffers}. */
+size_t swb_oz_gemm_nn_workspace_bytes_full(int64_t rows, int64_t K, int64_t M2);
+int swb_oz_layout_info(int64_t rows, int64_t K, int64_t M2, int64_t* info);
 /* measurement: back-to-back INT8 tcgen05 MMAs (M 128, N 256, K 32) on every
  * SM; *ops_out = 2 x MACs issued (bench.py's live INT8 roofline) */
 int swb_int8_peak_probe(int iters, double* ops_out, void* stream);
@@ -312,6 +325,16 @@ int swb_seed_fit_schedule(const double* V, int64_t ldv, const int32_t* col_map,
 int swb_prior_hat(const double* priors, int64_t ldp, int64_t row_begin, int64_t row_end,
                   int64_t L, const double* d_sqrt, const int64_t* seed_idx, int64_t S,
                   double* out, int64_t ldo, void* stream);
+/* swb_gemm_tn (symmetric, P = X^T Y over rows) whose diagonal tiles also
+ * emit the INT8 rotation's A digit planes of X into oz_workspace (sized by
+ * swb_oz_gemm_nn_workspace_bytes_full(rows, M, M2), zero-filled by the caller
+ * once), with row scales from row_amax (swb_oz_gemm_planes_ex of the rotation
+ * that produced X): bit-identical to swb_oz_split_rows, which the rotation
+ * then skips. */
+int swb_gemm_tn_sym_emit(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t rows, int64_t M,
+                         double* out, int64_t ldo, void* workspace, size_t workspace_bytes,
+                         const unsigned long long* row_amax, int64_t M2, void* oz_workspace,
+                         size_t oz_workspace_bytes, void* stream);
 /* Finalize + hard labels of a reconstruction computed elsewhere: uraw
  * (rows [r_begin, r_end), ld ldr) holds V'[x, :] coeff; then exactly the
  * tail of swb_reconstruct_label: u = (uraw + g_x*extra)/d_sqrt_x, clip >= 0,

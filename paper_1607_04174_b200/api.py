@@ -19,12 +19,14 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import weakref
 
 import numpy as np
 
 from . import _lib
-from .device import (CAPTURE, WORKSPACE, DeviceGraph, DevicePack, LatticeSpec, gather_vector, ptr, rotate_rows,
+from .device import (CAPTURE, WORKSPACE, DeviceGraph, DevicePack, LatticeSpec, gather_vector, oz_full_workspace, ptr,
+                     rotate_rows,
                      require_cuda, round_up, stream_handle, to_device, torch_mod)
 from .errors import (ImageMismatch, InsufficientBasis, InvalidParam, SingularSmallSystem)
 from .types import MAX_SEEDS, LabelMap, LaplacianMode, ProbabilityField, content_hash
@@ -286,7 +288,7 @@ def refresh_from_set(packs, image, new_beta: float, **kw) -> RefreshedPack:
 
 def update_basis(pack, image, new_beta: float | None = None, cut_edges=None, method: str = "first_order",
                  gap_guard: float = 0.5, *, connectivity=None, weight_mode=None, keep_P: bool = False, out=None,
-                 _pre_rotate=None):
+                 _pre_rotate=None, _m2=None):
     """Update the eigenbasis for a new beta and/or cut edges (north-star (a)).
 
     method="rayleigh": exactly the reference refresh (no rotation).
@@ -353,8 +355,24 @@ def update_basis(pack, image, new_beta: float | None = None, cut_edges=None, met
         ldp = round_up(m, 2)
         P = torch.empty((m, ldp), dtype=torch.float64, device="cuda")
         tws = WORKSPACE.get("gemm_tn", _lib.size("swb_gemm_tn_workspace_bytes", n, m, m))
+        # SWB_EMIT=1: the rotation's digit planes of V come out of the
+        # projection's diagonal tiles when V's row maxima are known (V came
+        # out of an INT8 rotation that recorded them) instead of a split pass
+        # over V; measured at c4 as a wash (the projection grows by what the
+        # split cost: 114.5 + 62.5 vs 93 + 82 ms, the step ~1% faster) for
+        # 46 GB more resident HBM, so the split stays the default
+        m2 = m if _m2 is None else int(_m2)
+        int8_rot = m <= 512 and not os.environ.get("SWB_ROTATION", "").startswith("d")
+        amax_in = getattr(dp, "row_amax_dev", None)
+        planes = None
         _mark("project")
-        _lib.call("swb_gemm_tn", ptr(dp.V), ldv, ptr(W), ldv, n, m, m, 1, ptr(P), ldp, ptr(tws), tws.numel(), st)
+        if int8_rot and amax_in is not None and os.environ.get("SWB_EMIT", "0") == "1":
+            planes = oz_full_workspace(n, m, m2)
+        if planes is not None:
+            _lib.call("swb_gemm_tn_sym_emit", ptr(dp.V), ldv, ptr(W), ldv, n, m, ptr(P), ldp, ptr(tws), tws.numel(),
+                      ptr(amax_in), m2, ptr(planes), planes.numel(), st)
+        else:
+            _lib.call("swb_gemm_tn", ptr(dp.V), ldv, ptr(W), ldv, n, m, m, 1, ptr(P), ldp, ptr(tws), tws.numel(), st)
         Cm = torch.empty((m, ldp), dtype=torch.float64, device="cuda")
         _mark("coeffs")
         _lib.call("swb_update_coeffs", 1, ptr(P), ldp, ptr(dp.values_dev), ptr(quad), ptr(norm2), m,
@@ -375,12 +393,18 @@ def update_basis(pack, image, new_beta: float | None = None, cut_edges=None, met
         # update_and_solve: the solve's seed system runs here, on V' rows
         # formed from V and C, and returns extra B columns for the rotation
         extra = _pre_rotate(out, dp, Cm, ldp) if _pre_rotate is not None else None
+        amax_out = torch.empty(n, dtype=torch.int64, device="cuda") if int8_rot else None
         _mark("rotate")
         if extra is None:
-            rotate_rows(dp.V, ldv, Cm, ldp, n, m, Vn, ldv, st, mark=_mark)
+            rotate_rows(dp.V, ldv, Cm, ldp, n, m, Vn, ldv, st, mark=_mark, m2=m2 if planes is not None else None,
+                        planes=planes, row_amax=amax_out)
         else:
-            m2, c_aug, ldca, out2, ldo2 = extra
-            rotate_rows(dp.V, ldv, c_aug, ldca, n, m, Vn, ldv, st, mark=_mark, m2=m2, out2=out2, ldo2=ldo2)
+            m2x, c_aug, ldca, out2, ldo2 = extra
+            if planes is not None and m2x != m2:
+                raise InvalidParam("update_and_solve: extra column count changed")
+            rotate_rows(dp.V, ldv, c_aug, ldca, n, m, Vn, ldv, st, mark=_mark, m2=m2x, out2=out2, ldo2=ldo2,
+                        planes=planes, row_amax=amax_out)
+        out.row_amax_dev = amax_out
         _mark("update_tail")
     out.base = pack if method == "rayleigh" else None   # an updated pack owns new memory: no strong ref
     out.new_beta = beta
@@ -641,7 +665,7 @@ def update_and_solve(pack, image, prob, new_beta: float | None = None, cut_edges
         return m2, c_aug, ldca, uraw, k
 
     up = update_basis(pack, image, new_beta, cut_edges, gap_guard=gap_guard, out=out, connectivity=connectivity,
-                      weight_mode=weight_mode, _pre_rotate=pre_rotate)
+                      weight_mode=weight_mode, _pre_rotate=pre_rotate, _m2=dp0.m + prob.K)
     d, uraw = state["d"], state["uraw"]
     n, k, dev = d["n"], d["k"], d["dp"]
     labels, top2, ldu = d["labels"], d["top2"], d["ldu"]

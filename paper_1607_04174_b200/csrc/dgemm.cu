@@ -15,6 +15,7 @@
 #include <cstdlib>
 
 #include "dmma_core.cuh"
+#include "oz_digits.cuh"
 
 namespace {
 using namespace swb_core;
@@ -215,11 +216,50 @@ __device__ __forceinline__ void diag_store(const double (&acc)[diag_max_cells(G)
   }
 }
 
+// The rotation's A digit planes, emitted by the projection's diagonal tiles
+// (each holds every V row block of its 80 columns in shared memory once):
+// row scales from row_amax (the previous rotation's row maxima), the same
+// digits and layout as oz_slice_rows_kernel (oz_digits.cuh), so the planes
+// -- and the rotation -- are bit-identical to the split pass they replace.
+struct EmitArgs {
+  const unsigned long long* row_amax;  // nullptr: no emission
+  uint8_t* planes;                     // buffer 0's planes; buffer b at + b * buf_stride
+  int64_t buf_stride, a_sl;            // bytes; a buffer's row scales start at its planes + a_sl
+  int64_t chunk_rows, nkc;
+};
+
+// 16 rows (from row r0, valid below r_end) x the 80 (or 64) columns of
+// block I held in sA ([k][A_LD], k-major): one 16-column group per thread
+template <int BM, int A_LD>
+__device__ __forceinline__ void emit_digits(const EmitArgs& em, const double* sA, int I, int64_t r0, int64_t r_end) {
+  constexpr int GPB = BM / 16;                      // 16-column groups per block
+  if (threadIdx.x >= BK * GPB) return;
+  const int k = threadIdx.x / GPB, g = threadIdx.x % GPB;
+  const int64_t r = r0 + k;
+  const int64_t gc = int64_t(I) * GPB + g;           // global 16-column group
+  if (r >= r_end || gc >= 2 * em.nkc) return;
+  const double amax = __longlong_as_double(static_cast<long long>(em.row_amax[r]));
+  const int e = oz_exponent(amax);
+  const double scale = ldexp(1.0, 54 - e);
+  double v[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) v[t] = sA[k * A_LD + 16 * g + t];
+  uint4 d[OZ_S];
+  oz_digits16(v, scale, d);
+  const int64_t b = r / em.chunk_rows, rl = r % em.chunk_rows;
+  uint8_t* base = em.planes + b * em.buf_stride;
+  uint8_t* p = base + ((rl / OZ_BM) * em.nkc + (gc >> 1)) * OZ_A_STAGE + (gc & 1) * (OZ_BM * 16) +
+               (rl % OZ_BM) * 16;
+#pragma unroll
+  for (int s = 0; s < OZ_S; ++s) *reinterpret_cast<uint4*>(p + s * OZ_A_SLICE) = d[s];
+  if (gc == 0) reinterpret_cast<double*>(base + em.a_sl)[rl] = ldexp(1.0, e - 28);
+}
+
 template <int W, int STAGES>
 __global__ void __launch_bounds__(128, 3)
 gemm_tn_sym_kernel(const double* __restrict__ X, int64_t ldx, const double* __restrict__ Y, int64_t ldy,
                    int64_t rows, int64_t M, int T, int per_full, int64_t chunk_full, int per_diag,
-                   int64_t chunk_diag, double* __restrict__ partial) {
+                   int64_t chunk_diag, double* __restrict__ partial, const EmitArgs em) {
   using Cf = Cfg<2, 2, W, W, STAGES, true>;
   constexpr int G = 2 * W;
   extern __shared__ __align__(16) double smem[];
@@ -263,9 +303,12 @@ gemm_tn_sym_kernel(const double* __restrict__ X, int64_t ldx, const double* __re
   for (int a = 0; a < diag_max_cells(G); ++a) acc[a][0] = acc[a][1] = 0.0;
   const int lr = lane >> 2, lc = lane & 3;
   if (kb < ke) {
+    int64_t r_stage = kb;
     pipeline<2, 2, W, W, STAGES, true>(
         smem, X, ldx, Y, ldy, kb, ke, int64_t(i) * Cf::BM, M, int64_t(i) * Cf::BN, M,
         [&](const double* sA, const double* sB) {
+          if (em.row_amax) emit_digits<Cf::BM, Cf::A_LD>(em, sA, i, r_stage, ke);
+          r_stage += BK;
           switch (warp) {
             case 0: diag_compute<G, 0, Cf::A_LD, Cf::B_LD>(acc, sA, sB, lr, lc); break;
             case 1: diag_compute<G, 1, Cf::A_LD, Cf::B_LD>(acc, sA, sB, lr, lc); break;
@@ -419,7 +462,8 @@ int run_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t r
 
 template <int W>
 int run_tn_sym(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t rows, int64_t M, double* out,
-               int64_t ldo, void* ws, size_t ws_bytes, cudaStream_t st, bool size_only, size_t* need) {
+               int64_t ldo, void* ws, size_t ws_bytes, cudaStream_t st, bool size_only, size_t* need,
+               const EmitArgs& em = EmitArgs{}) {
   using Cf = Cfg<2, 2, W, W, TN_STAGES, true>;
   constexpr int G = 2 * W;
   auto kern = gemm_tn_sym_kernel<W, TN_STAGES>;
@@ -441,7 +485,15 @@ int run_tn_sym(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64
   const int slots = swb_sm_count() * (occ > 0 ? occ : 8) * tn_waves();
   const int T = static_cast<int>((M + Cf::BM - 1) / Cf::BM);
   const int n_full = T * (T - 1) / 2;
-  const double ratio = double(diag_max_cells(G)) / double(W * W);  // diagonal / full tile cost
+  // diagonal / full tile cost; emitting diagonal tiles also convert their
+  // V block to digit planes, measured at ~0.1 of a full tile's stage
+  // (SWB_TN_EMIT_COST overrides; the CTA counts per tile, and so P's
+  // split-K summation order, then differ from the plain projection's)
+  static const double emit_cost = [] {
+    const char* e = getenv("SWB_TN_EMIT_COST");
+    return e ? atof(e) : 0.1;
+  }();
+  const double ratio = double(diag_max_cells(G)) / double(W * W) + (em.row_amax ? emit_cost : 0.0);
   int per_full = std::max(1, static_cast<int>(slots / (n_full + ratio * T)));
   const int64_t max_per = std::max<int64_t>(1, rows / 512);
   if (per_full > max_per) per_full = static_cast<int>(max_per);
@@ -458,7 +510,7 @@ int run_tn_sym(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64
   if (ws_bytes < *need || ws == nullptr) return SWB_WORKSPACE_TOO_SMALL;
   double* partial = reinterpret_cast<double*>(ws);
   kern<<<n_ctas, Cf::THREADS, smem_req, st>>>(X, ldx, Y, ldy, rows, M, T, per_full, chunk_full, per_diag, chunk_diag,
-                                              partial);
+                                              partial, em);
   SWB_CHECK_LAUNCH();
   const int64_t total = int64_t(T * (T + 1) / 2) * Cf::BM * Cf::BN;
   int rb = static_cast<int>(std::min<int64_t>((total + 255) / 256, int64_t(swb_sm_count()) * 8));
@@ -469,16 +521,16 @@ int run_tn_sym(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64
 
 int dispatch_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t rows, int64_t M1,
                 int64_t M2, int symmetric, double* out, int64_t ldo, void* ws, size_t ws_bytes,
-                cudaStream_t st, bool size_only, size_t* need) {
+                cudaStream_t st, bool size_only, size_t* need, const EmitArgs& em = EmitArgs{}) {
   switch (choose_tn(M1, M2)) {
     case TN_80x80:
       if (symmetric)
-        return run_tn_sym<5>(X, ldx, Y, ldy, rows, M1, out, ldo, ws, ws_bytes, st, size_only, need);
+        return run_tn_sym<5>(X, ldx, Y, ldy, rows, M1, out, ldo, ws, ws_bytes, st, size_only, need, em);
       return run_tn<2, 2, 5, 5>(X, ldx, Y, ldy, rows, M1, M2, symmetric, out, ldo, ws, ws_bytes, st,
                                 size_only, need);
     case TN_64x64:
       if (symmetric)
-        return run_tn_sym<4>(X, ldx, Y, ldy, rows, M1, out, ldo, ws, ws_bytes, st, size_only, need);
+        return run_tn_sym<4>(X, ldx, Y, ldy, rows, M1, out, ldo, ws, ws_bytes, st, size_only, need, em);
       return run_tn<2, 2, 4, 4>(X, ldx, Y, ldy, rows, M1, M2, symmetric, out, ldo, ws, ws_bytes, st,
                                 size_only, need);
     default:
@@ -488,6 +540,8 @@ int dispatch_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int6
 }
 
 }  // namespace
+
+extern "C" int swb_oz_layout_info(int64_t rows, int64_t K, int64_t M2, int64_t* info);
 
 extern "C" size_t swb_gemm_tn_workspace_bytes(int64_t rows, int64_t M1, int64_t M2) {
   size_t need = 0;
@@ -583,4 +637,30 @@ extern "C" int swb_fp64_peak_probe(int iters, double* sink, double* flops_out, v
   SWB_CHECK_LAUNCH();
   *flops_out = 2.0 * 256.0 * 8.0 * double(iters) * double(blocks) * 8.0;  // 8 warps per block
   return SWB_OK;
+}
+
+// The symmetric projection P = X^T Y (swb_gemm_tn, symmetric) whose diagonal
+// tiles also emit the INT8 rotation's A digit planes of X (rows x M) into an
+// oz workspace sized by swb_oz_gemm_nn_workspace_bytes_full(rows, M, M2), row
+// scales from row_amax (bits of max_c |X[r, c]|): the digit split of the
+// rotation that follows is then not needed (swb_oz_gemm_planes_ex on buffers
+// 0 .. chunks-1).  Column groups past M inside the last 32-column K chunk are
+// left untouched: the caller keeps them zero.
+extern "C" int swb_gemm_tn_sym_emit(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t rows,
+                                    int64_t M, double* out, int64_t ldo, void* workspace, size_t workspace_bytes,
+                                    const unsigned long long* row_amax, int64_t M2, void* oz_workspace,
+                                    size_t oz_workspace_bytes, void* stream) {
+  if (M <= 0 || rows <= 0 || !out || !row_amax || !oz_workspace || M2 < M) return SWB_INVALID_PARAM;
+  if (ldx < M || ldy < M || ldo < M || (ldx & 1) || (ldy & 1)) return SWB_INVALID_PARAM;
+  if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 15) return SWB_INVALID_PARAM;
+  if (choose_tn(M, M) == TN_80x16) return SWB_INVALID_PARAM;
+  int64_t info[5];
+  int rc = swb_oz_layout_info(rows, M, M2, info);
+  if (rc) return rc;
+  const int64_t nbuf = (rows + info[0] - 1) / info[0];
+  if (oz_workspace_bytes < size_t(info[2] + nbuf * info[4])) return SWB_WORKSPACE_TOO_SMALL;
+  EmitArgs em{row_amax, static_cast<uint8_t*>(oz_workspace) + info[2], info[4], info[3], info[0], info[1]};
+  size_t need = 0;
+  return dispatch_tn(X, ldx, Y, ldy, rows, M, M, 1, out, ldo, workspace, workspace_bytes, swb_stream(stream), false,
+                     &need, em);
 }

@@ -32,18 +32,14 @@
 #include <mutex>
 
 #include "swb_common.cuh"
+#include "oz_digits.cuh"
 
 namespace {
 
-constexpr int OZ_S = 7;                 // digits per operand
 constexpr int OZ_G = 7;                 // product groups g = i + j <= 6
-constexpr int OZ_BM = 128;              // rows per tile (MMA M)
 constexpr int OZ_BN = 64;               // columns per tile (MMA N)
-constexpr int OZ_KC = 32;               // bytes (= int8 K) per stage / per MMA
 constexpr int OZ_STAGES = 4;
-constexpr int OZ_A_SLICE = OZ_BM * OZ_KC;            // 4096 B: [kq 2][row 128][16 B]
 constexpr int OZ_B_SLICE = OZ_BN * OZ_KC;            // 2048 B: [kq 2][col 64][16 B]
-constexpr int OZ_A_STAGE = OZ_S * OZ_A_SLICE;        // 28 KB
 constexpr int OZ_B_STAGE = OZ_S * OZ_B_SLICE;        // 14 KB
 constexpr int OZ_STAGE = OZ_A_STAGE + OZ_B_STAGE;
 constexpr int OZ_EPI_WARPS = 8;
@@ -184,43 +180,6 @@ __device__ __forceinline__ void oz_issue_chunk(uint32_t tmem, uint32_t a0, uint3
                 (first && i == 0) ? 0u : 1u);
   }
 #endif
-}
-
-__device__ __forceinline__ int oz_exponent(double amax) {
-  if (!(amax > 0.0)) return 0;
-  int e;
-  frexp(amax, &e);          // amax = m 2^e, m in [0.5, 1)
-  return e < -960 ? -960 : e;
-}
-
-// 16 consecutive values -> 7 balanced digit vectors of 16 bytes.
-// With Y = X + 0x808080808080, the balanced digits are the bytes of Y:
-// d_s = byte (6 - s) of Y minus 128 (= byte ^ 0x80) for s = 1..6, and
-// d_0 = byte 6 of Y (the signed top, |d_0| <= 65).  Byte gathers are PRMTs.
-__device__ __forceinline__ void oz_digits16(const double (&v)[16], double scale, uint4 (&out)[OZ_S]) {
-  uint32_t lo[16], hi[16];
-#pragma unroll
-  for (int t = 0; t < 16; ++t) {
-    const unsigned long long Y =
-        static_cast<unsigned long long>(__double2ll_rn(v[t] * scale)) + 0x808080808080ull;
-    lo[t] = static_cast<uint32_t>(Y);
-    hi[t] = static_cast<uint32_t>(Y >> 32);
-  }
-#pragma unroll
-  for (int s = 0; s < OZ_S; ++s) {
-    const int p = 6 - s;                     // byte of Y
-    const uint32_t sel = (p & 3) | (((p & 3) + 4) << 4);
-    const uint32_t flip = s == 0 ? 0u : 0x80808080u;
-    uint32_t w[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint32_t* src = p < 4 ? lo : hi;
-      const uint32_t a = __byte_perm(src[4 * q], src[4 * q + 1], sel);
-      const uint32_t b = __byte_perm(src[4 * q + 2], src[4 * q + 3], sel);
-      w[q] = __byte_perm(a, b, 0x5410) ^ flip;
-    }
-    out[s] = make_uint4(w[0], w[1], w[2], w[3]);
-  }
 }
 
 // A (rows x K, row-major, lda) -> row-scaled digits, tiled
@@ -397,7 +356,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, const uint8_t* __restrict__ bsl,
                const double* __restrict__ sb, int64_t rows, int64_t M2, int64_t nkc, int64_t n_rb, int64_t n_cb,
                double* __restrict__ out, int64_t ldo, int32_t* __restrict__ raw, int64_t ncol_main,
-               double* __restrict__ out2, int64_t ldo2) {
+               double* __restrict__ out2, int64_t ldo2, unsigned long long* __restrict__ row_amax) {
   extern __shared__ __align__(1024) uint8_t oz_smem[];
   uint8_t* stages = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem) + 127) & ~uintptr_t(127));
   __shared__ __align__(8) uint64_t full_bar[OZ_STAGES], empty_bar[OZ_STAGES], tfull_bar, tempty_bar;
@@ -606,11 +565,14 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
 #endif
       if (r >= rows) continue;
       double* orow = out + r * ldo + gc0;
+      double amax = 0.0;   // max |out[r, c]| over this thread's columns c < ncol_main
       if (gc0 + OZ_EPI_COLS <= ncol_main) {
 #pragma unroll
         for (int q = 0; q < OZ_EPI_COLS; q += 2) {
           const double2 sc = *reinterpret_cast<const double2*>(sb + gc0 + q);
-          *reinterpret_cast<double2*>(orow + q) = make_double2(o[q >> 4][q & 15] * sc.x, o[q >> 4][(q & 15) + 1] * sc.y);
+          const double2 y = make_double2(o[q >> 4][q & 15] * sc.x, o[q >> 4][(q & 15) + 1] * sc.y);
+          *reinterpret_cast<double2*>(orow + q) = y;
+          amax = fmax(amax, fmax(fabs(y.x), fabs(y.y)));
         }
       } else {
         // the ragged last column tile: columns [ncol_main, M2) (extra B
@@ -618,10 +580,18 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
 #pragma unroll
         for (int q = 0; q < OZ_EPI_COLS; ++q) {
           const int64_t c = gc0 + q;
-          if (c < ncol_main) orow[q] = o[q >> 4][q & 15] * sb[c];
-          else if (c < M2) out2[r * ldo2 + (c - ncol_main)] = o[q >> 4][q & 15] * sb[c];
+          const double y = o[q >> 4][q & 15] * sb[c];
+          if (c < ncol_main) {
+            orow[q] = y;
+            amax = fmax(amax, fabs(y));
+          } else if (c < M2) {
+            out2[r * ldo2 + (c - ncol_main)] = y;
+          }
         }
       }
+      // the row maxima of the product: the next rotation's row scales, so a
+      // producer holding these rows can emit their digit planes (no split)
+      if (row_amax) atomicMax(row_amax + r, static_cast<unsigned long long>(__double_as_longlong(amax)));
     }
 #if OZ_PROF
     (void)t_rel;
@@ -692,6 +662,11 @@ int oz_check(int64_t rows, int64_t K, int64_t M2, void* ws, size_t ws_bytes, OzL
   if (rows < 0 || K <= 0 || M2 <= 0 || K > OZ_MAX_K || !ws) return SWB_INVALID_PARAM;
   *o = oz_layout(rows > 0 ? rows : 1, K, M2);
   if (ws_bytes < o->total) return SWB_WORKSPACE_TOO_SMALL;
+  // a workspace sized by swb_oz_gemm_nn_workspace_bytes_full holds one A-plane
+  // buffer per row chunk (planes emitted ahead of the GEMMs)
+  const int64_t per = int64_t(o->a_sl + o->sa);
+  const int64_t fit = (int64_t(ws_bytes) - int64_t(o->b_sl + o->sb)) / per;
+  if (fit > o->nbuf) o->nbuf = fit;
   return oz_set_attrs();
 }
 
@@ -734,7 +709,8 @@ extern "C" int swb_oz_split_rows(const double* A, int64_t lda, int64_t nr, int64
 // with ncol_main < M2 the columns [ncol_main, M2) go to out2 instead.
 int swb_oz_planes_gemm(int64_t nr, int64_t rows, int64_t K, int64_t M2, int buf, double* out, int64_t ldo,
                        int32_t* raw, void* workspace, size_t workspace_bytes, cudaStream_t st,
-                       int64_t ncol_main = -1, double* out2 = nullptr, int64_t ldo2 = 0) {
+                       int64_t ncol_main = -1, double* out2 = nullptr, int64_t ldo2 = 0,
+                       unsigned long long* row_amax = nullptr) {
   OzLayout o;
   int rc = oz_check(rows, K, M2, workspace, workspace_bytes, &o);
   if (rc) return rc;
@@ -751,7 +727,7 @@ int swb_oz_planes_gemm(int64_t nr, int64_t rows, int64_t K, int64_t M2, int buf,
   const int64_t grid = tiles < grid_cap ? tiles : grid_cap;
   oz_gemm_kernel<<<static_cast<unsigned>(grid), OZ_THREADS, OZ_SMEM, st>>>(q.a_sl, q.sa, q.b_sl, q.sb, nr, M2, o.nkc,
                                                                            n_rb, o.n_cb, out, ldo, raw, ncol_main,
-                                                                           out2, ldo2);
+                                                                           out2, ldo2, row_amax);
   SWB_CHECK_LAUNCH();
   return SWB_OK;
 }
@@ -770,6 +746,18 @@ extern "C" int swb_oz_gemm_planes_split(int64_t nr, int64_t rows, int64_t K, int
                             swb_stream(stream), ncol_main, out2, ldo2);
 }
 
+// The same, also recording row_amax[r] = max_c<ncol_main |out[r, c]| (as the
+// bits of a non-negative double; atomicMax, so row_amax must start at 0 --
+// the chunk's rows are indexed from out_chunk's first row)
+extern "C" int swb_oz_gemm_planes_ex(int64_t nr, int64_t rows, int64_t K, int64_t M2, int buf, double* out,
+                                     int64_t ldo, int64_t ncol_main, double* out2, int64_t ldo2,
+                                     unsigned long long* row_amax, void* workspace, size_t workspace_bytes,
+                                     void* stream) {
+  if (ncol_main < 0) return SWB_INVALID_PARAM;
+  return swb_oz_planes_gemm(nr, rows, K, M2, buf, out, ldo, nullptr, workspace, workspace_bytes,
+                            swb_stream(stream), ncol_main, out2, ldo2, row_amax);
+}
+
 #if OZ_PROF
 extern "C" int swb_oz_prof_read(unsigned long long* out) {
   SWB_CUDA_TRY(cudaDeviceSynchronize());
@@ -781,6 +769,29 @@ extern "C" int swb_oz_prof_read(unsigned long long* out) {
 extern "C" size_t swb_oz_gemm_nn_workspace_bytes(int64_t rows, int64_t K, int64_t M2) {
   if (rows <= 0 || K <= 0 || M2 <= 0) return 0;
   return oz_layout(rows, K, M2).total;
+}
+
+// one A-plane buffer per row chunk: all of A's planes resident at once
+extern "C" size_t swb_oz_gemm_nn_workspace_bytes_full(int64_t rows, int64_t K, int64_t M2) {
+  if (rows <= 0 || K <= 0 || M2 <= 0) return 0;
+  const OzLayout o = oz_layout(rows, K, M2);
+  const int64_t rows_p = (rows + OZ_BM - 1) / OZ_BM * OZ_BM;
+  const int64_t nch = (rows_p + o.chunk_rows - 1) / o.chunk_rows;
+  return o.b_sl + o.sb + size_t(nch) * (o.a_sl + o.sa);
+}
+
+// plane geometry for producers that write A planes themselves:
+// info = {chunk_rows, nkc, offset of buffer 0's planes, bytes of a buffer's
+// planes (its row scales follow), stride between buffers}
+extern "C" int swb_oz_layout_info(int64_t rows, int64_t K, int64_t M2, int64_t* info) {
+  if (rows <= 0 || K <= 0 || M2 <= 0 || K > OZ_MAX_K || !info) return SWB_INVALID_PARAM;
+  const OzLayout o = oz_layout(rows, K, M2);
+  info[0] = o.chunk_rows;
+  info[1] = o.nkc;
+  info[2] = int64_t(o.b_sl + o.sb);
+  info[3] = int64_t(o.a_sl);
+  info[4] = int64_t(o.a_sl + o.sa);
+  return SWB_OK;
 }
 
 extern "C" int64_t swb_oz_chunk_rows(int64_t rows, int64_t K, int64_t M2) {

@@ -71,8 +71,44 @@ class Workspace:
 WORKSPACE = Workspace()
 
 
+_OZ_FULL = {}
+
+
+def oz_full_workspace(rows: int, m: int, m2: int):
+    """The INT8 rotation workspace with one A-plane buffer per row chunk (all
+    of V's digit planes resident: the projection emits them, the rotation
+    skips its split).  Zero-filled once per shape: plane entries no producer
+    writes (columns past m in the last K chunk, rows past the end) stay 0.
+    None when it does not fit in device memory."""
+    from . import _lib
+    torch = torch_mod()
+    key = (torch.cuda.current_device(), rows, m, m2)
+    ws = _OZ_FULL.get(key)
+    if ws is False:
+        return None
+    if ws is None:
+        _OZ_FULL.clear()
+        nb = _lib.size("swb_oz_gemm_nn_workspace_bytes_full", rows, m, m2)
+        for attempt in range(2):
+            try:
+                ws = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+                break
+            except torch.OutOfMemoryError:
+                if attempt:
+                    # does not fit next to the bases: the rotation splits V itself
+                    _OZ_FULL[key] = False
+                    import warnings
+                    warnings.warn(f"oz_full_workspace: {nb / 2**30:.1f} GiB do not fit "
+                                  f"(allocated {torch.cuda.memory_allocated() / 2**30:.1f} GiB); "
+                                  "the rotation splits V instead", RuntimeWarning)
+                    return None
+                torch.cuda.empty_cache()
+        _OZ_FULL[key] = ws
+    return ws
+
+
 def rotate_rows(V, ldv: int, Cm, ldc: int, rows: int, m: int, out, ldo: int, stream=None, mark=None,
-                m2: int | None = None, out2=None, ldo2: int = 0) -> None:
+                m2: int | None = None, out2=None, ldo2: int = 0, planes=None, row_amax=None) -> None:
     """out[rows x m] = V[rows x m] Cm[m x m] (the first-order rotation,
     reference update.py V' = V C): on the INT8 tensor cores (csrc/ozaki.cu,
     FP64-accurate digit scheme) for m <= 512, else the FP64 DMMA GEMM.
@@ -82,7 +118,11 @@ def rotate_rows(V, ldv: int, Cm, ldc: int, rows: int, m: int, out, ldo: int, str
 
     ``m2 > m``: Cm is m x m2 and its columns [m, m2) are extra products
     V Cm[:, m:m2] written to ``out2`` (ld ``ldo2``); on the INT8 path they
-    ride in the last column tile's padding (update_and_solve)."""
+    ride in the last column tile's padding (update_and_solve).
+    ``planes``: an oz_full_workspace whose A planes of V were emitted by the
+    projection (swb_gemm_tn_sym_emit): no digit split.  ``row_amax`` (int64
+    N, zeroed here): receives max_c |out[r, c]| bits for the next update's
+    emission."""
     import os
     from . import _lib
     st = stream if stream is not None else stream_handle()
@@ -97,12 +137,28 @@ def rotate_rows(V, ldv: int, Cm, ldc: int, rows: int, m: int, out, ldo: int, str
         return
     mark = mark or (lambda name: None)
     torch = torch_mod()
-    nb = _lib.size("swb_oz_gemm_nn_workspace_bytes", rows, m, m2)
-    ws = WORKSPACE.get("oz_gemm", nb)
+    if planes is not None:
+        ws = planes
+    else:
+        nb = _lib.size("swb_oz_gemm_nn_workspace_bytes", rows, m, m2)
+        ws = WORKSPACE.get("oz_gemm", nb)
     chunk = _lib.size("swb_oz_chunk_rows", rows, m, m2)
     nch = (rows + chunk - 1) // chunk
+    if row_amax is not None:
+        row_amax.zero_()
     mark("rotate_split")
     _lib.call("swb_oz_split_cols", ptr(Cm), ldc, rows, m, m2, ptr(ws), ws.numel(), st)
+    if planes is not None:   # V's planes are already in buffers 0 .. nch-1
+        for i in range(nch):
+            r0 = i * chunk
+            mark("rotate_gemm")
+            _lib.call("swb_oz_gemm_planes_ex", min(chunk, rows - r0), rows, m, m2, i,
+                      C.c_void_p(out.data_ptr() + 8 * r0 * ldo), ldo, m,
+                      C.c_void_p(out2.data_ptr() + 8 * r0 * ldo2) if m2 > m else None, ldo2,
+                      C.c_void_p(row_amax.data_ptr() + 8 * r0) if row_amax is not None else None,
+                      ptr(ws), ws.numel(), st)
+            mark("rotate_join")
+        return
     main = torch.cuda.current_stream()
     # SWB_OZ_SERIAL=1 (measurement knob): split and GEMM in turn on one stream
     aux = _aux_stream() if nch > 1 and os.environ.get("SWB_OZ_SERIAL") != "1" else main
@@ -128,13 +184,11 @@ def rotate_rows(V, ldv: int, Cm, ldc: int, rows: int, m: int, out, ldo: int, str
         r0 = i * chunk
         main.wait_event(ev_split[i & 1])
         mark("rotate_gemm")
-        if m2 > m:
-            _lib.call("swb_oz_gemm_planes_split", min(chunk, rows - r0), rows, m, m2, i & 1,
-                      C.c_void_p(out.data_ptr() + 8 * r0 * ldo), ldo, m, C.c_void_p(out2.data_ptr() + 8 * r0 * ldo2),
-                      ldo2, ptr(ws), ws.numel(), st)
-        else:
-            _lib.call("swb_oz_gemm_planes", min(chunk, rows - r0), rows, m, m, i & 1,
-                      C.c_void_p(out.data_ptr() + 8 * r0 * ldo), ldo, ptr(ws), ws.numel(), st)
+        _lib.call("swb_oz_gemm_planes_ex", min(chunk, rows - r0), rows, m, m2, i & 1,
+                  C.c_void_p(out.data_ptr() + 8 * r0 * ldo), ldo, m,
+                  C.c_void_p(out2.data_ptr() + 8 * r0 * ldo2) if m2 > m else None, ldo2,
+                  C.c_void_p(row_amax.data_ptr() + 8 * r0) if row_amax is not None else None,
+                  ptr(ws), ws.numel(), st)
         ev_gemm[i & 1].record(main)
         mark("rotate_join")
 
