@@ -366,7 +366,8 @@ def update_basis(pack, image, new_beta: float | None = None, cut_edges=None, met
         amax_in = getattr(dp, "row_amax_dev", None)
         planes = None
         _mark("project")
-        if int8_rot and amax_in is not None and os.environ.get("SWB_EMIT", "0") == "1":
+        emit = int8_rot and os.environ.get("SWB_EMIT", "0") == "1"
+        if emit and amax_in is not None:
             planes = oz_full_workspace(n, m, m2)
         if planes is not None:
             _lib.call("swb_gemm_tn_sym_emit", ptr(dp.V), ldv, ptr(W), ldv, n, m, ptr(P), ldp, ptr(tws), tws.numel(),
@@ -393,7 +394,7 @@ def update_basis(pack, image, new_beta: float | None = None, cut_edges=None, met
         # update_and_solve: the solve's seed system runs here, on V' rows
         # formed from V and C, and returns extra B columns for the rotation
         extra = _pre_rotate(out, dp, Cm, ldp) if _pre_rotate is not None else None
-        amax_out = torch.empty(n, dtype=torch.int64, device="cuda") if int8_rot else None
+        amax_out = torch.empty(n, dtype=torch.int64, device="cuda") if emit else None
         _mark("rotate")
         if extra is None:
             rotate_rows(dp.V, ldv, Cm, ldp, n, m, Vn, ldv, st, mark=_mark, m2=m2 if planes is not None else None,

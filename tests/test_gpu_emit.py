@@ -77,7 +77,11 @@ def test_emitted_planes_equal_split(cuda_ok, n, m):
 def test_chained_update_through_emitted_planes(cuda_ok, dims, m):
     import paper_1607_04174_b200 as swb
     image, dp = _pack(dims, m, 11)
-    up1 = swb.update_basis(dp, image, 80.0, keep_P=True)          # split path, records row maxima
+    os.environ["SWB_EMIT"] = "1"
+    try:
+        up1 = swb.update_basis(dp, image, 80.0, keep_P=True)      # split path (no maxima yet), records them
+    finally:
+        os.environ.pop("SWB_EMIT", None)
     amax = torch.from_numpy(np.abs(up1.V[:, :m].cpu().numpy()).max(axis=1)).cuda()
     assert torch.equal(up1.row_amax_dev.view(torch.float64), amax)
     ref = swb.update_basis(up1, image, 60.0, keep_P=True)           # split path (default)
