@@ -66,6 +66,16 @@ constexpr int OZ_MAX_K = 512;
 #if OZ_WIDE
 constexpr uint32_t OZ_B_LBO = OZ_S * OZ_BN * 16;    // K-adjacent core matrices: past all 7 planes
 constexpr uint32_t OZ_B_PLANE = OZ_BN * 16;         // plane j's columns follow plane j-1's
+// A ragged last column block with <= 32 live columns (K = 400: 16, plus the
+// solve's extra columns in update_and_solve) runs as a narrow 128 x 32 tile:
+// planes of 32 columns side by side ([kq 2][plane 7][col 32][16 B], 7 KB per
+// stage), groups at TMEM column 32 g, one MMA per A digit (N = 32 (7 - i)):
+// half the MMA work and two thirds of the shared-memory traffic of a full
+// tile whose last 48 columns are padding.
+constexpr int OZ_BN_N = 32;
+constexpr uint32_t OZ_B_LBO_N = OZ_S * OZ_BN_N * 16;
+constexpr uint32_t OZ_B_PLANE_N = OZ_BN_N * 16;
+constexpr int OZ_B_STAGE_N = OZ_S * OZ_BN_N * OZ_KC;   // 7 KB
 #else
 constexpr uint32_t OZ_B_LBO = OZ_BN * 16;
 constexpr uint32_t OZ_B_PLANE = OZ_B_SLICE;
@@ -180,6 +190,25 @@ __device__ __forceinline__ void oz_issue_chunk(uint32_t tmem, uint32_t a0, uint3
                 (first && i == 0) ? 0u : 1u);
   }
 #endif
+}
+
+#if OZ_WIDE
+// the narrow last tile: A digit i x B digits 0 .. 6 - i -> groups i .. 6
+__device__ __forceinline__ void oz_issue_chunk_narrow(uint32_t tmem, uint32_t a0, uint32_t b0, bool first) {
+#pragma unroll
+  for (int i = 0; i < OZ_S; ++i)
+    tc_mma_i8(tmem + uint32_t(i * OZ_BN_N), smem_desc(a0 + i * OZ_A_SLICE, OZ_BM * 16, 128),
+              smem_desc(b0, OZ_B_LBO_N, 128), idesc_i8(1, 1, (OZ_S - i) * OZ_BN_N), (first && i == 0) ? 0u : 1u);
+}
+#endif
+
+// is column block cb of M2 columns a narrow (<= 32 live columns) last tile
+// (OZ_NARROW = 0, variant builds: full 64-column tiles throughout)
+#ifndef OZ_NARROW
+#define OZ_NARROW 1
+#endif
+__host__ __device__ __forceinline__ bool oz_narrow(int64_t cb, int64_t n_cb, int64_t M2) {
+  return OZ_WIDE && OZ_NARROW && cb == n_cb - 1 && M2 - cb * OZ_BN <= 32;
 }
 
 // A (rows x K, row-major, lda) -> row-scaled digits, tiled
@@ -301,12 +330,14 @@ __global__ void __launch_bounds__(OZ_BN) oz_slice_cols_kernel(const double* __re
   const int tid = threadIdx.x;
   const int64_t c = cb * OZ_BN + tid;
   const bool live = c < M2;
+  const bool nar = oz_narrow(cb, gridDim.x, M2);
   double amax = 0.0;
   if (live)
     for (int64_t k = 0; k < K; ++k) amax = fmax(amax, fabs(B[k * ldb + c]));
   const int f = oz_exponent(amax);
   const double scale = ldexp(1.0, 54 - f);
   sb[c] = ldexp(1.0, f);
+  if (nar && tid >= OZ_BN_N) return;
   const int64_t nch = nkc * 2;
   for (int64_t ch = 0; ch < nch; ++ch) {
     double v[16];
@@ -318,9 +349,14 @@ __global__ void __launch_bounds__(OZ_BN) oz_slice_cols_kernel(const double* __re
     uint4 d[OZ_S];
     oz_digits16(v, scale, d);
     const int64_t kc = ch >> 1, kq = ch & 1;
-    uint8_t* base = sl + (cb * nkc + kc) * OZ_B_STAGE + kq * OZ_B_LBO + tid * 16;
+#if OZ_WIDE
+    const uint32_t lbo = nar ? OZ_B_LBO_N : OZ_B_LBO, pl = nar ? OZ_B_PLANE_N : OZ_B_PLANE;
+#else
+    const uint32_t lbo = OZ_B_LBO, pl = OZ_B_PLANE;
+#endif
+    uint8_t* base = sl + (cb * nkc + kc) * OZ_B_STAGE + kq * lbo + tid * 16;
 #pragma unroll
-    for (int s = 0; s < OZ_S; ++s) *reinterpret_cast<uint4*>(base + s * OZ_B_PLANE) = d[s];
+    for (int s = 0; s < OZ_S; ++s) *reinterpret_cast<uint4*>(base + s * pl) = d[s];
   }
 }
 
@@ -394,10 +430,15 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
         for (int64_t kc = 0; kc < nkc; ++kc) {
           mbar_wait(smem_u32(&empty_bar[s]), ph ^ 1);
           const uint32_t fb = smem_u32(&full_bar[s]);
-          mbar_expect_tx(fb, OZ_STAGE);
+#if OZ_WIDE
+          const uint32_t bbytes = oz_narrow(cb, n_cb, M2) ? OZ_B_STAGE_N : OZ_B_STAGE;
+#else
+          const uint32_t bbytes = OZ_B_STAGE;
+#endif
+          mbar_expect_tx(fb, OZ_A_STAGE + bbytes);
           const uint32_t dst = smem_u32(stages + size_t(s) * OZ_STAGE);
           bulk_g2s(dst, asl + (rb * nkc + kc) * OZ_A_STAGE, OZ_A_STAGE, fb);
-          bulk_g2s(dst + OZ_A_STAGE, bsl + (cb * nkc + kc) * OZ_B_STAGE, OZ_B_STAGE, fb);
+          bulk_g2s(dst + OZ_A_STAGE, bsl + (cb * nkc + kc) * OZ_B_STAGE, bbytes, fb);
           if (++s == OZ_STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -411,6 +452,7 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
     OZ_T(t_begin);
 #endif
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const bool nar = oz_narrow(t % n_cb, n_cb, M2);
       OZ_T(t0);
       mbar_wait(smem_u32(&tempty_bar), tph ^ 1);
 #if OZ_PROF
@@ -426,7 +468,11 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
         tc_fence_after();
         if (lane == 0) {
           const uint32_t a0 = smem_u32(stages + size_t(s) * OZ_STAGE);
-          oz_issue_chunk(tmem, a0, a0 + OZ_A_STAGE, kc == 0);
+#if OZ_WIDE
+          if (nar) oz_issue_chunk_narrow(tmem, a0, a0 + OZ_A_STAGE, kc == 0);
+          else
+#endif
+            oz_issue_chunk(tmem, a0, a0 + OZ_A_STAGE, kc == 0);
           tc_commit(smem_u32(&empty_bar[s]));          // frees the stage when these finish
           if (kc + 1 == nkc) tc_commit(smem_u32(&tfull_bar));
         }
@@ -467,17 +513,56 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
 #endif
       tc_fence_after();
       tph ^= 1;
+      // narrow last tile: groups at TMEM column 32 g, the c0 = 32 warps idle
+      const bool nar = oz_narrow(cb, n_cb, M2);
+      const uint32_t gs = nar ? 32u : uint32_t(OZ_BN);
       if (raw) {
         const int64_t rows_p = n_rb * OZ_BM, np = n_cb * OZ_BN;
         for (int h = 0; h < OZ_EPI_COLS; h += 16)
           for (int g = 0; g < OZ_G; ++g) {
-            int32_t v[16];
-            tmem_ld16(tsrc + uint32_t(g * OZ_BN + h), v);
-            tmem_wait_ld();
+            int32_t v[16] = {};
+            if (!(nar && c0)) {
+              tmem_ld16(tsrc + uint32_t(g * gs + h), v);
+              tmem_wait_ld();
+            }
             for (int q = 0; q < 16; ++q) raw[(g * rows_p + r) * np + gc0 + h + q] = v[q];
           }
         tc_fence_before();
         mbar_arrive(smem_u32(&tempty_bar));
+        continue;
+      }
+      if (nar) {
+        // narrow tile: the two warps of a lane quarter take 16 columns each
+        // (one TMEM round: 7 groups x 16 columns), released after one wait
+        const int hf = ew >> 2;
+        int32_t v[OZ_G][16];
+#pragma unroll
+        for (int g = 0; g < OZ_G; ++g)
+          tmem_ld16(tmem + (uint32_t(quarter * 32) << 16) + uint32_t(g * OZ_BN_N + 16 * hf), v[g]);
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(smem_u32(&tempty_bar));
+        if (r >= rows) continue;
+        const int64_t gcn = cb * OZ_BN + 16 * hf;
+        double amax = 0.0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const long long H = (static_cast<long long>(v[0][q]) << 16) + (static_cast<long long>(v[1][q]) << 8) +
+                              static_cast<long long>(v[2][q]);
+          const long long L = (static_cast<long long>(v[3][q]) << 24) + (static_cast<long long>(v[4][q]) << 16) +
+                              (static_cast<long long>(v[5][q]) << 8) + static_cast<long long>(v[6][q]);
+          const int64_t c = gcn + q;
+          if (c < M2) {
+            const double y = fma(static_cast<double>(L), 0x1p-32, static_cast<double>(H)) * srow * sb[c];
+            if (c < ncol_main) {
+              out[r * ldo + c] = y;
+              amax = fmax(amax, fabs(y));
+            } else {
+              out2[r * ldo2 + (c - ncol_main)] = y;
+            }
+          }
+        }
+        if (row_amax) atomicMax(row_amax + r, static_cast<unsigned long long>(__double_as_longlong(amax)));
         continue;
       }
       // both 16-column rounds are combined in registers before any store, so
@@ -493,7 +578,7 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
         {
           int32_t v[OZ_G][16];
 #pragma unroll
-          for (int g = 0; g < OZ_G; ++g) tmem_ld16(tsrc + uint32_t(g * OZ_BN), v[g]);
+          for (int g = 0; g < OZ_G; ++g) tmem_ld16(tsrc + uint32_t(g * gs), v[g]);
           tmem_wait_ld();
           long long H0[16];
 #pragma unroll
@@ -501,7 +586,7 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
             H0[q] = (static_cast<long long>(v[0][q]) << 16) + (static_cast<long long>(v[1][q]) << 8) +
                     static_cast<long long>(v[2][q]);
 #pragma unroll
-          for (int g = 0; g < 3; ++g) tmem_ld16(tsrc + uint32_t(g * OZ_BN + 16), w[g]);
+          for (int g = 0; g < 3; ++g) tmem_ld16(tsrc + uint32_t(g * gs + 16), w[g]);
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             const long long L = (static_cast<long long>(v[3][q]) << 24) + (static_cast<long long>(v[4][q]) << 16) +
@@ -511,7 +596,7 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
         }
         int32_t x[4][16];
 #pragma unroll
-        for (int g = 0; g < 4; ++g) tmem_ld16(tsrc + uint32_t((g + 3) * OZ_BN + 16), x[g]);
+        for (int g = 0; g < 4; ++g) tmem_ld16(tsrc + uint32_t((g + 3) * gs + 16), x[g]);
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(smem_u32(&tempty_bar));         // the next tile's MMAs may start
@@ -537,7 +622,7 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
         {
           int32_t v[3][16];
 #pragma unroll
-          for (int g = 0; g < 3; ++g) tmem_ld16(tsrc + uint32_t(g * OZ_BN + h), v[g]);
+          for (int g = 0; g < 3; ++g) tmem_ld16(tsrc + uint32_t(g * gs + h), v[g]);
           tmem_wait_ld();
 #pragma unroll
           for (int q = 0; q < 16; ++q)
@@ -546,7 +631,7 @@ oz_gemm_kernel(const uint8_t* __restrict__ asl, const double* __restrict__ sa, c
         }
         int32_t v[4][16];
 #pragma unroll
-        for (int g = 0; g < 4; ++g) tmem_ld16(tsrc + uint32_t((g + 3) * OZ_BN + h), v[g]);
+        for (int g = 0; g < 4; ++g) tmem_ld16(tsrc + uint32_t((g + 3) * gs + h), v[g]);
         tmem_wait_ld();
         if (hh == 1) {                              // all of this thread's TMEM is in registers
           tc_fence_before();

@@ -121,3 +121,25 @@ def test_fused_many_labels_and_fallbacks(cuda_ok):
     up, f = swb.update_and_solve(dp, image, prob_g, p["beta1"], want_field=True)
     f1 = swb.solve_fast(swb.update_basis(dp, image, p["beta1"]), None, prob_g, want_field=True)
     np.testing.assert_allclose(f.values, f1.values, rtol=0, atol=1e-13)
+
+
+def test_fused_on_the_dmma_rotation(cuda_ok):
+    """SWB_ROTATION=dmma (and K > 512) rotate on the FP64 DMMA GEMM: the
+    extra columns V (C coeff) then come from a second DMMA product."""
+    import os
+    sys.path.insert(0, str(ROOT))
+    import bench
+    import paper_1607_04174_b200 as swb
+    s = bench.cpu_sample("c1", None, 50)
+    p = s["params"]
+    image, dp, _ = _device_pack(swb, s)
+    prob = swb.LabelProblem(num_labels=p["labels"], seeds=swb.SeedPartition(s["n"], s["seeds"], s["labs"]))
+    os.environ["SWB_ROTATION"] = "dmma"
+    try:
+        up1 = swb.update_basis(dp, image, p["beta1"])
+        f1 = swb.solve_fast(up1, None, prob, want_field=True)
+        up2, f2 = swb.update_and_solve(dp, image, prob, p["beta1"], want_field=True)
+    finally:
+        os.environ.pop("SWB_ROTATION", None)
+    assert torch.equal(up1.V[:, :up1.m], up2.V[:, :up2.m])
+    np.testing.assert_allclose(f2.values, f1.values, rtol=0, atol=1e-12)
