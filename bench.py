@@ -579,7 +579,7 @@ def run_sharded(args):
     from paper_1607_04174_b200 import workloads as W
     from paper_1607_04174_b200.device import LatticeSpec
     from paper_1607_04174_b200.sharded import (CudaBackend, DistComm, Shard, SlabPlan, sharded_init_vtg,
-                                                sharded_solve, sharded_update)
+                                                sharded_solve, sharded_update, sharded_update_and_solve)
 
     world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
@@ -616,8 +616,13 @@ def run_sharded(args):
     sharded_init_vtg([sh], comm, be)
     seeds, labs = W.seeds_for(w)
 
+    fused = os.environ.get("SWB_FUSED", "1") != "0"
+
     def step(i):
         beta = p["beta1"] if i % 2 == 0 else p["beta0"]
+        if fused:   # as the N = 1 step: the reconstruction rides in the rotation
+            (labels, _, _, rc), = sharded_update_and_solve([sh], comm, be, beta, seeds, labs, p["labels"])
+            return labels, rc
         sharded_update([sh], comm, be, beta)
         (labels, _, _, rc), = sharded_solve([sh], comm, be, seeds, labs, p["labels"])
         return labels, rc

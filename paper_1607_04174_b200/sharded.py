@@ -307,6 +307,52 @@ class CudaBackend:
     def rotate(self, V_own, Cm, m, out_own):
         rotate_rows(V_own, V_own.shape[1], Cm, Cm.shape[1], V_own.shape[0], m, out_own, out_own.shape[1])
 
+    def prefill_rows(self, V, plan, ell, sidx, Cm, m, V_new):
+        """V_new[y] = V[y] C for the local rows y the seed kernels read (the
+        seed stencil rows, clamped into the local range: every write is the
+        correct V' row of a local row, halos included)."""
+        t = self.torch
+        ell_idx = ell[0]
+        rows = t.where(ell_idx >= 0, ell_idx, sidx[:, None]).reshape(-1) - plan.row_base
+        rows = rows.clamp(0, V.shape[0] - 1)
+        ldv = V.shape[1]
+        vg = V.index_select(0, rows)
+        vp = t.zeros_like(vg)
+        _lib.call("swb_gemm_nn", ptr(vg), ldv, ptr(Cm), Cm.shape[1], rows.numel(), m, m, ptr(vp), ldv, 0,
+                  stream_handle())
+        V_new.index_copy_(0, rows, vp)
+
+    def rotate_extra(self, V_own, Cm, m, out_own, coeff, uraw):
+        """out_own = V_own C and uraw = V_own (C coeff) in one rotation (the
+        extra columns ride in the INT8 GEMM's padding)."""
+        t = self.torch
+        k = coeff.shape[1]
+        ccf = t.empty((m, round_up(k, 2)), dtype=t.float64, device="cuda")
+        _lib.call("swb_gemm_nn", ptr(Cm), Cm.shape[1], ptr(coeff), k, m, coeff.shape[0], k, ptr(ccf), ccf.shape[1], 0,
+                  stream_handle())
+        c_aug = t.zeros((m, round_up(m + k, 2)), dtype=t.float64, device="cuda")
+        c_aug[:, :m].copy_(Cm[:, :m])
+        c_aug[:, m:m + k].copy_(ccf[:, :k])
+        rotate_rows(V_own, V_own.shape[1], c_aug, c_aug.shape[1], V_own.shape[0], m, out_own, out_own.shape[1],
+                    m2=m + k, out2=uraw, ldo2=k)
+
+    def finalize(self, uraw, plan, k, extra, dnorm, d_sqrt, sidx, slab, s, want_u=False):
+        t = self.torch
+        rows = plan.own_end - plan.own_begin
+        ldu = round_up(k, 2)
+        labels = t.empty(rows, dtype=t.int32, device="cuda")
+        top2 = t.empty(rows, dtype=t.float64, device="cuda")
+        U = t.empty((rows, ldu), dtype=t.float64, device="cuda") if (want_u or k > 8) else None
+        src, lds = uraw, k
+        if k > 8:
+            U[:, :k].copy_(uraw)
+            src, lds = U, ldu
+        _lib.call("swb_finalize_label", plan.own_begin, plan.own_end, k, ptr(src), lds, ptr(extra), float(dnorm),
+                  ptr(d_sqrt), ptr(U), ldu, ptr(labels), ptr(top2), stream_handle())
+        _lib.call("swb_apply_seeds", ptr(sidx), ptr(slab), s, plan.own_begin, plan.own_end, k, ptr(U), ldu,
+                  ptr(labels), ptr(top2), stream_handle())
+        return labels, top2, (U[:, :k] if U is not None else None)
+
     def rotate_vector(self, vtd, Cm, m):
         t = self.torch
         ldp = Cm.shape[1]
@@ -440,6 +486,40 @@ def sum_in_order(xs):
 
 def sharded_update(shards: list, comm, backend, new_beta: float, gap_guard: float = 0.5, cut_mask=None):
     """First-order basis update of every local shard (one all-reduce)."""
+    staged = _update_to_coeffs(shards, comm, backend, new_beta, gap_guard, cut_mask)
+    for st in staged:
+        _update_finish(backend, new_beta, st)
+    return shards
+
+
+def _update_finish(backend, new_beta, st, extra_cols=None):
+    """Rotation of the owned rows and the shard's new state; ``extra_cols``
+    (update_and_solve): (C coeff, out2) -- the extra products V (C coeff)."""
+    sh, g_new, buf, Cm, lam, order, vtd = st
+    m = sh.m
+    V_new = buf
+    _mark("rotate")
+    if extra_cols is None:
+        backend.rotate(sh.own(), Cm, m, V_new[sh.plan.own_slice()])
+    else:
+        backend.rotate_extra(sh.own(), Cm, m, V_new[sh.plan.own_slice()], *extra_cols)
+    _mark("update_tail")
+    if V_new.shape[1] > m:
+        V_new[:, m:] = 0.0
+    sh.vtg = backend.rotate_vector(vtd, Cm, m) / g_new.dnorm
+    sh.extra["spare"] = sh.V
+    sh.V = V_new
+    sh.values = lam
+    sh.graph = g_new
+    sh.beta = float(new_beta)
+    sh.extra["order"] = order
+    sh.extra["C"] = Cm
+
+
+def _update_to_coeffs(shards: list, comm, backend, new_beta: float, gap_guard: float, cut_mask):
+    """The update through the coefficients C (halo exchange, stencil,
+    projection, the one all-reduce): per shard (sh, g_new, buf, C, lam,
+    order, V^T d)."""
     # the halo transfer overlaps the graph build and the interior stencil;
     # only the first / last owned unit needs the received planes
     _mark("halo")
@@ -486,6 +566,7 @@ def sharded_update(shards: list, comm, backend, new_beta: float, gap_guard: floa
         parts.append((sh, g_new, buf, flat))
     _mark("allreduce")
     comm.allreduce_sum([p[3] for p in parts])
+    out = []
     for sh, g_new, buf, flat in parts:
         _mark("coeffs")
         m = sh.m
@@ -493,21 +574,66 @@ def sharded_update(shards: list, comm, backend, new_beta: float, gap_guard: floa
         quad, norm2, vtd = flat[m * m: m * m + m], flat[m * m + m: m * m + 2 * m], flat[m * m + 2 * m: m * m + 3 * m]
         g_new.dnorm = float(flat[m * m + 3 * m:].sum().item() ** 0.5)   # global ||d_sqrt||
         Cm, lam, order = backend.update_coeffs(P, sh.values, quad, norm2, m, gap_guard)
-        V_new = buf
-        _mark("rotate")
-        backend.rotate(sh.own(), Cm, m, V_new[sh.plan.own_slice()])
-        _mark("update_tail")
-        if V_new.shape[1] > m:
-            V_new[:, m:] = 0.0
-        sh.vtg = backend.rotate_vector(vtd, Cm, m) / g_new.dnorm
-        sh.extra["spare"] = sh.V
-        sh.V = V_new
-        sh.values = lam
-        sh.graph = g_new
-        sh.beta = float(new_beta)
-        sh.extra["order"] = order
-        sh.extra["C"] = Cm
-    return shards
+        out.append((sh, g_new, buf, Cm, lam, order, vtd))
+    return out
+
+
+def sharded_update_and_solve(shards: list, comm, backend, new_beta: float, seed_idx, seed_lab, k: int,
+                             gap_guard: float = 0.5, cut_mask=None, want_u: bool = False):
+    """sharded_update + sharded_solve (gamma = 0) with one pass less over the
+    basis, as api.update_and_solve: the seed system is solved before the
+    rotation on the V' rows the seed kernels read (each rank forms its owned
+    ones as V[rows] C), and its coefficients ride as extra columns of the
+    rotation, V (C coeff) = V' coeff; a row-wise finalize gives the labels.
+    Two all-reduces, as the separate calls.  Returns what sharded_solve does."""
+    seed_idx, seed_lab = _sorted_seeds(seed_idx, seed_lab)
+    s = int(len(seed_idx))
+    if s == 0:
+        raise InvalidParam("update_and_solve needs seeds (gamma = 0)")
+    staged = _update_to_coeffs(shards, comm, backend, new_beta, gap_guard, cut_mask)
+    _mark("solve_seeds")
+    solve_in = []
+    for sh, g_new, buf, Cm, lam, order, vtd in staged:
+        m = sh.m
+        sidx, slab = backend.seeds(seed_idx, seed_lab)
+        ell = backend.seed_rows(g_new, sidx, s)
+        backend.prefill_rows(sh.V, sh.plan, ell, sidx, Cm, m, buf)
+        q_s, b_qn, bg, lsu, dsq = backend.seed_project(buf, sh.plan, m, sidx, slab, s, ell, g_new.d_sqrt_dev,
+                                                       g_new.dnorm, k)
+        parts = [q_s, b_qn, bg, lsu, dsq]
+        sizes = [x.numel() for x in parts]
+        flat = backend.zeros((sum(sizes),))
+        o = 0
+        for x, n in zip(parts, sizes):
+            flat[o:o + n] = x.reshape(-1)
+            o += n
+        solve_in.append((sidx, slab, parts, sizes, flat))
+    _mark("solve_allreduce")
+    comm.allreduce_sum([si[4] for si in solve_in])
+    out = []
+    for st, (sidx, slab, parts, sizes, flat) in zip(staged, solve_in):
+        sh, g_new, buf, Cm, lam, order, vtd = st
+        _mark("solve_system")
+        o = 0
+        views = []
+        for x, n in zip(parts, sizes):
+            views.append(flat[o:o + n].reshape(x.shape))
+            o += n
+        q_s, b_qn, bg, lsu, dsq = views
+        m = sh.m
+        vtg = backend.rotate_vector(vtd, Cm, m) / g_new.dnorm
+        coeff, extra, rcond = backend.small_solve(0.0, s, m, k, q_s, b_qn, bg, lsu, dsq, g_new.dnorm, slab, lam,
+                                                  vtg, None)
+        uraw = backend.empty((sh.plan.own_end - sh.plan.own_begin, k))
+        _update_finish(backend, new_beta, st, extra_cols=(coeff, uraw))
+        _mark("solve_finalize")
+        labels, top2, U = backend.finalize(uraw, sh.plan, k, extra, g_new.dnorm, g_new.d_sqrt_dev, sidx, slab, s,
+                                           want_u)
+        out.append((labels, top2, U, rcond))
+    if hasattr(backend, "join_side"):
+        backend.join_side()
+    _mark("solve_end")
+    return out
 
 
 def sharded_init_vtg(shards: list, comm, backend):

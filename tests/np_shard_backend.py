@@ -68,6 +68,25 @@ class NumpyBackend:
     def rotate(self, V_own, Cm, m, out_own):
         out_own[:, :m] = _t(V_own[:, :m].numpy() @ Cm[:, :m].numpy())
 
+    def prefill_rows(self, V, plan, ell, sidx, Cm, m, V_new):
+        # the numpy seed projection reads owned rows only: form them all
+        own = slice(plan.own_begin - plan.row_base, plan.own_end - plan.row_base)
+        V_new[own, :m] = _t(V[own, :m].numpy() @ Cm[:, :m].numpy())
+
+    def rotate_extra(self, V_own, Cm, m, out_own, coeff, uraw):
+        Vo = V_own[:, :m].numpy()
+        out_own[:, :m] = _t(Vo @ Cm[:, :m].numpy())
+        uraw[:] = _t(Vo @ (Cm[:, :m].numpy()[:, :coeff.shape[0]] @ coeff.numpy()))
+
+    def finalize(self, uraw, plan, k, extra, dnorm, d_sqrt, sidx, slab, s, want_u=False):
+        d = d_sqrt.numpy()[plan.own_begin: plan.own_end]
+        u = uraw.numpy() + np.outer(d / dnorm, extra.numpy())
+        u = u / d[:, None]
+        idx = sidx.numpy()
+        own = (idx >= plan.own_begin) & (idx < plan.own_end)
+        u = O.finalize(u, idx[own] - plan.own_begin, slab.numpy()[own], k)
+        return torch.from_numpy(O.hard_labels(u)), None, _t(u)
+
     def rotate_vector(self, vtd, Cm, m):
         return _t(Cm[:, :m].numpy().T @ vtd.numpy())
 

@@ -35,13 +35,14 @@ def _problem(dims, conn, mode, m, seed):
     return img, vecs[:, :m], vals[:m], lap0, seeds, labs, priors
 
 
-def _worker(rank, world, port, outdir, dims, conn, mode, m, gamma):
+def _worker(rank, world, port, outdir, dims, conn, mode, m, gamma, fused=False):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     from np_shard_backend import NumpyBackend
     from paper_1607_04174_b200.device import LatticeSpec
-    from paper_1607_04174_b200.sharded import DistComm, Shard, SlabPlan, sharded_solve, sharded_update
+    from paper_1607_04174_b200.sharded import (DistComm, Shard, SlabPlan, sharded_solve, sharded_update,
+                                                sharded_update_and_solve)
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -60,9 +61,12 @@ def _worker(rank, world, port, outdir, dims, conn, mode, m, gamma):
         Vl[-plan.unit:] = 1e30
     sh = Shard(plan, Vl, m, torch.from_numpy(lam.copy()), lattice, torch.from_numpy(img), be.graph(img, lattice, 10.0),
                10.0)
-    sharded_update([sh], comm, be, 14.0)
-    pri_own = [torch.from_numpy(priors[plan.own_begin: plan.own_end])] if gamma > 0 else None
-    (labels, _, U, rc), = sharded_solve([sh], comm, be, seeds, labs, 2, gamma=gamma, priors=pri_own)
+    if fused:
+        (labels, _, U, rc), = sharded_update_and_solve([sh], comm, be, 14.0, seeds, labs, 2)
+    else:
+        sharded_update([sh], comm, be, 14.0)
+        pri_own = [torch.from_numpy(priors[plan.own_begin: plan.own_end])] if gamma > 0 else None
+        (labels, _, U, rc), = sharded_solve([sh], comm, be, seeds, labs, 2, gamma=gamma, priors=pri_own)
     parts = [None] * world
     dist.all_gather_object(parts, (plan.own_begin, sh.own()[:, :m].numpy(), U.numpy(), labels.numpy(),
                                    sh.values.numpy()))
@@ -75,14 +79,19 @@ def _worker(rank, world, port, outdir, dims, conn, mode, m, gamma):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,dims,conn,mode,gamma", [(2, (8, 6, 10), 6, "abs", 0.0),
-                                                        (3, (8, 6, 10), 6, "sq", 0.0),
-                                                        (2, (12, 14), 8, "sq", 0.0),
-                                                        (2, (8, 6, 10), 6, "abs", 0.5)])
-def test_sharded_update_and_solve_gloo(world, dims, conn, mode, gamma):
+@pytest.mark.parametrize("world,dims,conn,mode,gamma,fused", [(2, (8, 6, 10), 6, "abs", 0.0, False),
+                                                              (3, (8, 6, 10), 6, "sq", 0.0, False),
+                                                              (2, (12, 14), 8, "sq", 0.0, False),
+                                                              (2, (8, 6, 10), 6, "abs", 0.5, False),
+                                                              (2, (8, 6, 10), 6, "abs", 0.0, True),
+                                                              (3, (12, 14), 8, "sq", 0.0, True)])
+def test_sharded_update_and_solve_gloo(world, dims, conn, mode, gamma, fused):
+    """fused: sharded_update_and_solve (the seed system before the rotation,
+    the reconstruction as extra rotation columns) -- same results."""
     m = 16
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(world, _free_port(), d, dims, conn, mode, m, gamma), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), d, dims, conn, mode, m, gamma, fused), nprocs=world,
+                 join=True)
         out = np.load(os.path.join(d, "out.npz"))
     img, V, lam, lap0, seeds, labs, priors = _problem(dims, conn, mode, m, 7)
     lap1 = O.build_laplacian(img, dims, 14.0, mode, conn)
