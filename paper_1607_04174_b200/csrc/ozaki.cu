@@ -38,7 +38,10 @@ namespace {
 
 constexpr int OZ_G = 7;                 // product groups g = i + j <= 6
 constexpr int OZ_BN = 64;               // columns per tile (MMA N)
-constexpr int OZ_STAGES = 4;
+#ifndef OZ_STAGES_CFG
+#define OZ_STAGES_CFG 4
+#endif
+constexpr int OZ_STAGES = OZ_STAGES_CFG;
 constexpr int OZ_B_SLICE = OZ_BN * OZ_KC;            // 2048 B: [kq 2][col 64][16 B]
 constexpr int OZ_B_STAGE = OZ_S * OZ_B_SLICE;        // 14 KB
 constexpr int OZ_STAGE = OZ_A_STAGE + OZ_B_STAGE;
