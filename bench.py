@@ -409,7 +409,7 @@ def _fused(state) -> bool:
     for the gamma = 0 configs with a fixed K; SWB_FUSED=0 times the two
     separate calls (update_basis, solve_fast) instead."""
     return (os.environ.get("SWB_FUSED", "1") != "0" and state.get("method") != "rayleigh"
-            and state["prob"] is not None and state["params"].get("epsilon") is None)
+            and state["prob"] is not None)
 
 
 def _next_pack_and_solve(state, beta, i, prob):
@@ -418,7 +418,9 @@ def _next_pack_and_solve(state, beta, i, prob):
     spare = state.pop("spare", None)
     old = state["pack"]
     cut = state.get("cut") if i % 2 == 0 else None
-    pack, field = swb.update_and_solve(old, state["image"], prob, beta, cut_edges=cut, out=spare)
+    eps = state["params"].get("epsilon")
+    policy = swb.AdaptivePolicy(epsilon=eps) if eps is not None else None
+    pack, field = swb.update_and_solve(old, state["image"], prob, beta, cut_edges=cut, out=spare, policy=policy)
     state["spare"] = old.V
     state["pack"] = pack
     return field
@@ -763,8 +765,8 @@ def run_gpu(args):
         # ping-pong back to where they started); the last pack's eigenvalues
         # and V'^T g are copied into the first pack's tensors so that every
         # replay continues the chain (swb.CapturedStep)
-        if not _fused(state):
-            raise SystemExit("--graph: configs whose step is one update_and_solve (c1, c2, c4)")
+        if not _fused(state) or state["params"].get("epsilon") is not None:
+            raise SystemExit("--graph: configs whose step is one update_and_solve at a fixed K (c1, c2, c4)")
         from paper_1607_04174_b200.capture import CapturedStep
 
         def two_steps():

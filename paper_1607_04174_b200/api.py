@@ -608,7 +608,7 @@ def solve_fast(pack, lap, prob, m_use: int | None = None, streaming_block: int |
 
 def update_and_solve(pack, image, prob, new_beta: float | None = None, cut_edges=None, *, gap_guard: float = 0.5,
                      m_use: int | None = None, want_field: bool = False, check: bool = True, out=None,
-                     connectivity=None, weight_mode=None):
+                     connectivity=None, weight_mode=None, policy=None):
     """``update_basis(pack, image, new_beta, cut_edges)`` followed by
     ``solve_fast(updated, None, prob, m_use)`` with one pass less over the
     basis: returns ``(updated_pack, field)``, the same objects the two calls
@@ -623,7 +623,10 @@ def update_and_solve(pack, image, prob, new_beta: float | None = None, cut_edges
     reconstruction (fastrw.py:456-466) costs no pass over V' and no tensor
     work; a row-wise finalize + argmax (solver.py:55-66, images.py:128-130)
     reads the N x L products.  gamma > 0 (priors) and the all-/no-seed
-    cases take the two separate calls."""
+    cases take the two separate calls.  ``policy`` (an AdaptivePolicy):
+    m_use = select_m(updated, prob, policy) first (adaptive.py:133-185; at
+    gamma = 0 it reads only the seed rows, which are formed before the
+    rotation); the chosen m is ``field.m_use``."""
     torch = require_cuda()
     seeds = prob.seeds
     s = int(seeds.n_seeds)
@@ -631,7 +634,11 @@ def update_and_solve(pack, image, prob, new_beta: float | None = None, cut_edges
     if float(prob.gamma) != 0 or s == 0 or s >= dp0.n_vertices:
         up = update_basis(pack, image, new_beta, cut_edges, gap_guard=gap_guard, out=out,
                           connectivity=connectivity, weight_mode=weight_mode)
-        return up, solve_fast(up, None, prob, m_use, want_field=want_field, check=check)
+        if policy is not None:
+            m_use, _ = select_m(up, prob, policy)
+        f = solve_fast(up, None, prob, m_use, want_field=want_field, check=check)
+        f.m_use = m_use
+        return up, f
     state = {}
 
     def pre_rotate(up, dp, Cm, ldp):
@@ -651,7 +658,11 @@ def update_and_solve(pack, image, prob, new_beta: float | None = None, cut_edges
         vp = torch.zeros_like(vg)
         _lib.call("swb_gemm_nn", ptr(vg), ldv, ptr(Cm), ldp, rows.numel(), m, m, ptr(vp), ldv, 0, st)
         up.V.index_copy_(0, rows, vp)
-        d = solve_fast(up, None, prob, m_use, want_field=want_field, check=check, _defer=True)
+        mu = m_use
+        if policy is not None:
+            mu, _ = select_m(up, prob, policy)
+        state["m_use"] = mu
+        d = solve_fast(up, None, prob, mu, want_field=want_field, check=check, _defer=True)
         k, mr, cf = d["k"], d["mr"], d["cf"]
         # C_aug = [C | C[:, :mr] coeff]; V C_aug[:, m:] = V' coeff
         m2 = m + k
@@ -691,6 +702,7 @@ def update_and_solve(pack, image, prob, new_beta: float | None = None, cut_edges
                 condition=1.0 / max(rc, 1e-300))
     field = DeviceField(dev.dims, k, labels, top2, U, recompute=lambda: d["reconstruct"](True))
     field.rcond_dev = d["rcond"]
+    field.m_use = state["m_use"]
     return up, field
 
 

@@ -143,3 +143,25 @@ def test_fused_on_the_dmma_rotation(cuda_ok):
         os.environ.pop("SWB_ROTATION", None)
     assert torch.equal(up1.V[:, :up1.m], up2.V[:, :up2.m])
     np.testing.assert_allclose(f2.values, f1.values, rtol=0, atol=1e-12)
+
+
+def test_fused_with_select_m(cuda_ok):
+    """update_and_solve(policy=...): select_m on the updated basis (its seed
+    rows formed before the rotation) picks the same m as select_m on the
+    update_basis result, and the field matches solve_fast at that m (c3's
+    adaptive workload on a 128 x 128 x 4 slab)."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    import paper_1607_04174_b200 as swb
+    s = bench.cpu_sample("c3", None, 150)
+    p = s["params"]
+    image, dp, _ = _device_pack(swb, s)
+    prob = swb.LabelProblem(num_labels=p["labels"], seeds=swb.SeedPartition(s["n"], s["seeds"], s["labs"]))
+    pol = swb.AdaptivePolicy(epsilon=p["epsilon"])
+    up1 = swb.update_basis(dp, image, p["beta1"])
+    m1, _ = swb.select_m(up1, prob, pol)
+    f1 = swb.solve_fast(up1, None, prob, m1, want_field=True)
+    up2, f2 = swb.update_and_solve(dp, image, prob, p["beta1"], policy=pol, want_field=True)
+    assert f2.m_use == m1
+    assert torch.equal(up1.V[:, :up1.m], up2.V[:, :up2.m])
+    np.testing.assert_allclose(f2.values, f1.values, rtol=0, atol=1e-12)
