@@ -426,9 +426,26 @@ def _next_pack_and_solve(state, beta, i, prob):
     return field
 
 
+def _registration_fused(state, beta, i, fixed, moving):
+    """c5 through update_and_solve: the similarity priors first (they do not
+    depend on the basis), then the update and the gamma > 0 solve with the
+    reconstruction in the rotation, then the expected displacement."""
+    import paper_1607_04174_b200 as swb
+    from paper_1607_04174_b200 import registration as R
+    p = state["params"]
+    pri = R.similarity_priors(fixed, moving, state["grid"], p["patch_radius"])
+    prob = swb.LabelProblem(num_labels=p["labels"], seeds=swb.SeedPartition(state["n"], [], []),
+                            priors=pri.values_dev, gamma=p["gamma"])
+    field = _next_pack_and_solve(state, beta, i, prob)
+    field.displacement_dev = R.expected_displacement_device(field, state["grid"])
+    return field
+
+
 def gpu_step(state, i):
     p = state["params"]
     beta = p["beta1"] if i % 2 == 0 else p["beta0"]
+    if state["prob"] is None and os.environ.get("SWB_FUSED", "1") != "0":
+        return _registration_fused(state, beta, i, state["image"], state["moving"])
     if _fused(state):
         return _next_pack_and_solve(state, beta, i, _round_prob(state, i))
     pack = _next_pack(state, beta, i)
@@ -448,8 +465,11 @@ def e2e_step(state, i, host_labels):
         # step), host label map + displacement field out
         fixed = swb.Image(state["w"].dims, state["w"].intensities)
         moving = swb.Image(state["w"].dims, p["moving"])
-        pack = _next_pack(state, beta, i)
-        field = registration_solve(state, pack, fixed, moving)
+        if os.environ.get("SWB_FUSED", "1") != "0":
+            field = _registration_fused(state, beta, i, fixed, moving)
+        else:
+            pack = _next_pack(state, beta, i)
+            field = registration_solve(state, pack, fixed, moving)
         host_labels.copy_(field.labels_dev, non_blocking=True)
         state["host_disp"].copy_(field.displacement_dev, non_blocking=True)
         return field

@@ -474,7 +474,8 @@ def _ell_from_lap(lap, seed_idx: np.ndarray):
 
 
 def solve_fast(pack, lap, prob, m_use: int | None = None, streaming_block: int | None = None,
-               *, want_field: bool = False, check: bool = True, _defer: bool = False) -> DeviceField:
+               *, want_field: bool = False, check: bool = True, _defer: bool = False,
+               _tp_basis=None) -> DeviceField:
     """fastrw.py:352-467 on the device.
 
     ``pack``: DevicePack / RefreshedPack / UpdatedPack, or a host pack
@@ -553,9 +554,21 @@ def solve_fast(pack, lap, prob, m_use: int | None = None, streaming_block: int |
                   ptr(ph), ldt, st)
         mr = dp.mr if col_map is not None else m_use
         tp_full = torch.empty((mr, ldt), dtype=torch.float64, device="cuda")
-        tws = WORKSPACE.get("gemm_tn", _lib.size("swb_gemm_tn_workspace_bytes", n, mr, k))
-        _lib.call("swb_gemm_tn", ptr(dp.V), dp.ldv, ptr(ph), ldt, n, mr, k, 0, ptr(tp_full), ldt, ptr(tws),
-                  tws.numel(), st)
+        if _tp_basis is not None:
+            # update_and_solve: V'^T P^ = C^T (V^T P^) from the basis before the rotation
+            Vb, ldvb, Cm, ldc = _tp_basis
+            mb = Cm.shape[0]
+            tb = torch.empty((mb, ldt), dtype=torch.float64, device="cuda")
+            tws = WORKSPACE.get("gemm_tn", _lib.size("swb_gemm_tn_workspace_bytes", n, mb, k))
+            _lib.call("swb_gemm_tn", ptr(Vb), ldvb, ptr(ph), ldt, n, mb, k, 0, ptr(tb), ldt, ptr(tws), tws.numel(),
+                      st)
+            tws = WORKSPACE.get("gemm_tn", _lib.size("swb_gemm_tn_workspace_bytes", mb, mr, k))
+            _lib.call("swb_gemm_tn", ptr(Cm), ldc, ptr(tb), ldt, mb, mr, k, 0, ptr(tp_full), ldt, ptr(tws),
+                      tws.numel(), st)
+        else:
+            tws = WORKSPACE.get("gemm_tn", _lib.size("swb_gemm_tn_workspace_bytes", n, mr, k))
+            _lib.call("swb_gemm_tn", ptr(dp.V), dp.ldv, ptr(ph), ldt, n, mr, k, 0, ptr(tp_full), ldt, ptr(tws),
+                      tws.numel(), st)
         if col_map is not None:
             t_p = torch.empty((m_use, ldt), dtype=torch.float64, device="cuda")
             _lib.call("swb_gather_rows", ptr(tp_full), ldt, ptr(col_map), m_use, k, ptr(t_p), ldt, st)
@@ -622,16 +635,19 @@ def update_and_solve(pack, image, prob, new_beta: float | None = None, cut_edges
     GEMM's last 64-column tile (K = 400: 48 free columns), so the
     reconstruction (fastrw.py:456-466) costs no pass over V' and no tensor
     work; a row-wise finalize + argmax (solver.py:55-66, images.py:128-130)
-    reads the N x L products.  gamma > 0 (priors) and the all-/no-seed
-    cases take the two separate calls.  ``policy`` (an AdaptivePolicy):
-    m_use = select_m(updated, prob, policy) first (adaptive.py:133-185; at
-    gamma = 0 it reads only the seed rows, which are formed before the
-    rotation); the chosen m is ``field.m_use``."""
+    reads the N x L products.  gamma > 0 (priors): the prior projection
+    V'^T P^ is C^T (V^T P^), from the basis before the rotation.  The
+    all-seeded case, gamma = 0 without seeds and a policy at gamma > 0 take
+    the two separate calls.  ``policy`` (an AdaptivePolicy): m_use =
+    select_m(updated, prob, policy) first (adaptive.py:133-185; at gamma = 0
+    it reads only the seed rows, which are formed before the rotation); the
+    chosen m is ``field.m_use``."""
     torch = require_cuda()
     seeds = prob.seeds
     s = int(seeds.n_seeds)
+    gamma = float(prob.gamma)
     dp0 = _as_device(pack, image, connectivity, weight_mode)
-    if float(prob.gamma) != 0 or s == 0 or s >= dp0.n_vertices:
+    if s >= dp0.n_vertices or (gamma == 0 and s == 0) or (policy is not None and gamma != 0):
         up = update_basis(pack, image, new_beta, cut_edges, gap_guard=gap_guard, out=out,
                           connectivity=connectivity, weight_mode=weight_mode)
         if policy is not None:
@@ -646,23 +662,25 @@ def update_and_solve(pack, image, prob, new_beta: float | None = None, cut_edges
         g_new = up.graph
         # V' rows at the seeds and their stencil neighbours: V[rows] C
         _mark("solve_prefill")
-        sidx, _ = seed_tensors(seeds)
-        R = 2 * g_new.lattice.ndir + 1
-        ell_idx = torch.empty((s, R), dtype=torch.int64, device="cuda")
-        ell_val = torch.empty((s, R), dtype=torch.float64, device="cuda")
-        lat = g_new.lattice.c_struct()
-        _lib.call("swb_seed_rows", C.byref(lat), ptr(g_new.what), ptr(g_new.diag), ptr(sidx), s, ptr(ell_idx),
-                  ptr(ell_val), st)
-        rows = torch.where(ell_idx >= 0, ell_idx, sidx[:, None]).reshape(-1)
-        vg = dp.V.index_select(0, rows)
-        vp = torch.zeros_like(vg)
-        _lib.call("swb_gemm_nn", ptr(vg), ldv, ptr(Cm), ldp, rows.numel(), m, m, ptr(vp), ldv, 0, st)
-        up.V.index_copy_(0, rows, vp)
+        if s:
+            sidx, _ = seed_tensors(seeds)
+            R = 2 * g_new.lattice.ndir + 1
+            ell_idx = torch.empty((s, R), dtype=torch.int64, device="cuda")
+            ell_val = torch.empty((s, R), dtype=torch.float64, device="cuda")
+            lat = g_new.lattice.c_struct()
+            _lib.call("swb_seed_rows", C.byref(lat), ptr(g_new.what), ptr(g_new.diag), ptr(sidx), s, ptr(ell_idx),
+                      ptr(ell_val), st)
+            rows = torch.where(ell_idx >= 0, ell_idx, sidx[:, None]).reshape(-1)
+            vg = dp.V.index_select(0, rows)
+            vp = torch.zeros_like(vg)
+            _lib.call("swb_gemm_nn", ptr(vg), ldv, ptr(Cm), ldp, rows.numel(), m, m, ptr(vp), ldv, 0, st)
+            up.V.index_copy_(0, rows, vp)
         mu = m_use
         if policy is not None:
             mu, _ = select_m(up, prob, policy)
         state["m_use"] = mu
-        d = solve_fast(up, None, prob, mu, want_field=want_field, check=check, _defer=True)
+        d = solve_fast(up, None, prob, mu, want_field=want_field, check=check, _defer=True,
+                       _tp_basis=(dp.V, ldv, Cm, ldp) if gamma != 0 else None)
         k, mr, cf = d["k"], d["mr"], d["cf"]
         # C_aug = [C | C[:, :mr] coeff]; V C_aug[:, m:] = V' coeff
         m2 = m + k
@@ -672,9 +690,12 @@ def update_and_solve(pack, image, prob, new_beta: float | None = None, cut_edges
         ccf = torch.empty((m, round_up(k, 2)), dtype=torch.float64, device="cuda")
         _lib.call("swb_gemm_nn", ptr(Cm), ldp, ptr(cf), k, m, mr, k, ptr(ccf), ccf.shape[1], 0, st)
         c_aug[:, m:m2].copy_(ccf[:, :k])
-        uraw = torch.empty((up.n_vertices, k), dtype=torch.float64, device="cuda")
+        # many labels: the products go straight into the field U (finalized
+        # in place); else a compact N x L block
+        ldr = d["ldu"] if k > 8 else k
+        uraw = torch.empty((up.n_vertices, ldr), dtype=torch.float64, device="cuda")
         state.update(d=d, uraw=uraw)
-        return m2, c_aug, ldca, uraw, k
+        return m2, c_aug, ldca, uraw, ldr
 
     up = update_basis(pack, image, new_beta, cut_edges, gap_guard=gap_guard, out=out, connectivity=connectivity,
                       weight_mode=weight_mode, _pre_rotate=pre_rotate, _m2=dp0.m + prob.K)
@@ -682,12 +703,12 @@ def update_and_solve(pack, image, prob, new_beta: float | None = None, cut_edges
     n, k, dev = d["n"], d["k"], d["dp"]
     labels, top2, ldu = d["labels"], d["top2"], d["ldu"]
     _mark("solve_finalize")
-    U = torch.empty((n, ldu), dtype=torch.float64, device="cuda") if (want_field or k > 8) else None
-    if k > 8:   # the many-label finalize works in place
-        U[:, :k].copy_(uraw)
+    if k > 8:   # the many-label finalize works in place, in U
+        U = uraw
         _lib.call("swb_finalize_label", 0, n, k, ptr(U), ldu, ptr(d["extra"]), dev.dnorm, ptr(dev.d_sqrt_dev),
                   ptr(U), ldu, ptr(labels), ptr(top2), stream_handle())
     else:
+        U = torch.empty((n, ldu), dtype=torch.float64, device="cuda") if want_field else None
         _lib.call("swb_finalize_label", 0, n, k, ptr(uraw), k, ptr(d["extra"]), dev.dnorm, ptr(dev.d_sqrt_dev),
                   ptr(U), ldu, ptr(labels), ptr(top2), stream_handle())
     _lib.call("swb_apply_seeds", ptr(d["sidx"]), ptr(d["slab"]), d["s"], 0, n, k, ptr(U), ldu, ptr(labels),

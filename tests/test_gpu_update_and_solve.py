@@ -120,7 +120,26 @@ def test_fused_many_labels_and_fallbacks(cuda_ok):
     prob_g = swb.LabelProblem(num_labels=3, seeds=swb.SeedPartition(n, [], []), priors=pri, gamma=0.5)
     up, f = swb.update_and_solve(dp, image, prob_g, p["beta1"], want_field=True)
     f1 = swb.solve_fast(swb.update_basis(dp, image, p["beta1"]), None, prob_g, want_field=True)
-    np.testing.assert_allclose(f.values, f1.values, rtol=0, atol=1e-13)
+    np.testing.assert_allclose(f.values, f1.values, rtol=0, atol=1e-12)
+
+
+def test_fused_gamma_priors(cuda_ok):
+    """gamma > 0 through update_and_solve: V'^T P^ formed as C^T (V^T P^)
+    before the rotation; 27 labels with priors, without and with seeds."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    import paper_1607_04174_b200 as swb
+    s = bench.cpu_sample("c1", None, 50)
+    p = s["params"]
+    image, dp, _ = _device_pack(swb, s)
+    rng = np.random.default_rng(8)
+    n = s["n"]
+    pri = rng.random((n, 27)) ** 4
+    pri /= pri.sum(1, keepdims=True)
+    seeds = np.sort(rng.choice(n, 30, replace=False))
+    for sp in (swb.SeedPartition(n, [], []), swb.SeedPartition(n, seeds, rng.integers(0, 27, seeds.size))):
+        prob = swb.LabelProblem(num_labels=27, seeds=sp, priors=pri, gamma=1.0)
+        _check_against_separate(swb, dp, image, prob, p["beta1"])
 
 
 def test_fused_on_the_dmma_rotation(cuda_ok):
