@@ -479,6 +479,18 @@ int swb_update_and_solve(const swb_lattice* lat, const double* image, double bet
                          double* top2_out, double* U_out, int64_t ldu, double* rcond_host, void* workspace,
                          size_t workspace_bytes, void* stream);
 
+/* Pieces of update_and_solve: the V rows of the seeds' stencil
+ * neighbourhoods (S x R entries of swb_seed_rows' ell_idx, -1 -> the seed;
+ * rows clamped into a buffer of global rows [row_base, row_base +
+ * local_rows)) gathered into out (S R x ldv, pad columns zero) / scattered
+ * back from src (columns < M); C_aug = [C | ccf | 0] (M x ldca). */
+int swb_ell_rows_gather(const double* V, int64_t ldv, int64_t row_base, int64_t local_rows, const int64_t* ell_idx,
+                        const int64_t* seed_idx, int64_t S, int64_t R, int64_t M, double* out, void* stream);
+int swb_ell_rows_scatter(const double* src, int64_t ldv, int64_t row_base, int64_t local_rows, const int64_t* ell_idx,
+                         const int64_t* seed_idx, int64_t S, int64_t R, int64_t M, double* V, void* stream);
+int swb_build_caug(const double* C, int64_t ldp, const double* ccf, int64_t ldk, int64_t M, int64_t K, double* caug,
+                   int64_t ldca, void* stream);
+
 /* ---- small helpers used by the host layer --------------------------- */
 /* out = sum_x v[x]^2 over n entries (deterministic). */
 int swb_sumsq(const double* v, int64_t n, double* out, void* workspace,

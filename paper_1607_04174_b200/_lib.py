@@ -98,6 +98,9 @@ SIGNATURES = {
     "swb_oz_layout_info": (C.c_int, [c_i64, c_i64, c_i64, c_vp]),
     "swb_gemm_tn_sym_emit": (C.c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_sz, c_vp, c_i64,
                                        c_vp, c_sz, c_vp]),
+    "swb_ell_rows_gather": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),
+    "swb_ell_rows_scatter": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),
+    "swb_build_caug": (C.c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp]),
     "swb_oz_gemm_planes_split": (C.c_int, [c_i64, c_i64, c_i64, c_i64, C.c_int, c_vp, c_i64, c_i64, c_vp, c_i64,
                                            c_vp, C.c_size_t, c_vp]),
     "swb_finalize_label": (C.c_int, [c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_dbl, c_vp, c_vp, c_i64, c_vp, c_vp,

@@ -670,11 +670,12 @@ def update_and_solve(pack, image, prob, new_beta: float | None = None, cut_edges
             lat = g_new.lattice.c_struct()
             _lib.call("swb_seed_rows", C.byref(lat), ptr(g_new.what), ptr(g_new.diag), ptr(sidx), s, ptr(ell_idx),
                       ptr(ell_val), st)
-            rows = torch.where(ell_idx >= 0, ell_idx, sidx[:, None]).reshape(-1)
-            vg = dp.V.index_select(0, rows)
-            vp = torch.zeros_like(vg)
-            _lib.call("swb_gemm_nn", ptr(vg), ldv, ptr(Cm), ldp, rows.numel(), m, m, ptr(vp), ldv, 0, st)
-            up.V.index_copy_(0, rows, vp)
+            vg = torch.empty((s * R, ldv), dtype=torch.float64, device="cuda")
+            vp = torch.empty_like(vg)
+            nv = up.n_vertices
+            _lib.call("swb_ell_rows_gather", ptr(dp.V), ldv, 0, nv, ptr(ell_idx), ptr(sidx), s, R, m, ptr(vg), st)
+            _lib.call("swb_gemm_nn", ptr(vg), ldv, ptr(Cm), ldp, s * R, m, m, ptr(vp), ldv, 0, st)
+            _lib.call("swb_ell_rows_scatter", ptr(vp), ldv, 0, nv, ptr(ell_idx), ptr(sidx), s, R, m, ptr(up.V), st)
         mu = m_use
         if policy is not None:
             mu, _ = select_m(up, prob, policy)
@@ -685,11 +686,10 @@ def update_and_solve(pack, image, prob, new_beta: float | None = None, cut_edges
         # C_aug = [C | C[:, :mr] coeff]; V C_aug[:, m:] = V' coeff
         m2 = m + k
         ldca = round_up(m2, 2)
-        c_aug = torch.zeros((m, ldca), dtype=torch.float64, device="cuda")
-        c_aug[:, :m].copy_(Cm[:, :m])
+        c_aug = torch.empty((m, ldca), dtype=torch.float64, device="cuda")
         ccf = torch.empty((m, round_up(k, 2)), dtype=torch.float64, device="cuda")
         _lib.call("swb_gemm_nn", ptr(Cm), ldp, ptr(cf), k, m, mr, k, ptr(ccf), ccf.shape[1], 0, st)
-        c_aug[:, m:m2].copy_(ccf[:, :k])
+        _lib.call("swb_build_caug", ptr(Cm), ldp, ptr(ccf), ccf.shape[1], m, k, ptr(c_aug), ldca, st)
         # many labels: the products go straight into the field U (finalized
         # in place); else a compact N x L block
         ldr = d["ldu"] if k > 8 else k

@@ -15,6 +15,7 @@
 //                            basis (api.update_and_solve): seed system first,
 //                            reconstruction as extra rotation columns
 #include "swb_common.cuh"
+#include <algorithm>
 #include <cstdlib>
 
 extern "C" size_t swb_oz_gemm_nn_workspace_bytes(int64_t rows, int64_t K, int64_t M2);
@@ -291,21 +292,31 @@ __device__ __forceinline__ int64_t ell_row(const int64_t* ell_idx, const int64_t
   return r >= 0 ? r : seed_idx[e / R];
 }
 
-__global__ void gather_ell_rows_kernel(const double* __restrict__ V, int64_t ldv, const int64_t* __restrict__ ell_idx,
-                                       const int64_t* __restrict__ seed_idx, int64_t E, int64_t R, int64_t M,
-                                       double* __restrict__ out) {
+// local row of entry e in a buffer holding global rows [row_base, row_base +
+// local_rows) (a slab shard: rows outside are clamped in, every write then
+// stores that local row's correct value)
+__device__ __forceinline__ int64_t ell_local(const int64_t* ell_idx, const int64_t* seed_idx, int64_t e, int64_t R,
+                                             int64_t row_base, int64_t local_rows) {
+  const int64_t y = ell_row(ell_idx, seed_idx, e, R) - row_base;
+  return y < 0 ? 0 : (y >= local_rows ? local_rows - 1 : y);
+}
+
+__global__ void gather_ell_rows_kernel(const double* __restrict__ V, int64_t ldv, int64_t row_base, int64_t local_rows,
+                                       const int64_t* __restrict__ ell_idx, const int64_t* __restrict__ seed_idx,
+                                       int64_t E, int64_t R, int64_t M, double* __restrict__ out) {
   for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
-    const double* src = V + ell_row(ell_idx, seed_idx, e, R) * ldv;
+    const double* src = V + ell_local(ell_idx, seed_idx, e, R, row_base, local_rows) * ldv;
     for (int64_t j = threadIdx.x; j < ldv; j += blockDim.x) out[e * ldv + j] = j < M ? src[j] : 0.0;
   }
 }
 
 // identical rows may appear several times: every writer stores the same values
-__global__ void scatter_ell_rows_kernel(const double* __restrict__ src, int64_t ldv, const int64_t* __restrict__ ell_idx,
+__global__ void scatter_ell_rows_kernel(const double* __restrict__ src, int64_t ldv, int64_t row_base,
+                                        int64_t local_rows, const int64_t* __restrict__ ell_idx,
                                         const int64_t* __restrict__ seed_idx, int64_t E, int64_t R, int64_t M,
                                         double* __restrict__ V) {
   for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
-    double* dst = V + ell_row(ell_idx, seed_idx, e, R) * ldv;
+    double* dst = V + ell_local(ell_idx, seed_idx, e, R, row_base, local_rows) * ldv;
     for (int64_t j = threadIdx.x; j < M; j += blockDim.x) dst[j] = src[e * ldv + j];
   }
 }
@@ -417,10 +428,10 @@ extern "C" int swb_update_and_solve(const swb_lattice* lat, const double* image,
   // ---- the seed system on V' rows formed as V[rows] C ----
   if ((rc = swb_seed_rows(lat, u.what_n, u.diag_n, seed_idx, S, w.ell_idx, w.ell_val, stream))) return rc;
   const unsigned eg = static_cast<unsigned>(E < 65535 ? E : 65535);
-  gather_ell_rows_kernel<<<eg, 128, 0, st>>>(V, ldv, w.ell_idx, seed_idx, E, R, M, f.rows_v);
+  gather_ell_rows_kernel<<<eg, 128, 0, st>>>(V, ldv, 0, N, w.ell_idx, seed_idx, E, R, M, f.rows_v);
   SWB_CHECK_LAUNCH();
   if ((rc = swb_gemm_nn(f.rows_v, ldv, u.C, ldp, E, M, M, f.rows_vp, ldv, 0, stream))) return rc;
-  scatter_ell_rows_kernel<<<eg, 128, 0, st>>>(f.rows_vp, ldv, w.ell_idx, seed_idx, E, R, M, V_out);
+  scatter_ell_rows_kernel<<<eg, 128, 0, st>>>(f.rows_vp, ldv, 0, N, w.ell_idx, seed_idx, E, R, M, V_out);
   SWB_CHECK_LAUNCH();
   if ((rc = swb_seed_project(V_out, ldv, 0, 0, N, m_use, nullptr, seed_idx, seed_lab, S, w.ell_idx, w.ell_val, R,
                              d_sqrt_out, dnorm, K, w.q_s, ldq, w.b_qn, w.bg, w.lsu, w.dsq_s, stream)))
@@ -458,4 +469,43 @@ extern "C" int swb_update_and_solve(const swb_lattice* lat, const double* image,
   SWB_CUDA_TRY(cudaStreamSynchronize(st));
   if (rcond_host) *rcond_host = rc_h;
   return swb_check_rcond(rc_h);
+}
+
+// ---------------------------------------------------------------------------
+// pieces of update_and_solve for the host layer (one launch each)
+// ---------------------------------------------------------------------------
+extern "C" int swb_ell_rows_gather(const double* V, int64_t ldv, int64_t row_base, int64_t local_rows,
+                                   const int64_t* ell_idx, const int64_t* seed_idx, int64_t S, int64_t R, int64_t M,
+                                   double* out, void* stream) {
+  if (!V || !ell_idx || !seed_idx || !out || S < 0 || R <= 0 || M <= 0 || ldv < M || local_rows <= 0)
+    return SWB_INVALID_PARAM;
+  const int64_t E = S * R;
+  if (E == 0) return SWB_OK;
+  gather_ell_rows_kernel<<<static_cast<unsigned>(E < 65535 ? E : 65535), 128, 0, swb_stream(stream)>>>(
+      V, ldv, row_base, local_rows, ell_idx, seed_idx, E, R, M, out);
+  SWB_CHECK_LAUNCH();
+  return SWB_OK;
+}
+
+extern "C" int swb_ell_rows_scatter(const double* src, int64_t ldv, int64_t row_base, int64_t local_rows,
+                                    const int64_t* ell_idx, const int64_t* seed_idx, int64_t S, int64_t R, int64_t M,
+                                    double* V, void* stream) {
+  if (!V || !ell_idx || !seed_idx || !src || S < 0 || R <= 0 || M <= 0 || ldv < M || local_rows <= 0)
+    return SWB_INVALID_PARAM;
+  const int64_t E = S * R;
+  if (E == 0) return SWB_OK;
+  scatter_ell_rows_kernel<<<static_cast<unsigned>(E < 65535 ? E : 65535), 128, 0, swb_stream(stream)>>>(
+      src, ldv, row_base, local_rows, ell_idx, seed_idx, E, R, M, V);
+  SWB_CHECK_LAUNCH();
+  return SWB_OK;
+}
+
+extern "C" int swb_build_caug(const double* C, int64_t ldp, const double* ccf, int64_t ldk, int64_t M, int64_t K,
+                              double* caug, int64_t ldca, void* stream) {
+  if (!C || !ccf || !caug || M <= 0 || K <= 0 || ldp < M || ldk < K || ldca < M + K) return SWB_INVALID_PARAM;
+  const int64_t total = M * ldca;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, int64_t(swb_sm_count()) * 8));
+  aug_kernel<<<grid, 256, 0, swb_stream(stream)>>>(C, ldp, ccf, ldk, M, K, caug, ldca);
+  SWB_CHECK_LAUNCH();
+  return SWB_OK;
 }

@@ -312,15 +312,16 @@ class CudaBackend:
         seed stencil rows, clamped into the local range: every write is the
         correct V' row of a local row, halos included)."""
         t = self.torch
-        ell_idx = ell[0]
-        rows = t.where(ell_idx >= 0, ell_idx, sidx[:, None]).reshape(-1) - plan.row_base
-        rows = rows.clamp(0, V.shape[0] - 1)
-        ldv = V.shape[1]
-        vg = V.index_select(0, rows)
-        vp = t.zeros_like(vg)
-        _lib.call("swb_gemm_nn", ptr(vg), ldv, ptr(Cm), Cm.shape[1], rows.numel(), m, m, ptr(vp), ldv, 0,
-                  stream_handle())
-        V_new.index_copy_(0, rows, vp)
+        ell_idx, _, R = ell
+        s = int(sidx.numel())
+        ldv, st = V.shape[1], stream_handle()
+        vg = t.empty((s * R, ldv), dtype=t.float64, device="cuda")
+        vp = t.empty_like(vg)
+        _lib.call("swb_ell_rows_gather", ptr(V), ldv, plan.row_base, V.shape[0], ptr(ell_idx), ptr(sidx), s, R, m,
+                  ptr(vg), st)
+        _lib.call("swb_gemm_nn", ptr(vg), ldv, ptr(Cm), Cm.shape[1], s * R, m, m, ptr(vp), ldv, 0, st)
+        _lib.call("swb_ell_rows_scatter", ptr(vp), ldv, plan.row_base, V.shape[0], ptr(ell_idx), ptr(sidx), s, R, m,
+                  ptr(V_new), st)
 
     def rotate_extra(self, V_own, Cm, m, out_own, coeff, uraw):
         """out_own = V_own C and uraw = V_own (C coeff) in one rotation (the
@@ -330,9 +331,9 @@ class CudaBackend:
         ccf = t.empty((m, round_up(k, 2)), dtype=t.float64, device="cuda")
         _lib.call("swb_gemm_nn", ptr(Cm), Cm.shape[1], ptr(coeff), k, m, coeff.shape[0], k, ptr(ccf), ccf.shape[1], 0,
                   stream_handle())
-        c_aug = t.zeros((m, round_up(m + k, 2)), dtype=t.float64, device="cuda")
-        c_aug[:, :m].copy_(Cm[:, :m])
-        c_aug[:, m:m + k].copy_(ccf[:, :k])
+        c_aug = t.empty((m, round_up(m + k, 2)), dtype=t.float64, device="cuda")
+        _lib.call("swb_build_caug", ptr(Cm), Cm.shape[1], ptr(ccf), ccf.shape[1], m, k, ptr(c_aug), c_aug.shape[1],
+                  stream_handle())
         rotate_rows(V_own, V_own.shape[1], c_aug, c_aug.shape[1], V_own.shape[0], m, out_own, out_own.shape[1],
                     m2=m + k, out2=uraw, ldo2=k)
 
