@@ -280,6 +280,12 @@ int swb_lu_factor(double* A, int64_t n, int64_t lda, int32_t* piv, double* anorm
 int swb_lu_rcond(const double* LU, int64_t n, int64_t lda, const int32_t* piv,
                  const double* anorm, double* rcond_out, void* workspace,
                  size_t workspace_bytes, void* stream);
+/* n <= 160 in one launch: anorm_out = ||A||_1, A <- its LU factors (piv),
+ * B <- A^-1 B, and (rcond_out non-null) rcond_out = dgecon's estimate.
+ * swb_small_solve uses it for seed systems of up to 160 unknowns, with
+ * rcond_out null and swb_lu_rcond on its side stream. */
+int swb_small_dense_solve(double* A, int64_t n, int64_t lda, int32_t* piv, double* B, int64_t nrhs, int64_t ldb,
+                          double* anorm_out, double* rcond_out, void* stream);
 size_t swb_lu_solve_workspace_bytes(int64_t n, int64_t nrhs);
 int swb_lu_solve(const double* LU, int64_t n, int64_t lda, const int32_t* piv, double* B,
                  int64_t nrhs, int64_t ldb, void* workspace, size_t workspace_bytes, void* stream);

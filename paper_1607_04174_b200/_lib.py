@@ -98,6 +98,7 @@ SIGNATURES = {
     "swb_oz_layout_info": (C.c_int, [c_i64, c_i64, c_i64, c_vp]),
     "swb_gemm_tn_sym_emit": (C.c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_sz, c_vp, c_i64,
                                        c_vp, c_sz, c_vp]),
+    "swb_small_dense_solve": (C.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "swb_ell_rows_gather": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),
     "swb_ell_rows_scatter": (C.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),
     "swb_build_caug": (C.c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp]),

@@ -584,6 +584,129 @@ extern "C" size_t swb_lu_workspace_bytes(int64_t n) {
          swb_align_up(sizeof(double) * size_t(n + 1), 256) + swb_align_up(sizeof(int32_t) * size_t(n + 1), 256);
 }
 
+// ---- small systems in one launch -----------------------------------------
+// n <= SMALL_N: the whole of A in shared memory (ld n | 1 against bank
+// conflicts on the column walks): the 1-norm, LU with partial pivoting
+// (dgetf2: idamax pivot with NaN as the largest, ties to the lowest row;
+// reciprocal scaling when |pivot| >= sfmin; a zero pivot leaves its column
+// unscaled), getrs on the nrhs right-hand sides in B, and dgecon's estimate
+// on the factors -- replacing the panel / swap / trsm / GEMM launches per
+// panel, getrs and gecon of the blocked path (the seed systems of the small
+// configurations are latency-bound).  The factors and pivots are written
+// back to A / piv as swb_lu_factor leaves them.
+constexpr int SMALL_N = 160;
+constexpr int SMALL_THREADS = 512;
+
+__global__ void __launch_bounds__(SMALL_THREADS)
+small_dense_kernel(double* __restrict__ A_g, int64_t n_, int64_t lda, int32_t* __restrict__ piv_g,
+                   double* __restrict__ B, int64_t nrhs, int64_t ldb, double* __restrict__ anorm_out,
+                   double* __restrict__ rcond_out, int with_rcond) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  __shared__ ArgMax sh[32];
+  __shared__ int flag;
+  __shared__ int zero_pivot;
+  const int n = static_cast<int>(n_);
+  const int ld = n | 1;
+  double* A = sm;
+  double* x = A + size_t(n) * ld;
+  int32_t* isgn = reinterpret_cast<int32_t*>(x + n);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < n * n; e += nt) A[(e / n) * ld + e % n] = A_g[int64_t(e / n) * lda + e % n];
+  if (tid == 0) zero_pivot = 0;
+  __syncthreads();
+  // 1-norm of A (max column sum)
+  double cmax = 0.0;
+  for (int j = tid; j < n; j += nt) {
+    double c = 0.0;
+    for (int i = 0; i < n; ++i) c += fabs(A[i * ld + j]);
+    cmax = (c > cmax || c != c) ? c : cmax;
+  }
+  {
+    ArgMax a{cmax, tid};
+    const double anorm = block_argmax(a, sh).v;
+    if (tid == 0) *anorm_out = anorm;
+  }
+  // LU with partial pivoting
+  for (int j = 0; j < n; ++j) {
+    ArgMax a{-1.0, 0x7fffffff};
+    for (int i = j + tid; i < n; i += nt) {
+      const double v = fabs(A[i * ld + j]);
+      a = argmax_merge(a, ArgMax{v != v ? __longlong_as_double(0x7ff0000000000000LL) : v, i});
+    }
+    const int p = block_argmax(a, sh).i;
+    if (tid == 0) piv_g[j] = p;
+    if (p != j)
+      for (int c = tid; c < n; c += nt) {
+        const double t = A[j * ld + c];
+        A[j * ld + c] = A[p * ld + c];
+        A[p * ld + c] = t;
+      }
+    __syncthreads();
+    const double pv = A[j * ld + j];
+    if (pv == 0.0) {
+      if (tid == 0) zero_pivot = 1;
+      continue;
+    }
+    const bool recip = fabs(pv) >= 2.2250738585072014e-308;
+    const double rp = 1.0 / pv;
+    for (int i = j + 1 + tid; i < n; i += nt) A[i * ld + j] = recip ? A[i * ld + j] * rp : A[i * ld + j] / pv;
+    __syncthreads();
+    const int w = n - j - 1;
+    for (int e = tid; e < w * w; e += nt) {
+      const int i = j + 1 + e / w, c = j + 1 + e % w;
+      A[i * ld + c] -= A[i * ld + j] * A[j * ld + c];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < n * n; e += nt) A_g[int64_t(e / n) * lda + e % n] = A[(e / n) * ld + e % n];
+  // B <- P B, then L and U solves (dgetrs)
+  for (int64_t c = tid; c < nrhs; c += nt)
+    for (int j = 0; j < n; ++j) {
+      const int p = piv_g[j];
+      if (p != j) {
+        const double t = B[int64_t(j) * ldb + c];
+        B[int64_t(j) * ldb + c] = B[int64_t(p) * ldb + c];
+        B[int64_t(p) * ldb + c] = t;
+      }
+    }
+  __syncthreads();
+  tri_solve(A, n, ld, B, nrhs, ldb, 0);
+  tri_solve(A, n, ld, B, nrhs, ldb, 1);
+  if (!with_rcond) return;   // the caller runs gecon on the factors (e.g. on a side stream)
+  // dgecon (norm '1') on the factors
+  const double anorm = *anorm_out;
+  if (!(anorm > 0.0)) { if (tid == 0) *rcond_out = (anorm == 0.0) ? 0.0 : anorm; return; }
+  if (tid == 0) flag = 0;
+  __syncthreads();
+  for (int i = tid; i < n; i += nt)
+    if (A[i * ld + i] == 0.0) flag = 1;
+  __syncthreads();
+  if (flag || zero_pivot) { if (tid == 0) *rcond_out = 0.0; return; }
+  auto inv = [&]() { tri_solve(A, n, ld, x, 1, 1, 0); tri_solve(A, n, ld, x, 1, 1, 1); };
+  auto inv_t = [&]() { tri_solve(A, n, ld, x, 1, 1, 2); tri_solve(A, n, ld, x, 1, 1, 3); };
+  const double est = dlacn2_est(n, x, isgn, inv, inv_t, red, sh, &flag);
+  if (tid == 0) *rcond_out = est != 0.0 ? (1.0 / est) / anorm : 0.0;
+}
+
+extern "C" int swb_small_dense_solve(double* A, int64_t n, int64_t lda, int32_t* piv, double* B, int64_t nrhs,
+                                     int64_t ldb, double* anorm_out, double* rcond_out, void* stream) {
+  if (n <= 0 || n > SMALL_N || !A || !piv || !B || !anorm_out || lda < n || nrhs < 0 || (nrhs > 0 && ldb < nrhs))
+    return SWB_INVALID_PARAM;
+  const size_t smem = sizeof(double) * (size_t(n) * size_t(n | 1) + n) + sizeof(int32_t) * n;
+  static unsigned long long attr = 0;
+  if (swb_first_on_device(&attr)) {
+    const size_t most = sizeof(double) * (size_t(SMALL_N) * size_t(SMALL_N | 1) + SMALL_N) + sizeof(int32_t) * SMALL_N;
+    SWB_CUDA_TRY(cudaFuncSetAttribute(small_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(most)));
+  }
+  // fewer warps for the smaller systems: every column step is a few CTA barriers
+  const unsigned threads = n <= 64 ? 128 : (n <= 128 ? 256 : SMALL_THREADS);
+  small_dense_kernel<<<1, threads, smem, swb_stream(stream)>>>(A, n, lda, piv, B, nrhs, ldb, anorm_out, rcond_out,
+                                                               rcond_out ? 1 : 0);
+  SWB_CHECK_LAUNCH();
+  return SWB_OK;
+}
+
 extern "C" int swb_lu_factor(double* A, int64_t n, int64_t lda, int32_t* piv, double* anorm_out, void* ws,
                              size_t ws_bytes, void* stream) {
   if (n < 0 || (n > 0 && (!A || !piv || lda < n || (lda & 1)))) return SWB_INVALID_PARAM;

@@ -754,6 +754,9 @@ extern "C" int swb_small_solve_ex(double gamma, int64_t S, int64_t m, int64_t L,
                                   double* rcond_out, void* workspace, size_t workspace_bytes, void* stream,
                                   void* rcond_stream, void* rcond_event);
 
+extern "C" int swb_small_dense_solve(double* A, int64_t n, int64_t lda, int32_t* piv, double* B, int64_t nrhs,
+                                     int64_t ldb, double* anorm_out, double* rcond_out, void* stream);
+
 extern "C" size_t swb_small_solve_workspace_bytes(int64_t S, int64_t m, int64_t L) {
   const SmallLayout a = small_layout(S, m, L, 1), b = small_layout(S, m, L, 0);
   return a.total > b.total ? a.total : b.total;
@@ -842,6 +845,9 @@ extern "C" int swb_small_solve_ex(double gamma, int64_t S, int64_t m, int64_t L,
   // (SWB_WOODBURY=0: always the LU of A)
   static const bool wb_env = [] { const char* e = getenv("SWB_WOODBURY"); return !(e && e[0] == '0'); }();
   const bool wood = wb_env && Ly.n >= Ly.r + 64;
+  // systems up to 64 unknowns: one launch (faster than the blocked LU there; SWB_SMALL_LU=0: blocked path)
+  static const bool small_env = [] { const char* e = getenv("SWB_SMALL_LU"); return !(e && e[0] == '0'); }();
+  const bool small_n = !wood && small_env && Ly.n <= 64;
   double* Ut = reinterpret_cast<double*>(base + Ly.off_ut);
   double* Vt = reinterpret_cast<double*>(base + Ly.off_vt);
   double* Kf = reinterpret_cast<double*>(base + Ly.off_k);
@@ -865,6 +871,9 @@ extern "C" int swb_small_solve_ex(double gamma, int64_t S, int64_t m, int64_t L,
                            swb_lu_solve_workspace_bytes(Ly.r, L), stream)))
       return rc;
     if ((rc = swb_gemm_nn_alpha(Ut, Ly.ldw, tb, Ly.ldr, Ly.n, Ly.r, L, rhs, Ly.ldr, 1, 1.0, st))) return rc;
+  } else if (small_n) {
+    // one launch: 1-norm, LU and the solve (lu.cu); gecon below, as for the blocked LU
+    if ((rc = swb_small_dense_solve(A, Ly.n, Ly.lda, piv, rhs, L, Ly.ldr, anorm, nullptr, stream))) return rc;
   } else {
     rc = swb_lu_factor(A, Ly.n, Ly.lda, piv, anorm, luws, swb_lu_workspace_bytes(Ly.n), stream);
     if (rc) return rc;

@@ -295,6 +295,55 @@ def test_lu_solve_and_rcond_match_lapack(cuda_ok, n):
     np.testing.assert_allclose(rc.item(), want, rtol=1e-6)
 
 
+@pytest.mark.parametrize("n,kind", [(1, "gen"), (5, "gen"), (41, "gen"), (41, "pivot"), (128, "gen"),
+                                    (160, "gen"), (97, "ill"), (33, "singular")])
+def test_small_dense_solve_matches_lapack(cuda_ok, n, kind):
+    """swb_small_dense_solve (n <= 160 in one launch) vs LAPACK: the solve,
+    the pivots (dgetrf's), ||A||_1 and dgecon's rcond; exactly singular ->
+    rcond 0."""
+    import scipy.linalg as sla
+    import torch
+    from paper_1607_04174_b200 import _lib
+    from paper_1607_04174_b200.device import ptr, round_up, stream_handle
+    rng = np.random.default_rng(n + len(kind))
+    A = np.eye(n) * 3 + rng.standard_normal((n, n)) / np.sqrt(n)
+    if kind == "pivot":
+        A = rng.standard_normal((n, n))               # partial pivoting does real work
+    if kind == "ill":
+        U, _, Vt = np.linalg.svd(rng.standard_normal((n, n)))
+        A = U @ np.diag(np.logspace(0, -11, n)) @ Vt
+    if kind == "singular":
+        A[:, 3] = A[:, 5]
+    B = rng.standard_normal((n, 4))
+    lda = round_up(n, 8)
+    Ad = torch.zeros((n, lda), dtype=torch.float64, device="cuda")
+    Ad[:, :n] = torch.from_numpy(A)
+    Bd = torch.from_numpy(B.copy()).cuda()
+    piv = torch.empty(n, dtype=torch.int32, device="cuda")
+    anorm = torch.empty(1, dtype=torch.float64, device="cuda")
+    rc = torch.empty(1, dtype=torch.float64, device="cuda")
+    _lib.call("swb_small_dense_solve", ptr(Ad), n, lda, ptr(piv), ptr(Bd), 4, 4, ptr(anorm), ptr(rc), stream_handle())
+    lu, p = sla.lu_factor(A)
+    assert abs(anorm.item() - np.linalg.norm(A, 1)) <= 1e-13 * np.linalg.norm(A, 1)
+    if kind == "singular":
+        assert rc.item() < 1e-14
+        return
+    np.testing.assert_array_equal(piv.cpu().numpy(), p)
+    want = sla.lapack.dgecon(lu, np.linalg.norm(A, 1), norm="1")[0]
+    if kind == "ill":
+        # cond ~1e11: factors / solutions agree only to ~cond * eps (LAPACK's
+        # recursive getrf orders the updates differently); the estimate, and
+        # the SingularSmallSystem decision on it, agree
+        np.testing.assert_allclose(rc.item(), want, rtol=1e-3)
+        r = A @ Bd.cpu().numpy() - B
+        assert np.abs(r).max() <= 1e-6 * np.abs(B).max()
+        return
+    np.testing.assert_allclose(Ad[:, :n].cpu().numpy(), lu, rtol=0, atol=1e-12 * np.abs(lu).max())
+    x = np.linalg.solve(A, B)
+    np.testing.assert_allclose(Bd.cpu().numpy(), x, rtol=1e-11, atol=1e-11 * np.abs(x).max())
+    np.testing.assert_allclose(rc.item(), want, rtol=1e-6)
+
+
 def test_singular_small_system_raises(cuda_ok):
     # duplicated eigenvector columns make the seed system singular
     z = load_golden("errors")
