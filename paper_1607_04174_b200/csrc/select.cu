@@ -10,9 +10,13 @@
 //      (Hestenes) Jacobi SVD of R_m in shared memory, sigma descending, the
 //      reference's cutoff 1e-13 * sigma_0 (adaptive.py:85), perp, and the
 //      ridge bisection on mu (<= 200 steps, tol 1e-6 * bound, :96-110).
+#include <cooperative_groups.h>
+
 #include <cstdlib>
 
 #include "swb_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -75,6 +79,78 @@ __global__ void __launch_bounds__(1024) householder_kernel(double* __restrict__ 
       }
     }
     __syncthreads();
+  }
+}
+
+// The same QR with the trailing columns spread over the whole GPU: one
+// cooperative launch, every CTA owns columns c = blockIdx.x + k * gridDim.x
+// of [q_s | U] (M + K columns).  Step j: each CTA forms reflector j from
+// column j itself (the same fixed-order block reduction everywhere, so every
+// CTA holds bit-identical tau / beta / v, staged in shared memory), applies
+// it to its own columns c > j, and a grid barrier closes the step; the owner
+// of column j writes v / beta back after the barrier (nobody reads column j
+// again).  The single-CTA kernel above spends ~16 us a column on its 32
+// warps walking ~150 columns in turn (S = 1000: 2.4 ms); here a step is two
+// block reductions and one grid barrier.
+constexpr int HH_THREADS = 256;
+
+__device__ __forceinline__ double block_sum_256(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int w = 0; w < HH_THREADS / 32; ++w) s += red[w];   // same order in every thread
+  __syncthreads();
+  return s;
+}
+
+__global__ void __launch_bounds__(HH_THREADS) householder_coop_kernel(double* __restrict__ At, int64_t S, int64_t M,
+                                                                      double* __restrict__ Ut, int64_t K) {
+  extern __shared__ double hv[];   // v = [1; x[j+1:] * scale] of the current step (S doubles)
+  __shared__ double red[HH_THREADS / 32];
+  cg::grid_group grid = cg::this_grid();
+  const int64_t r = S < M ? S : M;
+  const int64_t nc = M + K;
+  auto col = [&](int64_t c) { return c < M ? At + c * S : Ut + (c - M) * S; };
+  for (int64_t j = 0; j < r; ++j) {
+    const double* x = At + j * S;
+    double s = 0.0;
+    for (int64_t i = j + 1 + threadIdx.x; i < S; i += HH_THREADS) {
+      const double xi = __ldcg(x + i);
+      hv[i] = xi;
+      s = fma(xi, xi, s);
+    }
+    const double sigma = block_sum_256(s, red);
+    const double alpha = __ldcg(x + j);
+    double tau = 0.0, beta = alpha, scale = 0.0;
+    if (sigma != 0.0) {   // LAPACK dlarfg: H = I - tau v v^T, v[0] = 1, H x = beta e_1
+      const double nrm = sqrt(alpha * alpha + sigma);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    for (int64_t i = j + 1 + threadIdx.x; i < S; i += HH_THREADS) hv[i] *= scale;   // own entries: no sync needed
+    __syncthreads();
+    if (tau != 0.0) {
+      for (int64_t c = blockIdx.x; c < nc; c += gridDim.x) {
+        if (c <= j) continue;
+        double* y = col(c);
+        double w = threadIdx.x == 0 ? y[j] : 0.0;
+        for (int64_t i = j + 1 + threadIdx.x; i < S; i += HH_THREADS) w = fma(hv[i], y[i], w);
+        w = block_sum_256(w, red) * tau;
+        if (threadIdx.x == 0) y[j] -= w;
+        for (int64_t i = j + 1 + threadIdx.x; i < S; i += HH_THREADS) y[i] = fma(-w, hv[i], y[i]);
+      }
+    }
+    grid.sync();
+    if (j % gridDim.x == blockIdx.x) {   // owner of column j: v and beta in place
+      double* xo = At + j * S;
+      for (int64_t i = j + 1 + threadIdx.x; i < S; i += HH_THREADS) xo[i] = hv[i];
+      if (threadIdx.x == 0) xo[j] = beta;
+    }
+    __syncthreads();   // hv is rewritten by the next step
   }
 }
 
@@ -751,7 +827,28 @@ extern "C" int swb_seed_fit_schedule(const double* V, int64_t ldv, const int32_t
   const int allow_fast = !(fe && fe[0] == '0');
   seed_block_kernel<<<swb_sm_count() * 2, 256, 0, st>>>(V, ldv, col_map, seed_idx, seed_lab, d_sqrt, S, M, K, At, Ut, uu);
   SWB_CHECK_LAUNCH();
-  householder_kernel<<<1, 1024, 0, st>>>(At, S, M, Ut, K);
+  // QR: the cooperative whole-GPU kernel when column j fits in shared
+  // memory (S <= 16K seeds); SWB_HH_COOP=0 keeps the single-CTA kernel
+  static int hh_occ[64] = {};
+  int& occ = hh_occ[swb_device()];
+  const char* he = getenv("SWB_HH_COOP");
+  const size_t hh_smem = sizeof(double) * size_t(S);
+  bool coop = !(he && he[0] == '0') && S >= 64 && S <= 16384 && M + K >= 2;
+  if (coop && occ == 0) {
+    SWB_CUDA_TRY(cudaFuncSetAttribute(householder_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(16384 * sizeof(double))));
+    SWB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, householder_coop_kernel, HH_THREADS,
+                                                               16384 * sizeof(double)));
+    if (occ < 1) occ = -1;
+  }
+  if (coop && occ > 0) {
+    int g = static_cast<int>(std::min<int64_t>(M + K, int64_t(occ) * swb_sm_count()));
+    void* args[] = {&At, const_cast<int64_t*>(&S), const_cast<int64_t*>(&M), &Ut, const_cast<int64_t*>(&K)};
+    SWB_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(householder_coop_kernel), dim3(g),
+                                             dim3(HH_THREADS), args, hh_smem, st));
+  } else {
+    householder_kernel<<<1, 1024, 0, st>>>(At, S, M, Ut, K);
+  }
   SWB_CHECK_LAUNCH();
   // shared memory: W (n_max x r_max) + sigma + rank when they fit
   const int64_t nmax = (int64_t(max_step) + 1) / 2 * 2;
