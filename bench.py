@@ -363,6 +363,13 @@ def _next_pack(state, beta, i=0):
         pack = swb.refresh(base, state["image"], beta)
         state["pack"] = pack
         return pack
+    if state["params"].get("epsilon") is not None:   # c3: from the precomputed pack (_next_pack_and_solve)
+        base = state.setdefault("base", state["pack"])
+        pack = swb.update_basis(base, state["image"], state["params"]["beta1"], method="first_order",
+                                out=state.get("spare"))
+        state["spare"] = pack.V
+        state["pack"] = pack
+        return pack
     spare = state.pop("spare", None)
     old = state["pack"]
     cut = state.get("cut") if i % 2 == 0 else None
@@ -413,13 +420,29 @@ def _fused(state) -> bool:
 
 
 def _next_pack_and_solve(state, beta, i, prob):
-    """_next_pack + solve_fast as one update_and_solve call (ping-pong V')."""
+    """_next_pack + solve_fast as one update_and_solve call (ping-pong V').
+
+    c3 (K from an accuracy target, interaction rounds): every round updates
+    the PRECOMPUTED pack to beta1 -- the reference's flow, nearest_pack(packs,
+    beta) then the online update (cli.py:140-150) -- into one reused V'
+    buffer.  Chaining first-order updates of updates (as the other configs'
+    ping-pong does) accumulates the O(|dL|^2) loss of orthogonality step after
+    step; after ~80 beta flips the seed rows of V' become ill-conditioned and
+    select_m's seed fits leave the bidiagonal fast path (c3 step 11.7 -> 29
+    ms, tools/step_drift.py), a state no reference user reaches."""
     import paper_1607_04174_b200 as swb
+    eps = state["params"].get("epsilon")
+    policy = swb.AdaptivePolicy(epsilon=eps) if eps is not None else None
+    if policy is not None:
+        base = state.setdefault("base", state["pack"])
+        pack, field = swb.update_and_solve(base, state["image"], prob, state["params"]["beta1"],
+                                           out=state.get("spare"), policy=policy)
+        state["spare"] = pack.V
+        state["pack"] = pack
+        return field
     spare = state.pop("spare", None)
     old = state["pack"]
     cut = state.get("cut") if i % 2 == 0 else None
-    eps = state["params"].get("epsilon")
-    policy = swb.AdaptivePolicy(epsilon=eps) if eps is not None else None
     pack, field = swb.update_and_solve(old, state["image"], prob, beta, cut_edges=cut, out=spare, policy=policy)
     state["spare"] = old.V
     state["pack"] = pack
@@ -1020,7 +1043,9 @@ def run_gpu(args):
                                    f"topology update (cut <-> restore the edges crossing a "
                                    f"{state['params']['cut_block']}x{state['params']['cut_block']} block boundary, "
                                    f"beta {state['params']['beta0']}) + " if state.get("cut") is not None else
-                                   f"beta update {state['params']['beta0']}<->{state['params']['beta1']} + ") + (
+                                   (f"beta update {state['params']['beta0']}->{state['params']['beta1']} of the "
+                                    f"precomputed pack every round + " if rp else
+                                    f"beta update {state['params']['beta0']}<->{state['params']['beta1']} + ")) + (
                                    solve_desc if cfg != "c5" else
                                    f"similarity priors (grid {state['params']['grid']}, patch radius "
                                    f"{state['params']['patch_radius']}) + {state['params']['labels']}-label "
