@@ -1020,6 +1020,8 @@ extern "C" int swb_finalize_label(int64_t r_begin, int64_t r_end, int64_t L, con
   const int fg = swb_sm_count() * 8;
   if (L <= 32) finalize_many_reg_kernel<1><<<fg, 256, 0, st>>>(r_begin, r_end, L, extra, dnorm, d_sqrt, U, ldu, labels, top2);
   else if (L <= 64) finalize_many_reg_kernel<2><<<fg, 256, 0, st>>>(r_begin, r_end, L, extra, dnorm, d_sqrt, U, ldu, labels, top2);
+  else if (L <= 128) finalize_many_reg_kernel<4><<<fg, 256, 0, st>>>(r_begin, r_end, L, extra, dnorm, d_sqrt, U, ldu, labels, top2);
+  else if (L <= 256) finalize_many_reg_kernel<8><<<fg, 256, 0, st>>>(r_begin, r_end, L, extra, dnorm, d_sqrt, U, ldu, labels, top2);
   else finalize_many_kernel<<<fg, 256, 0, st>>>(r_begin, r_end, L, extra, dnorm, d_sqrt, U, ldu, labels, top2);
   SWB_CHECK_LAUNCH();
   return SWB_OK;

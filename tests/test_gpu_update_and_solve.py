@@ -142,6 +142,27 @@ def test_fused_gamma_priors(cuda_ok):
         _check_against_separate(swb, dp, image, prob, p["beta1"])
 
 
+@pytest.mark.parametrize("L", [70, 125, 200, 300])
+def test_fused_finalize_label_widths(cuda_ok, L):
+    """The many-label finalize of update_and_solve at every dispatch width
+    (register rows of <= 128 / <= 256 labels, the loop kernel beyond): c5 has
+    125 labels."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    import paper_1607_04174_b200 as swb
+    s = bench.cpu_sample("c1", None, 320)
+    p = s["params"]
+    image, dp, _ = _device_pack(swb, s)
+    rng = np.random.default_rng(L)
+    n = s["n"]
+    pri = rng.random((n, L)) ** 4
+    pri /= pri.sum(1, keepdims=True)
+    seeds = np.sort(rng.choice(n, 40, replace=False))
+    sp = swb.SeedPartition(n, seeds, rng.integers(0, L, seeds.size))
+    prob = swb.LabelProblem(num_labels=L, seeds=sp, priors=pri, gamma=1.0)
+    _check_against_separate(swb, dp, image, prob, p["beta1"])
+
+
 def test_fused_on_the_dmma_rotation(cuda_ok):
     """SWB_ROTATION=dmma (and K > 512) rotate on the FP64 DMMA GEMM: the
     extra columns V (C coeff) then come from a second DMMA product."""
