@@ -325,32 +325,58 @@ gemm_tn_sym_kernel(const double* __restrict__ X, int64_t ldx, const double* __re
   }
 }
 
-// out[i, j] (i <= j) = sum of the tile's CTA partials (fixed order), mirrored
+// out[i, j] (i <= j) = sum of the tile's CTA partials, mirrored.  A block
+// takes 32 consecutive elements; warp w sums the partials q = w, w + 8, ...
+// (four independent loads in flight), and the eight warp sums are added in
+// warp order: a fixed summation order, so P is reproducible run to run.
 template <int BM>
-__global__ void tn_sym_reduce_kernel(const double* __restrict__ partial, int T, int per_full, int per_diag, int64_t M,
-                                     double* __restrict__ out, int64_t ldo) {
+__global__ void __launch_bounds__(256)
+tn_sym_reduce_kernel(const double* __restrict__ partial, int T, int per_full, int per_diag, int64_t M,
+                     double* __restrict__ out, int64_t ldo) {
+  __shared__ double red[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int n_tiles = T * (T + 1) / 2;
   const int n_full = T * (T - 1) / 2;
   const int64_t total = int64_t(n_tiles) * BM * BM;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+  const int64_t e = int64_t(blockIdx.x) * 32 + lane;
+  bool ok = e < total;
+  int64_t i = 0, j = 0;
+  double s = 0.0;
+  if (ok) {
     const int t = static_cast<int>(e / (BM * BM));
     const int rc = static_cast<int>(e % (BM * BM));
     const int2 tt = decode_tile(t, T, 1);
-    const int64_t i = int64_t(tt.x) * BM + rc / BM, j = int64_t(tt.y) * BM + rc % BM;
-    if (i >= M || j >= M || j < i) continue;
-    int c0, cnt;
-    if (tt.x == tt.y) {
-      c0 = n_full * per_full + tt.x * per_diag;
-      cnt = per_diag;
-    } else {
-      int f = 0;
-      for (int a = 0; a < tt.x; ++a) f += T - 1 - a;
-      f += tt.y - tt.x - 1;
-      c0 = f * per_full;
-      cnt = per_full;
+    i = int64_t(tt.x) * BM + rc / BM;
+    j = int64_t(tt.y) * BM + rc % BM;
+    ok = i < M && j < M && j >= i;
+    if (ok) {
+      int c0, cnt;
+      if (tt.x == tt.y) {
+        c0 = n_full * per_full + tt.x * per_diag;
+        cnt = per_diag;
+      } else {
+        int f = 0;
+        for (int a = 0; a < tt.x; ++a) f += T - 1 - a;
+        f += tt.y - tt.x - 1;
+        c0 = f * per_full;
+        cnt = per_full;
+      }
+      const double* p = partial + int64_t(c0) * (BM * BM) + rc;
+      constexpr int64_t S = int64_t(BM) * BM;
+      int q = w;
+      for (; q + 24 < cnt; q += 32) {
+        const double a0 = p[q * S], a1 = p[(q + 8) * S], a2 = p[(q + 16) * S], a3 = p[(q + 24) * S];
+        s += a0; s += a1; s += a2; s += a3;
+      }
+      for (; q < cnt; q += 8) s += p[q * S];
     }
-    double s = 0.0;
-    for (int q = 0; q < cnt; ++q) s += partial[int64_t(c0 + q) * (BM * BM) + rc];
+  }
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && ok) {
+    s = red[0][lane];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) s += red[k][lane];
     out[i * ldo + j] = s;
     if (j != i) out[j * ldo + i] = s;
   }
@@ -495,7 +521,11 @@ int run_tn_sym(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64
   }();
   const double ratio = double(diag_max_cells(G)) / double(W * W) + (em.row_amax ? emit_cost : 0.0);
   int per_full = std::max(1, static_cast<int>(slots / (n_full + ratio * T)));
-  const int64_t max_per = std::max<int64_t>(1, rows / 512);
+  // >= 512 rows per chunk; when that leaves SMs without a CTA (c1: 16 K rows, one diagonal tile -> 18
+  // CTAs) down to 128 rows, so the latency-bound small problems use the whole GPU
+  int64_t min_rows = 512;
+  if ((n_full + ratio * T) * double(rows / 512) < double(swb_sm_count())) min_rows = 128;
+  const int64_t max_per = std::max<int64_t>(1, rows / min_rows);
   if (per_full > max_per) per_full = static_cast<int>(max_per);
   int per_diag = std::max(1, static_cast<int>(ratio * per_full + 0.5));
   int64_t chunk_full = std::max<int64_t>(BK, ((rows + per_full - 1) / per_full + BK - 1) / BK * BK);
@@ -513,7 +543,7 @@ int run_tn_sym(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64
                                               partial, em);
   SWB_CHECK_LAUNCH();
   const int64_t total = int64_t(T * (T + 1) / 2) * Cf::BM * Cf::BN;
-  int rb = static_cast<int>(std::min<int64_t>((total + 255) / 256, int64_t(swb_sm_count()) * 8));
+  const unsigned rb = static_cast<unsigned>((total + 31) / 32);
   tn_sym_reduce_kernel<Cf::BM><<<rb, 256, 0, st>>>(partial, T, per_full, per_diag, M, out, ldo);
   SWB_CHECK_LAUNCH();
   return SWB_OK;

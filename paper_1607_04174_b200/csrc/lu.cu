@@ -11,6 +11,9 @@
 // rcond follows LAPACK dgecon: Higham's dlacn2 estimator of
 // ||U^-1 L^-1||_1 (single CTA), rcond = 1/(anorm * est).
 #include "swb_common.cuh"
+#ifdef SWB_COL_PROF
+#include <cstdio>
+#endif
 
 namespace {
 
@@ -689,10 +692,205 @@ small_dense_kernel(double* __restrict__ A_g, int64_t n_, int64_t lda, int32_t* _
   if (tid == 0) *rcond_out = est != 0.0 ? (1.0 / est) / anorm : 0.0;
 }
 
+// n <= 64 without the condition estimate (the seed systems of c1-sized
+// problems; gecon runs on a side stream): column-owner threads.  Thread c
+// owns column c of the augmented matrix [A | B] in shared memory (ld odd:
+// conflict-free), so a column step needs ONE CTA barrier: the warp that owns
+// column j searches its pivot with shuffles (dgetf2's idamax, NaN largest,
+// ties to the lowest row), swaps rows j / p of that column and scales it
+// (the multipliers also go to a double-buffered broadcast array); after the
+// barrier every other thread swaps and updates its own column.  The
+// right-hand sides ride as columns c >= n (so L y = P b is done when the
+// factorization is), then one warp per right-hand side back-substitutes
+// column-wise.  Element for element the same operations as
+// small_dense_kernel's factorization (identical factors and pivots).
+constexpr int COL_N = 64;
+constexpr int COL_COLS = 256;
+
+__global__ void __launch_bounds__(COL_COLS)
+small_dense_col_kernel(double* __restrict__ A_g, int n, int64_t lda, int32_t* __restrict__ piv_g,
+                       double* __restrict__ B, int nrhs, int64_t ldb, double* __restrict__ anorm_out) {
+  extern __shared__ double sm[];
+  __shared__ ArgMax sh[32];
+  __shared__ double lbuf[2][COL_N + 8];
+  __shared__ int pbuf[2], skipbuf[2];
+  const int nc = n + nrhs;
+  const int ld = nc | 1;
+  double* Aug = sm;              // (n + 8) x ld: 8 pad rows so the 8-row update batches need no bounds checks
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+#ifdef SWB_COL_PROF
+  long long t_[8] = {0, 0, 0, 0, 0, 0, 0, 0}, c0_ = clock64(), c1_;
+#define COL_STAMP(k) do { c1_ = clock64(); t_[k] += c1_ - c0_; c0_ = c1_; } while (0)
+#else
+#define COL_STAMP(k) do { } while (0)
+#endif
+  // [A | B] -> shared memory, four independent global loads in flight per thread
+  for (int e0 = tid; e0 < n * nc; e0 += 4 * nt) {
+    double v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = e0 + k * nt, i = e / nc, c = e - i * nc;
+      v[k] = e < n * nc ? (c < n ? A_g[int64_t(i) * lda + c] : B[int64_t(i) * ldb + (c - n)]) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = e0 + k * nt, i = e / nc, c = e - i * nc;
+      if (e < n * nc) Aug[i * ld + c] = v[k];
+    }
+  }
+  for (int e = tid; e < 8 * ld; e += nt) Aug[n * ld + e] = 0.0;   // pad rows
+  if (tid < 2 * (COL_N + 8)) (&lbuf[0][0])[tid] = 0.0;
+  __syncthreads();
+  // 1-norm of A (max column sum), summed in row order as small_dense_kernel
+  {
+    double cmax = 0.0;
+    if (tid < n) {
+      double c = 0.0;
+      const double* col = Aug + tid;
+      for (int i0 = 0; i0 < n; i0 += 8, col += 8 * ld) {
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = fabs(col[k * ld]);   // pad rows are zero
+#pragma unroll
+        for (int k = 0; k < 8; ++k) c += v[k];
+      }
+      cmax = (c > cmax || c != c) ? c : cmax;
+    }
+    const double anorm = block_argmax(ArgMax{cmax, tid}, sh).v;
+    if (tid == 0) *anorm_out = anorm;
+  }
+  COL_STAMP(0);
+  for (int j = 0; j < n; ++j) {
+    const int b = j & 1;
+    COL_STAMP(1);
+    if (warp == (j >> 5)) {
+      __syncwarp();   // the owner's update of column j is visible to its warp
+      // rows j + lane and j + lane + 32 of column j in registers
+      const int i0 = j + lane, i1 = i0 + 32;
+      const double v0 = i0 < n ? Aug[i0 * ld + j] : 0.0, v1 = i1 < n ? Aug[i1 * ld + j] : 0.0;
+      const double aj = __shfl_sync(0xffffffffu, v0, 0);
+      ArgMax a{-1.0, 0x7fffffff};
+      if (i0 < n) { const double f = fabs(v0); a = ArgMax{f != f ? __longlong_as_double(0x7ff0000000000000LL) : f, i0}; }
+      if (i1 < n) { const double f = fabs(v1); a = argmax_merge(a, ArgMax{f != f ? __longlong_as_double(0x7ff0000000000000LL) : f, i1}); }
+      // |v| >= 0 (or +inf): its bit pattern orders like the value, so the
+      // warp argmax is three integer redux ops (high word, low word, lowest
+      // row among the ties); lanes without a row carry (0, INT_MAX) and lose
+      // every tie
+      const unsigned long long bits = a.i == 0x7fffffff ? 0ull : static_cast<unsigned long long>(__double_as_longlong(a.v));
+      const unsigned hi = static_cast<unsigned>(bits >> 32), lo = static_cast<unsigned>(bits);
+      const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+      bool cand = hi == mhi;
+      const unsigned mlo = __reduce_max_sync(0xffffffffu, cand ? lo : 0u);
+      cand = cand && lo == mlo;
+      const int p = static_cast<int>(__reduce_min_sync(0xffffffffu, cand ? static_cast<unsigned>(a.i) : 0x7fffffffu));
+      const double pv = Aug[p * ld + j];
+      if (lane == 0) {
+        Aug[j * ld + j] = pv;
+        if (p != j) Aug[p * ld + j] = aj;
+        pbuf[b] = p;
+        skipbuf[b] = pv == 0.0;
+        piv_g[j] = p;
+      }
+      if (pv != 0.0) {
+        const bool recip = fabs(pv) >= 2.2250738585072014e-308;
+        const double rp = __drcp_rn(pv);            // == 1.0 / pv (both correctly rounded)
+        if (lane > 0 && i0 < n) {
+          const double x = i0 == p ? aj : v0;
+          const double l = recip ? x * rp : x / pv;
+          Aug[i0 * ld + j] = l;
+          lbuf[b][i0] = l;
+        }
+        if (i1 < n) {
+          const double x = i1 == p ? aj : v1;
+          const double l = recip ? x * rp : x / pv;
+          Aug[i1 * ld + j] = l;
+          lbuf[b][i1] = l;
+        }
+      }
+    }
+    COL_STAMP(2);
+    __syncthreads();
+    COL_STAMP(3);
+    if (tid < nc && tid != j) {
+      const int p = pbuf[b];
+      double ajc = Aug[j * ld + tid];
+      if (p != j) {
+        const double t = Aug[p * ld + tid];
+        Aug[p * ld + tid] = ajc;
+        Aug[j * ld + tid] = t;
+        ajc = t;
+      }
+      if (tid > j && !skipbuf[b]) {
+        // batches of 8 rows in registers: loads, then FMAs, then stores (a
+        // plain loop serialises on the shared-memory store -> load order);
+        // the last batch runs into the pad rows
+        const double* l = lbuf[b] + j + 1;
+        double* col = Aug + (j + 1) * ld + tid;
+        for (int rem = n - j - 1; rem > 0; rem -= 8, col += 8 * ld, l += 8) {
+          double v[8], m[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            v[k] = col[k * ld];
+            m[k] = l[k];
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[k] -= m[k] * ajc;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) col[k * ld] = v[k];
+        }
+      }
+    }
+  }
+  COL_STAMP(1);
+  __syncthreads();
+  for (int i = warp; i < n; i += nw)
+    for (int c = lane; c < n; c += 32) A_g[int64_t(i) * lda + c] = Aug[i * ld + c];
+  COL_STAMP(4);
+  // U x = y, column-oriented: warp per right-hand side, the column in
+  // registers (rows lane and lane + 32), x_j broadcast by shuffle
+  for (int c = n + warp; c < nc; c += nw) {
+    const int r1 = lane + 32;
+    double y0 = lane < n ? Aug[lane * ld + c] : 0.0, y1 = r1 < n ? Aug[r1 * ld + c] : 0.0;
+    for (int j = n - 1; j >= 0; --j) {
+      const double u0 = lane < j ? Aug[lane * ld + j] : 0.0, u1 = r1 < j ? Aug[r1 * ld + j] : 0.0;
+      const double ujj = Aug[j * ld + j];
+      const double yj = __shfl_sync(0xffffffffu, j < 32 ? y0 : y1, j & 31);
+      const double x = yj / ujj;
+      if (lane == (j & 31)) { if (j < 32) y0 = x; else y1 = x; }
+      if (lane < j) y0 -= u0 * x;
+      if (r1 < j) y1 -= u1 * x;
+    }
+    if (lane < n) B[int64_t(lane) * ldb + (c - n)] = y0;
+    if (r1 < n) B[int64_t(r1) * ldb + (c - n)] = y1;
+  }
+  COL_STAMP(5);
+#ifdef SWB_COL_PROF
+  if (tid == 0 || tid == 40)
+    printf("col prof tid %d n %d: load+norm %lld  update %lld  search %lld  barrier %lld  storeA %lld  backsub %lld\n",
+           tid, n, t_[0], t_[1], t_[2], t_[3], t_[4], t_[5]);
+#endif
+}
+
 extern "C" int swb_small_dense_solve(double* A, int64_t n, int64_t lda, int32_t* piv, double* B, int64_t nrhs,
                                      int64_t ldb, double* anorm_out, double* rcond_out, void* stream) {
   if (n <= 0 || n > SMALL_N || !A || !piv || !B || !anorm_out || lda < n || nrhs < 0 || (nrhs > 0 && ldb < nrhs))
     return SWB_INVALID_PARAM;
+  // SWB_SMALL_COL=0 (measurement knob): always the row-parallel kernel
+  static const bool col_env = [] { const char* e = getenv("SWB_SMALL_COL"); return !(e && e[0] == '0'); }();
+  if (col_env && !rcond_out && n <= COL_N && n + nrhs <= COL_COLS) {
+    const int nc = static_cast<int>(n + nrhs);
+    const size_t smem_c = sizeof(double) * size_t(n + 8) * size_t(nc | 1);
+    static unsigned long long attr_c = 0;
+    if (swb_first_on_device(&attr_c)) {
+      SWB_CUDA_TRY(cudaFuncSetAttribute(small_dense_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(sizeof(double) * size_t(COL_N + 8) * size_t(COL_COLS | 1))));
+    }
+    const unsigned threads = static_cast<unsigned>(std::max(128, (nc + 31) / 32 * 32));   // >= 4 warps for the loads / stores
+    small_dense_col_kernel<<<1, threads, smem_c, swb_stream(stream)>>>(A, static_cast<int>(n), lda, piv, B,
+                                                                       static_cast<int>(nrhs), ldb, anorm_out);
+    SWB_CHECK_LAUNCH();
+    return SWB_OK;
+  }
   const size_t smem = sizeof(double) * (size_t(n) * size_t(n | 1) + n) + sizeof(int32_t) * n;
   static unsigned long long attr = 0;
   if (swb_first_on_device(&attr)) {

@@ -295,6 +295,55 @@ def test_lu_solve_and_rcond_match_lapack(cuda_ok, n):
     np.testing.assert_allclose(rc.item(), want, rtol=1e-6)
 
 
+@pytest.mark.parametrize("n,kind,nrhs", [(1, "gen", 2), (5, "gen", 4), (33, "singular", 2), (41, "gen", 2),
+                                         (41, "pivot", 4), (64, "pivot", 27), (64, "gen", 192), (37, "zero_col", 3)])
+def test_small_dense_column_owner_kernel(cuda_ok, n, kind, nrhs):
+    """swb_small_dense_solve without the condition estimate at n <= 64 (the
+    column-owner kernel, one barrier per column): factors and pivots
+    bit-equal to the row-parallel kernel's (same operations per element),
+    both equal to LAPACK's; solutions vs numpy."""
+    import scipy.linalg as sla
+    import torch
+    from paper_1607_04174_b200 import _lib
+    from paper_1607_04174_b200.device import ptr, round_up, stream_handle
+    rng = np.random.default_rng(n + len(kind) + nrhs)
+    A = np.eye(n) * 3 + rng.standard_normal((n, n)) / np.sqrt(n)
+    if kind == "pivot":
+        A = rng.standard_normal((n, n))
+    if kind == "singular":
+        A[:, 3] = A[:, 5]
+    if kind == "zero_col":
+        A[:, 7] = 0.0
+    B = rng.standard_normal((n, nrhs))
+    lda = round_up(n, 8)
+
+    def run(with_rcond):
+        Ad = torch.zeros((n, lda), dtype=torch.float64, device="cuda")
+        Ad[:, :n] = torch.from_numpy(A)
+        Bd = torch.from_numpy(B.copy()).cuda()
+        piv = torch.empty(n, dtype=torch.int32, device="cuda")
+        anorm = torch.empty(1, dtype=torch.float64, device="cuda")
+        rc = torch.empty(1, dtype=torch.float64, device="cuda")
+        _lib.call("swb_small_dense_solve", ptr(Ad), n, lda, ptr(piv), ptr(Bd), nrhs, nrhs, ptr(anorm),
+                  ptr(rc) if with_rcond else None, stream_handle())
+        torch.cuda.synchronize()
+        return Ad[:, :n].cpu().numpy(), piv.cpu().numpy(), Bd.cpu().numpy(), anorm.item()
+
+    lu_c, piv_c, x_c, an_c = run(False)
+    lu_r, piv_r, x_r, an_r = run(True)
+    np.testing.assert_array_equal(piv_c, piv_r)
+    np.testing.assert_array_equal(lu_c, lu_r)
+    assert an_c == an_r
+    if kind in ("singular", "zero_col"):
+        return
+    lu, p = sla.lu_factor(A)
+    np.testing.assert_array_equal(piv_c, p)
+    np.testing.assert_allclose(lu_c, lu, rtol=0, atol=1e-12 * np.abs(lu).max())
+    x = np.linalg.solve(A, B)
+    np.testing.assert_allclose(x_c, x, rtol=1e-11, atol=1e-11 * np.abs(x).max())
+    np.testing.assert_allclose(x_c, x_r, rtol=1e-12, atol=1e-12 * np.abs(x).max())
+
+
 @pytest.mark.parametrize("n,kind", [(1, "gen"), (5, "gen"), (41, "gen"), (41, "pivot"), (128, "gen"),
                                     (160, "gen"), (97, "ill"), (33, "singular")])
 def test_small_dense_solve_matches_lapack(cuda_ok, n, kind):
