@@ -317,6 +317,20 @@ struct ApplyArgs {
 // previous / current row and the previous row's +x coefficient, so the +-x
 // neighbours and the -x backward coefficient come from registers (5 shared
 // V loads per row instead of 7).
+// W is written once and not read by this kernel: SWB_ST_WCS=1 (default) stores it
+// with the streaming (evict-first) policy so it does not displace the V halo
+// lines neighbouring CTAs are about to read from L2
+#ifndef SWB_ST_WCS
+#define SWB_ST_WCS 1
+#endif
+__device__ __forceinline__ void st_w(double* p, double2 v) {
+#if SWB_ST_WCS
+  __stcs(reinterpret_cast<double2*>(p), v);
+#else
+  *reinterpret_cast<double2*>(p) = v;
+#endif
+}
+
 struct RowWin {
   double2 prev, cur, f0;
 };
@@ -410,7 +424,7 @@ __device__ __forceinline__ void row_compute(const double* sc, const double* sm1,
     sd.x = fma(c.x, d, sd.x);
     sd.y = fma(c.y, d, sd.y);
     if (DELTA) {
-      *reinterpret_cast<double2*>(wrow) = make_double2(dx, dy);
+      st_w(wrow, make_double2(dx, dy));
     } else if (wrow) {
       double ox = fma(ap.a, lx, ap.b * c.x), oy = fma(ap.a, ly, ap.b * c.y);
       if (zrow) {
@@ -418,7 +432,7 @@ __device__ __forceinline__ void row_compute(const double* sc, const double* sm1,
         ox = fma(ap.g, z.x, ox);
         oy = fma(ap.g, z.y, oy);
       }
-      *reinterpret_cast<double2*>(wrow) = make_double2(ox, oy);
+      st_w(wrow, make_double2(ox, oy));
     }
   }
 }

@@ -692,7 +692,7 @@ small_dense_kernel(double* __restrict__ A_g, int64_t n_, int64_t lda, int32_t* _
   if (tid == 0) *rcond_out = est != 0.0 ? (1.0 / est) / anorm : 0.0;
 }
 
-// n <= 64 without the condition estimate (the seed systems of c1-sized
+// n <= 160 without the condition estimate (the seed systems of c1 / c2-sized
 // problems; gecon runs on a side stream): column-owner threads.  Thread c
 // owns column c of the augmented matrix [A | B] in shared memory (ld odd:
 // conflict-free), so a column step needs ONE CTA barrier: the warp that owns
@@ -704,9 +704,12 @@ small_dense_kernel(double* __restrict__ A_g, int64_t n_, int64_t lda, int32_t* _
 // factorization is), then one warp per right-hand side back-substitutes
 // column-wise.  Element for element the same operations as
 // small_dense_kernel's factorization (identical factors and pivots).
-constexpr int COL_N = 64;
+constexpr int COL_N = 160;
 constexpr int COL_COLS = 256;
+constexpr size_t COL_SMEM_MAX = 220 * 1024;
 
+// RPL: rows per lane of the pivot search / back-substitution (n <= 32 RPL)
+template <int RPL>
 __global__ void __launch_bounds__(COL_COLS)
 small_dense_col_kernel(double* __restrict__ A_g, int n, int64_t lda, int32_t* __restrict__ piv_g,
                        double* __restrict__ B, int nrhs, int64_t ldb, double* __restrict__ anorm_out) {
@@ -765,13 +768,23 @@ small_dense_col_kernel(double* __restrict__ A_g, int n, int64_t lda, int32_t* __
     COL_STAMP(1);
     if (warp == (j >> 5)) {
       __syncwarp();   // the owner's update of column j is visible to its warp
-      // rows j + lane and j + lane + 32 of column j in registers
-      const int i0 = j + lane, i1 = i0 + 32;
-      const double v0 = i0 < n ? Aug[i0 * ld + j] : 0.0, v1 = i1 < n ? Aug[i1 * ld + j] : 0.0;
-      const double aj = __shfl_sync(0xffffffffu, v0, 0);
+      // rows j + lane + 32 k of column j in registers
+      double v[RPL];
+#pragma unroll
+      for (int k = 0; k < RPL; ++k) {
+        const int i = j + lane + 32 * k;
+        v[k] = i < n ? Aug[i * ld + j] : 0.0;
+      }
+      const double aj = __shfl_sync(0xffffffffu, v[0], 0);
       ArgMax a{-1.0, 0x7fffffff};
-      if (i0 < n) { const double f = fabs(v0); a = ArgMax{f != f ? __longlong_as_double(0x7ff0000000000000LL) : f, i0}; }
-      if (i1 < n) { const double f = fabs(v1); a = argmax_merge(a, ArgMax{f != f ? __longlong_as_double(0x7ff0000000000000LL) : f, i1}); }
+#pragma unroll
+      for (int k = 0; k < RPL; ++k) {
+        const int i = j + lane + 32 * k;
+        if (i < n) {
+          const double f = fabs(v[k]);
+          a = argmax_merge(a, ArgMax{f != f ? __longlong_as_double(0x7ff0000000000000LL) : f, i});
+        }
+      }
       // |v| >= 0 (or +inf): its bit pattern orders like the value, so the
       // warp argmax is three integer redux ops (high word, low word, lowest
       // row among the ties); lanes without a row carry (0, INT_MAX) and lose
@@ -794,17 +807,15 @@ small_dense_col_kernel(double* __restrict__ A_g, int n, int64_t lda, int32_t* __
       if (pv != 0.0) {
         const bool recip = fabs(pv) >= 2.2250738585072014e-308;
         const double rp = __drcp_rn(pv);            // == 1.0 / pv (both correctly rounded)
-        if (lane > 0 && i0 < n) {
-          const double x = i0 == p ? aj : v0;
-          const double l = recip ? x * rp : x / pv;
-          Aug[i0 * ld + j] = l;
-          lbuf[b][i0] = l;
-        }
-        if (i1 < n) {
-          const double x = i1 == p ? aj : v1;
-          const double l = recip ? x * rp : x / pv;
-          Aug[i1 * ld + j] = l;
-          lbuf[b][i1] = l;
+#pragma unroll
+        for (int k = 0; k < RPL; ++k) {
+          const int i = j + lane + 32 * k;
+          if (i > j && i < n) {
+            const double x = i == p ? aj : v[k];
+            const double l = recip ? x * rp : x / pv;
+            Aug[i * ld + j] = l;
+            lbuf[b][i] = l;
+          }
         }
       }
     }
@@ -849,19 +860,28 @@ small_dense_col_kernel(double* __restrict__ A_g, int n, int64_t lda, int32_t* __
   // U x = y, column-oriented: warp per right-hand side, the column in
   // registers (rows lane and lane + 32), x_j broadcast by shuffle
   for (int c = n + warp; c < nc; c += nw) {
-    const int r1 = lane + 32;
-    double y0 = lane < n ? Aug[lane * ld + c] : 0.0, y1 = r1 < n ? Aug[r1 * ld + c] : 0.0;
+    double y[RPL];
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) y[k] = lane + 32 * k < n ? Aug[(lane + 32 * k) * ld + c] : 0.0;
     for (int j = n - 1; j >= 0; --j) {
-      const double u0 = lane < j ? Aug[lane * ld + j] : 0.0, u1 = r1 < j ? Aug[r1 * ld + j] : 0.0;
+      double u[RPL];
+#pragma unroll
+      for (int k = 0; k < RPL; ++k) u[k] = lane + 32 * k < j ? Aug[(lane + 32 * k) * ld + j] : 0.0;
       const double ujj = Aug[j * ld + j];
-      const double yj = __shfl_sync(0xffffffffu, j < 32 ? y0 : y1, j & 31);
-      const double x = yj / ujj;
-      if (lane == (j & 31)) { if (j < 32) y0 = x; else y1 = x; }
-      if (lane < j) y0 -= u0 * x;
-      if (r1 < j) y1 -= u1 * x;
+      const int jk = j >> 5;
+      double ys = y[0];
+#pragma unroll
+      for (int k = 1; k < RPL; ++k) ys = k == jk ? y[k] : ys;
+      const double x = __shfl_sync(0xffffffffu, ys, j & 31) / ujj;
+#pragma unroll
+      for (int k = 0; k < RPL; ++k) {
+        if (k == jk && lane == (j & 31)) y[k] = x;
+        if (lane + 32 * k < j) y[k] -= u[k] * x;
+      }
     }
-    if (lane < n) B[int64_t(lane) * ldb + (c - n)] = y0;
-    if (r1 < n) B[int64_t(r1) * ldb + (c - n)] = y1;
+#pragma unroll
+    for (int k = 0; k < RPL; ++k)
+      if (lane + 32 * k < n) B[int64_t(lane + 32 * k) * ldb + (c - n)] = y[k];
   }
   COL_STAMP(5);
 #ifdef SWB_COL_PROF
@@ -877,17 +897,23 @@ extern "C" int swb_small_dense_solve(double* A, int64_t n, int64_t lda, int32_t*
     return SWB_INVALID_PARAM;
   // SWB_SMALL_COL=0 (measurement knob): always the row-parallel kernel
   static const bool col_env = [] { const char* e = getenv("SWB_SMALL_COL"); return !(e && e[0] == '0'); }();
-  if (col_env && !rcond_out && n <= COL_N && n + nrhs <= COL_COLS) {
+  const size_t smem_c = sizeof(double) * size_t(n + 8) * size_t((n + nrhs) | 1);
+  if (col_env && !rcond_out && n <= COL_N && n + nrhs <= COL_COLS && smem_c <= COL_SMEM_MAX) {
     const int nc = static_cast<int>(n + nrhs);
-    const size_t smem_c = sizeof(double) * size_t(n + 8) * size_t(nc | 1);
     static unsigned long long attr_c = 0;
     if (swb_first_on_device(&attr_c)) {
-      SWB_CUDA_TRY(cudaFuncSetAttribute(small_dense_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        int(sizeof(double) * size_t(COL_N + 8) * size_t(COL_COLS | 1))));
+      SWB_CUDA_TRY(cudaFuncSetAttribute(small_dense_col_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(COL_SMEM_MAX)));
+      SWB_CUDA_TRY(cudaFuncSetAttribute(small_dense_col_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(COL_SMEM_MAX)));
     }
     const unsigned threads = static_cast<unsigned>(std::max(128, (nc + 31) / 32 * 32));   // >= 4 warps for the loads / stores
-    small_dense_col_kernel<<<1, threads, smem_c, swb_stream(stream)>>>(A, static_cast<int>(n), lda, piv, B,
-                                                                       static_cast<int>(nrhs), ldb, anorm_out);
+    if (n <= 64)
+      small_dense_col_kernel<2><<<1, threads, smem_c, swb_stream(stream)>>>(A, static_cast<int>(n), lda, piv, B,
+                                                                            static_cast<int>(nrhs), ldb, anorm_out);
+    else
+      small_dense_col_kernel<5><<<1, threads, smem_c, swb_stream(stream)>>>(A, static_cast<int>(n), lda, piv, B,
+                                                                            static_cast<int>(nrhs), ldb, anorm_out);
     SWB_CHECK_LAUNCH();
     return SWB_OK;
   }

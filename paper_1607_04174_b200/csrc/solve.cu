@@ -845,9 +845,11 @@ extern "C" int swb_small_solve_ex(double gamma, int64_t S, int64_t m, int64_t L,
   // (SWB_WOODBURY=0: always the LU of A)
   static const bool wb_env = [] { const char* e = getenv("SWB_WOODBURY"); return !(e && e[0] == '0'); }();
   const bool wood = wb_env && Ly.n >= Ly.r + 64;
-  // systems up to 64 unknowns: one launch (faster than the blocked LU there; SWB_SMALL_LU=0: blocked path)
+  // systems up to 160 unknowns whose [A | rhs] fits in shared memory: one launch on column-owner threads
+  // (lu.cu; faster than the blocked LU there; SWB_SMALL_LU=0: blocked path)
   static const bool small_env = [] { const char* e = getenv("SWB_SMALL_LU"); return !(e && e[0] == '0'); }();
-  const bool small_n = !wood && small_env && Ly.n <= 64;
+  const bool small_n = !wood && small_env && Ly.n <= 160 && Ly.n + L <= 256 &&
+                       sizeof(double) * size_t(Ly.n + 8) * size_t((Ly.n + L) | 1) <= size_t(220) * 1024;
   double* Ut = reinterpret_cast<double*>(base + Ly.off_ut);
   double* Vt = reinterpret_cast<double*>(base + Ly.off_vt);
   double* Kf = reinterpret_cast<double*>(base + Ly.off_k);

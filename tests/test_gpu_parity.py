@@ -296,10 +296,11 @@ def test_lu_solve_and_rcond_match_lapack(cuda_ok, n):
 
 
 @pytest.mark.parametrize("n,kind,nrhs", [(1, "gen", 2), (5, "gen", 4), (33, "singular", 2), (41, "gen", 2),
-                                         (41, "pivot", 4), (64, "pivot", 27), (64, "gen", 192), (37, "zero_col", 3)])
+                                         (41, "pivot", 4), (64, "pivot", 27), (64, "gen", 192), (37, "zero_col", 3),
+                                         (65, "pivot", 3), (151, "gen", 3), (160, "pivot", 4), (129, "pivot", 12)])
 def test_small_dense_column_owner_kernel(cuda_ok, n, kind, nrhs):
-    """swb_small_dense_solve without the condition estimate at n <= 64 (the
-    column-owner kernel, one barrier per column): factors and pivots
+    """swb_small_dense_solve without the condition estimate (the
+    column-owner kernel, one barrier per column; n <= 160): factors and pivots
     bit-equal to the row-parallel kernel's (same operations per element),
     both equal to LAPACK's; solutions vs numpy."""
     import scipy.linalg as sla

@@ -1,0 +1,9 @@
+# A/B of library variants on the c4 step: bash tools/gpu_ab.sh variants/a.so variants/b.so ... ("default" = in-tree build)
+export PYTHONPATH=$PWD
+for v in "$@" "$@"; do
+  if [ $v = default ]; then unset SWB_LIB; else export SWB_LIB=$PWD/$v; fi
+  timeout 600 python bench.py --no-cpu --no-e2e --steps 6 2>/dev/null | python -c "
+import json,sys
+d=json.loads(sys.stdin.read()); p=d['phases_ms']
+print('$v', round(d['ms_per_step'],2), d['clocks']['sm_mhz'], 'stencil', round(p['stencil'],2), 'project', round(p['project'],2), 'gemm', round(p['rotate_gemm'],2), 'join', round(p['rotate_join'],2))"
+done
