@@ -11,9 +11,6 @@
 // rcond follows LAPACK dgecon: Higham's dlacn2 estimator of
 // ||U^-1 L^-1||_1 (single CTA), rcond = 1/(anorm * est).
 #include "swb_common.cuh"
-#ifdef SWB_COL_PROF
-#include <cstdio>
-#endif
 
 namespace {
 
@@ -695,22 +692,24 @@ small_dense_kernel(double* __restrict__ A_g, int64_t n_, int64_t lda, int32_t* _
 // n <= 160 without the condition estimate (the seed systems of c1 / c2-sized
 // problems; gecon runs on a side stream): column-owner threads.  Thread c
 // owns column c of the augmented matrix [A | B] in shared memory (ld odd:
-// conflict-free), so a column step needs ONE CTA barrier: the warp that owns
-// column j searches its pivot with shuffles (dgetf2's idamax, NaN largest,
-// ties to the lowest row), swaps rows j / p of that column and scales it
-// (the multipliers also go to a double-buffered broadcast array); after the
-// barrier every other thread swaps and updates its own column.  The
-// right-hand sides ride as columns c >= n (so L y = P b is done when the
-// factorization is), then one warp per right-hand side back-substitutes
-// column-wise.  Element for element the same operations as
-// small_dense_kernel's factorization (identical factors and pivots).
+// conflict-free) and a column step needs ONE CTA barrier.  A panel warp that
+// owns no column runs one column ahead: in iteration j it applies step j to
+// column j + 1 (lanes over the rows, in registers), finds that column's pivot
+// (dgetf2's idamax: NaN largest, ties to the lowest row), scales it and
+// publishes pivot and multipliers in a double-buffered broadcast array --
+// while every column thread swaps and updates its own column for step j.
+// The right-hand sides ride as columns c >= n (so L y = P b is done when
+// the factorization is), then one warp per right-hand side back-substitutes
+// column-wise with its column in registers.  Element for element the same
+// operations as small_dense_kernel's factorization (identical factors and
+// pivots).
 constexpr int COL_N = 160;
 constexpr int COL_COLS = 256;
 constexpr size_t COL_SMEM_MAX = 220 * 1024;
 
 // RPL: rows per lane of the pivot search / back-substitution (n <= 32 RPL)
 template <int RPL>
-__global__ void __launch_bounds__(COL_COLS)
+__global__ void __launch_bounds__(COL_COLS + 32)
 small_dense_col_kernel(double* __restrict__ A_g, int n, int64_t lda, int32_t* __restrict__ piv_g,
                        double* __restrict__ B, int nrhs, int64_t ldb, double* __restrict__ anorm_out) {
   extern __shared__ double sm[];
@@ -721,12 +720,6 @@ small_dense_col_kernel(double* __restrict__ A_g, int n, int64_t lda, int32_t* __
   const int ld = nc | 1;
   double* Aug = sm;              // (n + 8) x ld: 8 pad rows so the 8-row update batches need no bounds checks
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-#ifdef SWB_COL_PROF
-  long long t_[8] = {0, 0, 0, 0, 0, 0, 0, 0}, c0_ = clock64(), c1_;
-#define COL_STAMP(k) do { c1_ = clock64(); t_[k] += c1_ - c0_; c0_ = c1_; } while (0)
-#else
-#define COL_STAMP(k) do { } while (0)
-#endif
   // [A | B] -> shared memory, four independent global loads in flight per thread
   for (int e0 = tid; e0 < n * nc; e0 += 4 * nt) {
     double v[4];
@@ -762,67 +755,95 @@ small_dense_col_kernel(double* __restrict__ A_g, int n, int64_t lda, int32_t* __
     const double anorm = block_argmax(ArgMax{cmax, tid}, sh).v;
     if (tid == 0) *anorm_out = anorm;
   }
-  COL_STAMP(0);
-  for (int j = 0; j < n; ++j) {
-    const int b = j & 1;
-    COL_STAMP(1);
-    if (warp == (j >> 5)) {
-      __syncwarp();   // the owner's update of column j is visible to its warp
-      // rows j + lane + 32 k of column j in registers
-      double v[RPL];
+  // The last warp is the panel warp: it owns no column.  In iteration j it
+  // applies step j to column j + 1 (lanes over the rows), finds that column's
+  // pivot in registers and publishes step j + 1 -- while the column threads
+  // apply step j to every other column, so the pivot chain hides behind the
+  // trailing update.
+  const bool panel = warp == nw - 1;
+  auto panel_step = [&](int j) {   // j = -1: the first column, nothing to apply
+    const int jn = j + 1, bn = jn & 1;
+    double v[RPL];
 #pragma unroll
-      for (int k = 0; k < RPL; ++k) {
-        const int i = j + lane + 32 * k;
-        v[k] = i < n ? Aug[i * ld + j] : 0.0;
-      }
-      const double aj = __shfl_sync(0xffffffffu, v[0], 0);
-      ArgMax a{-1.0, 0x7fffffff};
+    for (int k = 0; k < RPL; ++k) {
+      const int i = jn + lane + 32 * k;
+      v[k] = i < n ? Aug[i * ld + jn] : 0.0;
+    }
+    if (j >= 0) {
+      const int b = j & 1;
+      const int p = pbuf[b];
+      const double a_j = Aug[j * ld + jn];
+      double ajc = a_j;
+      if (p != j) {                  // rows j / p swap: row p (>= jn, in registers) takes a_j
+        ajc = Aug[p * ld + jn];
 #pragma unroll
-      for (int k = 0; k < RPL; ++k) {
-        const int i = j + lane + 32 * k;
-        if (i < n) {
-          const double f = fabs(v[k]);
-          a = argmax_merge(a, ArgMax{f != f ? __longlong_as_double(0x7ff0000000000000LL) : f, i});
-        }
+        for (int k = 0; k < RPL; ++k)
+          if (jn + lane + 32 * k == p) v[k] = a_j;
+        if (lane == 0) Aug[j * ld + jn] = ajc;
       }
-      // |v| >= 0 (or +inf): its bit pattern orders like the value, so the
-      // warp argmax is three integer redux ops (high word, low word, lowest
-      // row among the ties); lanes without a row carry (0, INT_MAX) and lose
-      // every tie
-      const unsigned long long bits = a.i == 0x7fffffff ? 0ull : static_cast<unsigned long long>(__double_as_longlong(a.v));
-      const unsigned hi = static_cast<unsigned>(bits >> 32), lo = static_cast<unsigned>(bits);
-      const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
-      bool cand = hi == mhi;
-      const unsigned mlo = __reduce_max_sync(0xffffffffu, cand ? lo : 0u);
-      cand = cand && lo == mlo;
-      const int p = static_cast<int>(__reduce_min_sync(0xffffffffu, cand ? static_cast<unsigned>(a.i) : 0x7fffffffu));
-      const double pv = Aug[p * ld + j];
-      if (lane == 0) {
-        Aug[j * ld + j] = pv;
-        if (p != j) Aug[p * ld + j] = aj;
-        pbuf[b] = p;
-        skipbuf[b] = pv == 0.0;
-        piv_g[j] = p;
-      }
-      if (pv != 0.0) {
-        const bool recip = fabs(pv) >= 2.2250738585072014e-308;
-        const double rp = __drcp_rn(pv);            // == 1.0 / pv (both correctly rounded)
+      if (!skipbuf[b]) {
+        const double* l = lbuf[b];
 #pragma unroll
         for (int k = 0; k < RPL; ++k) {
-          const int i = j + lane + 32 * k;
-          if (i > j && i < n) {
-            const double x = i == p ? aj : v[k];
-            const double l = recip ? x * rp : x / pv;
-            Aug[i * ld + j] = l;
-            lbuf[b][i] = l;
-          }
+          const int i = jn + lane + 32 * k;
+          if (i < n) v[k] -= l[i] * ajc;
         }
       }
     }
-    COL_STAMP(2);
-    __syncthreads();
-    COL_STAMP(3);
-    if (tid < nc && tid != j) {
+    ArgMax a{-1.0, 0x7fffffff};
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) {
+      const int i = jn + lane + 32 * k;
+      if (i < n) {
+        const double f = fabs(v[k]);
+        a = argmax_merge(a, ArgMax{f != f ? __longlong_as_double(0x7ff0000000000000LL) : f, i});
+      }
+    }
+    // |v| >= 0 (or +inf): its bit pattern orders like the value, so the warp
+    // argmax is three integer redux ops (high word, low word, lowest row
+    // among the ties); lanes without a row carry (0, INT_MAX) and lose every tie
+    const unsigned long long bits = a.i == 0x7fffffff ? 0ull : static_cast<unsigned long long>(__double_as_longlong(a.v));
+    const unsigned hi = static_cast<unsigned>(bits >> 32), lo = static_cast<unsigned>(bits);
+    const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+    bool cand = hi == mhi;
+    const unsigned mlo = __reduce_max_sync(0xffffffffu, cand ? lo : 0u);
+    cand = cand && lo == mlo;
+    const int p2 = static_cast<int>(__reduce_min_sync(0xffffffffu, cand ? static_cast<unsigned>(a.i) : 0x7fffffffu));
+    const int ks = (p2 - jn) >> 5;
+    double vs = v[0];
+#pragma unroll
+    for (int k = 1; k < RPL; ++k) vs = k == ks ? v[k] : vs;
+    const double pv = __shfl_sync(0xffffffffu, vs, (p2 - jn) & 31);
+    const double aj = __shfl_sync(0xffffffffu, v[0], 0);
+    if (lane == 0) {
+      pbuf[bn] = p2;
+      skipbuf[bn] = pv == 0.0;
+      piv_g[jn] = p2;
+    }
+    const bool recip = fabs(pv) >= 2.2250738585072014e-308;
+    const double rp = __drcp_rn(pv);              // == 1.0 / pv (both correctly rounded)
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) {
+      const int i = jn + lane + 32 * k;
+      if (i < n) {
+        double x = i == p2 ? aj : v[k];
+        if (i == jn) {
+          x = pv;
+        } else if (pv != 0.0) {                   // a zero pivot leaves its column unscaled (dgetf2)
+          x = recip ? x * rp : x / pv;
+          lbuf[bn][i] = x;
+        }
+        Aug[i * ld + jn] = x;
+      }
+    }
+  };
+  if (panel) panel_step(-1);
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    const int b = j & 1;
+    if (panel) {
+      if (j + 1 < n) panel_step(j);
+    } else if (tid < nc && tid != j && tid != j + 1) {
       const int p = pbuf[b];
       double ajc = Aug[j * ld + tid];
       if (p != j) {
@@ -851,12 +872,10 @@ small_dense_col_kernel(double* __restrict__ A_g, int n, int64_t lda, int32_t* __
         }
       }
     }
+    __syncthreads();
   }
-  COL_STAMP(1);
-  __syncthreads();
   for (int i = warp; i < n; i += nw)
     for (int c = lane; c < n; c += 32) A_g[int64_t(i) * lda + c] = Aug[i * ld + c];
-  COL_STAMP(4);
   // U x = y, column-oriented: warp per right-hand side, the column in
   // registers (rows lane and lane + 32), x_j broadcast by shuffle
   for (int c = n + warp; c < nc; c += nw) {
@@ -883,12 +902,6 @@ small_dense_col_kernel(double* __restrict__ A_g, int n, int64_t lda, int32_t* __
     for (int k = 0; k < RPL; ++k)
       if (lane + 32 * k < n) B[int64_t(lane + 32 * k) * ldb + (c - n)] = y[k];
   }
-  COL_STAMP(5);
-#ifdef SWB_COL_PROF
-  if (tid == 0 || tid == 40)
-    printf("col prof tid %d n %d: load+norm %lld  update %lld  search %lld  barrier %lld  storeA %lld  backsub %lld\n",
-           tid, n, t_[0], t_[1], t_[2], t_[3], t_[4], t_[5]);
-#endif
 }
 
 extern "C" int swb_small_dense_solve(double* A, int64_t n, int64_t lda, int32_t* piv, double* B, int64_t nrhs,
@@ -907,7 +920,7 @@ extern "C" int swb_small_dense_solve(double* A, int64_t n, int64_t lda, int32_t*
       SWB_CUDA_TRY(cudaFuncSetAttribute(small_dense_col_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         int(COL_SMEM_MAX)));
     }
-    const unsigned threads = static_cast<unsigned>(std::max(128, (nc + 31) / 32 * 32));   // >= 4 warps for the loads / stores
+    const unsigned threads = static_cast<unsigned>(std::max(128, (nc + 31) / 32 * 32)) + 32;   // column warps (>= 4 for the loads / stores) + the panel warp
     if (n <= 64)
       small_dense_col_kernel<2><<<1, threads, smem_c, swb_stream(stream)>>>(A, static_cast<int>(n), lda, piv, B,
                                                                             static_cast<int>(nrhs), ldb, anorm_out);
