@@ -236,13 +236,24 @@ __host__ __device__ __forceinline__ bool oz_narrow(int64_t cb, int64_t n_cb, int
 constexpr int OZ_SLICE_WARPS = OZ_SLICE_WARPS_CFG;
 constexpr int OZ_SLICE_ROWS = OZ_SLICE_ROWS_CFG;
 constexpr int OZ_SLICE_MAXCH = 32;   // K <= 512
+#ifndef OZ_SLICE_NARROW
+#define OZ_SLICE_NARROW 1            // 0: always the K <= 512 instance (measurement knob)
+#endif
+#ifndef OZ_SLICE_MINB_NARROW
+#define OZ_SLICE_MINB_NARROW 4
+#endif
 // staging: [chunk][slice][row 16] x 16 B plus one 16-B pad per chunk, so the
 // four chunks a warp's digit store touches land in different banks (without
 // the pad the chunk stride is 0 mod 32 words: a 4-way conflict on every
 // store, and the co-running GEMM is bound by the same shared-memory port)
 constexpr int OZ_SLICE_CH_STRIDE = OZ_S * OZ_SLICE_ROWS + 1;   // uint4 per chunk
 constexpr size_t OZ_SLICE_SMEM = size_t(OZ_SLICE_MAXCH) * OZ_SLICE_CH_STRIDE * 16;
-__global__ void __launch_bounds__(OZ_SLICE_WARPS * 32, OZ_SLICE_MINB) oz_slice_rows_kernel(const double* __restrict__ A,
+// NSEGMAX: 64-column segments a lane can hold (K <= 64 NSEGMAX).  The K <= 256
+// instance keeps two row buffers of 4 segments instead of 8, so more blocks
+// are resident and enough bytes are in flight for the narrow bases (c3:
+// K = 150, c2: K = 200), whose rows are only 1.2-1.6 KB.
+template <int NSEGMAX, int MINB>
+__global__ void __launch_bounds__(OZ_SLICE_WARPS * 32, MINB) oz_slice_rows_kernel(const double* __restrict__ A,
                                                                             int64_t lda, int64_t rows, int64_t K,
                                                                             int64_t nkc, uint8_t* __restrict__ sl,
                                                                             double* __restrict__ sa) {
@@ -253,7 +264,6 @@ __global__ void __launch_bounds__(OZ_SLICE_WARPS * 32, OZ_SLICE_MINB) oz_slice_r
   const int nch = static_cast<int>(nkc * 2);
   const int nseg = (nch + 3) / 4;                // 64-element segments
   constexpr int RPW = OZ_SLICE_ROWS / OZ_SLICE_WARPS;   // rows per warp
-  constexpr int NSEGMAX = OZ_SLICE_MAXCH / 4;
   // coalesced: lane holds elements 64 g + 2 lane, +1 of every segment g;
   // the next row's loads are issued before this row's digits
   auto load_row = [&](int jj, double2 (&x)[NSEGMAX]) {
@@ -290,7 +300,7 @@ __global__ void __launch_bounds__(OZ_SLICE_WARPS * 32, OZ_SLICE_MINB) oz_slice_r
     if (lane == 0) sa[r] = ldexp(1.0, e - 28);
     const double scale = ldexp(1.0, 54 - e);
 #pragma unroll
-    for (int g = 0; g < OZ_SLICE_MAXCH / 4; ++g) {
+    for (int g = 0; g < NSEGMAX; ++g) {
       if (g >= nseg) break;
       // Y = X + 0x808080808080: balanced digit s = byte (6 - s) of Y (^ 0x80 for s >= 1)
       const unsigned long long Y0 = static_cast<unsigned long long>(__double2ll_rn(x[g].x * scale)) + 0x808080808080ull;
@@ -740,8 +750,10 @@ int oz_set_attrs() {
   if (swb_first_on_device(&attr)) {
     SWB_CUDA_TRY(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(OZ_SMEM)));
-    SWB_CUDA_TRY(cudaFuncSetAttribute(oz_slice_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(OZ_SLICE_SMEM)));
+    SWB_CUDA_TRY(cudaFuncSetAttribute(oz_slice_rows_kernel<OZ_SLICE_MAXCH / 4, OZ_SLICE_MINB>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(OZ_SLICE_SMEM)));
+    SWB_CUDA_TRY(cudaFuncSetAttribute(oz_slice_rows_kernel<4, OZ_SLICE_MINB_NARROW>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(OZ_SLICE_SMEM / 2)));
   }
   return SWB_OK;
 }
@@ -787,8 +799,13 @@ extern "C" int swb_oz_split_rows(const double* A, int64_t lda, int64_t nr, int64
   const int64_t nrp = (nr + OZ_BM - 1) / OZ_BM * OZ_BM;
   // staging for this K only (2 nkc 16-column halves), not the K <= 512 maximum
   const size_t split_smem = size_t(2 * o.nkc) * OZ_SLICE_CH_STRIDE * 16;
-  oz_slice_rows_kernel<<<static_cast<unsigned>(nrp / OZ_SLICE_ROWS), OZ_SLICE_WARPS * 32, split_smem,
-                         swb_stream(stream)>>>(A, lda, nr, K, o.nkc, q.a_sl, q.sa);
+  if (K <= 256 && OZ_SLICE_NARROW)
+    oz_slice_rows_kernel<4, OZ_SLICE_MINB_NARROW><<<static_cast<unsigned>(nrp / OZ_SLICE_ROWS), OZ_SLICE_WARPS * 32,
+                                                    split_smem, swb_stream(stream)>>>(A, lda, nr, K, o.nkc, q.a_sl, q.sa);
+  else
+    oz_slice_rows_kernel<OZ_SLICE_MAXCH / 4, OZ_SLICE_MINB><<<static_cast<unsigned>(nrp / OZ_SLICE_ROWS),
+                                                               OZ_SLICE_WARPS * 32, split_smem, swb_stream(stream)>>>(
+        A, lda, nr, K, o.nkc, q.a_sl, q.sa);
   SWB_CHECK_LAUNCH();
   return SWB_OK;
 }
