@@ -242,6 +242,13 @@ constexpr int OZ_SLICE_MAXCH = 32;   // K <= 512
 #ifndef OZ_SLICE_MINB_NARROW
 #define OZ_SLICE_MINB_NARROW 4
 #endif
+// middle instance (K <= 64 OZ_SLICE_MID_SEGS; c4: K = 400 -> seven segments, no dead eighth: digit split 18.2 -> 17.6 ms), 0: none
+#ifndef OZ_SLICE_MID_SEGS
+#define OZ_SLICE_MID_SEGS 7
+#endif
+#ifndef OZ_SLICE_MINB_MID
+#define OZ_SLICE_MINB_MID 2
+#endif
 // staging: [chunk][slice][row 16] x 16 B plus one 16-B pad per chunk, so the
 // four chunks a warp's digit store touches land in different banks (without
 // the pad the chunk stride is 0 mod 32 words: a 4-way conflict on every
@@ -754,6 +761,10 @@ int oz_set_attrs() {
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(OZ_SLICE_SMEM)));
     SWB_CUDA_TRY(cudaFuncSetAttribute(oz_slice_rows_kernel<4, OZ_SLICE_MINB_NARROW>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(OZ_SLICE_SMEM / 2)));
+#if OZ_SLICE_MID_SEGS
+    SWB_CUDA_TRY(cudaFuncSetAttribute(oz_slice_rows_kernel<OZ_SLICE_MID_SEGS, OZ_SLICE_MINB_MID>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(OZ_SLICE_SMEM)));
+#endif
   }
   return SWB_OK;
 }
@@ -802,6 +813,12 @@ extern "C" int swb_oz_split_rows(const double* A, int64_t lda, int64_t nr, int64
   if (K <= 256 && OZ_SLICE_NARROW)
     oz_slice_rows_kernel<4, OZ_SLICE_MINB_NARROW><<<static_cast<unsigned>(nrp / OZ_SLICE_ROWS), OZ_SLICE_WARPS * 32,
                                                     split_smem, swb_stream(stream)>>>(A, lda, nr, K, o.nkc, q.a_sl, q.sa);
+#if OZ_SLICE_MID_SEGS
+  else if (K <= 64 * OZ_SLICE_MID_SEGS)
+    oz_slice_rows_kernel<OZ_SLICE_MID_SEGS, OZ_SLICE_MINB_MID><<<static_cast<unsigned>(nrp / OZ_SLICE_ROWS),
+                                                                 OZ_SLICE_WARPS * 32, split_smem, swb_stream(stream)>>>(
+        A, lda, nr, K, o.nkc, q.a_sl, q.sa);
+#endif
   else
     oz_slice_rows_kernel<OZ_SLICE_MAXCH / 4, OZ_SLICE_MINB><<<static_cast<unsigned>(nrp / OZ_SLICE_ROWS),
                                                                OZ_SLICE_WARPS * 32, split_smem, swb_stream(stream)>>>(
