@@ -219,7 +219,8 @@ def _time_cpu(s, threads, steps):
     from threadpoolctl import threadpool_limits
     p = s["params"]
     t = []
-    with threadpool_limits(limits=threads):
+    # None = every host core, stated explicitly: torchrun exports OMP_NUM_THREADS=1
+    with threadpool_limits(limits=threads or os.cpu_count()):
         used = blas_threads()
         for i in range(steps):
             b0, b1 = (p["beta0"], p["beta1"]) if i % 2 == 0 else (p["beta1"], p["beta0"])
@@ -279,14 +280,17 @@ def run_reference(args):
     m = args.m or W.CONFIGS[cfg]["m"]
     s = cpu_sample(cfg, dims, m)
     p = s["params"]
-    threads = blas_threads()
-    for i in range(args.warmup):
-        cpu_step(s, p["beta0"], p["beta1"], p["labels"])
-    t0 = time.perf_counter()
-    for i in range(args.steps):
-        b0, b1 = (p["beta0"], p["beta1"]) if i % 2 == 0 else (p["beta1"], p["beta0"])
-        cpu_step(s, b0, b1, p["labels"])
-    sec = (time.perf_counter() - t0) / max(args.steps, 1)
+    # all the host threads, also under torchrun (which exports OMP_NUM_THREADS=1 to every rank)
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=os.cpu_count()):
+        threads = blas_threads()
+        for i in range(args.warmup):
+            cpu_step(s, p["beta0"], p["beta1"], p["labels"])
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            b0, b1 = (p["beta0"], p["beta1"]) if i % 2 == 0 else (p["beta1"], p["beta0"])
+            cpu_step(s, b0, b1, p["labels"])
+        sec = (time.perf_counter() - t0) / max(args.steps, 1)
     value = s["n"] * m / sec
     dims_full = dims or W.CONFIGS[cfg]["dims"]
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
