@@ -177,9 +177,10 @@ def rotate_rows(V, ldv: int, Cm, ldc: int, rows: int, m: int, out, ldo: int, str
                   m, m2, i & 1, ptr(ws), ws.numel(), C.c_void_p(aux.cuda_stream))
         ev_split[i & 1].record(aux)
 
+    split_first = os.environ.get("SWB_OZ_SPLIT_FIRST") == "1"   # measurement knob: the other enqueue order
     split(0)
     for i in range(nch):
-        if i + 1 < nch:
+        if split_first and i + 1 < nch:
             split(i + 1)
         r0 = i * chunk
         main.wait_event(ev_split[i & 1])
@@ -190,6 +191,13 @@ def rotate_rows(V, ldv: int, Cm, ldc: int, rows: int, m: int, out, ldo: int, str
                   C.c_void_p(row_amax.data_ptr() + 8 * r0) if row_amax is not None else None,
                   ptr(ws), ws.numel(), st)
         ev_gemm[i & 1].record(main)
+        # GEMM i is enqueued before split i+1: both become runnable together
+        # (when GEMM i-1 and split i end) and cannot share an SM, so the
+        # order decides which runs first -- the GEMM, with the split in the
+        # SMs it frees; the other order charged the split's time to the
+        # GEMM's events on some runs (same total either way)
+        if not split_first and i + 1 < nch:
+            split(i + 1)
         mark("rotate_join")
 
 
