@@ -53,13 +53,13 @@ struct BoxGeom {
   int tx, ty, tz;      // output tile
   int r, rz;           // halo (rz = 0 for 2-D)
   int ex, ey, ez;      // extended tile
-  __host__ __device__ int n_e() const { return ex * ey * ez; }
-  __host__ __device__ int n_bx() const { return tx * ey * ez; }
-  __host__ __device__ int n_t() const { return tx * ty * tz; }
+  __host__ __device__ constexpr int n_e() const { return ex * ey * ez; }
+  __host__ __device__ constexpr int n_bx() const { return tx * ey * ez; }
+  __host__ __device__ constexpr int n_t() const { return tx * ty * tz; }
 };
 
-__host__ __device__ inline BoxGeom box_geom(int ndim, int r) {
-  BoxGeom g;
+__host__ __device__ constexpr BoxGeom box_geom(int ndim, int r) {
+  BoxGeom g{};
   g.tx = SC_TX;
   g.ty = ndim == 3 ? 8 : 32;
   g.tz = ndim == 3 ? 4 : 1;
@@ -75,13 +75,18 @@ inline size_t box_smem_bytes(const BoxGeom& g) {
   return sizeof(double) * (size_t(g.n_e()) + size_t(g.n_bx()) + size_t(g.n_t()) * SC_KC);
 }
 
+// CT_NDIM / CT_R > 0: the tile geometry is a compile-time constant (every
+// index split below divides by constants); CT_NDIM = 0: the runtime geometry.
+template <int CT_NDIM, int CT_R>
 __global__ void __launch_bounds__(SC_THREADS) box_scores_kernel(const double* __restrict__ F,
                                                                  const double* __restrict__ Mv, int nx, int ny,
-                                                                 int nz, int ndim, const int32_t* __restrict__ disp,
-                                                                 int K, int radius, double* __restrict__ scores,
+                                                                 int nz, int ndim_rt, const int32_t* __restrict__ disp,
+                                                                 int K, int radius_rt, double* __restrict__ scores,
                                                                  int64_t ld) {
   extern __shared__ double sm[];
-  const BoxGeom g = box_geom(ndim, radius);
+  const int ndim = CT_NDIM ? CT_NDIM : ndim_rt;
+  const int radius = CT_NDIM ? CT_R : radius_rt;
+  const BoxGeom g = CT_NDIM ? box_geom(CT_NDIM ? CT_NDIM : 3, CT_R) : box_geom(ndim_rt, radius_rt);
   double* E = sm;                     // extended tile; reused for the y-pass output
   double* Bx = E + g.n_e();
   double* res = Bx + g.n_bx();        // [voxel][SC_KC]
@@ -290,11 +295,21 @@ extern "C" int swb_similarity_priors(const double* fixed, const double* moving, 
   const size_t smem = box_smem_bytes(g);
   const int64_t tiles = int64_t((nx + g.tx - 1) / g.tx) * ((ny + g.ty - 1) / g.ty) * ((nz + g.tz - 1) / g.tz);
   if (smem <= 227 * 1024 && tiles < INT32_MAX && (K + SC_KC - 1) / SC_KC <= 65535) {
-    if (smem > 48 * 1024)
-      SWB_CUDA_TRY(cudaFuncSetAttribute(box_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     dim3 bg(unsigned(tiles), unsigned((K + SC_KC - 1) / SC_KC));
-    box_scores_kernel<<<bg, SC_THREADS, smem, st>>>(fixed, moving, int(nx), int(ny), int(nz), ndim, disp, int(K),
-                                                    patch_radius, scores, ld);
+#define SWB_BOX(ND, R)                                                                                            \
+  do {                                                                                                            \
+    if (smem > 48 * 1024)                                                                                         \
+      SWB_CUDA_TRY(cudaFuncSetAttribute(box_scores_kernel<ND, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                        int(smem)));                                                              \
+    box_scores_kernel<ND, R><<<bg, SC_THREADS, smem, st>>>(fixed, moving, int(nx), int(ny), int(nz), ndim, disp,  \
+                                                           int(K), patch_radius, scores, ld);                     \
+  } while (0)
+    if (ndim == 3 && patch_radius == 1) SWB_BOX(3, 1);
+    else if (ndim == 3 && patch_radius == 2) SWB_BOX(3, 2);
+    else if (ndim == 2 && patch_radius == 1) SWB_BOX(2, 1);
+    else if (ndim == 2 && patch_radius == 2) SWB_BOX(2, 2);
+    else SWB_BOX(0, 0);
+#undef SWB_BOX
   } else {
     patch_scores_kernel<<<grid, 256, 0, st>>>(fixed, moving, nx, ny, nz, ndim, disp, K, patch_radius, scores, ld);
   }
