@@ -79,7 +79,10 @@ def _bound(A, B):
     return 2.0 ** -50 * A.shape[1] * ra * cb
 
 
-@pytest.mark.parametrize("rows,K,M2", [(1, 1, 1), (129, 33, 65), (5000, 400, 400), (777, 96, 130)])
+@pytest.mark.parametrize("rows,K,M2", [(1, 1, 1), (129, 33, 65), (5000, 400, 400), (777, 96, 130),
+                                       # the digit split's instance boundaries (K <= 256 / <= 448 / <= 512)
+                                       (300, 256, 256), (300, 257, 100), (260, 448, 64), (260, 449, 64),
+                                       (200, 512, 512)])
 def test_fp64_product_within_bound(cuda_ok, rows, K, M2):
     rng = np.random.default_rng(7 * rows + K)
     A = rng.standard_normal((rows, K)) * np.exp(rng.uniform(-3, 3, (rows, 1)))
