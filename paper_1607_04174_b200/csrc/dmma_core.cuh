@@ -62,7 +62,15 @@ __device__ __forceinline__ void load_stage(double* sA, double* sB, const double*
       if (TOTAL % T != 0 && c >= TOTAL) break;
       const int r = c / CH, cc = (c % CH) * 2;
       const bool p = (r < a_rows) && (cc < a_cols);
-      cp_async16(sA + r * Cf::A_LD + cc, p ? A_t + r * lda + cc : A_t, p);
+      if (TN) {
+        cp_async16(sA + r * Cf::A_LD + cc, p ? A_t + r * lda + cc : A_t, p);
+      } else {
+        // NN: the columns are the reduction index.  An odd K ends in half a
+        // chunk: copy its 8 bytes and zero-fill the rest, so whatever sits
+        // past column K - 1 (a padding column, possibly NaN) never meets
+        // B's zero row (NaN * 0)
+        cp_async16_n(sA + r * Cf::A_LD + cc, p ? A_t + r * lda + cc : A_t, p ? (cc + 1 < a_cols ? 16 : 8) : 0);
+      }
     }
   }
   if (b_vec) {

@@ -73,23 +73,41 @@ __device__ __forceinline__ bool in_grid(const LatticeDev& L, int64_t x, int64_t 
 
 // --- graph build -----------------------------------------------------------
 
+// one thread per voxel, its forward edges in turn; 32-bit index splits when
+// the lattice allows (a 64-bit division by a runtime divisor is ~100
+// instructions, and the per-edge version paid five of them)
+template <typename IT>
+__device__ __forceinline__ void voxel_xyz(const LatticeDev& L, int64_t v, int64_t& x, int64_t& y, int64_t& z) {
+  const IT vv = static_cast<IT>(v), nx = static_cast<IT>(L.nx), ny = static_cast<IT>(L.ny);
+  const IT q = vv / nx;
+  x = static_cast<int64_t>(vv - q * nx);
+  const IT q2 = q / ny;
+  y = static_cast<int64_t>(q - q2 * ny);
+  z = static_cast<int64_t>(q2);
+}
+
 __global__ void edge_weight_kernel(const StencilGeom g, const double* __restrict__ I, double beta, int weight_mode,
                                    const uint8_t* __restrict__ cut, double* __restrict__ w, int64_t N) {
   const int nd = g.lat.ndir;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < N * nd;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t v = e / nd;
-    const int d = static_cast<int>(e % nd);
-    const int64_t x = v % g.lat.nx, y = (v / g.lat.nx) % g.lat.ny, z = v / (g.lat.nx * g.lat.ny);
-    const int64_t x2 = x + g.lat.dx[d], y2 = y + g.lat.dy[d], z2 = z + g.lat.dz[d];
-    double out = 0.0;
-    if (in_grid(g.lat, x2, y2, z2) && !(cut && cut[e])) {
-      const int64_t u = x2 + g.lat.nx * (y2 + g.lat.ny * z2);
-      const double diff = __dadd_rn(I[v], -I[u]);
-      const double arg = weight_mode == 0 ? fabs(diff) : __dmul_rn(diff, diff);
-      out = fmax(exp(__dmul_rn(-beta, arg)), W_MIN);  // graphs.py:136
+  const bool small = N < (int64_t(1) << 31);
+  for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < N; v += int64_t(gridDim.x) * blockDim.x) {
+    int64_t x, y, z;
+    if (small) voxel_xyz<uint32_t>(g.lat, v, x, y, z);
+    else voxel_xyz<int64_t>(g.lat, v, x, y, z);
+    const double iv = I[v];
+#pragma unroll 4
+    for (int d = 0; d < nd; ++d) {
+      const int64_t e = v * nd + d;
+      const int64_t x2 = x + g.lat.dx[d], y2 = y + g.lat.dy[d], z2 = z + g.lat.dz[d];
+      double out = 0.0;
+      if (in_grid(g.lat, x2, y2, z2) && !(cut && cut[e])) {
+        const int64_t u = x2 + g.lat.nx * (y2 + g.lat.ny * z2);
+        const double diff = __dadd_rn(iv, -I[u]);
+        const double arg = weight_mode == 0 ? fabs(diff) : __dmul_rn(diff, diff);
+        out = fmax(exp(__dmul_rn(-beta, arg)), W_MIN);  // graphs.py:136
+      }
+      w[e] = out;
     }
-    w[e] = out;
   }
 }
 
@@ -100,7 +118,9 @@ __global__ void degree_kernel(const StencilGeom g, const double* __restrict__ w,
   const int nd = g.lat.ndir;
   for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < N;
        v += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t x = v % g.lat.nx, y = (v / g.lat.nx) % g.lat.ny, z = v / (g.lat.nx * g.lat.ny);
+    int64_t x, y, z;
+    if (N < (int64_t(1) << 31)) voxel_xyz<uint32_t>(g.lat, v, x, y, z);
+    else voxel_xyz<int64_t>(g.lat, v, x, y, z);
     double deg = 0.0;
     for (int e = 0; e < g.nbr.n; ++e) {
       const int kind = g.nbr.kind[e];
@@ -127,17 +147,19 @@ __global__ void degree_kernel(const StencilGeom g, const double* __restrict__ w,
 // what = 0.5*((inv_x*w)*inv_y + (inv_y*w)*inv_x), in place over w
 __global__ void normalize_kernel(const StencilGeom g, double* __restrict__ w, const double* __restrict__ d_sqrt, int64_t N) {
   const int nd = g.lat.ndir;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < N * nd;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    const double we = w[e];
-    if (we == 0.0) continue;
-    const int64_t v = e / nd;
-    const int d = static_cast<int>(e % nd);
-    const int64_t u = v + g.lat.dx[d] + g.lat.nx * (g.lat.dy[d] + g.lat.ny * int64_t(g.lat.dz[d]));
-    const double iv = 1.0 / d_sqrt[v], iu = 1.0 / d_sqrt[u];
-    const double a = __dmul_rn(__dmul_rn(iv, we), iu);
-    const double b = __dmul_rn(__dmul_rn(iu, we), iv);
-    w[e] = __dmul_rn(__dadd_rn(a, b), 0.5);
+  for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < N; v += int64_t(gridDim.x) * blockDim.x) {
+    const double iv = 1.0 / d_sqrt[v];
+#pragma unroll 4
+    for (int d = 0; d < nd; ++d) {
+      const int64_t e = v * nd + d;
+      const double we = w[e];
+      if (we == 0.0) continue;
+      const int64_t u = v + g.lat.dx[d] + g.lat.nx * (g.lat.dy[d] + g.lat.ny * int64_t(g.lat.dz[d]));
+      const double iu = 1.0 / d_sqrt[u];
+      const double a = __dmul_rn(__dmul_rn(iv, we), iu);
+      const double b = __dmul_rn(__dmul_rn(iu, we), iv);
+      w[e] = __dmul_rn(__dadd_rn(a, b), 0.5);
+    }
   }
 }
 

@@ -88,6 +88,11 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pr
   int sz = pred ? 16 : 0;
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" :: "r"(s), "l"(gmem), "r"(sz));
 }
+// 16-byte slot, `bytes` (0, 8 or 16) copied from gmem and the rest zero-filled
+__device__ __forceinline__ void cp_async16_n(void* smem, const void* gmem, int bytes) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" :: "r"(s), "l"(gmem), "r"(bytes));
+}
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   int sz = pred ? 8 : 0;

@@ -265,6 +265,26 @@ def test_gemm_nn(cuda_ok, rows, k, m2):
     np.testing.assert_allclose(out.cpu().numpy()[:, :m2], want, rtol=1e-11, atol=1e-12 * np.abs(want).max())
 
 
+@pytest.mark.parametrize("rows,k,m2", [(500, 125, 3), (300, 7, 3), (257, 33, 64)])
+def test_gemm_nn_odd_k_ignores_padding_columns(cuda_ok, rows, k, m2):
+    """An odd reduction length ends in half a 16-byte chunk: the column past
+    K - 1 (here NaN, as uninitialised padding of a probability field can be)
+    must not reach the product (expected_displacement: 125 labels, ld 126)."""
+    import torch
+    from paper_1607_04174_b200 import _lib
+    from paper_1607_04174_b200.device import ptr, round_up, stream_handle
+    rng = np.random.default_rng(k + rows)
+    lda, ldb = round_up(k, 2), round_up(m2, 2)
+    A = rng.standard_normal((rows, lda))
+    A[:, k:] = np.nan
+    B = rng.standard_normal((k, ldb))
+    ad, bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    out = torch.zeros((rows, ldb), dtype=torch.float64, device="cuda")
+    _lib.call("swb_gemm_nn", ptr(ad), lda, ptr(bd), ldb, rows, k, m2, ptr(out), ldb, 0, stream_handle())
+    want = A[:, :k] @ B[:, :m2]
+    np.testing.assert_allclose(out.cpu().numpy()[:, :m2], want, rtol=1e-11, atol=1e-12 * np.abs(want).max())
+
+
 @pytest.mark.parametrize("n", [1, 5, 33, 64, 201, 801, 1001])
 def test_lu_solve_and_rcond_match_lapack(cuda_ok, n):
     import scipy.linalg as sla
