@@ -30,4 +30,10 @@ def cuda_ok():
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
+    if os.environ.get("SWB_TEST_NANFILL") == "1":
+        # debugging aid: every torch.empty comes back full of NaN, so a kernel
+        # that lets a padding element reach a result (NaN * 0) fails loudly
+        # instead of depending on what the allocator handed out
+        torch.use_deterministic_algorithms(True, warn_only=True)
+        torch.utils.deterministic.fill_uninitialized_memory = True
     return True
