@@ -865,13 +865,23 @@ extern "C" int swb_small_solve_ex(double gamma, int64_t S, int64_t m, int64_t L,
     SWB_CHECK_LAUNCH();
     if ((rc = swb_norm1(A, Ly.n, Ly.lda, anorm, base + Ly.off_nrm, sizeof(double) * size_t(Ly.n + 1), stream)))
       return rc;
-    if ((rc = swb_lu_factor(Kf, Ly.r, Ly.ldk, pk, nullptr, base + Ly.off_luk, swb_lu_workspace_bytes(Ly.r), stream)))
-      return rc;
     double* tb = reinterpret_cast<double*>(base + Ly.off_t);
-    if ((rc = swb_gemm_tn(Vt, Ly.ldw, rhs, Ly.ldr, Ly.n, Ly.r, L, 0, tb, Ly.ldr, tnw, tnw_bytes, stream))) return rc;
-    if ((rc = swb_lu_solve(Kf, Ly.r, Ly.ldk, pk, tb, L, Ly.ldr, base + Ly.off_rsk,
-                           swb_lu_solve_workspace_bytes(Ly.r, L), stream)))
-      return rc;
+    // K of up to 160 unknowns (c3: r = m + 2 <= 152): factors, pivots and K^-1 (Vt^T rhs) in one launch on
+    // column-owner threads (lu.cu); larger K (c4: r = 402): the blocked LU
+    const bool small_k = small_env && Ly.r <= 160 && Ly.r + L <= 256 &&
+                         sizeof(double) * size_t(Ly.r + 8) * size_t((Ly.r + L) | 1) <= size_t(220) * 1024;
+    if (small_k) {
+      if ((rc = swb_gemm_tn(Vt, Ly.ldw, rhs, Ly.ldr, Ly.n, Ly.r, L, 0, tb, Ly.ldr, tnw, tnw_bytes, stream))) return rc;
+      double* knorm = reinterpret_cast<double*>(base + Ly.off_luk);   // ||K||_1: not used (rcond is A's, below)
+      if ((rc = swb_small_dense_solve(Kf, Ly.r, Ly.ldk, pk, tb, L, Ly.ldr, knorm, nullptr, stream))) return rc;
+    } else {
+      if ((rc = swb_lu_factor(Kf, Ly.r, Ly.ldk, pk, nullptr, base + Ly.off_luk, swb_lu_workspace_bytes(Ly.r), stream)))
+        return rc;
+      if ((rc = swb_gemm_tn(Vt, Ly.ldw, rhs, Ly.ldr, Ly.n, Ly.r, L, 0, tb, Ly.ldr, tnw, tnw_bytes, stream))) return rc;
+      if ((rc = swb_lu_solve(Kf, Ly.r, Ly.ldk, pk, tb, L, Ly.ldr, base + Ly.off_rsk,
+                             swb_lu_solve_workspace_bytes(Ly.r, L), stream)))
+        return rc;
+    }
     if ((rc = swb_gemm_nn_alpha(Ut, Ly.ldw, tb, Ly.ldr, Ly.n, Ly.r, L, rhs, Ly.ldr, 1, 1.0, st))) return rc;
   } else if (small_n) {
     // one launch: 1-norm, LU and the solve (lu.cu); gecon below, as for the blocked LU
